@@ -1,0 +1,238 @@
+/*
+ * cgs_b200.h -- C ABI of the B200-native ContraGS training hot path.
+ *
+ * The reference (`contrags` 0.1.0, /root/reference/pkg/src/contrags) is pure
+ * Python with no FFI, so there is no C interface to replace; the entry points
+ * below are what a host binding of that package's hot path binds (see
+ * INTEGRATION.md for the ctypes stub).  Each function names the reference
+ * Python function(s) whose semantics it implements.
+ *
+ * Conventions
+ *   - all array arguments are DEVICE pointers unless marked "host";
+ *   - every call is asynchronous on `stream` (a cudaStream_t) unless marked
+ *     "synchronizes";
+ *   - all buffers, including workspaces, are caller-allocated; the library
+ *     holds no global state besides a thread-local last-error string;
+ *   - functions return 0 on success and a nonzero CGS_E* code otherwise,
+ *     never throwing across the ABI; cgs_last_error() describes the failure.
+ *
+ * Layouts follow the reference exactly (pkg/src/contrags/model.py:121-154):
+ *   positions (N,3) f32, opacity_logits (N,) f32, g2sh/g2sr (N,) i32,
+ *   SH rows (cap_sh, 3(d+1)^2) f32 coefficient-major row[b*3+ch] (sh.py:3-5),
+ *   SR rows (cap_sr, 7) f32 = [log-scale(3); quaternion w,x,y,z (4)].
+ * Images are (views, H, W, 3) f32, row-major, views concatenated.
+ */
+#ifndef CGS_B200_H
+#define CGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGS_ABI_VERSION 1
+#define CGS_MAX_VIEWS 16
+
+#define CGS_OK 0
+#define CGS_EINVAL 1     /* invalid argument (reference: ValueError)          */
+#define CGS_ECUDA 2      /* CUDA runtime error                                */
+#define CGS_EWORKSPACE 3 /* workspace too small                               */
+#define CGS_ENONFINITE 4 /* non-finite gradients (reference: SamplerError)    */
+
+#if defined(__GNUC__)
+#define CGS_API __attribute__((visibility("default")))
+#else
+#define CGS_API
+#endif
+
+typedef void* cgs_stream_t; /* cudaStream_t */
+
+/* Pinhole camera, reference camera.py:10-36: R is the row-major
+ * world->camera rotation, t the world->camera translation. */
+typedef struct cgs_camera {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} cgs_camera_t;
+
+/* Scene state S = {G, C}, reference model.py:121-154 (device pointers). */
+typedef struct cgs_scene {
+  int64_t n;
+  const float* positions;
+  const float* opacity_logits;
+  const int32_t* g2sh;
+  const int32_t* g2sr;
+  const float* sh_rows;
+  int64_t sh_capacity;
+  int32_t sh_degree; /* 0..3 */
+  const float* sr_rows;
+  int64_t sr_capacity;
+} cgs_scene_t;
+
+/* Counters a frame writes into its workspace header (device); read them
+ * with cgs_frame_stats. */
+typedef struct cgs_frame_stats {
+  int64_t n_onscreen;   /* splats with a non-empty pixel rect, all views       */
+  int64_t n_pairs;      /* (tile, splat) pairs P                               */
+  int64_t n_processed;  /* pairs inside each tile's processed prefix, P_x      */
+  int64_t n_touched;    /* (view, gaussian) pull-back entries U                */
+  int64_t pair_capacity;
+  int32_t overflow;     /* P exceeded pair_capacity: raster skipped            */
+  int32_t n_views;
+  int32_t zero_quaternion; /* a visible splat uses a zero quaternion (ValueError,
+                              render.py:40-41); its splat is dropped           */
+  int32_t pad_;
+} cgs_frame_stats_t;
+
+/* SGLD parameters, reference sampler.py:262-300 + SamplerConfig :45-55. */
+typedef struct cgs_sgld_params {
+  double step_pos, step_opacity, step_sh, step_sr;
+  double noise_pos, noise_opacity, noise_sh, noise_sr;
+  double grad_scale;     /* multiplies every gradient (1/views for a mean)   */
+  uint64_t seed;         /* device Philox stream (noise_source == 0)         */
+  uint64_t offset;
+  int32_t noise_source;  /* 0: device Philox, 1: caller arrays (parity)      */
+  int32_t pad_;
+} cgs_sgld_params_t;
+
+/* ---- library --------------------------------------------------------- */
+CGS_API int cgs_abi_version(void);
+CGS_API const char* cgs_last_error(void); /* thread-local, host */
+
+/* ---- render: rasterize_forward / rasterize_backward ------------------- */
+/* Workspace for one batched frame of n_views cameras (host cams).
+ * pair_capacity bounds the (tile, splat) pairs P (render.py:240-254). */
+CGS_API size_t cgs_frame_workspace_bytes(int64_t n, const cgs_camera_t* cams, int32_t n_views,
+                                 int64_t pair_capacity, int64_t sr_capacity);
+
+/* rasterize_forward (render.py:287-315) for n_views cameras at once:
+ * fused projection + codebook gather + SH (render.py:145-203), onesweep
+ * depth sort (render.py:203), tile duplication + stable tile sort
+ * (render.py:240-254), per-tile front-to-back blend (render.py:265-311).
+ * If P > pair_capacity the raster is skipped and stats.overflow is set. */
+CGS_API int cgs_render_forward(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                       void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                       float* image, float* final_T, int32_t* contrib_counts,
+                       cgs_stream_t stream);
+
+/* Device counters -> host struct. Synchronizes the stream. */
+CGS_API int cgs_frame_stats(const void* workspace, cgs_frame_stats_t* out_host, cgs_stream_t stream);
+
+/* The frame accessors below re-derive the workspace layout from the same
+ * (cams, n_views, n, pair_capacity, sr_capacity) the forward was given. */
+
+/* RenderArtifacts.tile_splats (render.py:296-302) as CSR: for view v and
+ * row-major tile t, ids[offsets[v*T+t] .. offsets[v*T+t+1]) are Gaussian
+ * indices in compositing order.  offsets: total_tiles+1 int64, ids: P int32. */
+CGS_API int cgs_frame_tile_lists(const cgs_camera_t* cams, int32_t n_views, int64_t n,
+                         int64_t pair_capacity, int64_t sr_capacity, const void* workspace,
+                         size_t workspace_bytes, int64_t* offsets, int32_t* ids,
+                         cgs_stream_t stream);
+
+/* Per-splat projection records for view v (for stage parity): mean2d (N,2)
+ * f64, conic (N,3) f64 [A,B,C], opacity (N) f64, color (N,3) f32, n_tiles (N)
+ * u32 (0 = culled or empty rect); only splats with n_tiles > 0 are defined. */
+CGS_API int cgs_frame_splats(const cgs_camera_t* cams, int32_t n_views, int64_t n, int64_t pair_capacity,
+                     int64_t sr_capacity, const void* workspace, size_t workspace_bytes,
+                     int32_t view, double* mean2d, double* conic, double* opacity, float* color,
+                     uint32_t* n_tiles, cgs_stream_t stream);
+
+CGS_API size_t cgs_backward_workspace_bytes(int64_t n, const cgs_camera_t* cams, int32_t n_views,
+                                    int64_t pair_capacity);
+
+/* rasterize_backward + _pull_back (render.py:318-459), reusing the frame's
+ * sorted pairs: reverse-order tile blend with in-CTA warp-shuffle reductions
+ * (one partial per processed pair), a stable sort of processed pairs by
+ * Gaussian, fixed-order per-Gaussian reduction + chain rule, then codebook
+ * gradients as sort-by-row segmented reductions (render.py:456-458, no
+ * atomics).  All four gradient arrays are fully written (zeros where the
+ * reference writes zeros), multiplied by `scale`.  final_T is the forward's
+ * output.  Deterministic. */
+CGS_API int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                        const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
+                        const float* final_T, const float* dL_dimage, float scale,
+                        void* workspace, size_t workspace_bytes,
+                        float* grad_positions, float* grad_logits,
+                        float* grad_sh_rows, float* grad_sr_rows, cgs_stream_t stream);
+
+/* ---- loss: recon_loss / recon_loss_grad (metrics.py:122-140) --------- */
+CGS_API size_t cgs_loss_workspace_bytes(int32_t n_views, int32_t height, int32_t width);
+
+/* Per view v: losses[3v..3v+2] = (l1, ssim, recon) as f64.  SSIM is computed
+ * when lambda != 0 or want_ssim != 0 and both sides are >= 11 (else NaN,
+ * metrics.py:126-128); if dL_dimage is non-null it receives d recon / d image
+ * scaled by grad_scale.  lambda != 0 with a side < 11 is CGS_EINVAL. */
+CGS_API int cgs_recon_loss(const float* image, const float* gt, int32_t n_views, int32_t height,
+                   int32_t width, double lambda_ssim, int32_t want_ssim, float grad_scale,
+                   float* dL_dimage, double* losses, void* workspace, size_t workspace_bytes,
+                   cgs_stream_t stream);
+
+/* ---- SGLD update (sampler.py:262-300) --------------------------------- */
+/* Checks every gradient for finiteness first; if any is non-finite nothing
+ * is written and flags[0] = 1 (host raises SamplerError).  Live rows are
+ * given as index lists; the finiteness check covers all sh_capacity /
+ * sr_capacity gradient rows (GradientSet.all_finite, render.py:222-224).
+ * Parity noise arrays (noise_source 1) hold the reference's standard
+ * normals: (N,3), (N,), (live_sh, D), (live_sr, 7). */
+CGS_API int cgs_sgld_update(float* positions, float* opacity_logits, int64_t n,
+                    float* sh_rows, int32_t sh_dim, const int32_t* sh_live, int64_t n_sh_live,
+                    float* sr_rows, const int32_t* sr_live, int64_t n_sr_live,
+                    int64_t sh_capacity, int64_t sr_capacity,
+                    const float* grad_positions, const float* grad_logits,
+                    const float* grad_sh_rows, const float* grad_sr_rows,
+                    const cgs_sgld_params_t* params_host,
+                    const double* noise_pos, const double* noise_logit,
+                    const double* noise_sh, const double* noise_sr,
+                    int32_t* flags, cgs_stream_t stream);
+
+/* ---- MCMC / densify device helpers (sampler.py:184-259, model.py:235-267) */
+/* Ascending Gaussian ids i with refcount[idx[i]] >= 2 (sampler.py:344);
+ * count written to *count (device int64).  Workspace from
+ * cgs_scan_workspace_bytes(n). */
+CGS_API int cgs_split_eligible(const int32_t* idx, int64_t n, const int32_t* refcount,
+                       int32_t* eligible, int64_t* count, void* workspace,
+                       size_t workspace_bytes, cgs_stream_t stream);
+
+/* Accepted splits in proposal order (sampler.py:202-209): for each j,
+ * rows[new_row[j]] = f32(f64(rows[old_row[j]]) + u[j]) and idx[gauss[j]] =
+ * new_row[j].  u: (k, dim) f64. */
+CGS_API int cgs_apply_splits(float* rows, int32_t dim, int32_t* idx, const int64_t* gauss,
+                     const int32_t* old_row, const int32_t* new_row, const double* u,
+                     int64_t k, cgs_stream_t stream);
+
+/* Accepted merges composed into one row remap (sampler.py:240-247):
+ * idx[i] = remap[idx[i]] where remap[r] >= 0. */
+CGS_API int cgs_apply_remap(int32_t* idx, int64_t n, const int32_t* remap, int64_t remap_len,
+                    cgs_stream_t stream);
+
+/* densify clones (model.py:256-266): Gaussian n+j copies src[j] with
+ * position f32(f64(pos[src[j]]) + jitter[j]). */
+CGS_API int cgs_densify_append(float* positions, float* opacity_logits, int32_t* g2sh, int32_t* g2sr,
+                       int64_t n, const int64_t* src, const double* jitter, int64_t k,
+                       cgs_stream_t stream);
+
+/* counts[r] = #{i : idx[i] == r} (validate_state, model.py:297). */
+CGS_API int cgs_refcount_histogram(const int32_t* idx, int64_t n, int32_t* counts, int64_t capacity,
+                           cgs_stream_t stream);
+
+/* ---- primitives (exported for unit tests) ---------------------------- */
+CGS_API size_t cgs_scan_workspace_bytes(int64_t n);
+/* exclusive prefix sum of u32 into u32; total into *total (device u64). */
+CGS_API int cgs_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint64_t* total,
+                           void* workspace, size_t workspace_bytes, cgs_stream_t stream);
+
+CGS_API size_t cgs_sort_workspace_bytes(int64_t n, int32_t key_bytes);
+/* Stable LSD onesweep radix sort of (key, value) pairs on the low key_bits.
+ * key_bytes in {2,4,8}.  keys/vals are sorted in place (alt buffers of the
+ * same size are carved from the workspace). */
+CGS_API int cgs_radix_sort_pairs(void* keys, uint32_t* vals, int64_t n, int32_t key_bytes,
+                         int32_t key_bits, void* workspace, size_t workspace_bytes,
+                         cgs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGS_B200_H */

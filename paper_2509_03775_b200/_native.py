@@ -1,0 +1,158 @@
+"""ctypes binding of ``libcgs_b200.so`` (C ABI: include/cgs_b200.h).
+
+The product path has no CPU fallback: if the library is missing or a CUDA
+device is absent, every compute entry point raises.  Pointers passed here
+are raw device addresses of torch tensors; every call is enqueued on the
+caller's current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .camera import CCamera
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcgs_b200.so")
+
+CGS_OK, CGS_EINVAL, CGS_ECUDA, CGS_EWORKSPACE, CGS_ENONFINITE = 0, 1, 2, 3, 4
+MAX_VIEWS = 16
+
+
+class CScene(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("positions", ctypes.c_void_p),
+        ("opacity_logits", ctypes.c_void_p),
+        ("g2sh", ctypes.c_void_p),
+        ("g2sr", ctypes.c_void_p),
+        ("sh_rows", ctypes.c_void_p),
+        ("sh_capacity", ctypes.c_int64),
+        ("sh_degree", ctypes.c_int32),
+        ("sr_rows", ctypes.c_void_p),
+        ("sr_capacity", ctypes.c_int64),
+    ]
+
+
+class CFrameStats(ctypes.Structure):
+    _fields_ = [
+        ("n_onscreen", ctypes.c_int64),
+        ("n_pairs", ctypes.c_int64),
+        ("n_processed", ctypes.c_int64),
+        ("n_touched", ctypes.c_int64),
+        ("pair_capacity", ctypes.c_int64),
+        ("overflow", ctypes.c_int32),
+        ("n_views", ctypes.c_int32),
+        ("zero_quaternion", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+    ]
+
+
+class CSgldParams(ctypes.Structure):
+    _fields_ = [
+        ("step_pos", ctypes.c_double), ("step_opacity", ctypes.c_double),
+        ("step_sh", ctypes.c_double), ("step_sr", ctypes.c_double),
+        ("noise_pos", ctypes.c_double), ("noise_opacity", ctypes.c_double),
+        ("noise_sh", ctypes.c_double), ("noise_sr", ctypes.c_double),
+        ("grad_scale", ctypes.c_double),
+        ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64),
+        ("noise_source", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    ]
+
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+SZ = ctypes.c_size_t
+F32 = ctypes.c_float
+F64 = ctypes.c_double
+CAMP = ctypes.POINTER(CCamera)
+SCNP = ctypes.POINTER(CScene)
+
+# name -> (restype, argtypes); must match include/cgs_b200.h
+SIGNATURES = {
+    "cgs_abi_version": (I32, []),
+    "cgs_last_error": (ctypes.c_char_p, []),
+    "cgs_frame_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64]),
+    "cgs_render_forward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
+    "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),
+    "cgs_frame_tile_lists": (I32, [CAMP, I32, I64, I64, I64, P, SZ, P, P, P]),
+    "cgs_frame_splats": (I32, [CAMP, I32, I64, I64, I64, P, SZ, I32, P, P, P, P, P, P]),
+    "cgs_backward_workspace_bytes": (SZ, [I64, CAMP, I32, I64]),
+    "cgs_render_backward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, F32, P, SZ, P, P, P, P, P]),
+    "cgs_loss_workspace_bytes": (SZ, [I32, I32, I32]),
+    "cgs_recon_loss": (I32, [P, P, I32, I32, I32, F64, I32, F32, P, P, P, SZ, P]),
+    "cgs_sgld_update": (I32, [P, P, I64, P, I32, P, I64, P, P, I64, I64, I64, P, P, P, P,
+                              ctypes.POINTER(CSgldParams), P, P, P, P, P, P]),
+    "cgs_split_eligible": (I32, [P, I64, P, P, P, P, SZ, P]),
+    "cgs_apply_splits": (I32, [P, I32, P, P, P, P, P, I64, P]),
+    "cgs_apply_remap": (I32, [P, I64, P, I64, P]),
+    "cgs_densify_append": (I32, [P, P, P, P, I64, P, P, I64, P]),
+    "cgs_refcount_histogram": (I32, [P, I64, P, I64, P]),
+    "cgs_scan_workspace_bytes": (SZ, [I64]),
+    "cgs_exclusive_scan_u32": (I32, [P, P, I64, P, P, SZ, P]),
+    "cgs_sort_workspace_bytes": (SZ, [I64, I32]),
+    "cgs_radix_sort_pairs": (I32, [P, P, I64, I32, I32, P, SZ, P]),
+}
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def library() -> ctypes.CDLL:
+    """Load (once) the CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return library().cgs_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = ""):
+    if rc == CGS_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == CGS_EINVAL:
+        raise ValueError(msg)
+    if rc == CGS_ENONFINITE:
+        from .sampler import SamplerError
+        raise SamplerError(msg)
+    raise NativeError(f"cgs error {rc}: {msg}")
+
+
+def call(name: str, *args):
+    """Invoke an ABI function and raise the reference's exception type on failure."""
+    rc = getattr(library(), name)(*args)
+    check(rc, name)
+
+
+def cams_array(cams) -> ctypes.Array:
+    arr = (CCamera * len(cams))()
+    for i, c in enumerate(cams):
+        arr[i] = c.to_c()
+    return arr
+
+
+def ptr(t) -> int:
+    """Device address of a torch tensor (0 for None)."""
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream

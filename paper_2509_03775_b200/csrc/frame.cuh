@@ -1,0 +1,121 @@
+// Frame workspace layout shared by the forward and backward render paths.
+#pragma once
+
+#include "common.cuh"
+#include "sort_scan.cuh"
+
+namespace cgs {
+
+struct FrameLayout {
+  FrameHeader* hdr;
+  SplatRec* recs;          // V*N
+  uint64_t* depth_key;     // V*N (f64 bits of camera z)
+  uint32_t* n_tiles;       // V*N
+  uint64_t* rect;          // V*N packed tile rect
+  uint64_t* skeys;         // V*N compacted depth keys
+  uint32_t* svals;         // V*N compacted splat ids
+  SortWs<uint64_t> dsort;
+  uint64_t* pair_off;      // V*N exclusive pair offsets in depth order
+  void* pkeys;             // pair_cap tile keys (u16 or u32)
+  uint32_t* pvals;         // pair_cap splat ids
+  SortWs<uint16_t> psort16;
+  SortWs<uint32_t> psort32;
+  uint2* ranges;           // total_tiles [start, end)
+  uint32_t* px_last;       // total_pixels
+  uint32_t* tile_nproc;    // total_tiles
+  ScanWs scan;
+  double* sr_cov;          // sr_cap * 8 (Sigma3 + zero-quaternion flag)
+  // results of the sorts (set by forward, re-derived identically by backward)
+  size_t bytes;
+  int64_t n, vn, pair_cap;
+  int tile_key_bytes;      // 2 or 4
+  int tile_key_bits;
+  int depth_result_alt;    // 1 if sorted depth results live in dsort alt buffers
+  int pair_result_alt;
+};
+
+inline int bits_for(int64_t v) {
+  int b = 1;
+  while ((1LL << b) < v) ++b;
+  return b;
+}
+
+inline FrameDesc make_frame_desc(const cgs_camera_t* cams, int n_views) {
+  FrameDesc fd{};
+  fd.n_views = n_views;
+  int tiles = 0;
+  int64_t pix = 0;
+  for (int v = 0; v < n_views; ++v) {
+    CamDev& c = fd.cam[v];
+    for (int k = 0; k < 9; ++k) c.R[k] = cams[v].R[k];
+    for (int k = 0; k < 3; ++k) c.t[k] = cams[v].t[k];
+    c.fx = cams[v].fx; c.fy = cams[v].fy; c.cx = cams[v].cx; c.cy = cams[v].cy;
+    // center = -R^T t (camera.py:34-36)
+    for (int j = 0; j < 3; ++j)
+      c.center[j] = -(c.R[0 * 3 + j] * c.t[0] + c.R[1 * 3 + j] * c.t[1] + c.R[2 * 3 + j] * c.t[2]);
+    c.width = cams[v].width;
+    c.height = cams[v].height;
+    c.ntx = (c.width + kTile - 1) / kTile;
+    c.nty = (c.height + kTile - 1) / kTile;
+    c.tile_base = tiles;
+    c.pix_base = pix;
+    tiles += c.ntx * c.nty;
+    pix += static_cast<int64_t>(c.width) * c.height;
+  }
+  fd.total_tiles = tiles;
+  fd.total_pixels = pix;
+  return fd;
+}
+
+inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const FrameDesc& fd,
+                              int64_t pair_cap, int64_t sr_cap) {
+  FrameLayout L{};
+  Carver c(base, cap_bytes);
+  const int64_t vn = n * fd.n_views;
+  const int64_t vn1 = vn > 0 ? vn : 1;
+  const int64_t pc = pair_cap > 0 ? pair_cap : 1;
+  L.n = n;
+  L.vn = vn;
+  L.pair_cap = pair_cap;
+  L.tile_key_bytes = fd.total_tiles <= 65535 ? 2 : 4;
+  L.tile_key_bits = bits_for(fd.total_tiles + 1);
+  L.hdr = c.take<FrameHeader>(1);
+  L.recs = c.take<SplatRec>(vn1);
+  L.depth_key = c.take<uint64_t>(vn1);
+  L.n_tiles = c.take<uint32_t>(vn1);
+  L.rect = c.take<uint64_t>(vn1);
+  L.skeys = c.take<uint64_t>(vn1);
+  L.svals = c.take<uint32_t>(vn1);
+  L.dsort = carve_sort<uint64_t>(c, vn1);
+  L.pair_off = c.take<uint64_t>(vn1);
+  if (L.tile_key_bytes == 2) {
+    L.pkeys = c.take<uint16_t>(pc);
+    L.psort16 = carve_sort<uint16_t>(c, pc);
+  } else {
+    L.pkeys = c.take<uint32_t>(pc);
+    L.psort32 = carve_sort<uint32_t>(c, pc);
+  }
+  L.pvals = c.take<uint32_t>(pc);
+  L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
+  L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.scan = carve_scan(c, vn1 > fd.total_tiles ? vn1 : fd.total_tiles);
+  L.sr_cov = c.take<double>((sr_cap > 0 ? sr_cap : 1) * 8);
+  L.bytes = c.off + 256;
+  // pass parity: 8 passes for f64 depth keys -> result back in the input buffers
+  L.depth_result_alt = (8 % 2) == 1;
+  const int ppasses = (L.tile_key_bits + 7) / 8;
+  L.pair_result_alt = (ppasses % 2) == 1;
+  return L;
+}
+
+// Sorted (splat id) list in depth order and sorted pair arrays.
+inline const uint32_t* sorted_splats(const FrameLayout& L) {
+  return L.depth_result_alt ? L.dsort.vals_alt : L.svals;
+}
+inline const uint32_t* sorted_pair_vals(const FrameLayout& L) {
+  if (!L.pair_result_alt) return L.pvals;
+  return L.tile_key_bytes == 2 ? L.psort16.vals_alt : L.psort32.vals_alt;
+}
+
+}  // namespace cgs

@@ -1,0 +1,155 @@
+// Device helpers shared by the forward and backward render kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace cgs {
+
+constexpr double kLog2e = 1.4426950408889634;
+
+// Unit quaternion (w,x,y,z) -> rotation, reference render.py:45-58.
+__device__ __forceinline__ void quat_to_rot(double w, double x, double y, double z, double* R) {
+  R[0] = 1 - 2 * (y * y + z * z);
+  R[1] = 2 * (x * y - w * z);
+  R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z);
+  R[4] = 1 - 2 * (x * x + z * z);
+  R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y);
+  R[7] = 2 * (y * z + w * x);
+  R[8] = 1 - 2 * (x * x + y * y);
+}
+
+// Real SH basis, reference sh.py:27-53 (same constants and sign convention).
+template <int DEG>
+__device__ __forceinline__ void sh_basis(double x, double y, double z, double* o) {
+  o[0] = kC0;
+  if constexpr (DEG >= 1) {
+    o[1] = -kC1 * y;
+    o[2] = kC1 * z;
+    o[3] = -kC1 * x;
+  }
+  if constexpr (DEG >= 2) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    o[4] = kC2_0 * x * y;
+    o[5] = kC2_1 * y * z;
+    o[6] = kC2_2 * (2.0 * zz - xx - yy);
+    o[7] = kC2_3 * x * z;
+    o[8] = kC2_4 * (xx - yy);
+  }
+  if constexpr (DEG >= 3) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    o[9] = kC3_0 * y * (3.0 * xx - yy);
+    o[10] = kC3_1 * x * y * z;
+    o[11] = kC3_2 * y * (4.0 * zz - xx - yy);
+    o[12] = kC3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    o[13] = kC3_4 * x * (4.0 * zz - xx - yy);
+    o[14] = kC3_5 * z * (xx - yy);
+    o[15] = kC3_6 * x * (xx - 3.0 * yy);
+  }
+}
+
+// Single SH basis function b at direction (x,y,z) (runtime index).
+__device__ __forceinline__ double sh_basis_one(int b, double x, double y, double z) {
+  const double xx = x * x, yy = y * y, zz = z * z;
+  switch (b) {
+    case 0: return kC0;
+    case 1: return -kC1 * y;
+    case 2: return kC1 * z;
+    case 3: return -kC1 * x;
+    case 4: return kC2_0 * x * y;
+    case 5: return kC2_1 * y * z;
+    case 6: return kC2_2 * (2.0 * zz - xx - yy);
+    case 7: return kC2_3 * x * z;
+    case 8: return kC2_4 * (xx - yy);
+    case 9: return kC3_0 * y * (3.0 * xx - yy);
+    case 10: return kC3_1 * x * y * z;
+    case 11: return kC3_2 * y * (4.0 * zz - xx - yy);
+    case 12: return kC3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    case 13: return kC3_4 * x * (4.0 * zz - xx - yy);
+    case 14: return kC3_5 * z * (xx - yy);
+    default: return kC3_6 * x * (xx - 3.0 * yy);
+  }
+}
+
+// d basis_b / d dir accumulated against weights: g += sum_b w[b] * dB_b/d(x,y,z)
+// (reference sh.py:56-100).
+template <int DEG>
+__device__ __forceinline__ void sh_basis_grad_dot(double x, double y, double z, const double* w,
+                                                  double* g) {
+  g[0] = g[1] = g[2] = 0.0;
+  if constexpr (DEG >= 1) {
+    g[1] += -kC1 * w[1];
+    g[2] += kC1 * w[2];
+    g[0] += -kC1 * w[3];
+  }
+  if constexpr (DEG >= 2) {
+    g[0] += kC2_0 * y * w[4];
+    g[1] += kC2_0 * x * w[4];
+    g[1] += kC2_1 * z * w[5];
+    g[2] += kC2_1 * y * w[5];
+    g[0] += -2.0 * kC2_2 * x * w[6];
+    g[1] += -2.0 * kC2_2 * y * w[6];
+    g[2] += 4.0 * kC2_2 * z * w[6];
+    g[0] += kC2_3 * z * w[7];
+    g[2] += kC2_3 * x * w[7];
+    g[0] += 2.0 * kC2_4 * x * w[8];
+    g[1] += -2.0 * kC2_4 * y * w[8];
+  }
+  if constexpr (DEG >= 3) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    g[0] += kC3_0 * 6.0 * x * y * w[9];
+    g[1] += kC3_0 * (3.0 * xx - 3.0 * yy) * w[9];
+    g[0] += kC3_1 * y * z * w[10];
+    g[1] += kC3_1 * x * z * w[10];
+    g[2] += kC3_1 * x * y * w[10];
+    g[0] += -2.0 * kC3_2 * x * y * w[11];
+    g[1] += kC3_2 * (4.0 * zz - xx - 3.0 * yy) * w[11];
+    g[2] += 8.0 * kC3_2 * y * z * w[11];
+    g[0] += -6.0 * kC3_3 * x * z * w[12];
+    g[1] += -6.0 * kC3_3 * y * z * w[12];
+    g[2] += kC3_3 * (6.0 * zz - 3.0 * xx - 3.0 * yy) * w[12];
+    g[0] += kC3_4 * (4.0 * zz - 3.0 * xx - yy) * w[13];
+    g[1] += -2.0 * kC3_4 * x * y * w[13];
+    g[2] += 8.0 * kC3_4 * x * z * w[13];
+    g[0] += 2.0 * kC3_5 * x * z * w[14];
+    g[1] += -2.0 * kC3_5 * y * z * w[14];
+    g[2] += kC3_5 * (xx - yy) * w[14];
+    g[0] += kC3_6 * (3.0 * xx - 3.0 * yy) * w[15];
+    g[1] += -6.0 * kC3_6 * x * y * w[15];
+  }
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// fp64 record -> fp32 shared-memory form for one tile whose first pixel
+// centre is (ox + 0.5, oy + 0.5).  The offset is formed in fp64 so the fp32
+// pixel offsets stay exact to fp32 rounding of small numbers even at
+// ~2000-pixel coordinates.  The conic is pre-scaled by -0.5*log2(e) (A, C)
+// and -log2(e) (B) so the exponent is three FMAs and one ex2.
+//   a = (dx0, dy0, A2, B2)   b = (C2, opacity, red, green)   c = blue
+__device__ __forceinline__ void stage_splat(const SplatRec& r, double ox, double oy, float4& a,
+                                            float4& b, float& c) {
+  a.x = static_cast<float>(ox + 0.5 - r.mx);
+  a.y = static_cast<float>(oy + 0.5 - r.my);
+  a.z = static_cast<float>(-0.5 * kLog2e * r.ca);
+  a.w = static_cast<float>(-kLog2e * r.cb);
+  b.x = static_cast<float>(-0.5 * kLog2e * r.cc);
+  b.y = static_cast<float>(r.opac);
+  b.z = r.r;
+  b.w = r.g;
+  c = r.b;
+}
+
+// alpha = min(o * exp(power), 0.99) (render.py:274-278); skip test by caller.
+__device__ __forceinline__ float splat_alpha(const float4& a, const float4& b, float dx, float dy) {
+  const float p2 = fmaf(a.z * dx, dx, fmaf(a.w * dx, dy, b.x * dy * dy));
+  const float al = b.y * fast_exp2(p2);
+  return fminf(al, kAlphaClampVal);
+}
+
+}  // namespace cgs

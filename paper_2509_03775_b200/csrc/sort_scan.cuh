@@ -1,0 +1,397 @@
+// Single-pass primitives for sm_100a: decoupled-lookback exclusive scan and
+// onesweep (decoupled-lookback) LSD radix sort, both stable and
+// deterministic.  Element counts may live in device memory so the whole
+// frame can be enqueued (and graph-captured) without host round trips; the
+// grid is sized for a capacity and surplus CTAs exit after claiming an
+// out-of-range partition id.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace cgs {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_volatile(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
+template <typename T>
+__device__ __forceinline__ void st_volatile(T* p, T v) {
+  *reinterpret_cast<volatile T*>(p) = v;
+}
+
+__device__ __forceinline__ int64_t dev_count(const unsigned long long* n_dev, int64_t n_host) {
+  return n_dev ? static_cast<int64_t>(ld_volatile(n_dev)) : n_host;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ===========================================================================
+// Exclusive scan.  Op provides:
+//   __device__ uint64_t load(int64_t i) const;
+//   __device__ void store(int64_t i, uint64_t exclusive, uint64_t value) const;
+// Partitions of 8 warps x 8 rounds x 32 lanes; within a warp every round is
+// 32 consecutive elements (coalesced), so the running sum follows index
+// order.  Status words: value in bits 0..61, flag in 62..63.
+// ===========================================================================
+constexpr int kScanWarps = 8;
+constexpr int kScanRounds = 8;
+constexpr int kScanTile = kScanWarps * kScanRounds * 32;  // 2048
+constexpr unsigned long long kScanAgg = 1ULL << 62;
+constexpr unsigned long long kScanPre = 2ULL << 62;
+constexpr unsigned long long kScanVal = (1ULL << 62) - 1;
+
+struct ScanWs {
+  unsigned long long* status;  // max_parts
+  unsigned* counter;
+  int64_t max_parts;
+};
+
+inline size_t scan_ws_bytes(int64_t n_cap) {
+  int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanTile);
+  return align_up(parts * sizeof(unsigned long long)) + 256;
+}
+
+inline ScanWs carve_scan(Carver& c, int64_t n_cap) {
+  ScanWs w;
+  w.max_parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanTile);
+  w.status = c.take<unsigned long long>(w.max_parts);
+  w.counter = c.take<unsigned>(64);
+  return w;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long long* n_dev,
+                                                   int64_t n_host, ScanWs ws,
+                                                   unsigned long long* total) {
+  __shared__ unsigned s_part;
+  __shared__ unsigned long long s_warp[kScanWarps];
+  __shared__ unsigned long long s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_part = atomicAdd(ws.counter, 1u);
+  __syncthreads();
+  const int64_t part = s_part;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t nparts = n > 0 ? ceil_div(n, kScanTile) : 1;
+  if (part >= nparts) return;
+  const int64_t wbase = part * kScanTile + static_cast<int64_t>(warp) * kScanRounds * 32;
+
+  unsigned long long v[kScanRounds], ex[kScanRounds];
+  unsigned long long run = 0;
+#pragma unroll
+  for (int j = 0; j < kScanRounds; ++j) {
+    const int64_t i = wbase + j * 32 + lane;
+    v[j] = (i < n) ? op.load(i) : 0ULL;
+    unsigned long long inc = warp_incl_scan(v[j]);
+    ex[j] = run + inc - v[j];
+    run += __shfl_sync(kFull, inc, 31);
+  }
+  if (lane == 0) s_warp[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long wv = lane < kScanWarps ? s_warp[lane] : 0ULL;
+    unsigned long long winc = warp_incl_scan(wv);
+    const unsigned long long agg = __shfl_sync(kFull, winc, kScanWarps - 1);
+    if (lane < kScanWarps) s_warp[lane] = winc - wv;
+    unsigned long long excl = 0;
+    if (part == 0) {
+      if (lane == 0) st_volatile(&ws.status[0], kScanPre | agg);
+    } else {
+      if (lane == 0) st_volatile(&ws.status[part], kScanAgg | agg);
+      int64_t p = part - 1;
+      while (true) {
+        const int64_t q = p - lane;
+        unsigned long long s = (q >= 0) ? ld_volatile(&ws.status[q]) : kScanPre;
+        const unsigned long long flag = s >> 62;
+        const unsigned is_pre = __ballot_sync(kFull, flag == 2);
+        const unsigned not_ready = __ballot_sync(kFull, flag == 0);
+        const int first_pre = is_pre ? __ffs(is_pre) - 1 : 32;
+        const unsigned relevant = first_pre >= 31 ? kFull : ((2u << first_pre) - 1u);
+        if (not_ready & relevant) continue;  // spin until the window is published
+        unsigned long long val = (lane <= first_pre) ? (s & kScanVal) : 0ULL;
+        excl += warp_sum(val);
+        if (first_pre < 32) break;
+        p -= 32;
+      }
+      if (lane == 0) st_volatile(&ws.status[part], kScanPre | (excl + agg));
+    }
+    if (lane == 0) {
+      s_prefix = excl;
+      if (part == nparts - 1 && total) *total = excl + agg;
+    }
+  }
+  __syncthreads();
+  const unsigned long long base = s_prefix + s_warp[warp];
+#pragma unroll
+  for (int j = 0; j < kScanRounds; ++j) {
+    const int64_t i = wbase + j * 32 + lane;
+    if (i < n) op.store(i, base + ex[j], v[j]);
+  }
+}
+
+template <class Op>
+int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t n_cap,
+                const ScanWs& ws, unsigned long long* total, cudaStream_t st) {
+  CGS_CUDA(cudaMemsetAsync(ws.status, 0, ws.max_parts * sizeof(unsigned long long), st));
+  CGS_CUDA(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st));
+  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanTile);
+  scan_kernel<Op><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total);
+  CGS_CHECK_LAUNCH("scan_kernel");
+  return CGS_OK;
+}
+
+// ===========================================================================
+// Onesweep LSD radix sort, 8-bit digits.  One histogram kernel for all
+// passes, then one kernel per pass: per-warp match_any ranking (stable),
+// per-digit decoupled lookback across partitions, smem reorder, coalesced
+// scatter.  Status words: 30-bit count, flag in bits 30..31.
+// ===========================================================================
+constexpr int kSortWarps = 8;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortWarps * 32 * kSortItems;  // 4096
+constexpr unsigned kSortAgg = 1u << 30;
+constexpr unsigned kSortPre = 2u << 30;
+constexpr unsigned kSortVal = (1u << 30) - 1;
+
+template <typename K>
+struct SortWs {
+  K* keys_alt;
+  uint32_t* vals_alt;
+  uint32_t* hist;     // passes * 256
+  uint32_t* status;   // passes * max_parts * 256
+  unsigned* counter;  // passes
+  int64_t max_parts;
+  int passes_cap;
+};
+
+template <typename K>
+inline size_t sort_ws_bytes(int64_t n_cap) {
+  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kSortTile);
+  const int passes = static_cast<int>(sizeof(K));
+  return align_up(n_cap * sizeof(K)) + align_up(n_cap * sizeof(uint32_t)) +
+         align_up(passes * 256 * 4) + align_up(passes * parts * 256 * 4) + 256 + 4 * 256;
+}
+
+template <typename K>
+inline SortWs<K> carve_sort(Carver& c, int64_t n_cap) {
+  SortWs<K> w;
+  w.max_parts = ceil_div(n_cap > 0 ? n_cap : 1, kSortTile);
+  w.passes_cap = static_cast<int>(sizeof(K));
+  w.keys_alt = c.take<K>(n_cap > 0 ? n_cap : 1);
+  w.vals_alt = c.take<uint32_t>(n_cap > 0 ? n_cap : 1);
+  w.hist = c.take<uint32_t>(w.passes_cap * 256);
+  w.status = c.take<uint32_t>(static_cast<size_t>(w.passes_cap) * w.max_parts * 256);
+  w.counter = c.take<unsigned>(64);
+  return w;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ keys,
+                                                        const unsigned long long* n_dev,
+                                                        int64_t n_host, int passes,
+                                                        uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_h[8 * 256];
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const int64_t n = dev_count(n_dev, n_host);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = static_cast<uint64_t>(keys[i]);
+    for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+    if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+template <typename K>
+struct SortSmem {
+  uint32_t wcnt[kSortWarps * 256];
+  uint32_t dstart[256];
+  int32_t goff[256];
+  uint32_t scan_tmp[kSortWarps];
+  unsigned part;
+  K keys[kSortTile];
+  uint32_t vals[kSortTile];
+};
+
+template <typename K>
+__global__ void __launch_bounds__(256) onesweep_kernel(
+    const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+    const unsigned long long* n_dev, int64_t n_host, int shift,
+    const uint32_t* __restrict__ hist, uint32_t* status, unsigned* counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem<K>& S = *reinterpret_cast<SortSmem<K>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) S.part = atomicAdd(counter, 1u);
+  for (int i = tid; i < kSortWarps * 256; i += 256) S.wcnt[i] = 0;
+  __syncthreads();
+  const int64_t part = S.part;
+  const int64_t n = dev_count(n_dev, n_host);
+  const int64_t nparts = ceil_div(n, kSortTile);
+  if (part >= nparts) return;
+  const int64_t base = part * kSortTile;
+  const int64_t wbase = base + static_cast<int64_t>(warp) * 32 * kSortItems;
+
+  K key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t rank[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const int64_t i = wbase + j * 32 + lane;
+    const bool ok = i < n;
+    key[j] = ok ? keys_in[i] : static_cast<K>(~static_cast<K>(0));
+    val[j] = ok ? vals_in[i] : 0u;
+  }
+  uint32_t* wc = S.wcnt + warp * 256;
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & 255u);
+    const unsigned peers = __match_any_sync(kFull, d);
+    const unsigned before = wc[d];
+    rank[j] = before + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (lane == __ffs(peers) - 1) wc[d] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // thread tid owns digit d = tid: exclusive over warps, then over digits
+  const int d = tid;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) {
+    const uint32_t c = S.wcnt[w * 256 + d];
+    S.wcnt[w * 256 + d] = cnt;
+    cnt += c;
+  }
+  {
+    const uint32_t inc = warp_incl_scan(cnt);
+    if (lane == 31) S.scan_tmp[warp] = inc;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += S.scan_tmp[w];
+    S.dstart[d] = wpre + inc - cnt;
+  }
+  // global digit base = exclusive scan of the pass histogram
+  const uint32_t h = hist[d];
+  uint32_t gbase;
+  {
+    __syncthreads();
+    const uint32_t inc = warp_incl_scan(h);
+    if (lane == 31) S.scan_tmp[warp] = inc;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += S.scan_tmp[w];
+    gbase = wpre + inc - h;
+  }
+  // decoupled lookback for digit d over previous partitions
+  const int64_t tail = base + kSortTile - n;
+  const uint32_t agg = cnt - ((d == 255 && tail > 0) ? static_cast<uint32_t>(tail) : 0u);
+  uint32_t excl = 0;
+  uint32_t* st = status + part * 256 + d;
+  if (part == 0) {
+    st_volatile(st, kSortPre | agg);
+  } else {
+    st_volatile(st, kSortAgg | agg);
+    int64_t p = part - 1;
+    while (true) {
+      const uint32_t s = ld_volatile(status + p * 256 + d);
+      const uint32_t flag = s >> 30;
+      if (flag == 0) continue;
+      excl += s & kSortVal;
+      if (flag == 2) break;
+      --p;
+    }
+    st_volatile(st, kSortPre | (excl + agg));
+  }
+  S.goff[d] = static_cast<int32_t>(gbase + excl) - static_cast<int32_t>(S.dstart[d]);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & 255u);
+    const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
+    S.keys[pos] = key[j];
+    S.vals[pos] = val[j];
+  }
+  __syncthreads();
+  const int nvalid = static_cast<int>(n - base < kSortTile ? n - base : kSortTile);
+  for (int i = tid; i < nvalid; i += 256) {
+    const K k = S.keys[i];
+    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & 255u);
+    const int64_t o = static_cast<int64_t>(S.goff[dd]) + i;
+    keys_out[o] = k;
+    vals_out[o] = S.vals[i];
+  }
+}
+
+// Sorts (keys, vals) of length n (device count n_dev if non-null, else
+// n_host; n_cap bounds it) on the low key_bits.  Returns, through
+// out_keys/out_vals, the buffers holding the result (the inputs or the
+// workspace alternates, depending on the pass count).
+template <typename K>
+int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, int64_t n_host,
+                      int64_t n_cap, int key_bits, const SortWs<K>& ws, K** out_keys,
+                      uint32_t** out_vals, cudaStream_t st) {
+  int passes = (key_bits + 7) / 8;
+  if (passes < 1) passes = 1;
+  if (passes > ws.passes_cap) return CGS_EINVAL;
+  CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
+  CGS_CUDA(cudaMemsetAsync(ws.status, 0,
+                           static_cast<size_t>(passes) * ws.max_parts * 256 * sizeof(uint32_t), st));
+  CGS_CUDA(cudaMemsetAsync(ws.counter, 0, 64 * sizeof(unsigned), st));
+  sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist);
+  CGS_CHECK_LAUNCH("sort_hist_kernel");
+  static bool attr_set = false;
+  const size_t smem = sizeof(SortSmem<K>);
+  if (!attr_set) {
+    CGS_CUDA(cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    attr_set = true;
+  }
+  K* kin = keys;
+  uint32_t* vin = vals;
+  K* kout = ws.keys_alt;
+  uint32_t* vout = ws.vals_alt;
+  const unsigned grid = static_cast<unsigned>(ceil_div(n_cap > 0 ? n_cap : 1, kSortTile));
+  for (int p = 0; p < passes; ++p) {
+    onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p,
+                                                ws.hist + p * 256,
+                                                ws.status + static_cast<size_t>(p) * ws.max_parts * 256,
+                                                ws.counter + p);
+    CGS_CHECK_LAUNCH("onesweep_kernel");
+    K* tk = kin; kin = kout; kout = tk;
+    uint32_t* tv = vin; vin = vout; vout = tv;
+  }
+  *out_keys = kin;
+  *out_vals = vin;
+  return CGS_OK;
+}
+
+}  // namespace cgs

@@ -1,0 +1,294 @@
+// SGLD update (reference sampler.py:262-300) and the MCMC / densify device
+// helpers (sampler.py:184-259, model.py:235-267).  Arithmetic mirrors numpy's
+// un-fused float64 sequence exactly (explicit _rn intrinsics, no FMA
+// contraction), so identical gradients and noise give bit-identical float32
+// state.
+#include <cmath>
+
+#include "common.cuh"
+#include "sort_scan.cuh"
+
+namespace cgs {
+
+// ---- Philox4x32-10 + Box-Muller (device noise, throughput mode) ----------
+__device__ __forceinline__ uint4 philox(uint4 ctr, uint2 key) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    key.x += 0x9E3779B9u;
+    key.y += 0xBB67AE85u;
+  }
+  return ctr;
+}
+
+__device__ __forceinline__ double philox_normal(uint64_t seed, uint64_t offset, uint32_t stream,
+                                                uint64_t idx) {
+  const uint4 c = philox(make_uint4(static_cast<unsigned>(idx), static_cast<unsigned>(idx >> 32),
+                                    stream, static_cast<unsigned>(offset)),
+                         make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32)));
+  const uint64_t a = (static_cast<uint64_t>(c.x) << 21) ^ c.y;
+  const uint64_t b = (static_cast<uint64_t>(c.z) << 21) ^ c.w;
+  const double u1 = (static_cast<double>(a & ((1ULL << 53) - 1)) + 0.5) * 0x1.0p-53;
+  const double u2 = static_cast<double>(b & ((1ULL << 53) - 1)) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+struct SgldDev {
+  double c_pos, c_op, c_sh, c_sr;  // 0.5 * eps per group
+  double k_pos, k_op, k_sh, k_sr;  // mult * sqrt(eps) (0 = no noise)
+  int on_pos, on_op, on_sh, on_sr;
+  double gscale;
+  uint64_t seed, offset;
+  int noise_src;
+};
+
+__device__ __forceinline__ float sgld_one(float v, float g, double c, double k, double gscale,
+                                          const double* noise_arr, int64_t nidx, int noise_src,
+                                          uint64_t seed, uint64_t offset, uint32_t stream) {
+  double gg = static_cast<double>(g);
+  if (gscale != 1.0) gg = __dmul_rn(gg, gscale);
+  double nv = __dsub_rn(static_cast<double>(v), __dmul_rn(c, gg));
+  if (k != 0.0) {
+    const double eta = noise_src == 1 ? noise_arr[nidx] : philox_normal(seed, offset, stream, nidx);
+    nv = __dadd_rn(nv, __dmul_rn(k, eta));
+  }
+  return __double2float_rn(nv);
+}
+
+__global__ void __launch_bounds__(256) finite_check_kernel(const float* __restrict__ a, int64_t na,
+                                                           const float* __restrict__ b, int64_t nb,
+                                                           const float* __restrict__ c, int64_t nc,
+                                                           const float* __restrict__ d, int64_t nd,
+                                                           int32_t* flags) {
+  const int64_t tot = na + nb + nc + nd;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float x;
+    if (i < na) x = a[i];
+    else if (i < na + nb) x = b[i - na];
+    else if (i < na + nb + nc) x = c[i - na - nb];
+    else x = d[i - na - nb - nc];
+    if (!isfinite(x)) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flags[0] = 1;
+}
+
+__global__ void __launch_bounds__(256) sgld_kernel(
+    float* __restrict__ pos, float* __restrict__ logit, int64_t n, float* __restrict__ sh,
+    int D, const int32_t* __restrict__ sh_live, int64_t n_sh, float* __restrict__ sr,
+    const int32_t* __restrict__ sr_live, int64_t n_sr, const float* __restrict__ gpos,
+    const float* __restrict__ glogit, const float* __restrict__ gsh,
+    const float* __restrict__ gsr, SgldDev p, const double* __restrict__ npos,
+    const double* __restrict__ nlog, const double* __restrict__ nsh,
+    const double* __restrict__ nsr, const int32_t* __restrict__ flags) {
+  if (flags[0]) return;  // non-finite gradients: reject before any mutation
+  const int64_t a = p.on_pos ? 3 * n : 0;
+  const int64_t b = p.on_op ? n : 0;
+  const int64_t c = p.on_sh ? n_sh * D : 0;
+  const int64_t d = p.on_sr ? n_sr : 0;
+  const int64_t tot = a + b + c + d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < a) {
+      pos[i] = sgld_one(pos[i], gpos[i], p.c_pos, p.k_pos, p.gscale, npos, i, p.noise_src, p.seed,
+                        p.offset, 0);
+    } else if (i < a + b) {
+      const int64_t j = i - a;
+      logit[j] = sgld_one(logit[j], glogit[j], p.c_op, p.k_op, p.gscale, nlog, j, p.noise_src,
+                          p.seed, p.offset, 1);
+    } else if (i < a + b + c) {
+      const int64_t j = i - a - b;
+      const int64_t li = j / D, col = j - li * D;
+      const int64_t e = static_cast<int64_t>(sh_live[li]) * D + col;
+      sh[e] = sgld_one(sh[e], gsh[e], p.c_sh, p.k_sh, p.gscale, nsh, j, p.noise_src, p.seed,
+                       p.offset, 2);
+    } else {
+      const int64_t li = i - a - b - c;
+      const int64_t r = sr_live[li];
+      double v[7];
+#pragma unroll
+      for (int k = 0; k < 7; ++k) {
+        double gg = static_cast<double>(gsr[r * 7 + k]);
+        if (p.gscale != 1.0) gg = __dmul_rn(gg, p.gscale);
+        double nv = __dsub_rn(static_cast<double>(sr[r * 7 + k]), __dmul_rn(p.c_sr, gg));
+        if (p.k_sr != 0.0) {
+          const double eta = p.noise_src == 1 ? nsr[li * 7 + k]
+                                              : philox_normal(p.seed, p.offset, 3, li * 7 + k);
+          nv = __dadd_rn(nv, __dmul_rn(p.k_sr, eta));
+        }
+        v[k] = nv;
+      }
+      // q / ||q||, numpy's sequential ((q0^2+q1^2)+q2^2)+q3^2 (sampler.py:298-299)
+      const double s = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(v[3], v[3]), __dmul_rn(v[4], v[4])),
+                                           __dmul_rn(v[5], v[5])),
+                                 __dmul_rn(v[6], v[6]));
+      const double nq = __dsqrt_rn(s);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) sr[r * 7 + k] = __double2float_rn(v[k]);
+#pragma unroll
+      for (int k = 3; k < 7; ++k) sr[r * 7 + k] = __double2float_rn(__ddiv_rn(v[k], nq));
+    }
+  }
+}
+
+int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int32_t* sh_live,
+                int64_t n_sh, float* sr, const int32_t* sr_live, int64_t n_sr, const float* gpos,
+                const float* glogit, const float* gsh, const float* gsr, int64_t sh_cap,
+                int64_t sr_cap, const cgs_sgld_params_t* hp, const double* npos,
+                const double* nlog, const double* nsh, const double* nsr, int32_t* flags,
+                cudaStream_t st) {
+  CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+  const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
+  finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
+                                                                          nc, gsr, nd, flags);
+  CGS_CHECK_LAUNCH("finite_check_kernel");
+  SgldDev p{};
+  // exactly numpy's scalar sub-expressions: 0.5 * eps and mult * sqrt(eps)
+  p.c_pos = 0.5 * hp->step_pos;
+  p.c_op = 0.5 * hp->step_opacity;
+  p.c_sh = 0.5 * hp->step_sh;
+  p.c_sr = 0.5 * hp->step_sr;
+  p.k_pos = (hp->noise_pos != 0.0 && hp->step_pos > 0.0) ? hp->noise_pos * std::sqrt(hp->step_pos) : 0.0;
+  p.k_op = (hp->noise_opacity != 0.0 && hp->step_opacity > 0.0) ? hp->noise_opacity * std::sqrt(hp->step_opacity) : 0.0;
+  p.k_sh = (hp->noise_sh != 0.0 && hp->step_sh > 0.0) ? hp->noise_sh * std::sqrt(hp->step_sh) : 0.0;
+  p.k_sr = (hp->noise_sr != 0.0 && hp->step_sr > 0.0) ? hp->noise_sr * std::sqrt(hp->step_sr) : 0.0;
+  p.on_pos = hp->step_pos > 0.0;
+  p.on_op = hp->step_opacity > 0.0;
+  p.on_sh = hp->step_sh > 0.0;
+  p.on_sr = hp->step_sr > 0.0;
+  p.gscale = hp->grad_scale;
+  p.seed = hp->seed;
+  p.offset = hp->offset;
+  p.noise_src = hp->noise_source;
+  if (p.noise_src == 1) {
+    if ((p.k_pos != 0.0 && !npos) || (p.k_op != 0.0 && !nlog) || (p.k_sh != 0.0 && !nsh) ||
+        (p.k_sr != 0.0 && !nsr)) {
+      set_error("sgld: noise_source=1 needs the noise array of every noisy group");
+      return CGS_EINVAL;
+    }
+  }
+  const int64_t tot = (p.on_pos ? 3 * n : 0) + (p.on_op ? n : 0) + (p.on_sh ? n_sh * D : 0) +
+                      (p.on_sr ? n_sr : 0);
+  if (tot > 0) {
+    sgld_kernel<<<grid_for(tot, 256, 8), 256, 0, st>>>(pos, logit, n, sh, D, sh_live, n_sh, sr,
+                                                       sr_live, n_sr, gpos, glogit, gsh, gsr, p,
+                                                       npos, nlog, nsh, nsr, flags);
+    CGS_CHECK_LAUNCH("sgld_kernel");
+  }
+  return CGS_OK;
+}
+
+// ---- MCMC helpers ---------------------------------------------------------
+struct EligibleOp {
+  const int32_t* idx;
+  const int32_t* rc;
+  int32_t* out;
+  __device__ uint64_t load(int64_t i) const { return rc[idx[i]] >= 2 ? 1ULL : 0ULL; }
+  __device__ void store(int64_t i, uint64_t ex, uint64_t v) const {
+    if (v) out[ex] = static_cast<int32_t>(i);
+  }
+};
+
+__global__ void copy_count_kernel(const unsigned long long* src, int64_t* dst) {
+  *dst = static_cast<int64_t>(*src);
+}
+
+int split_eligible(const int32_t* idx, int64_t n, const int32_t* rc, int32_t* out, int64_t* count,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
+  Carver c(ws, ws_bytes);
+  ScanWs sw = carve_scan(c, n);
+  unsigned long long* tot = c.take<unsigned long long>(1);
+  if (!c.fits()) {
+    set_error("split_eligible: workspace too small");
+    return CGS_EWORKSPACE;
+  }
+  int r = launch_scan(EligibleOp{idx, rc, out}, nullptr, n, n, sw, tot, st);
+  if (r) return r;
+  copy_count_kernel<<<1, 1, 0, st>>>(tot, count);
+  CGS_CHECK_LAUNCH("copy_count_kernel");
+  return CGS_OK;
+}
+
+__global__ void apply_splits_kernel(float* rows, int dim, int32_t* idx, const int64_t* gauss,
+                                    const int32_t* old_row, const int32_t* new_row,
+                                    const double* u, int64_t k) {
+  const int64_t tot = k * dim;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e / dim, c = e - j * dim;
+    const double val = __dadd_rn(static_cast<double>(rows[static_cast<int64_t>(old_row[j]) * dim + c]), u[e]);
+    rows[static_cast<int64_t>(new_row[j]) * dim + c] = __double2float_rn(val);
+    if (c == 0) idx[gauss[j]] = new_row[j];
+  }
+}
+
+int apply_splits(float* rows, int dim, int32_t* idx, const int64_t* gauss, const int32_t* old_row,
+                 const int32_t* new_row, const double* u, int64_t k, cudaStream_t st) {
+  if (k <= 0) return CGS_OK;
+  apply_splits_kernel<<<grid_for(k * dim, 256, 8), 256, 0, st>>>(rows, dim, idx, gauss, old_row,
+                                                                 new_row, u, k);
+  CGS_CHECK_LAUNCH("apply_splits_kernel");
+  return CGS_OK;
+}
+
+__global__ void remap_kernel(int32_t* idx, int64_t n, const int32_t* remap, int64_t len) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = idx[i];
+    if (r >= 0 && r < len) {
+      const int32_t t = remap[r];
+      if (t >= 0) idx[i] = t;
+    }
+  }
+}
+
+int apply_remap(int32_t* idx, int64_t n, const int32_t* remap, int64_t len, cudaStream_t st) {
+  if (n <= 0) return CGS_OK;
+  remap_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(idx, n, remap, len);
+  CGS_CHECK_LAUNCH("remap_kernel");
+  return CGS_OK;
+}
+
+__global__ void densify_kernel(float* pos, float* logit, int32_t* g2sh, int32_t* g2sr, int64_t n,
+                               const int64_t* src, const double* jit, int64_t k) {
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < k;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = src[j], d = n + j;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      pos[3 * d + c] = __double2float_rn(__dadd_rn(static_cast<double>(pos[3 * s + c]), jit[3 * j + c]));
+    logit[d] = logit[s];
+    g2sh[d] = g2sh[s];
+    g2sr[d] = g2sr[s];
+  }
+}
+
+int densify_append(float* pos, float* logit, int32_t* g2sh, int32_t* g2sr, int64_t n,
+                   const int64_t* src, const double* jit, int64_t k, cudaStream_t st) {
+  if (k <= 0) return CGS_OK;
+  densify_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(pos, logit, g2sh, g2sr, n, src, jit, k);
+  CGS_CHECK_LAUNCH("densify_kernel");
+  return CGS_OK;
+}
+
+__global__ void histogram_kernel(const int32_t* idx, int64_t n, int32_t* counts, int64_t cap) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t r = idx[i];
+    if (r >= 0 && r < cap) atomicAdd(&counts[r], 1);  // integer: order-independent
+  }
+}
+
+int refcount_histogram(const int32_t* idx, int64_t n, int32_t* counts, int64_t cap,
+                       cudaStream_t st) {
+  if (cap > 0) CGS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * cap, st));
+  if (n <= 0) return CGS_OK;
+  histogram_kernel<<<grid_for(n, 256, 8), 256, 0, st>>>(idx, n, counts, cap);
+  CGS_CHECK_LAUNCH("histogram_kernel");
+  return CGS_OK;
+}
+
+}  // namespace cgs

@@ -1,0 +1,575 @@
+"""Markov-chain training engine (reference `pkg/src/contrags/sampler.py`).
+
+Same API, same transition semantics and the same consumption of the
+caller's ``np.random.Generator``, so split / merge /
+densify decisions are bit-identical to the reference.  The continuous work
+runs on the device: rendering and gradients through the C ABI, SGLD through
+``cgs_sgld_update``, split/merge/densify applies through the MCMC kernels.
+Host work is only the inherently sequential accept/reject bookkeeping on the
+refcount / lineage / free-list mirrors.
+
+Noise: by default (parity mode) SGLD noise is drawn from the caller's
+Generator in the reference's order and uploaded.  With
+``SamplerConfig.device_noise=True`` (throughput mode) it is drawn on the
+device from Philox(seed, iteration) and the host stream no longer matches
+the reference after the first noisy update (documented in DESIGN.md).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .metrics import LossWorkspace, total_loss
+from .model import ModelState, _book_of, densify, validate_state
+from .render import Frame, GradientSet, rasterize_forward
+
+
+class SamplerError(RuntimeError):
+    pass
+
+
+@dataclass
+class SamplerConfig:
+    """sampler.py:29-93 (same fields and defaults) + device_noise."""
+
+    p_update: float = 0.98
+    p_split: float = 0.01
+    p_merge: float = 0.01
+    eps_split_sh: float = 0.1
+    eps_merge_sh: float = 0.05
+    eps_split_sr: float = 0.1
+    eps_merge_sr: float = 0.05
+    lambda_sh: float = 2.3
+    lambda_sr: float = 3.0
+    lambda_ssim: float = 0.2
+    step_pos: float = 0.5
+    step_opacity: float = 10.0
+    step_sh: float = 20.0
+    step_sr: float = 2.0
+    noise_pos: float = 1.0
+    noise_opacity: float = 0.0
+    noise_sh: float = 0.0
+    noise_sr: float = 0.0
+    split_fraction: float = 0.01
+    densify_every: int = 100
+    densify_growth: float = 0.05
+    densify_jitter: float = 0.02
+    gaussian_cap: int = 2_000_000
+    normalization_correction: bool = False
+    exact_ratio: bool = False
+    seed: int = 0
+    device_noise: bool = False
+
+    def validate(self) -> None:
+        if abs(self.p_update + self.p_split + self.p_merge - 1.0) > 1e-12:
+            raise ValueError("mixture probabilities must sum to 1")
+        for name in ("eps_split_sh", "eps_merge_sh", "eps_split_sr", "eps_merge_sr"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+
+    @classmethod
+    def for_synthetic_fixture(cls, seed: int = 0) -> "SamplerConfig":
+        return cls(step_pos=4.0, step_opacity=80.0, step_sh=150.0, step_sr=15.0,
+                   noise_pos=0.0, gaussian_cap=256, seed=seed)
+
+    def eps_for(self, which: str):
+        if which == "sh":
+            return self.eps_split_sh, self.eps_merge_sh
+        if which == "sr":
+            return self.eps_split_sr, self.eps_merge_sr
+        raise ValueError(f"unknown codebook {which!r}")
+
+    def lambda_for(self, which: str) -> float:
+        return self.lambda_sh if which == "sh" else self.lambda_sr
+
+
+class TransitionRecord:
+    """sampler.py:96-110; ``recon`` may be a device scalar read on first access."""
+
+    def __init__(self, iteration: int, kind: str, codebook: str, attempts: int = 0,
+                 accepts: int = 0, delta_sh: int = 0, delta_sr: int = 0, live_sh: int = 0,
+                 live_sr: int = 0, recon=float("nan"), psnr: float = float("nan"),
+                 accept_probs=None, lambdas=(2.3, 3.0)):
+        self.iteration = iteration
+        self.kind = kind
+        self.codebook = codebook
+        self.attempts = attempts
+        self.accepts = accepts
+        self.delta_sh = delta_sh
+        self.delta_sr = delta_sr
+        self.live_sh = live_sh
+        self.live_sr = live_sr
+        self._recon = recon
+        self.psnr = psnr
+        self.accept_probs = [] if accept_probs is None else accept_probs
+        self._lambdas = lambdas
+
+    @property
+    def recon(self) -> float:
+        if isinstance(self._recon, torch.Tensor):
+            self._recon = float(self._recon.item())
+        return self._recon
+
+    @recon.setter
+    def recon(self, v):
+        self._recon = v
+
+    @property
+    def total(self) -> float:
+        r = self.recon
+        if not np.isfinite(r):
+            return float("nan")
+        return total_loss(r, self.live_sh, self.live_sr, *self._lambdas).total
+
+    def __repr__(self):
+        return (f"TransitionRecord(iteration={self.iteration}, kind={self.kind!r}, "
+                f"codebook={self.codebook!r}, attempts={self.attempts}, accepts={self.accepts}, "
+                f"live_sh={self.live_sh}, live_sr={self.live_sr})")
+
+
+def choose_transition(config: SamplerConfig, rng: np.random.Generator) -> str:
+    """sampler.py:113-119"""
+    r = rng.random()
+    if r < config.p_update:
+        return "update"
+    if r < config.p_update + config.p_split:
+        return "split"
+    return "merge"
+
+
+def _log_q_sm(u, eps_split, eps_merge, correction):
+    u = np.atleast_1d(np.asarray(u, dtype=np.float64))
+    u2 = float(u @ u)
+    log_q = -0.5 * u2 * (1.0 / eps_split ** 2 - 1.0 / eps_merge ** 2)
+    if correction:
+        log_q += u.size * math.log(eps_merge / eps_split)
+    return log_q
+
+
+def q_sm(u, eps_split: float, eps_merge: float, correction: bool = False) -> float:
+    """sampler.py:122-135"""
+    with np.errstate(over="ignore"):
+        return float(np.exp(_log_q_sm(u, eps_split, eps_merge, correction)))
+
+
+def acceptance_probability(kind: str, u, lam: float, eps_split: float, eps_merge: float,
+                           correction: bool = False, extra_log_ratio: float = 0.0) -> float:
+    """sampler.py:147-164"""
+    log_q = _log_q_sm(u, eps_split, eps_merge, correction)
+    if kind == "split":
+        log_a = -lam - log_q + extra_log_ratio
+    elif kind == "merge":
+        log_a = lam + log_q + extra_log_ratio
+    else:
+        raise ValueError(f"unknown transition kind {kind!r}")
+    return float(np.exp(min(0.0, log_a)))
+
+
+@dataclass
+class SplitProposal:
+    which: str
+    gaussian: int
+    row: int
+    u: np.ndarray
+    new_value: np.ndarray
+
+
+@dataclass
+class MergeProposal:
+    which: str
+    child: int
+    parent: int
+    u: np.ndarray
+
+
+# ---------------------------------------------------------------------------
+# single-move API (per-call device round trips; train_step batches instead)
+def propose_split(state: ModelState, which: str, i: int, config: SamplerConfig,
+                  rng: np.random.Generator) -> Optional[SplitProposal]:
+    """sampler.py:184-199"""
+    book, idx = _book_of(state, which)
+    row = int(idx[i])
+    if book.refcount[row] < 2:
+        return None
+    eps_split, _ = config.eps_for(which)
+    u = rng.normal(0.0, eps_split, size=book.dim)
+    return SplitProposal(which=which, gaussian=int(i), row=row, u=u,
+                         new_value=book.row(row).astype(np.float64) + u)
+
+
+def _apply_split_batch(state: ModelState, which: str, moves):
+    """Device apply of accepted splits: moves = [(gaussian, old_row, new_row, u)]."""
+    if not moves:
+        return
+    book, idx = _book_of(state, which)
+    dev = book.device
+    g = torch.as_tensor(np.array([m[0] for m in moves], np.int64)).to(dev)
+    o = torch.as_tensor(np.array([m[1] for m in moves], np.int32)).to(dev)
+    nw = torch.as_tensor(np.array([m[2] for m in moves], np.int32)).to(dev)
+    u = torch.as_tensor(np.ascontiguousarray(np.stack([m[3] for m in moves]), np.float64)).to(dev)
+    nat.call("cgs_apply_splits", nat.ptr(book.rows), book.dim, nat.ptr(idx), nat.ptr(g), nat.ptr(o),
+             nat.ptr(nw), nat.ptr(u), len(moves), nat.stream_handle(dev))
+    book.mutations += 1
+    state.touch()
+
+
+def apply_split(state: ModelState, proposal: SplitProposal) -> int:
+    """sampler.py:202-209"""
+    book, _ = _book_of(state, proposal.which)
+    new_row = book.alloc_index(parent=proposal.row)
+    book.decref(proposal.row)
+    _apply_split_batch(state, proposal.which,
+                       [(proposal.gaussian, proposal.row, new_row, np.asarray(proposal.u, np.float64))])
+    return new_row
+
+
+def accept_split(state: ModelState, proposal: SplitProposal, lam: float, config: SamplerConfig,
+                 rng: np.random.Generator, extra_log_ratio: float = 0.0) -> bool:
+    """sampler.py:212-221"""
+    es, em = config.eps_for(proposal.which)
+    prob = acceptance_probability("split", proposal.u, lam, es, em,
+                                  config.normalization_correction, extra_log_ratio)
+    if rng.random() < prob:
+        apply_split(state, proposal)
+        return True
+    return False
+
+
+def _rows_host(book, rows: np.ndarray) -> np.ndarray:
+    if len(rows) == 0:
+        return np.zeros((0, book.dim), np.float32)
+    t = torch.as_tensor(rows.astype(np.int64)).to(book.device)
+    return book.rows.index_select(0, t).cpu().numpy()
+
+
+class _RowCache:
+    """Host copy of the codebook rows a merge step can touch (values are fixed within it)."""
+
+    def __init__(self, book, pairs):
+        self.idx = np.unique(pairs.reshape(-1)) if len(pairs) else np.zeros(0, np.int64)
+        self.vals = _rows_host(book, self.idx)
+        self.pos = {int(r): k for k, r in enumerate(self.idx)}
+
+    def get(self, rows):
+        return self.vals[[self.pos[int(r)] for r in rows]]
+
+
+def _pick_merge(book, which, config, rng, cache: _RowCache) -> Optional[MergeProposal]:
+    pairs = book.lineage_pairs()
+    if len(pairs) == 0:
+        return None
+    _, eps_merge = config.eps_for(which)
+    diffs = cache.get(pairs[:, 1]).astype(np.float64) - cache.get(pairs[:, 0]).astype(np.float64)
+    log_w = -0.5 * np.einsum("nd,nd->n", diffs, diffs) / eps_merge ** 2
+    w = np.exp(log_w - log_w.max())
+    k = int(rng.choice(len(pairs), p=w / w.sum()))
+    return MergeProposal(which=which, child=int(pairs[k, 0]), parent=int(pairs[k, 1]), u=diffs[k])
+
+
+def propose_merge(state: ModelState, which: str, config: SamplerConfig,
+                  rng: np.random.Generator) -> Optional[MergeProposal]:
+    """sampler.py:224-237"""
+    book, _ = _book_of(state, which)
+    return _pick_merge(book, which, config, rng, _RowCache(book, book.lineage_pairs()))
+
+
+def _merge_bookkeeping(book, child: int, parent: int):
+    """Refcount effect of remapping every member of child to parent (sampler.py:244-247)."""
+    members = int(book.refcount[child])
+    book.refcount[parent] += members
+    book.refcount[child] = 1
+    book.decref(child)
+
+
+def _apply_remap(state: ModelState, which: str, remap: dict):
+    if not remap:
+        return
+    book, idx = _book_of(state, which)
+    table = np.full(book.capacity, -1, np.int32)
+    for c, p in remap.items():
+        table[c] = p
+    t = torch.as_tensor(table).to(book.device)
+    nat.call("cgs_apply_remap", nat.ptr(idx), state.num_gaussians, nat.ptr(t), len(table),
+             nat.stream_handle(book.device))
+    state.touch()
+
+
+def apply_merge(state: ModelState, proposal: MergeProposal) -> None:
+    """sampler.py:240-247"""
+    book, _ = _book_of(state, proposal.which)
+    _merge_bookkeeping(book, proposal.child, proposal.parent)
+    _apply_remap(state, proposal.which, {proposal.child: proposal.parent})
+
+
+def accept_merge(state: ModelState, proposal: MergeProposal, lam: float, config: SamplerConfig,
+                 rng: np.random.Generator, extra_log_ratio: float = 0.0) -> bool:
+    """sampler.py:250-259"""
+    es, em = config.eps_for(proposal.which)
+    prob = acceptance_probability("merge", proposal.u, lam, es, em,
+                                  config.normalization_correction, extra_log_ratio)
+    if rng.random() < prob:
+        apply_merge(state, proposal)
+        return True
+    return False
+
+
+# ---------------------------------------------------------------------------
+def _sgld_params(config: SamplerConfig, grad_scale: float, seed: int, offset: int,
+                 source: int) -> nat.CSgldParams:
+    p = nat.CSgldParams()
+    p.step_pos, p.step_opacity = config.step_pos, config.step_opacity
+    p.step_sh, p.step_sr = config.step_sh, config.step_sr
+    p.noise_pos, p.noise_opacity = config.noise_pos, config.noise_opacity
+    p.noise_sh, p.noise_sr = config.noise_sh, config.noise_sr
+    p.grad_scale = grad_scale
+    p.seed, p.offset = seed & (2 ** 64 - 1), offset & (2 ** 64 - 1)
+    p.noise_source = source
+    return p
+
+
+def _host_noise(state: ModelState, config: SamplerConfig, rng, n_sh_live, n_sr_live):
+    """The reference's noise draws, in group order (sampler.py:276-297)."""
+    out = [None, None, None, None]
+    specs = [(config.step_pos, config.noise_pos, (state.num_gaussians, 3)),
+             (config.step_opacity, config.noise_opacity, (state.num_gaussians,)),
+             (config.step_sh, config.noise_sh, (n_sh_live, state.sh.dim)),
+             (config.step_sr, config.noise_sr, (n_sr_live, 7))]
+    dev = state.device
+    for k, (eps, mult, shape) in enumerate(specs):
+        if eps > 0.0 and mult != 0.0:
+            out[k] = torch.as_tensor(rng.standard_normal(shape)).to(dev)
+    return out
+
+
+def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
+                rng: np.random.Generator, flags: torch.Tensor = None, check: bool = True) -> None:
+    """SGLD step per group (sampler.py:262-300) on the device."""
+    dev = state.device
+    g = state.gaussians
+    sh_live = state.sh.device_live()
+    sr_live = state.sr.device_live()
+    if config.device_noise:
+        noise = [None] * 4
+        params = _sgld_params(config, 1.0, config.seed, state.iteration, 0)
+    else:
+        noise = _host_noise(state, config, rng, sh_live.numel(), sr_live.numel())
+        params = _sgld_params(config, 1.0, 0, 0, 1)
+    if flags is None:
+        flags = torch.zeros((1,), dtype=torch.int32, device=dev)
+    nat.call("cgs_sgld_update", nat.ptr(g.positions), nat.ptr(g.opacity_logits), g.count,
+             nat.ptr(state.sh.rows), state.sh.dim, nat.ptr(sh_live), sh_live.numel(),
+             nat.ptr(state.sr.rows), nat.ptr(sr_live), sr_live.numel(), state.sh.capacity,
+             state.sr.capacity, nat.ptr(grads.positions), nat.ptr(grads.opacity_logits),
+             nat.ptr(grads.sh_rows), nat.ptr(grads.sr_rows), ctypes.byref(params),
+             nat.ptr(noise[0]), nat.ptr(noise[1]), nat.ptr(noise[2]), nat.ptr(noise[3]),
+             nat.ptr(flags), nat.stream_handle(dev))
+    state.touch()
+    state.sh.mutations += 1
+    state.sr.mutations += 1
+    if check and int(flags[0].item()) != 0:
+        raise SamplerError(f"non-finite gradients at iteration {state.iteration}")
+
+
+def _candidate_count(fraction: float, population: int) -> int:
+    """sampler.py:303-306"""
+    if population <= 0:
+        return 0
+    return max(1, int(round(fraction * population)))
+
+
+def _exact_log_ratio(state, views, config, rng, mutate):
+    """log p(S')/p(S) from one rendered view by trial-applying the move (sampler.py:309-317)."""
+    from .metrics import recon_loss
+    cam, gt = views[int(rng.integers(len(views)))]
+    before = recon_loss(rasterize_forward(state, cam).image, gt, config.lambda_ssim)[2]
+    trial = clone_state(state)
+    mutate(trial)
+    after = recon_loss(rasterize_forward(trial, cam).image, gt, config.lambda_ssim)[2]
+    return before - after
+
+
+def clone_state(state: ModelState) -> ModelState:
+    """Deep copy (device arrays cloned, host mirrors copied)."""
+    h = state.to_host()
+    st = ModelState.from_arrays(h["positions"], h["opacity_logits"], h["g2sh"], h["g2sr"],
+                                h["sh_rows"], h["sr_rows"], h["sh_refcount"], h["sr_refcount"],
+                                h["sh_parent"], h["sr_parent"], device=state.device,
+                                iteration=state.iteration, rng_seed=state.rng_seed)
+    for src, dst in ((state.sh, st.sh), (state.sr, st.sr)):
+        dst._free = list(src._free)
+    return st
+
+
+def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: TransitionRecord):
+    """Split branch of train_step (sampler.py:339-364): device eligibility compaction,
+    host accept loop over the Generator, one batched device apply."""
+    which = "sh" if rng.random() < 0.5 else "sr"
+    rec.codebook = which
+    book, idx = _book_of(state, which)
+    n = state.num_gaussians
+    dev = state.device
+    elig = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
+    count = torch.zeros((1,), dtype=torch.int64, device=dev)
+    ws = torch.empty((nat.library().cgs_scan_workspace_bytes(max(n, 1)) + 1024,), dtype=torch.uint8,
+                     device=dev)
+    nat.call("cgs_split_eligible", nat.ptr(idx), n, nat.ptr(book.device_refcount()), nat.ptr(elig),
+             nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream_handle(dev))
+    n_elig = int(count.item())
+    n_cand = min(_candidate_count(config.split_fraction, n), n_elig)
+    if n_cand <= 0:
+        return
+    pos = rng.choice(n_elig, size=n_cand, replace=False)
+    cand_t = elig.index_select(0, torch.as_tensor(pos.astype(np.int64)).to(dev))
+    rows = idx.index_select(0, cand_t.long()).cpu().numpy()
+    cand = cand_t.cpu().numpy()
+    lam = config.lambda_for(which)
+    es, em = config.eps_for(which)
+    moves = []
+    for i, row in zip(cand.tolist(), rows.tolist()):
+        if book.refcount[row] < 2:
+            continue
+        u = rng.normal(0.0, es, size=book.dim)
+        extra = 0.0
+        if config.exact_ratio:
+            # flush pending applies so the trial render sees the current state
+            _apply_split_batch(state, which, moves)
+            moves = []
+            prop = SplitProposal(which, i, row, u, book.row(row).astype(np.float64) + u)
+            extra = _exact_log_ratio(state, views, config, rng, lambda s: apply_split(s, prop))
+        prob = acceptance_probability("split", u, lam, es, em, config.normalization_correction, extra)
+        rec.accept_probs.append(prob)
+        rec.attempts += 1
+        if rng.random() < prob:
+            new_row = book.alloc_index(parent=row)
+            book.decref(row)
+            moves.append((i, row, new_row, u))
+            rec.accepts += 1
+    _apply_split_batch(state, which, moves)
+
+
+def merge_step(state: ModelState, views, config: SamplerConfig, rng, rec: TransitionRecord):
+    """Merge branch of train_step (sampler.py:365-385)."""
+    which = "sh" if rng.random() < 0.5 else "sr"
+    rec.codebook = which
+    book, _ = _book_of(state, which)
+    lam = config.lambda_for(which)
+    pairs0 = book.lineage_pairs()
+    n_cand = _candidate_count(config.split_fraction, len(pairs0))
+    cache = _RowCache(book, pairs0)
+    remap: dict = {}
+    es, em = config.eps_for(which)
+    for _ in range(n_cand):
+        prop = _pick_merge(book, which, config, rng, cache)
+        if prop is None:
+            break
+        extra = 0.0
+        if config.exact_ratio:
+            _apply_remap(state, which, remap)
+            remap = {}
+            extra = _exact_log_ratio(state, views, config, rng, lambda s: apply_merge(s, prop))
+        prob = acceptance_probability("merge", prop.u, lam, es, em, config.normalization_correction,
+                                      extra)
+        rec.accept_probs.append(prob)
+        rec.attempts += 1
+        if rng.random() < prob:
+            _merge_bookkeeping(book, prop.child, prop.parent)
+            for c in list(remap):
+                if remap[c] == prop.child:
+                    remap[c] = prop.parent
+            remap[prop.child] = prop.parent
+            rec.accepts += 1
+    _apply_remap(state, which, remap)
+
+
+class _GtCache:
+    def __init__(self):
+        self.key = None
+        self.val = None
+
+    def get(self, img, device):
+        if isinstance(img, torch.Tensor) and img.is_cuda:
+            return img.to(torch.float32).contiguous()
+        k = (id(img), getattr(img, "shape", None))
+        if self.key != k:
+            self.key = k
+            self.val = torch.as_tensor(np.ascontiguousarray(img, dtype=np.float32)).to(device)
+        return self.val
+
+
+_gt_cache = _GtCache()
+
+
+def update_step(state: ModelState, cams, gts, config: SamplerConfig, rng, check: bool = True):
+    """Batched SGLD update over views (mean of per-view gradients; reduces to the
+    reference's single-view update when len(cams) == 1).  Returns the device
+    recon loss (mean over views)."""
+    v = len(cams)
+    fr = Frame(state, cams).run_checked()
+    h, w = cams[0].height, cams[0].width
+    if any((c.height, c.width) != (h, w) for c in cams):
+        raise ValueError("a batched update needs equal image sizes")
+    lw = LossWorkspace(v, h, w, state.device)
+    dL = torch.empty_like(fr.image)
+    losses = lw.run(fr.image, gts, config.lambda_ssim, dL, 1.0)
+    grads = fr.backward(dL, scale=1.0 / v)
+    sgld_update(state, grads, config, rng, check=check)
+    return losses.view(v, 3)[:, 2].mean()
+
+
+def train_step(state: ModelState, views: list, config: SamplerConfig,
+               rng: np.random.Generator) -> TransitionRecord:
+    """One MH transition plus the densification schedule (sampler.py:320-399)."""
+    if not views:
+        raise ValueError("at least one view is required")
+    kind = choose_transition(config, rng)
+    sh_before, sr_before = state.sh.live_count, state.sr.live_count
+    rec = TransitionRecord(iteration=state.iteration + 1, kind=kind, codebook="-",
+                           lambdas=(config.lambda_sh, config.lambda_sr))
+    if kind == "update":
+        cam, gt = views[int(rng.integers(len(views)))]
+        gt_d = _gt_cache.get(gt, state.device)
+        if tuple(gt_d.shape) != (cam.height, cam.width, 3):
+            raise ValueError("ground-truth image shape mismatch")
+        rec.recon = update_step(state, [cam], gt_d, config, rng)
+        rec.attempts, rec.accepts = 1, 1
+        rec.accept_probs.append(1.0)
+    elif kind == "split":
+        split_step(state, views, config, rng, rec)
+    else:
+        merge_step(state, views, config, rng, rec)
+    state.iteration += 1
+    if config.densify_every > 0 and state.iteration % config.densify_every == 0:
+        densify(state, config.densify_growth, config.gaussian_cap, rng,
+                jitter_sigma=config.densify_jitter)
+    rec.live_sh = state.sh.live_count
+    rec.live_sr = state.sr.live_count
+    rec.delta_sh = rec.live_sh - sh_before
+    rec.delta_sr = rec.live_sr - sr_before
+    return rec
+
+
+def train(state: ModelState, views: list, config: SamplerConfig, iters: int,
+          rng: Optional[np.random.Generator] = None, eval_every: int = 0,
+          eval_views: Optional[list] = None, check_invariants: bool = False) -> list:
+    """sampler.py:402-420"""
+    from .metrics import psnr as psnr_fn
+    if rng is None:
+        rng = np.random.default_rng(config.seed)
+    records = []
+    for _ in range(iters):
+        rec = train_step(state, views, config, rng)
+        if check_invariants:
+            validate_state(state)
+        if eval_every > 0 and state.iteration % eval_every == 0:
+            targets = eval_views if eval_views else views
+            vals = [psnr_fn(rasterize_forward(state, cam).image, gt) for cam, gt in targets]
+            rec.psnr = float(np.mean(vals))
+        records.append(rec)
+    return records

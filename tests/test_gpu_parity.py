@@ -1,0 +1,303 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the reference goldens and
+the CPU oracle.  Tolerance (BASELINE.json north_star): images and gradients
+within rtol 1e-4 / atol 1e-6 (fp32 device math vs the reference's fp64);
+tile lists, depth orders, code assignments and MCMC decisions bit-exact."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL, ATOL = 1e-4, 1e-6
+
+
+@pytest.fixture(scope="module")
+def cg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2509_03775_b200 as m
+    m._native.library()
+    return m
+
+
+def render_names():
+    return [str(n) for n in golden("render_cases")["names"]]
+
+
+@pytest.mark.parametrize("name", render_names())
+def test_forward_matches_reference(cg, name):
+    from gpu_helpers import cam_from, state_from
+    d = golden("render_cases")
+    p = name + "_"
+    st = state_from(d, p + "in_")
+    cam = cam_from(d, p + "cam_")
+    art = cg.rasterize_forward(st, cam)
+    img = art.image.cpu().numpy()
+    T = art.final_transmittance.cpu().numpy()
+    assert np.allclose(img, d[p + "image"], rtol=RTOL, atol=ATOL), np.abs(img - d[p + "image"]).max()
+    assert np.allclose(T, d[p + "final_T"], rtol=RTOL, atol=ATOL)
+    # discrete outputs: bit-exact
+    offs, ids = art.frame.tile_lists()
+    assert np.array_equal(offs, d[p + "tile_offsets"])
+    assert np.array_equal(ids, d[p + "tile_ids"])
+    assert np.array_equal(art.contrib_counts.cpu().numpy(), d[p + "counts"])
+    tiles = art.tile_splats
+    ntx = (cam.width + 15) // 16
+    for (ty, tx), lst in tiles.items():
+        t = ty * ntx + tx
+        assert np.array_equal(lst, d[p + "tile_ids"][d[p + "tile_offsets"][t]:d[p + "tile_offsets"][t + 1]])
+    # projection stage (render.py:145-203) on the visible splats that have tiles
+    sp = art.frame.splats(0)
+    idx = d[p + "proj_idx"]
+    on = sp["n_tiles"][idx] > 0
+    assert np.allclose(sp["mean2d"][idx][on], d[p + "proj_mean2d"][on], rtol=1e-12, atol=1e-9)
+    con = d[p + "proj_conic"]
+    ref_con = np.stack([con[:, 0, 0], con[:, 0, 1], con[:, 1, 1]], 1)
+    assert np.allclose(sp["conic"][idx][on], ref_con[on], rtol=1e-10, atol=1e-14)
+    assert np.allclose(sp["opac"][idx][on], d[p + "proj_opac"][on], rtol=1e-13)
+    assert np.allclose(sp["colors"][idx][on], d[p + "proj_colors"][on], rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", [n for n in render_names() if n != "behind"])
+def test_loss_and_backward_match_reference(cg, name):
+    from gpu_helpers import cam_from, group_rel, state_from
+    d = golden("render_cases")
+    p = name + "_"
+    st = state_from(d, p + "in_")
+    cam = cam_from(d, p + "cam_")
+    lam = float(d[p + "lambda"])
+    art = cg.rasterize_forward(st, cam)
+    # loss on the reference image (isolates the loss kernels)
+    vals = cg.recon_loss(d[p + "image"], d[p + "gt"], lam)
+    assert np.allclose(vals, d[p + "loss"], rtol=1e-6, atol=1e-9, equal_nan=True)
+    g = cg.rasterize_backward(st, cam, art, d[p + "dL"]).numpy()
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        ref = d[p + "g_" + k]
+        assert group_rel(g[k], ref) <= 1e-4, (k, group_rel(g[k], ref))
+        assert np.allclose(g[k], ref, rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - ref).max())
+
+
+def test_loss_grad_matches_reference(cg):
+    d = golden("loss_sh")
+    for k in range(4):
+        a, b, lam = d[f"loss{k}_a"], d[f"loss{k}_b"], float(d[f"loss{k}_lam"])
+        vals = cg.recon_loss(a, b, lam)
+        assert np.allclose(vals, d[f"loss{k}_vals"], rtol=1e-6, atol=1e-9)
+        g = cg.recon_loss_grad(a, b, lam).cpu().numpy()
+        ref = d[f"loss{k}_grad"]
+        assert np.allclose(g, ref, rtol=1e-4, atol=1e-3 * np.abs(ref).max()), np.abs(g - ref).max()
+
+
+def test_gradcheck_against_finite_differences(cg):
+    """tests/test_render.py:171-182 on the device path: group-rel <= 1e-4 vs FD."""
+    from gpu_helpers import cam_from, group_rel, state_from
+    d = golden("gradcheck")
+    for name in d["names"]:
+        p = str(name) + "_"
+        st = state_from(d, p + "in_")
+        cam = cam_from(d, p + "cam_")
+        art = cg.rasterize_forward(st, cam)
+        g = cg.rasterize_backward(st, cam, art, d[p + "dL"]).numpy()
+        for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+            assert group_rel(g[k], d[p + "fd_" + k]) <= 1e-4, (name, k)
+
+
+def test_known_pixels(cg):
+    """tests/test_render.py:90-123 known answers."""
+    cam = cg.Camera(rotation=np.eye(3), translation=np.zeros(3), fx=32.0, fy=32.0, cx=16.0,
+                    cy=16.0, width=32, height=32)
+    st = cg.init_one_to_one(2, 0, seed=0)
+    off_f, off_b = 0.5 * 2.0 / 32, 0.5 * 3.0 / 32
+    st.gaussians.positions = np.array([[off_f, off_f, 2.0], [off_b, off_b, 3.0]], np.float32)
+    st.gaussians.opacity_logits = np.zeros(2, np.float32)
+    rows = np.stack([(np.array([1.0, 0, 0]) - 0.5) / 0.28209479177387814,
+                     (np.array([0, 1.0, 0]) - 0.5) / 0.28209479177387814]).astype(np.float32)
+    st.sh.rows = rows
+    sr = np.zeros((2, 7), np.float32)
+    sr[:, 0:3] = -1.0
+    sr[:, 3] = 1.0
+    st.sr.rows = sr
+    img = cg.rasterize_forward(st, cam).image.cpu().numpy()
+    assert np.allclose(img[16, 16], [0.5, 0.25, 0.0], atol=1e-6)
+    st.gaussians.positions = np.array([[0, 0, -3.0], [0, 0, -1.0]], np.float32)
+    art = cg.rasterize_forward(st, cam)
+    assert float(art.image.abs().max()) == 0.0
+    assert bool((art.final_transmittance == 1).all()) and int(art.contrib_counts.max()) == 0
+    g = cg.rasterize_backward(st, cam, art, np.ones((32, 32, 3)))
+    assert float(g.flat.abs().max()) == 0.0
+
+
+def test_zero_upstream_and_stale_artifacts(cg):
+    from gpu_helpers import cam_from, state_from
+    d = golden("render_cases")
+    st = state_from(d, "synth1_in_")
+    cam = cam_from(d, "synth1_cam_")
+    art = cg.rasterize_forward(st, cam)
+    g = cg.rasterize_backward(st, cam, art, np.zeros((cam.height, cam.width, 3)))
+    assert float(g.flat.abs().max()) == 0.0
+    st.gaussians.positions[0, 0] += 0.25
+    with pytest.raises(ValueError):
+        cg.rasterize_backward(st, cam, art, np.zeros((cam.height, cam.width, 3)))
+    art = cg.rasterize_forward(st, cam)
+    with pytest.raises(ValueError):
+        cg.rasterize_backward(st, cam, art, np.zeros((cam.height + 1, cam.width, 3)))
+
+
+def test_deterministic_and_batched_frame_equals_single_views(cg):
+    from gpu_helpers import cam_from, state_from
+    d = golden("render_cases")
+    st = state_from(d, "cfg1s_v0_in_")
+    c0, c1 = cam_from(d, "cfg1s_v0_cam_"), cam_from(d, "cfg1s_v1_cam_")
+    f = cg.render_frame(st, [c0, c1])
+    a0 = cg.rasterize_forward(st, c0)
+    a1 = cg.rasterize_forward(st, c1)
+    assert torch.equal(f.view_image(0), a0.image) and torch.equal(f.view_image(1), a1.image)
+    dl = torch.as_tensor(np.random.default_rng(0).normal(size=(2 * 96 * 96 * 3,)).astype(np.float32),
+                         device="cuda") * 1e-4
+    g_b = f.backward(dl).numpy()
+    g_b2 = f.backward(dl).numpy()
+    for k in g_b:
+        assert np.array_equal(g_b[k], g_b2[k]), "backward must be bit-deterministic"
+    g0 = a0.frame.backward(dl[: 96 * 96 * 3].contiguous()).numpy()
+    g1 = a1.frame.backward(dl[96 * 96 * 3:].contiguous()).numpy()
+    for k in g_b:
+        assert np.allclose(g_b[k], g0[k] + g1[k], rtol=1e-5, atol=1e-9), k
+
+
+def test_sgld_bit_exact(cg):
+    from gpu_helpers import assert_state_equal, state_from
+    d = golden("sgld")
+    for name in d["names"]:
+        st = state_from(d, "in_")
+        grads = cg.GradientSet.empty(st)
+        for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+            getattr(grads, k).copy_(torch.as_tensor(d["g_" + k].astype(np.float32)))
+        kw = {}
+        for key, v in d.items():
+            pre = f"{name}_cfg_"
+            if key.startswith(pre):
+                kw[key[len(pre):]] = v.item() if v.shape == () else v
+        cfg = cg.SamplerConfig(**kw)
+        rng = np.random.default_rng(1234)
+        cg.sgld_update(st, grads, cfg, rng)
+        assert_state_equal(st, d, f"{name}_out_")
+        assert np.array_equal(rng.random(4), d[f"{name}_rng_after"])
+
+
+def test_sgld_rejects_nonfinite(cg):
+    from gpu_helpers import state_from
+    d = golden("sgld")
+    st = state_from(d, "in_")
+    grads = cg.GradientSet.empty(st)
+    grads.flat.zero_()
+    grads.sr_rows[3, 2] = float("nan")
+    before = st.gaussians.positions.clone()
+    with pytest.raises(cg.SamplerError):
+        cg.sgld_update(st, grads, cg.SamplerConfig(), np.random.default_rng(0))
+    assert torch.equal(before, st.gaussians.positions)
+
+
+@pytest.mark.parametrize("chain", ["defaults", "always", "corrected"])
+def test_mcmc_chain_bit_exact(cg, chain):
+    """train_step split/merge branches + densify vs the reference, step by step."""
+    from gpu_helpers import assert_state_equal, state_from
+    d = golden("mcmc")
+    st = state_from(d, f"{chain}_s0_")
+    kw = {}
+    for key, v in d.items():
+        pre = f"{chain}_cfg_"
+        if key.startswith(pre):
+            kw[key[len(pre):]] = v.item() if v.shape == () else v
+    rng = np.random.default_rng(int(d[f"{chain}_seed"]))
+    cam = cg.ring_cameras(1, (0, 0, 0), 3.0, 0.0, 64, 64, 64)[0]
+    for step in range(1, int(d[f"{chain}_steps"]) + 1):
+        p = f"{chain}_s{step}_"
+        kind = str(d[p + "kind"])
+        mix = (0.0, 1.0, 0.0) if kind == "split" else (0.0, 0.0, 1.0)
+        cfg = cg.SamplerConfig(**{**kw, "p_update": mix[0], "p_split": mix[1], "p_merge": mix[2]})
+        rec = cg.train_step(st, [(cam, None)], cfg, rng)
+        cg.validate_state(st)
+        assert_state_equal(st, d, p)
+        assert [rec.attempts, rec.accepts, rec.delta_sh, rec.delta_sr, rec.live_sh,
+                rec.live_sr] == d[p + "rec"].tolist()
+        assert rec.codebook == str(d[p + "rec_codebook"])
+        assert np.array_equal(np.array(rec.accept_probs), d[p + "accept_probs"])
+    assert np.array_equal(rng.random(4), d[f"{chain}_rng_after"])
+
+
+def test_densify_bit_exact(cg):
+    from gpu_helpers import assert_state_equal, state_from
+    d = golden("mcmc")
+    st = state_from(d, "defaults_s0_")
+    rng = np.random.default_rng(7)
+    assert cg.densify(st, 0.05, 2_000_000, rng, jitter_sigma=0.02) == int(d["densify_added"])
+    assert_state_equal(st, d, "densify_out_")
+    cg.validate_state(st)
+
+
+def test_update_step_matches_oracle(cg):
+    """One full reference update transition (forward, L1+SSIM loss, backward,
+    SGLD with host noise) vs the oracle from identical inputs."""
+    from oracle import cgs_oracle as O
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config1(3, n=3000, k=256, views=2, size=96)
+    g = scenes.config1(4, n=3000, k=256, views=2, size=96)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows, g.sr_rows)
+    views = [(c, cg.rasterize_forward(gst, c).image.cpu().numpy()) for c in a.cameras]
+    cfg = cg.SamplerConfig(p_update=1.0, p_split=0.0, p_merge=0.0, noise_pos=0.0)
+    ost = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    oviews = [(O.cam_from_any(c), im.astype(np.float64)) for c, im in views]
+    r1, r2 = np.random.default_rng(5), np.random.default_rng(5)
+    rec = cg.train_step(st, views, cfg, r1)
+    orec = O.train_step(ost, oviews, O.config(p_update=1.0, p_split=0.0, p_merge=0.0, noise_pos=0.0), r2)
+    assert abs(rec.recon - orec["recon"]) <= 1e-5 * abs(orec["recon"])
+    h = st.to_host()
+    # one SGLD step moves parameters by 0.5*eps*grad; compare the motion
+    for k, ok, base in (("positions", "positions", a.positions),
+                        ("opacity_logits", "logits", a.opacity_logits)):
+        mine = h[k].astype(np.float64) - base
+        ref = getattr(ost, ok).astype(np.float64) - base
+        assert np.abs(mine - ref).max() <= 1e-4 * max(np.abs(ref).max(), 1e-12) + 2e-7, k
+    assert np.array_equal(r1.random(3), r2.random(3))
+
+
+@pytest.mark.parametrize("key_bytes,bits", [(2, 14), (4, 22), (8, 64), (4, 32)])
+def test_onesweep_sort_is_stable(cg, key_bytes, bits):
+    nat = cg._native
+    rng = np.random.default_rng(key_bytes * 100 + bits)
+    for n in (0, 1, 1000, 4097, 300_000):
+        dt = {2: np.uint16, 4: np.uint32, 8: np.uint64}[key_bytes]
+        hi = min(2 ** bits, 2 ** 63) if bits < 64 else 2 ** 63
+        keys = rng.integers(0, min(hi, 1000 if n > 1000 else hi), size=n).astype(dt)
+        if key_bytes == 8 and n:
+            keys = (keys.astype(np.uint64) << np.uint64(40)) | rng.integers(0, 2 ** 40, n).astype(np.uint64)
+        vals = np.arange(n, dtype=np.uint32)
+        kt = torch.as_tensor(keys.view(np.int16 if key_bytes == 2 else np.int32 if key_bytes == 4 else np.int64)).cuda()
+        vt = torch.as_tensor(vals.view(np.int32)).cuda()
+        ws = torch.empty(nat.library().cgs_sort_workspace_bytes(max(n, 1), key_bytes), dtype=torch.uint8, device="cuda")
+        nat.call("cgs_radix_sort_pairs", nat.ptr(kt), nat.ptr(vt), n, key_bytes, bits, nat.ptr(ws),
+                 ws.numel(), nat.stream_handle())
+        order = np.argsort(keys, kind="stable")
+        got_v = vt.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got_v, vals[order])
+        assert np.array_equal(kt.cpu().numpy().view(dt), keys[order])
+
+
+def test_scan(cg):
+    nat = cg._native
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 2047, 2048, 2049, 1_000_003):
+        x = rng.integers(0, 50, size=n).astype(np.uint32)
+        xt = torch.as_tensor(x.view(np.int32)).cuda()
+        out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        tot = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws = torch.empty(nat.library().cgs_scan_workspace_bytes(max(n, 1)), dtype=torch.uint8, device="cuda")
+        nat.call("cgs_exclusive_scan_u32", nat.ptr(xt), nat.ptr(out), n, nat.ptr(tot), nat.ptr(ws),
+                 ws.numel(), nat.stream_handle())
+        ref = np.cumsum(x, dtype=np.uint64) - x
+        assert np.array_equal(out.cpu().numpy()[:n].view(np.uint32), ref.astype(np.uint32))
+        assert int(tot.item()) == int(x.sum())
