@@ -1,0 +1,391 @@
+"""Benchmark: ContraGS training iterations on B200 (BASELINE.json metric
+"train iters/s & rendered Mpix/s ... HBM roofline fraction").
+
+Workload (default ``--config 1``, BASELINE.json configs[1]): N=100k Gaussians,
+SR K=4096, [opacity; SH-3] K=4096, a batch of 4 views at 256x256 per GPU per
+iteration, L1+SSIM (lambda 0.2) loss, SGLD update, forced split + merge MCMC
+transitions every 25 iterations, densify every 100 (reference defaults).
+Synthetic seeded scene; targets are renders of the seed+1
+scene.  At N GPUs each rank renders its own 4 views of a 4N-view ring
+(weak scaling) and the flat gradient buffer is summed with one NCCL
+allreduce; `value` counts config-1 iterations (4 views) of the whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+VIEWS_PER_GPU = {0: 1, 1: 4, 2: 1, 3: 1}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--mcmc-every", type=int, default=25)
+    ap.add_argument("--noise-pos", type=float, default=0.01)
+    ap.add_argument("--profile-kernel", default="raster_bwd_kernel")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def make_scene(config, seed, rank, world):
+    from paper_2509_03775_b200 import camera, scenes
+    if config == 1:
+        a = scenes.config1(seed, views=4 * world)
+        g = scenes.config1(seed + 1, views=4 * world)
+        cams = a.cameras[4 * rank: 4 * rank + 4]
+    else:
+        a = scenes.build(config, seed)
+        g = scenes.build(config, seed + 1)
+        nv = VIEWS_PER_GPU.get(config, 1)
+        cams = [a.cameras[(rank * nv + k) % len(a.cameras)] for k in range(nv)]
+    return a, g, cams
+
+
+def workload_name(config):
+    return {0: "config0: N=4096 SH-1 K=256, 1x64^2 view, L1",
+            1: "config1: N=100k, SR K=4096, SH-3 K=4096, 4x256^2 views/GPU, L1+SSIM, MCMC every 25",
+            2: "config2: N=1M clustered, SR 8192, SH-3 16384, 1x1280x720 view/GPU",
+            3: "config3: N=4M outdoor, SR 16384, SH-3 65536, 1x1960x1088 view/GPU"}[config]
+
+
+class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled every 20 ms through NVML
+    during the timed region (same fields as the recipe's nvidia-smi clocks line)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, gpu_index, period=0.02):
+        import threading
+        self.gpu = gpu_index
+        self.period = period
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.err = None
+
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self.stop_ev.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                util = nv.nvmlDeviceGetUtilizationRates(h).gpu
+                self.samples.append((sm, rs, util))
+                time.sleep(self.period)
+        except Exception as e:  # NVML missing: report it instead of inventing clocks
+            self.err = repr(e)
+
+    def start(self):
+        self.thread.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        busy = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = set()
+        for _, rs, _ in busy:
+            for nm, bit in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": self.max_sm,
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "samples_under_load": len(busy)}
+
+
+# ---------------------------------------------------------------------------
+def _oracle_view(args):
+    """One config view: oracle forward + L1/SSIM loss + backward (worker process)."""
+    from oracle import cgs_oracle as O
+    arrays, gt_arrays, cam, lam = args
+    st = O.OState.from_arrays(*arrays)
+    t0 = time.perf_counter()
+    fw = O.raster_forward(st, cam)
+    dL = O.recon_loss_grad(fw["image"], gt_arrays, lam)
+    g = O.raster_backward(st, cam, dL)
+    return time.perf_counter() - t0, g
+
+
+def _oracle_iteration(a, gts, cams, lam, pool):
+    """One full reference update iteration on host cores: the views' forward /
+    loss / backward in parallel worker processes, then the mean gradient and
+    the SGLD update (reference sampler.py:320-338, 262-300)."""
+    from oracle import cgs_oracle as O
+    arrays = (a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    jobs = [(arrays, gts[k], O.cam_from_any(c), lam) for k, c in enumerate(cams)]
+    t0 = time.perf_counter()
+    res = pool.map(_oracle_view, jobs)
+    grads = {k: sum(r[1][k] for r in res) / len(res) for k in res[0][1]}
+    st = O.OState.from_arrays(*arrays)
+    O.sgld_update(st, grads, O.config(), np.random.default_rng(0))
+    return time.perf_counter() - t0
+
+
+def _oracle_gts(g, cams):
+    from oracle import cgs_oracle as O
+    gst = O.OState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows, g.sr_rows)
+    return [O.raster_forward(gst, O.cam_from_any(c))["image"] for c in cams]
+
+
+def cpu_iteration_timer(config, seed):
+    """Returns (fn() -> seconds per iteration, cores, sample description)."""
+    a, g, cams = make_scene(config, seed, 0, 1)
+    gts = _oracle_gts(g, cams)
+    cores = max(1, min(len(cams), os.cpu_count() or 1))
+    ctx = mp.get_context("fork")
+    pool = ctx.Pool(cores)
+    lam = 0.0 if config == 0 else 0.2
+
+    def run():
+        return _oracle_iteration(a, gts, cams, lam, pool)
+
+    sample = (f"one full {workload_name(config).split(':')[0]} update iteration "
+              f"({len(cams)} views fwd+L1/SSIM+bwd in {cores} worker processes, mean grad, SGLD) "
+              "through the numpy oracle port (oracle/cgs_oracle.py) of the reference")
+    return run, cores, sample, pool
+
+
+def run_reference(args):
+    """--impl reference: the reference's algorithm (oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    run, cores, sample, pool = cpu_iteration_timer(args.config, args.seed)
+    first = run()  # warm-up (at most one; a CPU has nothing to warm beyond caches)
+    budget = 150.0
+    k_eff = max(2, min(args.steps, int(budget / max(first, 1e-3))))
+    times = [run() for _ in range(k_eff)]
+    pool.close()
+    total = sum(times)
+    value = k_eff / total
+    out = {"impl": "reference", "metric": "train iters/s", "value": value, "unit": "it/s",
+           "n_gpus": args.gpus, "steps": k_eff, "warmup": 1, "ms_per_step": 1000 * total / k_eff,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded scene, SURVEY.md §8(d))",
+           "config": {"workload": workload_name(args.config), "seed": args.seed},
+           "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "port",
+                            "sample": sample + f"; {k_eff} timed iterations (bounded to ~{budget:.0f} s)"},
+           "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2509_03775_b200 as cg
+    from paper_2509_03775_b200 import _native as nat
+    from paper_2509_03775_b200.engine import Trainer
+
+    a, g, cams = make_scene(args.config, args.seed, rank, world)
+    dev = torch.device("cuda", local)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows, device=dev, gaussian_headroom=0.25)
+    gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows,
+                                    g.sr_rows, device=dev)
+    gt_frame = cg.render_frame(gst, cams)
+    H, W = cams[0].height, cams[0].width
+    gts = gt_frame.image.view(len(cams), H, W, 3).clone()
+    del gt_frame, gst
+    lam = 0.0 if args.config == 0 else 0.2
+    # Reference defaults except the position Langevin noise: the default
+    # noise_pos=1.0 with step_pos=0.5 adds N(0, 0.5) per coordinate per update,
+    # which diffuses this scene out of the views within ~10 iterations (the
+    # raster work then collapses).  noise_pos=0.01 keeps the noise draw (device
+    # Philox) in every update while the scene stays in view, so the GPU step and
+    # the CPU baseline (initial scene) measure the same workload.
+    cfg = cg.SamplerConfig(lambda_ssim=lam, device_noise=True, seed=args.seed,
+                           noise_pos=args.noise_pos)
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    rng = np.random.default_rng(args.seed)
+    tr = Trainer(st, cams, gts, cfg, rng, mcmc_every=args.mcmc_every, world=world,
+                 allreduce=allreduce)
+
+    flush = torch.empty((64 * 1024 * 1024,), dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        tr.step()
+    torch.cuda.synchronize()
+    tr.check()
+
+    lib = nat.library()
+    lib.cgs_profile_kernel(args.profile_kernel.encode())
+    clocks = ClockSampler(local)
+    launches0 = lib.cgs_launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    views_done = 0
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        starts[k].record()
+        tr.step()
+        ends[k].record()
+        views_done += len(cams)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = int(lib.cgs_launch_count() - launches0)
+    tr.check()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    prof_ms, prof_n = nat.F64(0.0), nat.I64(0)
+    lib.cgs_profile_read(prof_ms, prof_n)
+    lib.cgs_profile_kernel(b"")
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    iters_value = (args.steps * world) / (total_ms / 1000.0)  # config-1 iterations, whole job
+    mpix = views_done * world * H * W / (total_ms / 1000.0) / 1e6
+    stats = tr.frame.stats()
+
+    # roofline of the profiled kernel (algorithmic bytes)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        try:
+            peak = float(json.load(open(peaks_path))["hbm_gbs"])
+            peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    px = sum(c.width * c.height for c in cams)
+    P_x = int(stats.n_processed)
+    name = args.profile_kernel
+    if name == "raster_bwd_kernel":
+        alg = 44 * P_x + 36 * P_x + 32 * px
+    elif name == "raster_fwd_kernel":
+        alg = 44 * P_x + 24 * px
+    elif name == "project_kernel":
+        n = st.num_gaussians
+        alg = 24 * n * len(cams) + 4 * (7 * st.sr.capacity + st.sh.dim * st.sh.capacity) + 52 * int(stats.n_onscreen)
+    else:
+        alg = 0
+    avg_s = (prof_ms.value / max(prof_n.value, 1)) / 1000.0
+    achieved = alg / avg_s / 1e9 if avg_s > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
+                "alg_bytes_per_launch": alg, "P_x": P_x, "pixels": px,
+                "note": "raster kernels are FP32/MUFU-bound at config 1; HBM fraction uses "
+                        "processed-prefix bytes only (SURVEY.md §8(d))"}
+
+    # e2e: same step through the public API with host buffers (pinned H2D of the
+    # step's target images, D2H of the recon loss) inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host_gt = gts.cpu().pin_memory()
+        host_loss = torch.empty((3 * len(cams),), dtype=torch.float64).pin_memory()
+        e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            if not args.no_flush:
+                flush.zero_()
+            e_s[k].record()
+            tr.gts.copy_(host_gt, non_blocking=True)
+            tr.step()
+            host_loss.copy_(tr.last_loss, non_blocking=True)
+            e_e[k].record()
+        torch.cuda.synchronize()
+        barrier()
+        tr.check()
+        e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e))
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": (args.steps * world) / (e_ms / 1000.0), "unit": "it/s",
+               "h2d_bytes_per_step": int(host_gt.numel() * 4),
+               "d2h_bytes_per_step": int(host_loss.numel() * 8)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        run, cores, sample, pool = cpu_iteration_timer(args.config, args.seed)
+        secs = run()
+        pool.close()
+        cpu = {"value": 1.0 / secs, "unit": "it/s", "cores": cores, "kind": "port",
+               "sample": sample, "seconds": secs}
+
+    if rank == 0:
+        out = {"metric": "train iters/s", "value": iters_value, "unit": "it/s", "n_gpus": world,
+               "steps": args.steps, "warmup": max(3, args.warmup),
+               "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f32 (fp64 projection geometry)",
+               "data": "synthetic (seeded scene, SURVEY.md §8(d)); random-init codebooks",
+               "config": {"workload": workload_name(args.config), "views_per_gpu": len(cams),
+                          "image": f"{W}x{H}", "gaussians": st.num_gaussians,
+                          "l2": "flushed (256 MB write) between timed iterations"
+                          if not args.no_flush else "not flushed",
+                          "mcmc_every": args.mcmc_every,
+                          "sgld_noise": f"device Philox, noise_pos={args.noise_pos} (reference default 1.0 "
+                                        "diffuses the scene out of view; see DESIGN.md)",
+                          "parallelism": f"dp{world} (views sharded, NCCL allreduce)"},
+               "mpix_per_s": mpix, "gpu_launches": launches, "roofline": roofline,
+               "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+               "frame": {"pairs": int(stats.n_pairs), "processed_pairs": P_x,
+                         "touched": int(stats.n_touched), "onscreen": int(stats.n_onscreen)},
+               "recon": tr.recon(), "mcmc_events": tr.mcmc_events,
+               "mcmc_ms": tr.mcmc_ms}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -102,6 +102,16 @@ typedef struct cgs_sgld_params {
 CGS_API int cgs_abi_version(void);
 CGS_API const char* cgs_last_error(void); /* thread-local, host */
 
+/* ---- instrumentation (host; used by bench.py) ------------------------ */
+/* Number of kernels this library has launched since load. */
+CGS_API uint64_t cgs_launch_count(void);
+/* Bracket every launch of the kernel called `name` (e.g. "raster_bwd_kernel")
+ * with CUDA events on its launch stream; "" or NULL disables.  Resets the
+ * accumulated events. */
+CGS_API int cgs_profile_kernel(const char* name);
+/* Sum of the recorded launches' durations (synchronizes those events). */
+CGS_API int cgs_profile_read(double* total_ms, int64_t* launches);
+
 /* ---- render: rasterize_forward / rasterize_backward ------------------- */
 /* Workspace for one batched frame of n_views cameras (host cams).
  * pair_capacity bounds the (tile, splat) pairs P (render.py:240-254). */

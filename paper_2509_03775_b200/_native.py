@@ -73,6 +73,9 @@ SCNP = ctypes.POINTER(CScene)
 SIGNATURES = {
     "cgs_abi_version": (I32, []),
     "cgs_last_error": (ctypes.c_char_p, []),
+    "cgs_launch_count": (ctypes.c_uint64, []),
+    "cgs_profile_kernel": (I32, [ctypes.c_char_p]),
+    "cgs_profile_read": (I32, [ctypes.POINTER(F64), ctypes.POINTER(I64)]),
     "cgs_frame_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64]),
     "cgs_render_forward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
     "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),

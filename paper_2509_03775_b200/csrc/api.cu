@@ -1,8 +1,11 @@
 // C ABI (include/cgs_b200.h): argument checking, workspace planning and the
 // error channel.  No C++ exception crosses this boundary.
+#include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "frame.cuh"
 
@@ -11,6 +14,42 @@ namespace cgs {
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
+
+// ---- instrumentation -----------------------------------------------------
+static std::atomic<unsigned long long> g_launches{0};
+static std::mutex g_prof_mu;
+static std::string g_prof_name;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(const char* name, cudaStream_t s) : on(false), st(s) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (!g_prof_name.empty() && g_prof_name == name) {
+    on = true;
+    cudaEvent_t a = prof_event(), b = prof_event();
+    cudaEventRecord(a, st);
+    g_prof_events.emplace_back(a, b);
+  }
+}
+
+ProfScope::~ProfScope() {
+  if (!on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEventRecord(g_prof_events.back().second, st);
+}
 
 int cuda_status(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -94,6 +133,33 @@ extern "C" {
 int cgs_abi_version(void) { return CGS_ABI_VERSION; }
 
 const char* cgs_last_error(void) { return g_err.c_str(); }
+
+uint64_t cgs_launch_count(void) { return g_launches.load(); }
+
+int cgs_profile_kernel(const char* name) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& pr : g_prof_events) {
+    g_prof_pool.push_back(pr.first);
+    g_prof_pool.push_back(pr.second);
+  }
+  g_prof_events.clear();
+  g_prof_name = name ? name : "";
+  return CGS_OK;
+}
+
+int cgs_profile_read(double* total_ms, int64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  double tot = 0.0;
+  for (auto& pr : g_prof_events) {
+    CGS_CUDA(cudaEventSynchronize(pr.second));
+    float ms = 0.0f;
+    CGS_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = static_cast<int64_t>(g_prof_events.size());
+  return CGS_OK;
+}
 
 size_t cgs_frame_workspace_bytes(int64_t n, const cgs_camera_t* cams, int32_t n_views,
                                  int64_t pair_capacity, int64_t sr_capacity) {

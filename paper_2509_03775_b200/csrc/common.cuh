@@ -85,10 +85,29 @@ int cuda_status(cudaError_t e, const char* where);
     if (e_ != cudaSuccess) return cgs::cuda_status(e_, #call); \
   } while (0)
 
+// Instrumentation: every launch bumps a counter (cgs_launch_count); the one
+// kernel named by cgs_profile_kernel is bracketed by CUDA events recorded on
+// its own launch stream (cgs_profile_read).
+void note_launch();
+struct ProfScope {
+  bool on;
+  cudaStream_t st;
+  ProfScope(const char* name, cudaStream_t s);
+  ~ProfScope();
+};
+
 #define CGS_CHECK_LAUNCH(name)                                              \
   do {                                                                      \
+    cgs::note_launch();                                                     \
     cudaError_t e_ = cudaGetLastError();                                    \
     if (e_ != cudaSuccess) return cgs::cuda_status(e_, name);               \
+  } while (0)
+
+// Launch a kernel inside an optional profiling scope.
+#define CGS_PROFILED(name, st, ...) \
+  do {                              \
+    cgs::ProfScope p_(name, st);    \
+    __VA_ARGS__;                    \
   } while (0)
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }

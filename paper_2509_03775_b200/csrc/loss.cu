@@ -272,13 +272,13 @@ int recon_loss(const float* img, const float* gt, int nv, int H, int W, double l
   }
   const bool has_ssim = (H >= 11 && W >= 11) && (lam != 0.0 || want_ssim);
   const dim3 grid(blocks_x(W), blocks_y(H), 3 * nv);
-  ssim_stats_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, has_ssim ? 1 : 0, L);
+  CGS_PROFILED("ssim_stats_kernel", st, ssim_stats_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, has_ssim ? 1 : 0, L));
   CGS_CHECK_LAUNCH("ssim_stats_kernel");
   const double inv_size = 1.0 / (3.0 * H * W);
   const double inv_count = has_ssim ? 1.0 / (3.0 * (H - 10.0) * (W - 10.0)) : 0.0;
   if (dL) {
-    ssim_grad_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
-                                           (has_ssim && lam != 0.0) ? 1 : 0, L, dL);
+    CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
+                                           (has_ssim && lam != 0.0) ? 1 : 0, L, dL));
     CGS_CHECK_LAUNCH("ssim_grad_kernel");
   }
   const int64_t nb = static_cast<int64_t>(blocks_x(W)) * blocks_y(H) * 3;

@@ -120,6 +120,56 @@ __device__ __forceinline__ void sh_basis_grad_dot(double x, double y, double z, 
   }
 }
 
+// Transposed (reduce-scatter) warp sum of 9 values in 12 shuffles instead of
+// 9 x 5 = 45: at each butterfly level a lane keeps the half of its values its
+// partner does not and adds the partner's copy of them.  Lanes
+// 0,2,4,8,10,16,18,20,24 return the sums of values 0..8 (reduce9_slot); the
+// order of additions is fixed, so the result is deterministic.
+__device__ __forceinline__ float warp_reduce9(const float (&o)[9]) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  float v5[5];
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const float lo = o[j], hi = j < 4 ? o[5 + j] : 0.0f;
+      v5[j] = (up ? hi : lo) + __shfl_xor_sync(full, up ? lo : hi, 16);
+    }
+  }
+  float v3[3];
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float lo = v5[j], hi = j < 2 ? v5[3 + j] : 0.0f;
+      v3[j] = (up ? hi : lo) + __shfl_xor_sync(full, up ? lo : hi, 8);
+    }
+  }
+  float v2[2];
+  {
+    const bool up = lane & 4;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float lo = v3[j], hi = j < 1 ? v3[2 + j] : 0.0f;
+      v2[j] = (up ? hi : lo) + __shfl_xor_sync(full, up ? lo : hi, 4);
+    }
+  }
+  float v1;
+  {
+    const bool up = lane & 2;
+    v1 = (up ? v2[1] : v2[0]) + __shfl_xor_sync(full, up ? v2[0] : v2[1], 2);
+  }
+  return v1 + __shfl_xor_sync(full, v1, 1);
+}
+
+// Value index held by `lane` after warp_reduce9, or -1.
+__device__ __forceinline__ int reduce9_slot(int lane) {
+  constexpr unsigned kMask = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 8) | (1u << 10) |
+                             (1u << 16) | (1u << 18) | (1u << 20) | (1u << 24);
+  return ((kMask >> lane) & 1u) ? __popc(kMask & ((1u << lane) - 1u)) : -1;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

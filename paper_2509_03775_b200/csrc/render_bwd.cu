@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
   __shared__ float4 s_a[256];
   __shared__ float4 s_b[256];
   __shared__ float4 s_n[256];  // natural conic A, B, C and blue
+  __shared__ float s_io[256];  // 1 / opacity
   __shared__ float s_red[8][32][9];
   if (fh->stats.overflow) return;
   const int tile = blockIdx.x;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
       s_b[tid] = b;
       s_n[tid] = make_float4(static_cast<float>(r.ca), static_cast<float>(r.cb),
                              static_cast<float>(r.cc), c);
+      s_io[tid] = static_cast<float>(1.0 / r.opac);
       const unsigned long long q = qbase + b0 + tid;
       const uint32_t vv = sid / static_cast<uint32_t>(n);
       const uint32_t gi = sid - vv * static_cast<uint32_t>(n);
@@ -168,25 +170,25 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
           const float al = splat_alpha(a, b, dx, dy);
           if (al >= kAlphaSkipF) {
             const float4 nc = s_n[j];
-            const float om = 1.0f - al;
-            const float Tb = T / om;
+            const float iom = __frcp_rn(1.0f - al);
+            const float Tb = T * iom;
             const float w = al * Tb;
             o[0] = w * gr;
             o[1] = w * gg;
             o[2] = w * gb;
-            const float dCr = b.z * Tb - sr / om;
-            const float dCg = b.w * Tb - sg / om;
-            const float dCb = nc.w * Tb - sb / om;
+            const float dCr = fmaf(b.z, Tb, -sr * iom);
+            const float dCg = fmaf(b.w, Tb, -sg * iom);
+            const float dCb = fmaf(nc.w, Tb, -sb * iom);
             const float da = dCr * gr + dCg * gg + dCb * gb;
             sr = fmaf(w, b.z, sr);
             sg = fmaf(w, b.w, sg);
             sb = fmaf(w, nc.w, sb);
             T = Tb;
             if (al < kAlphaClampVal) {
-              o[3] = da * al / b.y;
               const float dp = da * al;
-              o[4] = dp * (nc.x * dx + nc.y * dy);
-              o[5] = dp * (nc.y * dx + nc.z * dy);
+              o[3] = dp * s_io[j];
+              o[4] = dp * fmaf(nc.x, dx, nc.y * dy);
+              o[5] = dp * fmaf(nc.y, dx, nc.z * dy);
               o[6] = dp * (-0.5f * dx * dx);
               o[7] = dp * (-dx * dy);
               o[8] = dp * (-0.5f * dy * dy);
@@ -194,14 +196,12 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
             any = true;
           }
         }
-        if (__any_sync(kFull, any)) {
-#pragma unroll
-          for (int u = 0; u < 9; ++u) o[u] = warp_sum(o[u]);
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int u = 0; u < 9; ++u) s_red[warp][j - ss][u] = o[u];
-        }
+        // 12-shuffle transposed reduction; lanes 0,2,4,8,10,16,18,20,24 end
+        // up holding the warp sums of values 0..8 and store them in one STS.
+        float red = 0.0f;
+        if (__any_sync(kFull, any)) red = warp_reduce9(o);
+        const int slot = reduce9_slot(lane);
+        if (slot >= 0) s_red[warp][j - ss][slot] = red;
       }
       __syncthreads();
       const int cnt = (se - ss) * 9;
@@ -231,6 +231,12 @@ struct RunStarts {
 __global__ void run_sentinel_kernel(uint32_t* starts, const unsigned long long* n_runs,
                                     const unsigned long long* n_items) {
   starts[*n_runs] = static_cast<uint32_t>(*n_items);
+}
+
+// Publish the backward's counters in the frame header (cgs_frame_stats).
+__global__ void bwd_stats_kernel(FrameHeader* fh, const BwdHeader* bh) {
+  fh->stats.n_processed = static_cast<int64_t>(bh->n_processed);
+  fh->stats.n_touched = static_cast<int64_t>(bh->n_runs);
 }
 
 struct GaussIn {
@@ -563,15 +569,15 @@ __global__ void __launch_bounds__(256) sr_code_reduce_kernel(
 template <int DEG>
 static void launch_gauss(const BwdLayout& B, const uint32_t* sk, const uint32_t* sv, int nv,
                          const GaussIn& gi, const FrameDesc& fd, cudaStream_t st) {
-  gauss_reduce_kernel<DEG><<<148 * 4, 256, 0, st>>>(sk, sv, B.run_start, B.hdr, B.partials, nv, gi,
-                                                    fd, B);
+  CGS_PROFILED("gauss_reduce_kernel", st, gauss_reduce_kernel<DEG><<<148 * 4, 256, 0, st>>>(sk, sv, B.run_start, B.hdr, B.partials, nv, gi,
+                                                    fd, B));
 }
 
 template <int DEG>
 static void launch_sh_reduce(const BwdLayout& B, const uint32_t* k, const uint32_t* v, float scale,
                              float* gsh, cudaStream_t st) {
-  sh_code_reduce_kernel<DEG><<<148 * 8, 256, 0, st>>>(k, v, B.crun, &B.hdr->n_sh_runs, B.e_view,
-                                                      B.e_draw, scale, gsh);
+  CGS_PROFILED("sh_code_reduce_kernel", st, sh_code_reduce_kernel<DEG><<<148 * 8, 256, 0, st>>>(k, v, B.crun, &B.hdr->n_sh_runs, B.e_view,
+                                                      B.e_draw, scale, gsh));
 }
 
 static int code_pass(BwdLayout& B, const int32_t* g2x, int64_t cap_rows,
@@ -604,9 +610,9 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
   int rc = launch_scan(TileProcScan{L.tile_nproc, B.proc_off}, nullptr, fd.total_tiles,
                        fd.total_tiles, B.scan, &B.hdr->n_processed, st);
   if (rc) return rc;
-  raster_bwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.ranges, sorted_pair_vals(L), L.recs, L.hdr,
+  CGS_PROFILED("raster_bwd_kernel", st, raster_bwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.ranges, sorted_pair_vals(L), L.recs, L.hdr,
                                                     L.px_last, L.tile_nproc, final_T, dL, B.proc_off,
-                                                    fd.n_views, L.n, B.partials, B.pkeys, B.pvals);
+                                                    fd.n_views, L.n, B.partials, B.pkeys, B.pvals));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   uint32_t *sk, *sv;
   rc = launch_radix_sort<uint32_t>(B.pkeys, B.pvals, &B.hdr->n_processed, 0, L.pair_cap,
@@ -625,7 +631,7 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
     default: launch_gauss<3>(B, sk, sv, fd.n_views, gi, fd, st); break;
   }
   CGS_CHECK_LAUNCH("gauss_reduce_kernel");
-  gauss_write_kernel<<<grid_for(B.ecap, 256, 8), 256, 0, st>>>(B.hdr, B, scale, gpos, glogit);
+  CGS_PROFILED("gauss_write_kernel", st, gauss_write_kernel<<<grid_for(B.ecap, 256, 8), 256, 0, st>>>(B.hdr, B, scale, gpos, glogit));
   CGS_CHECK_LAUNCH("gauss_write_kernel");
   // SH codebook rows
   uint32_t *ck, *cv;
@@ -641,9 +647,11 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
   // SR codebook rows
   rc = code_pass(B, sc->g2sr, sc->sr_capacity, &B.hdr->n_sr_runs, &ck, &cv, st);
   if (rc) return rc;
-  sr_code_reduce_kernel<<<148 * 8, 256, 0, st>>>(ck, cv, B.crun, &B.hdr->n_sr_runs, B.e_s3a, B.e_s3b,
-                                                 sc->sr_rows, scale, gsr);
+  CGS_PROFILED("sr_code_reduce_kernel", st, sr_code_reduce_kernel<<<148 * 8, 256, 0, st>>>(ck, cv, B.crun, &B.hdr->n_sr_runs, B.e_s3a, B.e_s3b,
+                                                 sc->sr_rows, scale, gsr));
   CGS_CHECK_LAUNCH("sr_code_reduce_kernel");
+  bwd_stats_kernel<<<1, 1, 0, st>>>(const_cast<FrameHeader*>(L.hdr), B.hdr);
+  CGS_CHECK_LAUNCH("bwd_stats_kernel");
   return CGS_OK;
 }
 

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
 template <int DEG>
 static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut& out,
                            int64_t vn, cudaStream_t st) {
-  project_kernel<DEG><<<grid_for(vn, 256, 16), 256, 0, st>>>(in, fd, out);
+  CGS_PROFILED("project_kernel", st, project_kernel<DEG><<<grid_for(vn, 256, 16), 256, 0, st>>>(in, fd, out));
 }
 
 template <typename KT>
@@ -401,8 +401,8 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   const int64_t vn = L.vn;
   CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
   if (sc->sr_capacity > 0) {
-    sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(sc->sr_rows,
-                                                                            sc->sr_capacity, sr_cov);
+    CGS_PROFILED("sr_precompute_kernel", st, sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(sc->sr_rows,
+                                                                            sc->sr_capacity, sr_cov));
     CGS_CHECK_LAUNCH("sr_precompute_kernel");
   }
   if (vn > 0) {
@@ -431,21 +431,21 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
   const int eg = grid_for(vn, 256, 16);
   if (L.tile_key_bytes == 2) {
-    emit_pairs_kernel<uint16_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
-                                                    L.n, static_cast<uint16_t*>(L.pkeys), L.pvals);
+    CGS_PROFILED("emit_pairs_kernel", st, emit_pairs_kernel<uint16_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
+                                                    L.n, static_cast<uint16_t*>(L.pkeys), L.pvals));
     CGS_CHECK_LAUNCH("emit_pairs_kernel");
     rc = sort_and_range<uint16_t>(L, fd, L.psort16, st);
   } else {
-    emit_pairs_kernel<uint32_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
-                                                    L.n, static_cast<uint32_t*>(L.pkeys), L.pvals);
+    CGS_PROFILED("emit_pairs_kernel", st, emit_pairs_kernel<uint32_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
+                                                    L.n, static_cast<uint32_t*>(L.pkeys), L.pvals));
     CGS_CHECK_LAUNCH("emit_pairs_kernel");
     rc = sort_and_range<uint32_t>(L, fd, L.psort32, st);
   }
   if (rc) return rc;
   if (fd.total_tiles > 0) {
-    raster_fwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.ranges, sorted_pair_vals(L), L.recs,
+    CGS_PROFILED("raster_fwd_kernel", st, raster_fwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.ranges, sorted_pair_vals(L), L.recs,
                                                       L.hdr, image, final_T, counts, L.px_last,
-                                                      L.tile_nproc);
+                                                      L.tile_nproc));
     CGS_CHECK_LAUNCH("raster_fwd_kernel");
   }
   return CGS_OK;

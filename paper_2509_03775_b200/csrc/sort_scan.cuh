@@ -161,7 +161,7 @@ int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t 
   CGS_CUDA(cudaMemsetAsync(ws.status, 0, ws.max_parts * sizeof(unsigned long long), st));
   CGS_CUDA(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st));
   const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanTile);
-  scan_kernel<Op><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total);
+  CGS_PROFILED("scan_kernel", st, scan_kernel<Op><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total));
   CGS_CHECK_LAUNCH("scan_kernel");
   return CGS_OK;
 }
@@ -366,7 +366,7 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
   CGS_CUDA(cudaMemsetAsync(ws.status, 0,
                            static_cast<size_t>(passes) * ws.max_parts * 256 * sizeof(uint32_t), st));
   CGS_CUDA(cudaMemsetAsync(ws.counter, 0, 64 * sizeof(unsigned), st));
-  sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist);
+  CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist));
   CGS_CHECK_LAUNCH("sort_hist_kernel");
   static bool attr_set = false;
   const size_t smem = sizeof(SortSmem<K>);
@@ -381,10 +381,10 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
   uint32_t* vout = ws.vals_alt;
   const unsigned grid = static_cast<unsigned>(ceil_div(n_cap > 0 ? n_cap : 1, kSortTile));
   for (int p = 0; p < passes; ++p) {
-    onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p,
+    CGS_PROFILED("onesweep_kernel", st, onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p,
                                                 ws.hist + p * 256,
                                                 ws.status + static_cast<size_t>(p) * ws.max_parts * 256,
-                                                ws.counter + p);
+                                                ws.counter + p));
     CGS_CHECK_LAUNCH("onesweep_kernel");
     K* tk = kin; kin = kout; kout = tk;
     uint32_t* tv = vin; vin = vout; vout = tv;

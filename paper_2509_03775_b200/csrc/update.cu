@@ -142,8 +142,8 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
                 cudaStream_t st) {
   CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
   const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
-  finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
-                                                                          nc, gsr, nd, flags);
+  CGS_PROFILED("finite_check_kernel", st, finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
+                                                                          nc, gsr, nd, flags));
   CGS_CHECK_LAUNCH("finite_check_kernel");
   SgldDev p{};
   // exactly numpy's scalar sub-expressions: 0.5 * eps and mult * sqrt(eps)
@@ -173,9 +173,9 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
   const int64_t tot = (p.on_pos ? 3 * n : 0) + (p.on_op ? n : 0) + (p.on_sh ? n_sh * D : 0) +
                       (p.on_sr ? n_sr : 0);
   if (tot > 0) {
-    sgld_kernel<<<grid_for(tot, 256, 8), 256, 0, st>>>(pos, logit, n, sh, D, sh_live, n_sh, sr,
+    CGS_PROFILED("sgld_kernel", st, sgld_kernel<<<grid_for(tot, 256, 8), 256, 0, st>>>(pos, logit, n, sh, D, sh_live, n_sh, sr,
                                                        sr_live, n_sr, gpos, glogit, gsh, gsr, p,
-                                                       npos, nlog, nsh, nsr, flags);
+                                                       npos, nlog, nsh, nsr, flags));
     CGS_CHECK_LAUNCH("sgld_kernel");
   }
   return CGS_OK;

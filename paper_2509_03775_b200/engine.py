@@ -1,0 +1,134 @@
+"""Batched, device-resident training loop (the bench's "step").
+
+One iteration = one SGLD update transition over a batch of views rendered as
+one frame (mean of per-view gradients -- the batch extension of
+`sampler.py:329-338`; with one view it is exactly the reference update),
+followed, on the schedule, by one forced split and one forced merge
+transition (`sampler.py:339-385`) and densify when due (`sampler.py:387-390`).
+
+No host synchronisation inside an update: the frame's pair buffers are sized
+from a warm-up render and any overflow is latched in a sticky device flag
+that is checked when the caller reads results; non-finite gradients make the
+SGLD kernel skip the update and latch a flag as well.  Across GPUs, views are
+sharded by rank and the flat gradient buffer is summed with one NCCL
+allreduce (``torch.distributed``); MCMC decisions use the same host
+Generator seed on every rank, so replicas stay identical with no broadcast.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .metrics import LossWorkspace
+from .model import ModelState, densify
+from .render import Frame, GradientSet
+from .sampler import (SamplerConfig, SamplerError, TransitionRecord, merge_step, sgld_update,
+                      split_step)
+
+
+class Trainer:
+    def __init__(self, state: ModelState, cams, gts: torch.Tensor, config: SamplerConfig,
+                 rng: np.random.Generator, mcmc_every: int = 25, world: int = 1,
+                 pair_headroom: float = 1.5, allreduce=None):
+        self.state = state
+        self.cams = list(cams)
+        self.config = config
+        self.rng = rng
+        self.mcmc_every = mcmc_every
+        self.world = world
+        self.allreduce = allreduce
+        self.headroom = pair_headroom
+        h, w = self.cams[0].height, self.cams[0].width
+        if any((c.height, c.width) != (h, w) for c in self.cams):
+            raise ValueError("batched views need equal sizes")
+        self.V = len(self.cams)
+        self.dev = state.device
+        self.gts = gts
+        self.loss_ws = LossWorkspace(self.V, h, w, self.dev)
+        self.flags = torch.zeros((1,), dtype=torch.int32, device=self.dev)
+        self.sticky = torch.zeros((1,), dtype=torch.int32, device=self.dev)
+        self.frame = None
+        self.grads = None
+        self.bws = None
+        self.dL = None
+        self.pair_cap = None
+        self.updates = 0
+        self.mcmc_events = 0
+        self.mcmc_ms = []
+        self.last_loss = None
+
+    # -- buffers ---------------------------------------------------------------
+    def _prepare(self):
+        st = self.state
+        fr = self.frame
+        if fr is None or fr.n != st.num_gaussians or fr.sr_cap != st.sr.capacity:
+            if self.pair_cap is None:
+                probe = Frame(st, self.cams).run_checked()
+                self.pair_cap = int(probe.stats().n_pairs * self.headroom) + 4096
+            self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap)
+            nb = nat.library().cgs_backward_workspace_bytes(st.num_gaussians, self.frame.c_cams,
+                                                            self.V, self.pair_cap)
+            self.bws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+            self.dL = torch.empty_like(self.frame.image)
+        g = self.grads
+        if (g is None or g.positions.shape[0] != st.num_gaussians
+                or g.sh_rows.shape[0] != st.sh.capacity or g.sr_rows.shape[0] != st.sr.capacity):
+            self.grads = GradientSet.empty(st)
+
+    # -- transitions -------------------------------------------------------------
+    def update(self):
+        """SGLD update over the view batch (device only)."""
+        self._prepare()
+        st = self.state
+        fr = self.frame
+        fr.run()
+        ov = fr.ws[40:44].view(torch.int32)  # cgs_frame_stats_t.overflow (byte 40)
+        torch.maximum(self.sticky, ov, out=self.sticky)
+        losses = self.loss_ws.run(fr.image, self.gts, self.config.lambda_ssim, self.dL, 1.0)
+        fr.backward(self.dL, scale=1.0 / (self.V * self.world), grads=self.grads, ws=self.bws)
+        if self.allreduce is not None:
+            self.allreduce(self.grads.flat)
+        sgld_update(st, self.grads, self.config, self.rng, flags=self.flags, check=False)
+        torch.maximum(self.sticky, self.flags * 2, out=self.sticky)
+        self.last_loss = losses
+        self.updates += 1
+        self._advance()
+
+    def _advance(self):
+        st = self.state
+        st.iteration += 1
+        c = self.config
+        if c.densify_every > 0 and st.iteration % c.densify_every == 0:
+            densify(st, c.densify_growth, c.gaussian_cap, self.rng, jitter_sigma=c.densify_jitter)
+
+    def mcmc(self):
+        """One forced split and one forced merge transition (reference rules)."""
+        import time
+        t0 = time.perf_counter()
+        for fn in (split_step, merge_step):
+            rec = TransitionRecord(iteration=self.state.iteration + 1, kind="mcmc", codebook="-")
+            fn(self.state, None, self.config, self.rng, rec)
+            self._advance()
+        self.mcmc_events += 1
+        self.mcmc_ms.append(1000.0 * (time.perf_counter() - t0))
+
+    def step(self):
+        self.update()
+        if self.mcmc_every and self.updates % self.mcmc_every == 0:
+            self.mcmc()
+
+    # -- results -----------------------------------------------------------------
+    def check(self):
+        """Raise if any update overflowed its pair buffers or saw non-finite gradients."""
+        v = int(self.sticky.item())
+        if v & 1:
+            raise RuntimeError("pair capacity overflow during the run (raise pair_headroom)")
+        if v & 2:
+            raise SamplerError("non-finite gradients during the run")
+
+    def recon(self) -> float:
+        return float(self.last_loss.view(self.V, 3)[:, 2].mean().item())

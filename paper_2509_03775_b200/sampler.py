@@ -432,10 +432,19 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
     lam = config.lambda_for(which)
     es, em = config.eps_for(which)
     moves = []
+    # The sequential accept loop is the host's only per-candidate work; the
+    # acceptance arithmetic is inlined with exactly the float expressions of
+    # acceptance_probability / _log_q_sm (sampler.py:138-164).
+    dim = book.dim
+    c_q = 1.0 / es ** 2 - 1.0 / em ** 2
+    corr = dim * math.log(em / es) if config.normalization_correction else None
+    refcount = book.refcount
+    normal, uniform, npexp = rng.normal, rng.random, np.exp
+    probs = rec.accept_probs
     for i, row in zip(cand.tolist(), rows.tolist()):
-        if book.refcount[row] < 2:
+        if refcount[row] < 2:
             continue
-        u = rng.normal(0.0, es, size=book.dim)
+        u = normal(0.0, es, size=dim)
         extra = 0.0
         if config.exact_ratio:
             # flush pending applies so the trial render sees the current state
@@ -443,12 +452,16 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
             moves = []
             prop = SplitProposal(which, i, row, u, book.row(row).astype(np.float64) + u)
             extra = _exact_log_ratio(state, views, config, rng, lambda s: apply_split(s, prop))
-        prob = acceptance_probability("split", u, lam, es, em, config.normalization_correction, extra)
-        rec.accept_probs.append(prob)
+        log_q = -0.5 * float(u @ u) * c_q
+        if corr is not None:
+            log_q += corr
+        prob = float(npexp(min(0.0, -lam - log_q + extra)))
+        probs.append(prob)
         rec.attempts += 1
-        if rng.random() < prob:
+        if uniform() < prob:
             new_row = book.alloc_index(parent=row)
             book.decref(row)
+            refcount = book.refcount  # alloc may have grown the array
             moves.append((i, row, new_row, u))
             rec.accepts += 1
     _apply_split_batch(state, which, moves)
