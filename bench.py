@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true")
     return ap.parse_args()
 
 
@@ -245,7 +246,7 @@ def main():
     allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
     rng = np.random.default_rng(args.seed)
     tr = Trainer(st, cams, gts, cfg, rng, mcmc_every=args.mcmc_every, world=world,
-                 allreduce=allreduce)
+                 allreduce=allreduce, use_graphs=not args.no_graphs)
 
     flush = torch.empty((64 * 1024 * 1024,), dtype=torch.float32, device=dev)  # 256 MB > L2
 
@@ -268,11 +269,14 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    host_s = 0.0
     for k in range(args.steps):
         if not args.no_flush:
             flush.zero_()
         starts[k].record()
+        h0 = time.perf_counter()
         tr.step()
+        host_s += time.perf_counter() - h0
         ends[k].record()
         views_done += len(cams)
     torch.cuda.synchronize()
@@ -380,7 +384,8 @@ def main():
                "frame": {"pairs": int(stats.n_pairs), "processed_pairs": P_x,
                          "touched": int(stats.n_touched), "onscreen": int(stats.n_onscreen)},
                "recon": tr.recon(), "mcmc_events": tr.mcmc_events,
-               "mcmc_ms": tr.mcmc_ms}
+               "mcmc_ms": tr.mcmc_ms, "host_enqueue_ms_per_step": 1000.0 * host_s / args.steps,
+               "cuda_graphs": tr.use_graphs, "graph_captures": tr.captures}
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -96,6 +96,9 @@ typedef struct cgs_sgld_params {
   uint64_t offset;
   int32_t noise_source;  /* 0: device Philox, 1: caller arrays (parity)      */
   int32_t pad_;
+  uint64_t* offset_dev;  /* optional device counter: incremented by the update
+                            and used as the Philox offset instead of `offset`
+                            (CUDA-graph replays then draw fresh noise)       */
 } cgs_sgld_params_t;
 
 /* ---- library --------------------------------------------------------- */
@@ -151,22 +154,35 @@ CGS_API int cgs_frame_splats(const cgs_camera_t* cams, int32_t n_views, int64_t 
                      uint32_t* n_tiles, cgs_stream_t stream);
 
 CGS_API size_t cgs_backward_workspace_bytes(int64_t n, const cgs_camera_t* cams, int32_t n_views,
-                                    int64_t pair_capacity);
+                                    int64_t pair_capacity, int64_t sh_capacity,
+                                    int64_t sr_capacity);
 
 /* rasterize_backward + _pull_back (render.py:318-459), reusing the frame's
- * sorted pairs: reverse-order tile blend with in-CTA warp-shuffle reductions
- * (one partial per processed pair), a stable sort of processed pairs by
- * Gaussian, fixed-order per-Gaussian reduction + chain rule, then codebook
- * gradients as sort-by-row segmented reductions (render.py:456-458, no
- * atomics).  All four gradient arrays are fully written (zeros where the
- * reference writes zeros), multiplied by `scale`.  final_T is the forward's
- * output.  Deterministic. */
+ * (tile, depth)-sorted pairs: reverse-order tile blend with in-CTA warp
+ * reductions (one 9-float partial per processed pair); per splat a
+ * fixed-order walk of its pairs (row-major tile order) through the inverse
+ * pair map + fp64 chain rule; per codebook row a segmented reduction over
+ * its members (render.py:456-458) -- no atomics, no per-step sorts.
+ * The code -> members CSRs (cgs_code_csr) are optional: pass NULL to have
+ * them built in the workspace (two extra sorts).  All four gradient arrays
+ * are fully written (zeros where the reference writes zeros), multiplied by
+ * `scale`.  final_T is the forward's output.  Deterministic. */
 CGS_API int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
                         const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
                         const float* final_T, const float* dL_dimage, float scale,
+                        const int32_t* sh_csr_offsets, const int32_t* sh_csr_members,
+                        const int32_t* sr_csr_offsets, const int32_t* sr_csr_members,
                         void* workspace, size_t workspace_bytes,
                         float* grad_positions, float* grad_logits,
                         float* grad_sh_rows, float* grad_sr_rows, cgs_stream_t stream);
+
+/* code -> members CSR of an index array (g2sh or g2sr): offsets (capacity+1)
+ * and members (n, ascending Gaussian index within each row).  Rebuild only
+ * when assignments change (split / merge / densify). */
+CGS_API size_t cgs_code_csr_workspace_bytes(int64_t n, int64_t capacity);
+CGS_API int cgs_code_csr(const int32_t* idx, int64_t n, int64_t capacity, int32_t* offsets,
+                         int32_t* members, void* workspace, size_t workspace_bytes,
+                         cgs_stream_t stream);
 
 /* ---- loss: recon_loss / recon_loss_grad (metrics.py:122-140) --------- */
 CGS_API size_t cgs_loss_workspace_bytes(int32_t n_views, int32_t height, int32_t width);

@@ -57,6 +57,7 @@ class CSgldParams(ctypes.Structure):
         ("grad_scale", ctypes.c_double),
         ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64),
         ("noise_source", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("offset_dev", ctypes.c_void_p),
     ]
 
 
@@ -81,8 +82,11 @@ SIGNATURES = {
     "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),
     "cgs_frame_tile_lists": (I32, [CAMP, I32, I64, I64, I64, P, SZ, P, P, P]),
     "cgs_frame_splats": (I32, [CAMP, I32, I64, I64, I64, P, SZ, I32, P, P, P, P, P, P]),
-    "cgs_backward_workspace_bytes": (SZ, [I64, CAMP, I32, I64]),
-    "cgs_render_backward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, F32, P, SZ, P, P, P, P, P]),
+    "cgs_backward_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64, I64]),
+    "cgs_render_backward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, F32, P, P, P, P, P, SZ, P, P,
+                                  P, P, P]),
+    "cgs_code_csr_workspace_bytes": (SZ, [I64, I64]),
+    "cgs_code_csr": (I32, [P, I64, I64, P, P, P, SZ, P]),
     "cgs_loss_workspace_bytes": (SZ, [I32, I32, I32]),
     "cgs_recon_loss": (I32, [P, P, I32, I32, I32, F64, I32, F32, P, P, P, SZ, P]),
     "cgs_sgld_update": (I32, [P, P, I64, P, I32, P, I64, P, P, I64, I64, I64, P, P, P, P,

@@ -38,6 +38,9 @@ static cudaEvent_t prof_event() {
 ProfScope::ProfScope(const char* name, cudaStream_t s) : on(false), st(s) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (!g_prof_name.empty() && g_prof_name == name) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return;  // events are not re-armed per replay
     on = true;
     cudaEvent_t a = prof_event(), b = prof_event();
     cudaEventRecord(a, st);
@@ -60,11 +63,16 @@ int cuda_status(cudaError_t e, const char* where) {
 int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, float* image,
                   float* final_T, int32_t* counts, double* sr_cov, cudaStream_t st);
 struct BwdLayout;
-size_t bwd_ws_bytes(int64_t n, int n_views, int total_tiles, int64_t pair_cap);
+size_t bwd_ws_bytes(int64_t n, int n_views, int total_tiles, int64_t pair_cap, int64_t sh_cap,
+                    int64_t sr_cap);
 int frame_backward_entry(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                          void* ws, size_t ws_bytes, const float* dL, const float* final_T,
                          float scale, float* gpos, float* glogit, float* gsh, float* gsr,
+                         const int32_t* const csr_off[2], const int32_t* const csr_mem[2],
                          cudaStream_t st);
+size_t code_csr_ws_bytes(int64_t n, int64_t cap);
+int build_code_csr(const int32_t* idx, int64_t n, int64_t cap, int32_t* off, int32_t* mem,
+                   void* ws, size_t ws_bytes, cudaStream_t st);
 size_t loss_ws_bytes(int nv, int h, int w);
 int recon_loss(const float* img, const float* gt, int nv, int H, int W, double lam, float gscale,
                float* dL, double* losses, int want_ssim, void* ws, size_t ws_bytes,
@@ -310,15 +318,32 @@ int cgs_frame_splats(const cgs_camera_t* cams, int32_t n_views, int64_t n, int64
 }
 
 size_t cgs_backward_workspace_bytes(int64_t n, const cgs_camera_t* cams, int32_t n_views,
-                                    int64_t pair_capacity) {
+                                    int64_t pair_capacity, int64_t sh_capacity,
+                                    int64_t sr_capacity) {
   if (check_cams(cams, n_views)) return 0;
   FrameDesc fd = make_frame_desc(cams, n_views);
-  return bwd_ws_bytes(n, n_views, fd.total_tiles, pair_capacity);
+  return bwd_ws_bytes(n, n_views, fd.total_tiles, pair_capacity, sh_capacity, sr_capacity);
+}
+
+size_t cgs_code_csr_workspace_bytes(int64_t n, int64_t capacity) {
+  return code_csr_ws_bytes(n, capacity);
+}
+
+int cgs_code_csr(const int32_t* idx, int64_t n, int64_t capacity, int32_t* offsets,
+                 int32_t* members, void* workspace, size_t workspace_bytes, cgs_stream_t stream) {
+  if (n < 0 || capacity < 0 || !offsets || (n > 0 && (!idx || !members))) {
+    set_error("code_csr: invalid arguments");
+    return CGS_EINVAL;
+  }
+  return build_code_csr(idx, n, capacity, offsets, members, workspace, workspace_bytes,
+                        static_cast<cudaStream_t>(stream));
 }
 
 int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
                         const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
                         const float* final_T, const float* dL_dimage, float scale,
+                        const int32_t* sh_csr_offsets, const int32_t* sh_csr_members,
+                        const int32_t* sr_csr_offsets, const int32_t* sr_csr_members,
                         void* workspace, size_t workspace_bytes, float* grad_positions,
                         float* grad_logits, float* grad_sh_rows, float* grad_sr_rows,
                         cgs_stream_t stream) {
@@ -333,8 +358,10 @@ int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* cams, int3
     set_error("frame workspace too small");
     return CGS_EWORKSPACE;
   }
+  const int32_t* const off[2] = {sh_csr_offsets, sr_csr_offsets};
+  const int32_t* const mem[2] = {sh_csr_members, sr_csr_members};
   return frame_backward_entry(scene, fd, L, workspace, workspace_bytes, dL_dimage, final_T, scale,
-                              grad_positions, grad_logits, grad_sh_rows, grad_sr_rows,
+                              grad_positions, grad_logits, grad_sh_rows, grad_sr_rows, off, mem,
                               static_cast<cudaStream_t>(stream));
 }
 

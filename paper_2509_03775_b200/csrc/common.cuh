@@ -60,9 +60,9 @@ struct FrameDesc {
 struct __align__(16) SplatRec {
   double mx, my;        // mean2d (f64, render.py:157-158)
   double ca, cb, cc;    // conic [[A,B],[B,C]] (f64, render.py:176-181)
-  double opac;          // sigmoid(logit) (f64, render.py:200)
+  float opac;           // sigmoid(logit) (computed in f64, render.py:200)
   float r, g, b;        // clamped colour (render.py:196-198)
-  uint32_t rect;        // packed tile rect: tx0 | ty0<<8 ... (unused by raster)
+  uint16_t px0, px1, py0, py1;  // inclusive pixel rect (render.py:110-115)
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must be 64 bytes");
 

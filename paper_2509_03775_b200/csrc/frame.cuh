@@ -6,32 +6,34 @@
 
 namespace cgs {
 
+// Tiles whose list is at most this long are depth-sorted in shared memory
+// (bitonic); longer lists take a stable in-CTA radix path through global
+// scratch.
+constexpr int kTileSortCap = 4096;
+
 struct FrameLayout {
   FrameHeader* hdr;
   SplatRec* recs;          // V*N
   uint64_t* depth_key;     // V*N (f64 bits of camera z)
   uint32_t* n_tiles;       // V*N
   uint64_t* rect;          // V*N packed tile rect
-  uint64_t* skeys;         // V*N compacted depth keys
-  uint32_t* svals;         // V*N compacted splat ids
-  SortWs<uint64_t> dsort;
-  uint64_t* pair_off;      // V*N exclusive pair offsets in depth order
+  uint64_t* pair_off;      // V*N exclusive pair offsets (index order)
   void* pkeys;             // pair_cap tile keys (u16 or u32)
   uint32_t* pvals;         // pair_cap splat ids
   SortWs<uint16_t> psort16;
   SortWs<uint32_t> psort32;
+  uint32_t* inv;           // pair_cap: emission index -> final pair position
+  uint32_t* scratch;       // pair_cap: long-tile radix scratch
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
   uint32_t* tile_nproc;    // total_tiles
   ScanWs scan;
   double* sr_cov;          // sr_cap * 8 (Sigma3 + zero-quaternion flag)
-  // results of the sorts (set by forward, re-derived identically by backward)
   size_t bytes;
   int64_t n, vn, pair_cap;
   int tile_key_bytes;      // 2 or 4
   int tile_key_bits;
-  int depth_result_alt;    // 1 if sorted depth results live in dsort alt buffers
-  int pair_result_alt;
+  int pair_result_alt;     // 1 if the tile-sorted pairs live in the sort's alt buffers
 };
 
 inline int bits_for(int64_t v) {
@@ -84,9 +86,6 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.depth_key = c.take<uint64_t>(vn1);
   L.n_tiles = c.take<uint32_t>(vn1);
   L.rect = c.take<uint64_t>(vn1);
-  L.skeys = c.take<uint64_t>(vn1);
-  L.svals = c.take<uint32_t>(vn1);
-  L.dsort = carve_sort<uint64_t>(c, vn1);
   L.pair_off = c.take<uint64_t>(vn1);
   if (L.tile_key_bytes == 2) {
     L.pkeys = c.take<uint16_t>(pc);
@@ -96,26 +95,43 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
     L.psort32 = carve_sort<uint32_t>(c, pc);
   }
   L.pvals = c.take<uint32_t>(pc);
+  L.inv = c.take<uint32_t>(pc);
+  L.scratch = c.take<uint32_t>(pc);
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.scan = carve_scan(c, vn1 > fd.total_tiles ? vn1 : fd.total_tiles);
   L.sr_cov = c.take<double>((sr_cap > 0 ? sr_cap : 1) * 8);
   L.bytes = c.off + 256;
-  // pass parity: 8 passes for f64 depth keys -> result back in the input buffers
-  L.depth_result_alt = (8 % 2) == 1;
   const int ppasses = (L.tile_key_bits + 7) / 8;
   L.pair_result_alt = (ppasses % 2) == 1;
   return L;
 }
 
-// Sorted (splat id) list in depth order and sorted pair arrays.
-inline const uint32_t* sorted_splats(const FrameLayout& L) {
-  return L.depth_result_alt ? L.dsort.vals_alt : L.svals;
-}
-inline const uint32_t* sorted_pair_vals(const FrameLayout& L) {
+// Final (tile, depth)-ordered splat ids of the pairs.
+inline uint32_t* sorted_pair_vals(const FrameLayout& L) {
   if (!L.pair_result_alt) return L.pvals;
   return L.tile_key_bytes == 2 ? L.psort16.vals_alt : L.psort32.vals_alt;
+}
+
+// Raster launches (raster.cu).
+int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
+                      float* image, float* final_T, int32_t* counts, cudaStream_t st);
+int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
+                      const float* dL, float* partials, cudaStream_t st);
+
+// Emission index of pair (splat s, tile t): pairs of a splat are emitted in
+// row-major order over its tile rect starting at pair_off[s].
+__device__ __forceinline__ uint64_t emission_index(const uint64_t* pair_off, const uint64_t* rect,
+                                                   const FrameDesc& fd, int64_t n, uint32_t s,
+                                                   int tile) {
+  const uint64_t rc = rect[s];
+  const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
+  const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
+  const int v = static_cast<int>(s / static_cast<uint64_t>(n));
+  const int lt = tile - fd.cam[v].tile_base;
+  const int ty = lt / fd.cam[v].ntx, tx = lt - ty * fd.cam[v].ntx;
+  return pair_off[s] + static_cast<uint64_t>((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
 }
 
 }  // namespace cgs

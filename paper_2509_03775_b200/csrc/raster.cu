@@ -1,0 +1,348 @@
+// Tile rasterizer kernels, forward and backward (reference render.py:265-377).
+//
+// Both kernels run one 128-thread CTA per 16x16 tile.  Warp w owns the 8x8
+// quadrant ((w & 1) * 8, (w >> 1) * 8) of the tile and each lane two pixels
+// (x, y) and (x, y + 4) of it.  A splat whose pixel rect (render.py:110-115)
+// misses a warp's quadrant is skipped by that warp without evaluating it:
+// outside the rect alpha < opacity / 255 < 1/255 by construction of the
+// footprint radius (render.py:32-34), so the skip changes no result.
+//
+// Splat records are gathered by the bulk-copy engine (cp.async.bulk, one
+// 64-byte record per copy, completion on an mbarrier) one batch of 256 ahead
+// of the blending, and converted once per batch to tile-relative fp32 form
+// in shared memory.
+#include "frame.cuh"
+#include "raster_common.cuh"
+
+namespace cgs {
+
+// Tile-local inclusive pixel rect of a splat as 4 signed bytes (x0, x1, y0, y1),
+// clamped to [-1, 16].
+__device__ __forceinline__ uint32_t local_rect(const SplatRec& r, int tx0, int ty0) {
+  auto c = [](int v) { return static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(v < -1 ? -1 : (v > 16 ? 16 : v)))); };
+  return c(r.px0 - tx0) | (c(r.px1 - tx0) << 8) | (c(r.py0 - ty0) << 16) | (c(r.py1 - ty0) << 24);
+}
+
+__device__ __forceinline__ bool quad_hit(uint32_t rc, int qx, int qy) {
+  const int x0 = static_cast<int8_t>(rc & 0xff), x1 = static_cast<int8_t>((rc >> 8) & 0xff);
+  const int y0 = static_cast<int8_t>((rc >> 16) & 0xff), y1 = static_cast<int8_t>(rc >> 24);
+  return x1 >= qx && x0 <= qx + 7 && y1 >= qy && y0 <= qy + 7;
+}
+
+struct PixState {
+  float T, r, g, b;
+  int cnt;
+  uint32_t last;
+  bool done;
+};
+
+// Front-to-back blend of one splat into one pixel (render.py:274-283, 302-311).
+__device__ __forceinline__ void blend(PixState& p, float al, float cr, float cg, float cb,
+                                      uint32_t idx) {
+  if (p.done || !(al >= kAlphaSkipF)) return;
+  const float w = al * p.T;
+  p.r = fmaf(w, cr, p.r);
+  p.g = fmaf(w, cg, p.g);
+  p.b = fmaf(w, cb, p.b);
+  p.T = p.T * (1.0f - al);
+  ++p.cnt;
+  if (!(p.T >= kTMinF)) {  // every later splat is inactive (T_before < 1e-4)
+    p.done = true;
+    p.last = idx + 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) raster_fwd_kernel(
+    FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
+    const SplatRec* __restrict__ recs, const FrameHeader* __restrict__ hdr,
+    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ counts,
+    uint32_t* __restrict__ px_last, uint32_t* __restrict__ tile_nproc) {
+  __shared__ __align__(128) SplatRec s_raw[256];
+  __shared__ float4 s_a[256];
+  __shared__ float4 s_b[256];
+  __shared__ float s_c[256];
+  __shared__ uint32_t s_r[256];
+  __shared__ uint32_t s_max[4];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (hdr->stats.overflow) return;
+  const int tile = blockIdx.x;
+  int v = 0;
+  while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
+  const CamDev& cam = fd.cam[v];
+  const int lt = tile - cam.tile_base;
+  const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int qx = (warp & 1) * 8, qy = (warp >> 1) * 8;
+  const int lx = qx + (lane & 7), ly = qy + (lane >> 3);  // pixels (lx, ly), (lx, ly + 4)
+  const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
+  const bool in0 = px < cam.width && py0 < cam.height;
+  const bool in1 = px < cam.width && py1 < cam.height;
+  const uint2 rg = ranges[tile];
+  const int n = static_cast<int>(rg.y - rg.x);
+  const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
+  const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+
+  PixState p0{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in0};
+  PixState p1{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in1};
+
+  if (tid == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  bool pending = false;
+  if (n > 0) {
+    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(256, n), tid, 128);
+    pending = true;
+  }
+  for (int b0 = 0; b0 < n; b0 += 256) {
+    const int nb = min(256, n - b0);
+    mbar_wait(&s_bar, phase);
+    phase ^= 1;
+    pending = false;
+    for (int k = tid; k < nb; k += 128) {
+      float4 a, b;
+      float c;
+      stage_splat(s_raw[k], ox, oy, a, b, c);
+      s_a[k] = a;
+      s_b[k] = b;
+      s_c[k] = c;
+      s_r[k] = local_rect(s_raw[k], tx * kTile, ty * kTile);
+    }
+    __syncthreads();
+    if (b0 + 256 < n) {
+      fence_proxy_async_smem();
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + 256, min(256, n - b0 - 256), tid, 128);
+      pending = true;
+    }
+    if (!(p0.done && p1.done)) {
+      for (int j = 0; j < nb; ++j) {
+        if (!quad_hit(s_r[j], qx, qy)) continue;  // warp-uniform, exact (see header)
+        const float4 a = s_a[j];
+        const float4 b = s_b[j];
+        const float dx = a.x + flx;
+        const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
+        const float t0 = a.z * dx * dx, t1 = a.w * dx;
+        const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
+        const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
+        if (al0 >= kAlphaSkipF || al1 >= kAlphaSkipF) {
+          const float cb = s_c[j];
+          blend(p0, al0, b.z, b.w, cb, static_cast<uint32_t>(b0 + j));
+          blend(p1, al1, b.z, b.w, cb, static_cast<uint32_t>(b0 + j));
+          if (p0.done && p1.done) break;
+        }
+      }
+    }
+    if (__syncthreads_count(p0.done && p1.done) == 128) break;
+  }
+  if (pending) mbar_wait(&s_bar, phase);  // never exit with copies in flight
+  if (in0 && !p0.done) p0.last = static_cast<uint32_t>(n);
+  if (in1 && !p1.done) p1.last = static_cast<uint32_t>(n);
+  if (in0) {
+    const int64_t pix = cam.pix_base + static_cast<int64_t>(py0) * cam.width + px;
+    image[3 * pix + 0] = p0.r;
+    image[3 * pix + 1] = p0.g;
+    image[3 * pix + 2] = p0.b;
+    final_T[pix] = p0.T;
+    counts[pix] = p0.cnt;
+    px_last[pix] = p0.last;
+  }
+  if (in1) {
+    const int64_t pix = cam.pix_base + static_cast<int64_t>(py1) * cam.width + px;
+    image[3 * pix + 0] = p1.r;
+    image[3 * pix + 1] = p1.g;
+    image[3 * pix + 2] = p1.b;
+    final_T[pix] = p1.T;
+    counts[pix] = p1.cnt;
+    px_last[pix] = p1.last;
+  }
+  uint32_t m = max(in0 ? p0.last : 0u, in1 ? p1.last : 0u);
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) m = max(m, __shfl_xor_sync(kFull, m, k));
+  if (lane == 0) s_max[warp] = m;
+  __syncthreads();
+  if (tid == 0) tile_nproc[tile] = max(max(s_max[0], s_max[1]), max(s_max[2], s_max[3]));
+}
+
+// ---------------------------------------------------------------------------
+// Reverse traversal (render.py:343-377).  For pixel p and splat k < last_p,
+// T is the transmittance after k, T_before = T / (1 - alpha_k) and the
+// running suffix holds sum_{j>k} alpha_j T_j c_j.  Alpha is recomputed with
+// exactly the forward's fp32 code, so skip/clamp/termination decisions match.
+// Per splat the 9 gradient values (d_colour 3, d_opacity, d_mean2d 2,
+// d_conic 3) are summed over the tile's pixels in fixed order: per warp a
+// 12-shuffle transposed reduction, then the 4 warps in shared memory.
+struct PixBwd {
+  float T, gr, gg, gb, sr, sg, sb;
+  uint32_t last;
+};
+
+// Adds pixel p's contribution of splat k to o[9]; returns whether it had one.
+__device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const float4& b,
+                                          const float4& nc, float io, float dx, float dy,
+                                          float* o) {
+  if (!(k < p.last) || !(al >= kAlphaSkipF)) return false;
+  const float iom = __frcp_rn(1.0f - al);
+  const float Tb = p.T * iom;
+  const float w = al * Tb;
+  o[0] = fmaf(w, p.gr, o[0]);  // d colour += weight * dL (render.py:351-352)
+  o[1] = fmaf(w, p.gg, o[1]);
+  o[2] = fmaf(w, p.gb, o[2]);
+  // dC/dalpha = c T_before - suffix / (1 - alpha) (render.py:357-359)
+  const float dCr = fmaf(b.z, Tb, -p.sr * iom);
+  const float dCg = fmaf(b.w, Tb, -p.sg * iom);
+  const float dCb = fmaf(nc.w, Tb, -p.sb * iom);
+  const float da = dCr * p.gr + dCg * p.gg + dCb * p.gb;
+  p.sr = fmaf(w, b.z, p.sr);
+  p.sg = fmaf(w, b.w, p.sg);
+  p.sb = fmaf(w, nc.w, p.sb);
+  p.T = Tb;
+  if (al < kAlphaClampVal) {  // no gradient through the clamp (render.py:361)
+    const float dp = da * al;
+    o[3] = fmaf(dp, io, o[3]);                               // d opacity
+    o[4] = fmaf(dp, fmaf(nc.x, dx, nc.y * dy), o[4]);        // d mean2d
+    o[5] = fmaf(dp, fmaf(nc.y, dx, nc.z * dy), o[5]);
+    o[6] = fmaf(dp, -0.5f * dx * dx, o[6]);                  // d conic (A, B, C)
+    o[7] = fmaf(dp, -dx * dy, o[7]);
+    o[8] = fmaf(dp, -0.5f * dy * dy, o[8]);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(128) raster_bwd_kernel(
+    FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
+    const SplatRec* __restrict__ recs, const FrameHeader* __restrict__ fh,
+    const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
+    const float* __restrict__ final_T, const float* __restrict__ dL,
+    float* __restrict__ partials) {
+  __shared__ __align__(128) SplatRec s_raw[256];
+  __shared__ float4 s_a[256];
+  __shared__ float4 s_b[256];
+  __shared__ float4 s_n[256];  // natural conic A, B, C and blue
+  __shared__ float s_io[256];  // 1 / opacity
+  __shared__ uint32_t s_r[256];
+  __shared__ float s_red[4][32][9];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (fh->stats.overflow) return;
+  const int tile = blockIdx.x;
+  const int nproc = static_cast<int>(tile_nproc[tile]);
+  if (nproc == 0) return;
+  int v = 0;
+  while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
+  const CamDev& cam = fd.cam[v];
+  const int lt = tile - cam.tile_base;
+  const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int qx = (warp & 1) * 8, qy = (warp >> 1) * 8;
+  const int lx = qx + (lane & 7), ly = qy + (lane >> 3);
+  const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
+  const uint2 rg = ranges[tile];
+  const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
+  const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+
+  PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
+  PixBwd q1 = q0;
+  if (px < cam.width && py0 < cam.height) {
+    const int64_t pix = cam.pix_base + static_cast<int64_t>(py0) * cam.width + px;
+    q0.T = final_T[pix];
+    q0.last = px_last[pix];
+    q0.gr = dL[3 * pix + 0];
+    q0.gg = dL[3 * pix + 1];
+    q0.gb = dL[3 * pix + 2];
+  }
+  if (px < cam.width && py1 < cam.height) {
+    const int64_t pix = cam.pix_base + static_cast<int64_t>(py1) * cam.width + px;
+    q1.T = final_T[pix];
+    q1.last = px_last[pix];
+    q1.gr = dL[3 * pix + 0];
+    q1.gg = dL[3 * pix + 1];
+    q1.gb = dL[3 * pix + 2];
+  }
+  const int slot = reduce9_slot(lane);
+  uint32_t wlast = max(q0.last, q1.last);  // warp-uniform upper bound of k
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) wlast = max(wlast, __shfl_xor_sync(kFull, wlast, k));
+
+  if (tid == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  int b0 = ((nproc - 1) / 256) * 256;
+  issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(256, nproc - b0), tid, 128);
+  for (; b0 >= 0; b0 -= 256) {
+    const int nb = min(256, nproc - b0);
+    mbar_wait(&s_bar, phase);
+    phase ^= 1;
+    for (int k = tid; k < nb; k += 128) {
+      const SplatRec& r = s_raw[k];
+      float4 a, b;
+      float c;
+      stage_splat(r, ox, oy, a, b, c);
+      s_a[k] = a;
+      s_b[k] = b;
+      s_n[k] = make_float4(static_cast<float>(r.ca), static_cast<float>(r.cb),
+                           static_cast<float>(r.cc), c);
+      s_io[k] = 1.0f / r.opac;
+      s_r[k] = local_rect(r, tx * kTile, ty * kTile);
+    }
+    __syncthreads();
+    if (b0 > 0) {
+      fence_proxy_async_smem();
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - 256, 256, tid, 128);
+    }
+    for (int se = nb; se > 0; se -= 32) {
+      const int ss = se > 32 ? se - 32 : 0;
+      for (int j = se - 1; j >= ss; --j) {
+        const uint32_t k = static_cast<uint32_t>(b0 + j);
+        float red = 0.0f;
+        if (k < wlast && quad_hit(s_r[j], qx, qy)) {  // warp-uniform skip
+          float o[9];
+#pragma unroll
+          for (int u = 0; u < 9; ++u) o[u] = 0.0f;
+          const float4 a = s_a[j];
+          const float4 b = s_b[j];
+          const float4 nc = s_n[j];
+          const float io = s_io[j];
+          const float dx = a.x + flx;
+          const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
+          const float t0 = a.z * dx * dx, t1 = a.w * dx;
+          const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
+          const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
+          bool any = bwd_pixel(q0, k, al0, b, nc, io, dx, dy0, o);
+          any = bwd_pixel(q1, k, al1, b, nc, io, dx, dy1, o) || any;
+          // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
+          if (__any_sync(kFull, any)) red = warp_reduce9(o);
+        }
+        if (slot >= 0) s_red[warp][j - ss][slot] = red;
+      }
+      __syncthreads();
+      const int cnt = (se - ss) * 9;
+      for (int e = tid; e < cnt; e += 128) {
+        const int jj = e / 9, u = e - jj * 9;
+        const float acc = (s_red[0][jj][u] + s_red[1][jj][u]) + (s_red[2][jj][u] + s_red[3][jj][u]);
+        partials[(static_cast<int64_t>(rg.x) + b0 + ss + jj) * 9 + u] = acc;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
+                      float* image, float* final_T, int32_t* counts, cudaStream_t st) {
+  CGS_PROFILED("raster_fwd_kernel", st,
+               raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.ranges, vals, L.recs, L.hdr,
+                                                                 image, final_T, counts, L.px_last,
+                                                                 L.tile_nproc));
+  CGS_CHECK_LAUNCH("raster_fwd_kernel");
+  return CGS_OK;
+}
+
+int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
+                      const float* dL, float* partials, cudaStream_t st) {
+  CGS_PROFILED("raster_bwd_kernel", st,
+               raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.ranges, sorted_pair_vals(L),
+                                                                 L.recs, L.hdr, L.px_last,
+                                                                 L.tile_nproc, final_T, dL, partials));
+  CGS_CHECK_LAUNCH("raster_bwd_kernel");
+  return CGS_OK;
+}
+
+}  // namespace cgs

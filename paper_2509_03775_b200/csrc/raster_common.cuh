@@ -49,6 +49,36 @@ __device__ __forceinline__ void sh_basis(double x, double y, double z, double* o
   }
 }
 
+// fp32 twin of sh_basis (codebook-gradient reduction, where the inputs are
+// fp32 already and the sum is accumulated in fp64).
+template <int DEG>
+__device__ __forceinline__ void sh_basis_f(float x, float y, float z, float* o) {
+  o[0] = static_cast<float>(kC0);
+  if constexpr (DEG >= 1) {
+    o[1] = static_cast<float>(-kC1) * y;
+    o[2] = static_cast<float>(kC1) * z;
+    o[3] = static_cast<float>(-kC1) * x;
+  }
+  if constexpr (DEG >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    o[4] = static_cast<float>(kC2_0) * x * y;
+    o[5] = static_cast<float>(kC2_1) * y * z;
+    o[6] = static_cast<float>(kC2_2) * (2.0f * zz - xx - yy);
+    o[7] = static_cast<float>(kC2_3) * x * z;
+    o[8] = static_cast<float>(kC2_4) * (xx - yy);
+  }
+  if constexpr (DEG >= 3) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    o[9] = static_cast<float>(kC3_0) * y * (3.0f * xx - yy);
+    o[10] = static_cast<float>(kC3_1) * x * y * z;
+    o[11] = static_cast<float>(kC3_2) * y * (4.0f * zz - xx - yy);
+    o[12] = static_cast<float>(kC3_3) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    o[13] = static_cast<float>(kC3_4) * x * (4.0f * zz - xx - yy);
+    o[14] = static_cast<float>(kC3_5) * z * (xx - yy);
+    o[15] = static_cast<float>(kC3_6) * x * (xx - 3.0f * yy);
+  }
+}
+
 // Single SH basis function b at direction (x,y,z) (runtime index).
 __device__ __forceinline__ double sh_basis_one(int b, double x, double y, double z) {
   const double xx = x * x, yy = y * y, zz = z * z;
@@ -168,6 +198,58 @@ __device__ __forceinline__ int reduce9_slot(int lane) {
   constexpr unsigned kMask = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 8) | (1u << 10) |
                              (1u << 16) | (1u << 18) | (1u << 20) | (1u << 24);
   return ((kMask >> lane) & 1u) ? __popc(kMask & ((1u << lane) - 1u)) : -1;
+}
+
+// ---- bulk-copy (TMA engine) staging helpers, sm_90+/sm_100a PTX ------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Order earlier generic-proxy accesses of shared memory before later
+// async-proxy (bulk copy) writes to it.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 1-D bulk copy global -> shared (UBLKCP), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Bulk-copy records [first, first + nb) of a tile list into s_raw (all threads
+// of the CTA call it; thread 0 posts the expected byte count).
+__device__ __forceinline__ void issue_records(SplatRec* s_raw, uint64_t* bar,
+                                              const uint32_t* __restrict__ pair_vals,
+                                              const SplatRec* __restrict__ recs, uint32_t first,
+                                              int nb, int tid, int nthreads) {
+  if (tid == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nb) * sizeof(SplatRec));
+  for (int k = tid; k < nb; k += nthreads)
+    bulk_g2s(&s_raw[k], &recs[pair_vals[first + k]], sizeof(SplatRec), bar);
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {

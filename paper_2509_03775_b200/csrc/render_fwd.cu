@@ -3,12 +3,14 @@
 //   sr_precompute   Sigma3 per SR codebook row (render.py:85-91, 168-169)
 //   project         per (view, Gaussian): fp64 EWA projection, codebook gather,
 //                   SH colour, pixel/tile rect, depth key (render.py:145-203,110-115)
-//   compact + sort  on-screen splats, stable onesweep on fp64 depth bits
-//                   (= np.lexsort((idx, tz)), render.py:203)
-//   emit + sort     (tile, splat) pairs in depth order, stable sort by tile id
-//                   (= per-tile append order of _bin_tiles, render.py:240-254)
-//   raster_fwd      one 256-thread CTA per 16x16 tile, front-to-back blend with
-//                   tile-level early exit (render.py:265-311)
+//   pair offsets    one decoupled-lookback scan over the splats' tile counts
+//   emit + sort     (tile, splat) pairs in splat index order, stable onesweep
+//                   radix sort by tile id
+//   tile sort       per tile, stable sort by fp64 camera depth -- together with
+//                   the stable tile sort this is exactly the per-tile append
+//                   order of _bin_tiles over np.lexsort((idx, tz))
+//                   (render.py:203, 240-254)
+//   raster_fwd      raster.cu
 #include <cmath>
 
 #include "frame.cuh"
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
       sm0[k] = S[k * 3 + 0] * m0[0] + S[k * 3 + 1] * m0[1] + S[k * 3 + 2] * m0[2];
       sm1[k] = S[k * 3 + 0] * m1[0] + S[k * 3 + 1] * m1[1] + S[k * 3 + 2] * m1[2];
     }
+    // Sigma2 = M Sigma3 M^T + 0.3 I (render.py:171-174)
     const double a = m0[0] * sm0[0] + m0[1] * sm0[1] + m0[2] * sm0[2] + kBlur;
     const double b = m0[0] * sm1[0] + m0[1] * sm1[1] + m0[2] * sm1[2];
     const double c = m1[0] * sm1[0] + m1[1] * sm1[1] + m1[2] * sm1[2] + kBlur;
@@ -131,7 +134,9 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
     // view direction and SH colour (render.py:187-198)
     double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
     const double len = sqrt((ox * ox + oy * oy) + oz * oz);
-    ox /= len; oy /= len; oz /= len;
+    ox /= len;
+    oy /= len;
+    oz /= len;
     double B[NB];
     sh_basis<DEG>(ox, oy, oz, B);
     const float* row = in.sh_rows + static_cast<int64_t>(in.g2sh[i]) * D;
@@ -155,14 +160,17 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
     SplatRec rec;
     rec.mx = mx;
     rec.my = my;
-    rec.ca = c / det;
+    rec.ca = c / det;  // conic = adj(Sigma2) / det (render.py:176-181)
     rec.cb = -b / det;
     rec.cc = a / det;
-    rec.opac = 1.0 / (1.0 + exp(-static_cast<double>(in.logit[i])));
+    rec.opac = static_cast<float>(1.0 / (1.0 + exp(-static_cast<double>(in.logit[i]))));
     rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
     rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
     rec.b = static_cast<float>(fmax(col[2] + 0.5, 0.0));
-    rec.rect = 0u;
+    rec.px0 = static_cast<uint16_t>(x0);
+    rec.px1 = static_cast<uint16_t>(x1);
+    rec.py0 = static_cast<uint16_t>(y0);
+    rec.py1 = static_cast<uint16_t>(y1);
     out.recs[s] = rec;
     out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
     out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
@@ -172,30 +180,23 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
 }
 
 // ---------------------------------------------------------------------------
-struct CompactOnscreen {
-  const uint32_t* n_tiles;
-  const uint64_t* depth;
-  uint64_t* keys;
-  uint32_t* vals;
-  __device__ uint64_t load(int64_t i) const { return n_tiles[i] > 0 ? 1ULL : 0ULL; }
-  __device__ void store(int64_t i, uint64_t ex, uint64_t v) const {
-    if (v) {
-      keys[ex] = depth[i];
-      vals[ex] = static_cast<uint32_t>(i);
-    }
-  }
-};
-
+// Pair offsets in splat index order.  One scan carries both the pair count
+// (low 40 bits) and the on-screen splat count (high bits).
 struct PairOffsets {
-  const uint32_t* sorted;
   const uint32_t* n_tiles;
   uint64_t* off;
-  __device__ uint64_t load(int64_t j) const { return n_tiles[sorted[j]]; }
-  __device__ void store(int64_t j, uint64_t ex, uint64_t) const { off[j] = ex; }
+  __device__ uint64_t load(int64_t s) const {
+    const uint64_t c = n_tiles[s];
+    return c | (c ? (1ULL << 40) : 0ULL);
+  }
+  __device__ void store(int64_t s, uint64_t ex, uint64_t) const { off[s] = ex & ((1ULL << 40) - 1); }
 };
 
 __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views) {
-  const unsigned long long raw = hdr->n_pairs_raw;
+  const unsigned long long packed = hdr->scratch[0];
+  const unsigned long long raw = packed & ((1ULL << 40) - 1);
+  hdr->n_onscreen = packed >> 40;
+  hdr->n_pairs_raw = raw;
   const bool over = raw > static_cast<unsigned long long>(pair_cap);
   hdr->n_pairs = over ? 0ULL : raw;
   hdr->stats.n_onscreen = static_cast<int64_t>(hdr->n_onscreen);
@@ -205,26 +206,24 @@ __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n
   hdr->stats.n_views = n_views;
 }
 
-// Warp-cooperative pair emission: a warp takes 32 consecutive splats in depth
-// order and writes their concatenated pair range with all 32 lanes, so a
-// near-plane splat covering every tile does not serialise one thread.
+// Warp-cooperative pair emission in splat index order: a warp takes 32
+// consecutive splats and writes their concatenated pair range with all 32
+// lanes (a near-plane splat covering every tile does not serialise a thread).
+// Within one splat, tiles are emitted row-major over its tile rect.
 template <typename KT>
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
-    const uint32_t* __restrict__ sorted, const uint64_t* __restrict__ off,
-    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
-    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, KT* __restrict__ keys,
-    uint32_t* __restrict__ vals) {
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ n_tiles,
+    const uint64_t* __restrict__ rect, const FrameHeader* __restrict__ hdr, FrameDesc fd,
+    int64_t n, int64_t vn, KT* __restrict__ keys, uint32_t* __restrict__ vals) {
   if (hdr->stats.overflow) return;
-  const int64_t ns = static_cast<int64_t>(hdr->n_onscreen);
   const int lane = threadIdx.x & 31;
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-       w * 32 < ns; w += warps) {
-    const int64_t j = w * 32 + lane;
-    const bool ok = j < ns;
-    const uint32_t s = ok ? sorted[j] : 0u;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w * 32 < vn;
+       w += warps) {
+    const int64_t s = w * 32 + lane;
+    const bool ok = s < vn;
     const uint64_t cnt = ok ? n_tiles[s] : 0ULL;
-    uint64_t o = ok ? off[j] : ~0ULL;
+    const uint64_t o = ok ? off[s] : ~0ULL;
     uint64_t e = ok ? o + cnt : 0ULL;
 #pragma unroll
     for (int k = 16; k > 0; k >>= 1) {
@@ -232,7 +231,8 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
       e = t > e ? t : e;
     }
     const uint64_t start = __shfl_sync(kFull, o, 0);
-    const uint64_t rc = ok ? rect[s] : 0ULL;
+    if (start >= e) continue;  // no pairs in this group of splats
+    const uint64_t rc = (ok && cnt) ? rect[s] : 0ULL;
     const int v = ok ? static_cast<int>(s / n) : 0;
     const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
     const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
@@ -254,12 +254,11 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
       const int by = __shfl_sync(kFull, ty0, owner);
       const int nt = __shfl_sync(kFull, ntx, owner);
       const int tb = __shfl_sync(kFull, tbase, owner);
-      const uint32_t sid = __shfl_sync(kFull, s, owner);
       if (p < e) {
         const int k = static_cast<int>(p - oo);
         const int ty = by + k / sp, tx = bx + k % sp;
         keys[p] = static_cast<KT>(tb + ty * nt + tx);
-        vals[p] = sid;
+        vals[p] = static_cast<uint32_t>(w * 32 + owner);
       }
     }
   }
@@ -279,114 +278,211 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const KT* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Forward raster: 256 threads = 16x16 pixels of one tile.  Splats are staged
-// 256 at a time into shared memory (fp64 record -> tile-relative fp32
-// offsets), the next batch's records are prefetched into registers while
-// the current batch is blended, and the CTA exits as soon as every pixel's
-// transmittance is below 1e-4.
-__global__ void __launch_bounds__(256) raster_fwd_kernel(
-    FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
-    const SplatRec* __restrict__ recs, const FrameHeader* __restrict__ hdr,
-    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ counts,
-    uint32_t* __restrict__ px_last, uint32_t* __restrict__ tile_nproc) {
-  __shared__ float4 s_a[256];
-  __shared__ float4 s_b[256];
-  __shared__ float s_c[256];
-  __shared__ uint32_t s_max[8];
+// Per-tile depth order.  After the stable tile sort each tile's list holds
+// its splats in index order; a stable sort by depth then reproduces
+// np.lexsort((idx, tz)) restricted to the tile (render.py:203, 247-253).
+// Lists up to kTileSortCap are sorted in shared memory: a 4-pass stable LSD
+// radix on a 32-bit key (the fp64 depth rounded toward zero to fp32, which
+// is monotone), then runs of equal 32-bit keys -- rare -- are re-sorted by
+// the exact fp64 key with a stable insertion sort.  Longer lists take a
+// stable in-CTA 8-pass radix on the fp64 bits through global scratch.  The
+// kernel also records inv[emission index] = final position for the backward.
+struct TileSortSmem {
+  uint32_t key[2][kTileSortCap];
+  uint32_t val[2][kTileSortCap];
+  uint32_t wcnt[8][256];  // (round tag << 16) | count
+  uint32_t base[256];
+};
+
+__device__ __forceinline__ uint32_t depth_key32(uint64_t bits) {
+  return __float_as_uint(__double2float_rz(__longlong_as_double(static_cast<long long>(bits))));
+}
+
+__global__ void __launch_bounds__(256) tile_depth_sort_kernel(
+    const uint2* __restrict__ ranges, uint32_t* __restrict__ vals,
+    const uint64_t* __restrict__ depth_key, const uint64_t* __restrict__ pair_off,
+    const uint64_t* __restrict__ rect, uint32_t* __restrict__ inv, uint32_t* __restrict__ scratch,
+    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSortSmem& S = *reinterpret_cast<TileSortSmem*>(smem_raw);
   if (hdr->stats.overflow) return;
   const int tile = blockIdx.x;
-  int v = 0;
-  while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
-  const CamDev& cam = fd.cam[v];
-  const int lt = tile - cam.tile_base;
-  const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
-  const int tid = threadIdx.x;
-  const int lx = tid & 15, ly = tid >> 4;
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = px < cam.width && py < cam.height;
   const uint2 rg = ranges[tile];
-  const int n = static_cast<int>(rg.y - rg.x);
-  const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
-  const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
-
-  float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-  int cnt = 0;
-  uint32_t last = 0;
-  bool done = !inside;
-  bool terminated = false;
-
-  SplatRec nxt;
-  if (tid < n) nxt = recs[pair_vals[rg.x + tid]];
-  for (int b0 = 0; b0 < n; b0 += 256) {
-    const int nb = min(256, n - b0);
-    if (tid < nb) {
-      float4 a, b;
-      float c;
-      stage_splat(nxt, ox, oy, a, b, c);
-      s_a[tid] = a;
-      s_b[tid] = b;
-      s_c[tid] = c;
+  const int len = static_cast<int>(rg.y - rg.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (len <= 0) return;
+  uint32_t* seg = vals + rg.x;
+  if (len <= kTileSortCap) {
+    for (int j = tid; j < len; j += 256) {
+      const uint32_t s = seg[j];
+      S.val[0][j] = s;
+      S.key[0][j] = depth_key32(depth_key[s]);
     }
-    __syncthreads();
-    if (b0 + 256 + tid < n) nxt = recs[pair_vals[rg.x + b0 + 256 + tid]];
-    if (!done) {
-      for (int j = 0; j < nb; ++j) {
-        const float4 a = s_a[j];
-        const float4 b = s_b[j];
-        const float dx = a.x + flx, dy = a.y + fly;
-        const float al = splat_alpha(a, b, dx, dy);
-        if (al >= kAlphaSkipF) {
-          const float w = al * T;
-          cr = fmaf(w, b.z, cr);
-          cg = fmaf(w, b.w, cg);
-          cb = fmaf(w, s_c[j], cb);
-          T = T * (1.0f - al);
-          ++cnt;
-          if (!(T >= kTMinF)) {
-            done = true;
-            terminated = true;
-            last = static_cast<uint32_t>(b0 + j + 1);
-            break;
+    for (int q = tid; q < 8 * 256; q += 256) (&S.wcnt[0][0])[q] = 0xffff0000u;
+    int cur = 0;
+    uint32_t round = 0;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 8 * pass;
+      S.base[tid] = 0;
+      __syncthreads();
+      // histogram with warp-aggregated shared atomics
+      for (int c0 = 0; c0 < len; c0 += 256) {
+        const int j = c0 + tid;
+        const unsigned d = j < len ? (S.key[cur][j] >> shift) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(kFull, d);
+        if (j < len && lane == __ffs(peers) - 1) atomicAdd(&S.base[d], __popc(peers));
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of 256 counts, 8 per lane
+        uint32_t c[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          c[k] = S.base[lane * 8 + k];
+          sum += c[k];
+        }
+        const uint32_t inc = warp_incl_scan(sum);
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          S.base[lane * 8 + k] = run;
+          run += c[k];
+        }
+      }
+      __syncthreads();
+      for (int c0 = 0; c0 < len; c0 += 256, ++round) {
+        const int j = c0 + tid;
+        const bool ok = j < len;
+        const uint32_t key = ok ? S.key[cur][j] : 0u;
+        const uint32_t val = ok ? S.val[cur][j] : 0u;
+        const unsigned d = ok ? (key >> shift) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(kFull, d);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        const uint32_t tag = round << 16;
+        if (ok && lane == __ffs(peers) - 1) S.wcnt[warp][d] = tag | __popc(peers);
+        __syncthreads();
+        if (ok) {
+          uint32_t before = 0;
+          for (int w2 = 0; w2 < warp; ++w2) {
+            const uint32_t v = S.wcnt[w2][d];
+            before += (v & 0xffff0000u) == tag ? (v & 0xffffu) : 0u;
           }
+          const uint32_t pos = S.base[d] + before + rank;
+          S.key[cur ^ 1][pos] = key;
+          S.val[cur ^ 1][pos] = val;
+        }
+        __syncthreads();
+        {
+          uint32_t add = 0;
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) {
+            const uint32_t v = S.wcnt[w2][tid];
+            add += (v & 0xffff0000u) == tag ? (v & 0xffffu) : 0u;
+          }
+          S.base[tid] += add;
+        }
+        __syncthreads();
+      }
+      cur ^= 1;
+    }
+    // exact order inside runs of equal 32-bit keys (stable insertion sort on fp64 bits)
+    for (int j = tid; j < len; j += 256) {
+      const uint32_t k = S.key[cur][j];
+      if ((j == 0 || S.key[cur][j - 1] != k) && j + 1 < len && S.key[cur][j + 1] == k) {
+        int e = j + 1;
+        while (e < len && S.key[cur][e] == k) ++e;
+        for (int a = j + 1; a < e; ++a) {
+          const uint32_t va = S.val[cur][a];
+          const uint64_t ka = depth_key[va];
+          int b = a - 1;
+          while (b >= j && depth_key[S.val[cur][b]] > ka) {
+            S.val[cur][b + 1] = S.val[cur][b];
+            --b;
+          }
+          S.val[cur][b + 1] = va;
         }
       }
     }
-    if (__syncthreads_count(done) == 256) break;
+    __syncthreads();
+    for (int j = tid; j < len; j += 256) {
+      const uint32_t s = S.val[cur][j];
+      seg[j] = s;
+      inv[emission_index(pair_off, rect, fd, n, s, tile)] = rg.x + j;
+    }
+    return;
   }
-  if (inside && !terminated) last = static_cast<uint32_t>(n);
-  if (inside) {
-    const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
-    image[3 * pix + 0] = cr;
-    image[3 * pix + 1] = cg;
-    image[3 * pix + 2] = cb;
-    final_T[pix] = T;
-    counts[pix] = cnt;
-    px_last[pix] = last;
+  // long list: stable LSD radix over the 64-bit depth key, ping-ponging
+  // between the list and its scratch slice; 256-element chunks ranked with
+  // warp match_any so equal digits keep their order.
+  uint32_t* cnt = S.base;
+  uint32_t* wcnt = &S.wcnt[0][0];
+  uint32_t* src = seg;
+  uint32_t* dst = scratch + rg.x;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 8 * pass;
+    cnt[tid] = 0;
+    __syncthreads();
+    for (int j = tid; j < len; j += 256) atomicAdd(&cnt[(depth_key[src[j]] >> shift) & 255u], 1u);
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (int d = 0; d < 256; ++d) {
+        const uint32_t c = cnt[d];
+        cnt[d] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < len; c0 += 256) {
+      const int j = c0 + tid;
+      const bool ok = j < len;
+      const uint32_t s = ok ? src[j] : 0u;
+      const unsigned d = ok ? static_cast<unsigned>((depth_key[s] >> shift) & 255u) : 256u + lane;
+      for (int q = tid; q < 8 * 256; q += 256) wcnt[q] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(kFull, d);
+      const uint32_t rank = __popc(peers & lanemask_lt());
+      if (ok && lane == __ffs(peers) - 1) wcnt[warp * 256 + d] = __popc(peers);
+      __syncthreads();
+      if (ok) {
+        uint32_t before = 0;
+        for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2 * 256 + d];
+        dst[cnt[d] + before + rank] = s;
+      }
+      __syncthreads();
+      {
+        uint32_t add = 0;
+        for (int w2 = 0; w2 < 8; ++w2) add += wcnt[w2 * 256 + tid];
+        cnt[tid] += add;
+      }
+      __syncthreads();
+    }
+    uint32_t* t = src;
+    src = dst;
+    dst = t;
   }
-  uint32_t m = last;
-#pragma unroll
-  for (int k = 16; k > 0; k >>= 1) m = max(m, __shfl_xor_sync(kFull, m, k));
-  if ((tid & 31) == 0) s_max[tid >> 5] = m;
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t mm = 0;
-    for (int w = 0; w < 8; ++w) mm = max(mm, s_max[w]);
-    tile_nproc[tile] = mm;
-  }
+  // 8 passes: the result is back in seg
+  for (int j = tid; j < len; j += 256)
+    inv[emission_index(pair_off, rect, fd, n, seg[j], tile)] = rg.x + j;
 }
 
 // ---------------------------------------------------------------------------
 template <int DEG>
 static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut& out,
                            int64_t vn, cudaStream_t st) {
-  CGS_PROFILED("project_kernel", st, project_kernel<DEG><<<grid_for(vn, 256, 16), 256, 0, st>>>(in, fd, out));
+  CGS_PROFILED("project_kernel", st,
+               project_kernel<DEG><<<grid_for(vn, 256, 16), 256, 0, st>>>(in, fd, out));
 }
 
 template <typename KT>
-static int sort_and_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
-                          cudaStream_t st) {
+static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws, cudaStream_t st) {
   KT* kres;
   uint32_t* vres;
+  const int eg = grid_for(L.vn, 256, 16);
+  CGS_PROFILED("emit_pairs_kernel", st,
+               emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
+                                                          L.n, L.vn, static_cast<KT*>(L.pkeys),
+                                                          L.pvals));
+  CGS_CHECK_LAUNCH("emit_pairs_kernel");
   int rc = launch_radix_sort<KT>(static_cast<KT*>(L.pkeys), L.pvals, &L.hdr->n_pairs, 0,
                                  L.pair_cap, L.tile_key_bits, ws, &kres, &vres, st);
   if (rc) return rc;
@@ -401,8 +497,9 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   const int64_t vn = L.vn;
   CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
   if (sc->sr_capacity > 0) {
-    CGS_PROFILED("sr_precompute_kernel", st, sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(sc->sr_rows,
-                                                                            sc->sr_capacity, sr_cov));
+    CGS_PROFILED("sr_precompute_kernel", st,
+                 sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(
+                     sc->sr_rows, sc->sr_capacity, sr_cov));
     CGS_CHECK_LAUNCH("sr_precompute_kernel");
   }
   if (vn > 0) {
@@ -416,37 +513,30 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
     }
     CGS_CHECK_LAUNCH("project_kernel");
   }
-  int rc = launch_scan(CompactOnscreen{L.n_tiles, L.depth_key, L.skeys, L.svals}, nullptr, vn, vn,
-                       L.scan, &L.hdr->n_onscreen, st);
-  if (rc) return rc;
-  uint64_t* dk;
-  uint32_t* dv;
-  rc = launch_radix_sort<uint64_t>(L.skeys, L.svals, &L.hdr->n_onscreen, 0, vn, 64, L.dsort, &dk,
-                                   &dv, st);
-  if (rc) return rc;
-  rc = launch_scan(PairOffsets{dv, L.n_tiles, L.pair_off}, &L.hdr->n_onscreen, 0, vn, L.scan,
-                   &L.hdr->n_pairs_raw, st);
+  int rc = launch_scan(PairOffsets{L.n_tiles, L.pair_off}, nullptr, vn, vn, L.scan,
+                       &L.hdr->scratch[0], st);
   if (rc) return rc;
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
-  const int eg = grid_for(vn, 256, 16);
-  if (L.tile_key_bytes == 2) {
-    CGS_PROFILED("emit_pairs_kernel", st, emit_pairs_kernel<uint16_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
-                                                    L.n, static_cast<uint16_t*>(L.pkeys), L.pvals));
-    CGS_CHECK_LAUNCH("emit_pairs_kernel");
-    rc = sort_and_range<uint16_t>(L, fd, L.psort16, st);
-  } else {
-    CGS_PROFILED("emit_pairs_kernel", st, emit_pairs_kernel<uint32_t><<<eg, 256, 0, st>>>(dv, L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
-                                                    L.n, static_cast<uint32_t*>(L.pkeys), L.pvals));
-    CGS_CHECK_LAUNCH("emit_pairs_kernel");
-    rc = sort_and_range<uint32_t>(L, fd, L.psort32, st);
-  }
+  rc = L.tile_key_bytes == 2 ? emit_sort_range<uint16_t>(L, fd, L.psort16, st)
+                             : emit_sort_range<uint32_t>(L, fd, L.psort32, st);
   if (rc) return rc;
   if (fd.total_tiles > 0) {
-    CGS_PROFILED("raster_fwd_kernel", st, raster_fwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.ranges, sorted_pair_vals(L), L.recs,
-                                                      L.hdr, image, final_T, counts, L.px_last,
-                                                      L.tile_nproc));
-    CGS_CHECK_LAUNCH("raster_fwd_kernel");
+    static bool attr = false;
+    const int smem = static_cast<int>(sizeof(TileSortSmem));
+    if (!attr) {
+      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    uint32_t* vals = sorted_pair_vals(L);
+    CGS_PROFILED("tile_depth_sort_kernel", st,
+                 tile_depth_sort_kernel<<<fd.total_tiles, 256, smem, st>>>(
+                     L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr, fd,
+                     L.n));
+    CGS_CHECK_LAUNCH("tile_depth_sort_kernel");
+    rc = launch_raster_fwd(fd, L, vals, image, final_T, counts, st);
+    if (rc) return rc;
   }
   return CGS_OK;
 }

@@ -320,14 +320,26 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     st_volatile(st, kSortPre | agg);
   } else {
     st_volatile(st, kSortAgg | agg);
+    // Windowed lookback: 8 independent status loads per round trip, consumed
+    // in order until an inclusive prefix is found (an unpublished slot makes
+    // the next window start there).
     int64_t p = part - 1;
-    while (true) {
-      const uint32_t s = ld_volatile(status + p * 256 + d);
-      const uint32_t flag = s >> 30;
-      if (flag == 0) continue;
-      excl += s & kSortVal;
-      if (flag == 2) break;
-      --p;
+    bool done = false;
+    while (!done) {
+      uint32_t s[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] = (p - k >= 0) ? ld_volatile(status + (p - k) * 256 + d) : kSortPre;
+      int k = 0;
+      for (; k < 8; ++k) {
+        const uint32_t flag = s[k] >> 30;
+        if (flag == 0) break;
+        excl += s[k] & kSortVal;
+        if (flag == 2) {
+          done = true;
+          break;
+        }
+      }
+      p -= k;
     }
     st_volatile(st, kSortPre | (excl + agg));
   }

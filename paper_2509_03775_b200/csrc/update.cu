@@ -42,6 +42,7 @@ struct SgldDev {
   double gscale;
   uint64_t seed, offset;
   int noise_src;
+  const uint64_t* offset_dev;
 };
 
 __device__ __forceinline__ float sgld_one(float v, float g, double c, double k, double gscale,
@@ -61,7 +62,8 @@ __global__ void __launch_bounds__(256) finite_check_kernel(const float* __restri
                                                            const float* __restrict__ b, int64_t nb,
                                                            const float* __restrict__ c, int64_t nc,
                                                            const float* __restrict__ d, int64_t nd,
-                                                           int32_t* flags) {
+                                                           int32_t* flags, uint64_t* ctr) {
+  if (ctr && blockIdx.x == 0 && threadIdx.x == 0) *ctr += 1;  // noise offset for this update
   const int64_t tot = na + nb + nc + nd;
   bool bad = false;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(256) sgld_kernel(
     const double* __restrict__ nlog, const double* __restrict__ nsh,
     const double* __restrict__ nsr, const int32_t* __restrict__ flags) {
   if (flags[0]) return;  // non-finite gradients: reject before any mutation
+  const uint64_t offset = p.offset_dev ? *p.offset_dev : p.offset;
   const int64_t a = p.on_pos ? 3 * n : 0;
   const int64_t b = p.on_op ? n : 0;
   const int64_t c = p.on_sh ? n_sh * D : 0;
@@ -94,17 +97,17 @@ __global__ void __launch_bounds__(256) sgld_kernel(
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (i < a) {
       pos[i] = sgld_one(pos[i], gpos[i], p.c_pos, p.k_pos, p.gscale, npos, i, p.noise_src, p.seed,
-                        p.offset, 0);
+                        offset, 0);
     } else if (i < a + b) {
       const int64_t j = i - a;
       logit[j] = sgld_one(logit[j], glogit[j], p.c_op, p.k_op, p.gscale, nlog, j, p.noise_src,
-                          p.seed, p.offset, 1);
+                          p.seed, offset, 1);
     } else if (i < a + b + c) {
       const int64_t j = i - a - b;
       const int64_t li = j / D, col = j - li * D;
       const int64_t e = static_cast<int64_t>(sh_live[li]) * D + col;
       sh[e] = sgld_one(sh[e], gsh[e], p.c_sh, p.k_sh, p.gscale, nsh, j, p.noise_src, p.seed,
-                       p.offset, 2);
+                       offset, 2);
     } else {
       const int64_t li = i - a - b - c;
       const int64_t r = sr_live[li];
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(256) sgld_kernel(
         double nv = __dsub_rn(static_cast<double>(sr[r * 7 + k]), __dmul_rn(p.c_sr, gg));
         if (p.k_sr != 0.0) {
           const double eta = p.noise_src == 1 ? nsr[li * 7 + k]
-                                              : philox_normal(p.seed, p.offset, 3, li * 7 + k);
+                                              : philox_normal(p.seed, offset, 3, li * 7 + k);
           nv = __dadd_rn(nv, __dmul_rn(p.k_sr, eta));
         }
         v[k] = nv;
@@ -143,7 +146,7 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
   CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
   const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
   CGS_PROFILED("finite_check_kernel", st, finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
-                                                                          nc, gsr, nd, flags));
+                                                                          nc, gsr, nd, flags, hp->offset_dev));
   CGS_CHECK_LAUNCH("finite_check_kernel");
   SgldDev p{};
   // exactly numpy's scalar sub-expressions: 0.5 * eps and mult * sqrt(eps)
@@ -163,6 +166,7 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
   p.seed = hp->seed;
   p.offset = hp->offset;
   p.noise_src = hp->noise_source;
+  p.offset_dev = hp->offset_dev;
   if (p.noise_src == 1) {
     if ((p.k_pos != 0.0 && !npos) || (p.k_op != 0.0 && !nlog) || (p.k_sh != 0.0 && !nsh) ||
         (p.k_sr != 0.0 && !nsr)) {

@@ -25,7 +25,7 @@ import torch
 from . import _native as nat
 from .metrics import LossWorkspace
 from .model import ModelState, densify
-from .render import Frame, GradientSet
+from .render import Frame, GradientSet, backward_workspace_bytes
 from .sampler import (SamplerConfig, SamplerError, TransitionRecord, merge_step, sgld_update,
                       split_step)
 
@@ -33,7 +33,7 @@ from .sampler import (SamplerConfig, SamplerError, TransitionRecord, merge_step,
 class Trainer:
     def __init__(self, state: ModelState, cams, gts: torch.Tensor, config: SamplerConfig,
                  rng: np.random.Generator, mcmc_every: int = 25, world: int = 1,
-                 pair_headroom: float = 1.5, allreduce=None):
+                 pair_headroom: float = 1.5, allreduce=None, use_graphs: bool = False):
         self.state = state
         self.cams = list(cams)
         self.config = config
@@ -60,6 +60,11 @@ class Trainer:
         self.mcmc_events = 0
         self.mcmc_ms = []
         self.last_loss = None
+        self.use_graphs = use_graphs
+        self.noise_ctr = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        self._gkey = None
+        self._g_fwd = self._g_sgld = None
+        self.captures = 0
 
     # -- buffers ---------------------------------------------------------------
     def _prepare(self):
@@ -70,31 +75,78 @@ class Trainer:
                 probe = Frame(st, self.cams).run_checked()
                 self.pair_cap = int(probe.stats().n_pairs * self.headroom) + 4096
             self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap)
-            nb = nat.library().cgs_backward_workspace_bytes(st.num_gaussians, self.frame.c_cams,
-                                                            self.V, self.pair_cap)
-            self.bws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
             self.dL = torch.empty_like(self.frame.image)
+        nb = backward_workspace_bytes(st, self.frame)
+        if self.bws is None or self.bws.numel() < nb:
+            self.bws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
         g = self.grads
         if (g is None or g.positions.shape[0] != st.num_gaussians
                 or g.sh_rows.shape[0] != st.sh.capacity or g.sr_rows.shape[0] != st.sr.capacity):
             self.grads = GradientSet.empty(st)
 
     # -- transitions -------------------------------------------------------------
-    def update(self):
-        """SGLD update over the view batch (device only)."""
-        self._prepare()
-        st = self.state
+    # The update is enqueued in three parts: forward + loss, backward, SGLD.
+    # With graphs on, the forward and SGLD parts are replayed from CUDA graphs
+    # (re-captured whenever a buffer address or size they baked in changes);
+    # the backward stays an eager C-ABI call so the profiled raster kernel
+    # is bracketed by live CUDA events on its launch stream.
+    def _enqueue_forward(self):
         fr = self.frame
         fr.run()
         ov = fr.ws[40:44].view(torch.int32)  # cgs_frame_stats_t.overflow (byte 40)
         torch.maximum(self.sticky, ov, out=self.sticky)
-        losses = self.loss_ws.run(fr.image, self.gts, self.config.lambda_ssim, self.dL, 1.0)
-        fr.backward(self.dL, scale=1.0 / (self.V * self.world), grads=self.grads, ws=self.bws)
+        self.loss_ws.run(fr.image, self.gts, self.config.lambda_ssim, self.dL, 1.0)
+
+    def _enqueue_backward(self):
+        self.frame.backward(self.dL, scale=1.0 / (self.V * self.world), grads=self.grads,
+                            ws=self.bws)
         if self.allreduce is not None:
             self.allreduce(self.grads.flat)
-        sgld_update(st, self.grads, self.config, self.rng, flags=self.flags, check=False)
+
+    def _enqueue_sgld(self):
+        sgld_update(self.state, self.grads, self.config, self.rng, flags=self.flags, check=False,
+                    offset_dev=self.noise_ctr)
         torch.maximum(self.sticky, self.flags * 2, out=self.sticky)
-        self.last_loss = losses
+
+    def _graph_key(self):
+        st = self.state
+        g = st.gaussians
+        sl, rl = st.sh.device_live(), st.sr.device_live()
+        return (id(self.frame), id(self.grads), g.positions.data_ptr(), g.count,
+                g.g2sh.data_ptr(), g.g2sr.data_ptr(), st.sh.rows.data_ptr(), st.sr.rows.data_ptr(),
+                st.sh.capacity, st.sr.capacity, sl.data_ptr(), sl.numel(), rl.data_ptr(), rl.numel())
+
+    def _capture(self, fn):
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def update(self):
+        """SGLD update over the view batch (device only, no host synchronisation)."""
+        self._prepare()
+        self.state.code_csr("sh")
+        self.state.code_csr("sr")
+        if self.use_graphs:
+            key = self._graph_key()
+            if key != self._gkey:
+                self._enqueue_forward()
+                self._enqueue_backward()
+                self._enqueue_sgld()
+                self._g_fwd = self._capture(self._enqueue_forward)
+                self._g_sgld = self._capture(self._enqueue_sgld)
+                self._gkey = key
+                self.captures += 1
+            else:
+                self._g_fwd.replay()
+                self._enqueue_backward()
+                self._g_sgld.replay()
+        else:
+            self._enqueue_forward()
+            self._enqueue_backward()
+            self._enqueue_sgld()
+        self.last_loss = self.loss_ws.losses
         self.updates += 1
         self._advance()
 

@@ -304,6 +304,7 @@ class ModelState:
         self.iteration = iteration
         self.rng_seed = rng_seed
         self.mutations = 0
+        self.assign_version = 0
 
     @property
     def num_gaussians(self) -> int:
@@ -317,9 +318,37 @@ class ModelState:
     def device(self):
         return self.sh.device
 
-    def touch(self):
-        """Record an in-place mutation made by a kernel (staleness token)."""
+    def touch(self, assignments: bool = False):
+        """Record an in-place mutation made by a kernel (staleness token).
+
+        ``assignments`` marks a change of g2sh / g2sr (invalidates the code CSRs).
+        """
         self.mutations += 1
+        if assignments:
+            self.assign_version += 1
+
+    def code_csr(self, which: str):
+        """(offsets (cap+1,), members (N,)) int32 device CSR of one index array.
+
+        Cached; rebuilt (cgs_code_csr: one stable onesweep) only when the
+        assignments, N or the capacity changed.
+        """
+        from . import _native as nat
+        book, idx = _book_of(self, which)
+        key = (self.assign_version, idx.data_ptr(), idx._version, idx.shape[0], book.capacity)
+        cache = self.__dict__.setdefault("_csr", {})
+        hit = cache.get(which)
+        if hit is not None and hit[0] == key:
+            return hit[1], hit[2]
+        n, cap = idx.shape[0], book.capacity
+        off = torch.empty((cap + 1,), dtype=torch.int32, device=book.device)
+        mem = torch.empty((max(n, 1),), dtype=torch.int32, device=book.device)
+        nb = nat.library().cgs_code_csr_workspace_bytes(max(n, 1), cap)
+        ws = torch.empty((nb,), dtype=torch.uint8, device=book.device)
+        nat.call("cgs_code_csr", nat.ptr(idx), n, cap, nat.ptr(off), nat.ptr(mem), nat.ptr(ws),
+                 nb, nat.stream_handle(book.device))
+        cache[which] = (key, off, mem)
+        return off, mem
 
     def token(self) -> tuple:
         """Cheap identity of the state contents (replaces render.py:227-237's SHA-256)."""
@@ -413,7 +442,7 @@ def remap_gaussian(state: ModelState, i: int, which: str, new_row: int) -> None:
     book.incref(new_row)
     idx[i] = int(new_row)
     book.decref(old)
-    state.touch()
+    state.touch(assignments=True)
 
 
 def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Generator,
@@ -449,7 +478,7 @@ def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Gene
     np.add.at(state.sr.refcount, new_sr, 1)
     state.sh.mutations += 1
     state.sr.mutations += 1
-    state.touch()
+    state.touch(assignments=True)
     return k
 
 

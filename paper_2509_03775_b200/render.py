@@ -174,17 +174,25 @@ class Frame:
         dev = self.device
         if grads is None:
             grads = GradientSet.empty(st)
-        nb = nat.library().cgs_backward_workspace_bytes(self.n, self.c_cams, len(self.cams),
-                                                        self.pair_cap)
+        nb = backward_workspace_bytes(st, self)
         if ws is None or ws.numel() < nb:
             ws = torch.empty((nb,), dtype=torch.uint8, device=dev)
         self.scene = scene_struct(st)
+        sh_off, sh_mem = st.code_csr("sh")
+        sr_off, sr_mem = st.code_csr("sr")
         nat.call("cgs_render_backward", ctypes.byref(self.scene), self.c_cams, len(self.cams),
                  nat.ptr(self.ws), self.ws.numel(), self.pair_cap, nat.ptr(self.final_T),
-                 nat.ptr(dL), float(scale), nat.ptr(ws), ws.numel(), nat.ptr(grads.positions),
+                 nat.ptr(dL), float(scale), nat.ptr(sh_off), nat.ptr(sh_mem), nat.ptr(sr_off),
+                 nat.ptr(sr_mem), nat.ptr(ws), ws.numel(), nat.ptr(grads.positions),
                  nat.ptr(grads.opacity_logits), nat.ptr(grads.sh_rows), nat.ptr(grads.sr_rows),
                  nat.stream_handle(dev))
         return grads
+
+
+def backward_workspace_bytes(state: ModelState, frame: "Frame") -> int:
+    return nat.library().cgs_backward_workspace_bytes(frame.n, frame.c_cams, len(frame.cams),
+                                                      frame.pair_cap, state.sh.capacity,
+                                                      state.sr.capacity)
 
 
 @dataclass

@@ -217,7 +217,7 @@ def _apply_split_batch(state: ModelState, which: str, moves):
     nat.call("cgs_apply_splits", nat.ptr(book.rows), book.dim, nat.ptr(idx), nat.ptr(g), nat.ptr(o),
              nat.ptr(nw), nat.ptr(u), len(moves), nat.stream_handle(dev))
     book.mutations += 1
-    state.touch()
+    state.touch(assignments=True)
 
 
 def apply_split(state: ModelState, proposal: SplitProposal) -> int:
@@ -298,7 +298,7 @@ def _apply_remap(state: ModelState, which: str, remap: dict):
     t = torch.as_tensor(table).to(book.device)
     nat.call("cgs_apply_remap", nat.ptr(idx), state.num_gaussians, nat.ptr(t), len(table),
              nat.stream_handle(book.device))
-    state.touch()
+    state.touch(assignments=True)
 
 
 def apply_merge(state: ModelState, proposal: MergeProposal) -> None:
@@ -349,8 +349,13 @@ def _host_noise(state: ModelState, config: SamplerConfig, rng, n_sh_live, n_sr_l
 
 
 def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
-                rng: np.random.Generator, flags: torch.Tensor = None, check: bool = True) -> None:
-    """SGLD step per group (sampler.py:262-300) on the device."""
+                rng: np.random.Generator, flags: torch.Tensor = None, check: bool = True,
+                offset_dev: torch.Tensor = None) -> None:
+    """SGLD step per group (sampler.py:262-300) on the device.
+
+    ``offset_dev`` (int64 device counter) makes device-noise draws advance on
+    the device, so a captured CUDA graph of the update draws fresh noise on
+    every replay."""
     dev = state.device
     g = state.gaussians
     sh_live = state.sh.device_live()
@@ -358,6 +363,7 @@ def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
     if config.device_noise:
         noise = [None] * 4
         params = _sgld_params(config, 1.0, config.seed, state.iteration, 0)
+        params.offset_dev = nat.ptr(offset_dev)
     else:
         noise = _host_noise(state, config, rng, sh_live.numel(), sr_live.numel())
         params = _sgld_params(config, 1.0, 0, 0, 1)

@@ -1,6 +1,5 @@
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/bench3.json 2> gpurun_out/bench3.err; echo rc=$?
-tail -3 gpurun_out/bench3.err
-python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain3.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1b.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu3.log 2>&1; echo ncu=$?
+python -m pytest tests -m gpu -q -x 2>&1 | tail -4
+python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/bench7.json 2> gpurun_out/bench7.err; echo rc=$?
+tail -3 gpurun_out/bench7.err
+python scripts/host_profile.py --graphs 2>&1 | grep -E "span|raster_|tile_depth|pull_back|sh_code" | cut -c1-150
