@@ -243,7 +243,8 @@ def main():
     # the CPU baseline (initial scene) measure the same workload.
     cfg = cg.SamplerConfig(lambda_ssim=lam, device_noise=True, seed=args.seed,
                            noise_pos=args.noise_pos)
-    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else None
+    from paper_2509_03775_b200 import dist as cdist
+    allreduce = cdist.make_allreduce() if world > 1 else None
     rng = np.random.default_rng(args.seed)
     tr = Trainer(st, cams, gts, cfg, rng, mcmc_every=args.mcmc_every, world=world,
                  allreduce=allreduce, use_graphs=not args.no_graphs)
