@@ -380,7 +380,9 @@ def main():
                           "sgld_noise": f"device Philox, noise_pos={args.noise_pos} (reference default 1.0 "
                                         "diffuses the scene out of view; see DESIGN.md)",
                           "parallelism": f"dp{world} (views sharded, NCCL allreduce)"},
-               "mpix_per_s": mpix, "gpu_launches": launches, "roofline": roofline,
+               "mpix_per_s": mpix, "gpu_launches": launches,
+               "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms),
+                           "max": max(step_ms)}, "roofline": roofline,
                "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
                "frame": {"pairs": int(stats.n_pairs), "processed_pairs": P_x,
                          "touched": int(stats.n_touched), "onscreen": int(stats.n_onscreen)},

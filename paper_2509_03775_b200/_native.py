@@ -163,3 +163,17 @@ def ptr(t) -> int:
 def stream_handle(device=None) -> int:
     import torch
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def upload(a, device, dtype=None):
+    """Host array -> device tensor through pinned memory, enqueued on the current
+    stream without blocking the host (a pageable copy would wait for the
+    stream's queued work).  The caching host allocator keeps the pinned block
+    alive until the copy has completed."""
+    import numpy as np
+    import torch
+    arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    host = torch.from_numpy(arr)
+    if host.numel() == 0:
+        return torch.empty(host.shape, dtype=host.dtype, device=device)
+    return host.pin_memory().to(device, non_blocking=True)

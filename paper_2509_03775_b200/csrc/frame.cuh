@@ -27,6 +27,7 @@ struct FrameLayout {
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
   uint32_t* tile_nproc;    // total_tiles
+  uint32_t* tile_order;    // total_tiles: raster CTA -> tile, longest work first
   ScanWs scan;
   double* sr_cov;          // sr_cap * 8 (Sigma3 + zero-quaternion flag)
   size_t bytes;
@@ -100,6 +101,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.tile_order = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.scan = carve_scan(c, vn1 > fd.total_tiles ? vn1 : fd.total_tiles);
   L.sr_cov = c.take<double>((sr_cap > 0 ? sr_cap : 1) * 8);
   L.bytes = c.off + 256;

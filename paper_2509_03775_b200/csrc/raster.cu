@@ -7,6 +7,12 @@
 // outside the rect alpha < opacity / 255 < 1/255 by construction of the
 // footprint radius (render.py:32-34), so the skip changes no result.
 //
+// CTAs take tiles longest-work-first (tile_order_kernel): the block
+// scheduler hands out CTAs in blockIdx order as slots free up, so this is
+// greedy longest-processing-time scheduling of the uneven tile lists and the
+// last wave is made of short tiles.  Tiles are independent, so the order
+// changes no result.
+//
 // Splat records are gathered by the bulk-copy engine (cp.async.bulk, one
 // 64-byte record per copy, completion on an mbarrier) one batch of 256 ahead
 // of the blending, and converted once per batch to tile-relative fp32 form
@@ -27,6 +33,47 @@ __device__ __forceinline__ bool quad_hit(uint32_t rc, int qx, int qy) {
   const int x0 = static_cast<int8_t>(rc & 0xff), x1 = static_cast<int8_t>((rc >> 8) & 0xff);
   const int y0 = static_cast<int8_t>((rc >> 16) & 0xff), y1 = static_cast<int8_t>(rc >> 24);
   return x1 >= qx && x0 <= qx + 7 && y1 >= qy && y0 <= qy + 7;
+}
+
+// Counting sort of tiles by descending work (work / 16 in 256 buckets) in one
+// CTA.  work = list length (forward) or processed prefix (backward).  The
+// order inside a bucket is whatever the shared atomics give: scheduling only.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges,
+                                                          const uint32_t* __restrict__ nproc,
+                                                          int total_tiles,
+                                                          uint32_t* __restrict__ order) {
+  __shared__ uint32_t cnt[256];
+  const int tid = threadIdx.x;
+  auto bucket = [&](int t) -> uint32_t {
+    const uint32_t w = nproc ? nproc[t] : ranges[t].y - ranges[t].x;
+    return 255u - min(255u, w >> 4);
+  };
+  if (tid < 256) cnt[tid] = 0;
+  __syncthreads();
+  for (int t = tid; t < total_tiles; t += blockDim.x) atomicAdd(&cnt[bucket(t)], 1u);
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of 256 counts, 8 per lane
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c[k] = cnt[tid * 8 + k];
+      sum += c[k];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (tid >= o) inc += y;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cnt[tid * 8 + k] = run;
+      run += c[k];
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < total_tiles; t += blockDim.x) order[atomicAdd(&cnt[bucket(t)], 1u)] = t;
 }
 
 struct PixState {
@@ -53,9 +100,9 @@ __device__ __forceinline__ void blend(PixState& p, float al, float cr, float cg,
 }
 
 __global__ void __launch_bounds__(128) raster_fwd_kernel(
-    FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
-    const SplatRec* __restrict__ recs, const FrameHeader* __restrict__ hdr,
-    float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ counts,
+    FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
+    const FrameHeader* __restrict__ hdr, float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ counts,
     uint32_t* __restrict__ px_last, uint32_t* __restrict__ tile_nproc) {
   __shared__ __align__(128) SplatRec s_raw[256];
   __shared__ float4 s_a[256];
@@ -65,7 +112,7 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
   __shared__ uint32_t s_max[4];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
-  const int tile = blockIdx.x;
+  const int tile = static_cast<int>(order[blockIdx.x]);
   int v = 0;
   while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
   const CamDev& cam = fd.cam[v];
@@ -208,8 +255,9 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const
 }
 
 __global__ void __launch_bounds__(128) raster_bwd_kernel(
-    FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
-    const SplatRec* __restrict__ recs, const FrameHeader* __restrict__ fh,
+    FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
+    const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
+    const FrameHeader* __restrict__ fh,
     const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
     const float* __restrict__ final_T, const float* __restrict__ dL,
     float* __restrict__ partials) {
@@ -222,7 +270,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   __shared__ float s_red[4][32][9];
   __shared__ __align__(8) uint64_t s_bar;
   if (fh->stats.overflow) return;
-  const int tile = blockIdx.x;
+  const int tile = static_cast<int>(order[blockIdx.x]);
   const int nproc = static_cast<int>(tile_nproc[tile]);
   if (nproc == 0) return;
   int v = 0;
@@ -327,8 +375,11 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
 // ---------------------------------------------------------------------------
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
                       float* image, float* final_T, int32_t* counts, cudaStream_t st) {
+  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nullptr, fd.total_tiles, L.tile_order);
+  CGS_CHECK_LAUNCH("tile_order_kernel");
   CGS_PROFILED("raster_fwd_kernel", st,
-               raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.ranges, vals, L.recs, L.hdr,
+               raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges, vals,
+                                                                 L.recs, L.hdr,
                                                                  image, final_T, counts, L.px_last,
                                                                  L.tile_nproc));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
@@ -337,8 +388,11 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, cudaStream_t st) {
+  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, L.tile_nproc, fd.total_tiles, L.tile_order);
+  CGS_CHECK_LAUNCH("tile_order_kernel");
   CGS_PROFILED("raster_bwd_kernel", st,
-               raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.ranges, sorted_pair_vals(L),
+               raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges,
+                                                                 sorted_pair_vals(L),
                                                                  L.recs, L.hdr, L.px_last,
                                                                  L.tile_nproc, final_T, dL, partials));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");

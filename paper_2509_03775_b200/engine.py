@@ -65,6 +65,7 @@ class Trainer:
         self._gkey = None
         self._g_fwd = self._g_sgld = None
         self.captures = 0
+        state.prefetch_host_index()  # the MCMC loop reads the assignments from the host
 
     # -- buffers ---------------------------------------------------------------
     def _prepare(self):

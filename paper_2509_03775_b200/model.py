@@ -189,8 +189,8 @@ class Codebook:
         if (self._dev_rc is None or self._dev_rc_host is None
                 or self._dev_rc_host.shape != self.refcount.shape
                 or not np.array_equal(self._dev_rc_host, self.refcount)):
-            host = self.refcount.astype(np.int32)
-            self._dev_rc = torch.as_tensor(host).to(self._buf.device, non_blocking=False)
+            from . import _native as nat
+            self._dev_rc = nat.upload(self.refcount, self._buf.device, np.int32)
             self._dev_rc_host = self.refcount.copy()
         return self._dev_rc
 
@@ -198,8 +198,8 @@ class Codebook:
         """int32 device list of live row indices, ascending."""
         key = self.refcount.tobytes()
         if self._live_cache is None or self._live_cache[0] != key:
-            lv = self.live_indices().astype(np.int32)
-            self._live_cache = (key, torch.as_tensor(lv).to(self._buf.device))
+            from . import _native as nat
+            self._live_cache = (key, nat.upload(self.live_indices(), self._buf.device, np.int32))
         return self._live_cache[1]
 
 
@@ -350,6 +350,40 @@ class ModelState:
         cache[which] = (key, off, mem)
         return off, mem
 
+    # -- host mirror of the assignments -------------------------------------
+    # g2sh / g2sr change only through host-decided moves (split, merge,
+    # densify, remap), so the MCMC decision loop reads them from a host copy
+    # fetched asynchronously right after each change instead of synchronising
+    # with the device at the next transition.
+    def _index_key(self, which):
+        _, idx = _book_of(self, which)
+        return (self.assign_version, idx.data_ptr(), idx._version, idx.shape[0])
+
+    def prefetch_host_index(self, which=None):
+        """Enqueue a pinned D2H copy of g2sh / g2sr on the current stream."""
+        cache = self.__dict__.setdefault("_hidx", {})
+        for w in (("sh", "sr") if which is None else (which,)):
+            key = self._index_key(w)
+            ent = cache.get(w)
+            if ent is not None and ent[0] == key:
+                continue
+            _, idx = _book_of(self, w)
+            host = torch.empty((idx.shape[0],), dtype=torch.int32, pin_memory=idx.is_cuda)
+            host.copy_(idx, non_blocking=True)
+            ev = None
+            if idx.is_cuda:
+                ev = torch.cuda.Event()
+                ev.record()
+            cache[w] = (key, host, ev)
+
+    def host_index(self, which: str) -> np.ndarray:
+        """int32 host copy of g2sh ('sh') or g2sr ('sr'), current with the device."""
+        self.prefetch_host_index(which)
+        key, host, ev = self.__dict__["_hidx"][which]
+        if ev is not None:
+            ev.synchronize()
+        return host.numpy()
+
     def token(self) -> tuple:
         """Cheap identity of the state contents (replaces render.py:227-237's SHA-256)."""
         g = self.gaussians
@@ -462,23 +496,24 @@ def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Gene
     k = min(int(growth_rate * n), cap - n)
     if k <= 0:
         return 0
+    hsh, hsr = state.host_index("sh"), state.host_index("sr")
     opac = g.opacities()
     probs = opac / opac.sum()
     src = rng.choice(n, size=k, replace=True, p=probs)
     jitter = rng.normal(0.0, jitter_sigma, size=(k, 3))
     dev = state.device
     g.resize(n + k)
-    src_d = torch.as_tensor(np.ascontiguousarray(src, np.int64)).to(dev)
-    jit_d = torch.as_tensor(np.ascontiguousarray(jitter, np.float64)).to(dev)
+    src_d = nat.upload(src, dev, np.int64)
+    jit_d = nat.upload(jitter, dev, np.float64)
     nat.call("cgs_densify_append", nat.ptr(g._pos), nat.ptr(g._logit), nat.ptr(g._g2sh),
              nat.ptr(g._g2sr), n, nat.ptr(src_d), nat.ptr(jit_d), k, nat.stream_handle(dev))
-    new_sh = g._g2sh[n:n + k].cpu().numpy()
-    new_sr = g._g2sr[n:n + k].cpu().numpy()
+    new_sh, new_sr = hsh[src], hsr[src]  # clones share their source's rows (model.py:262-266)
     np.add.at(state.sh.refcount, new_sh, 1)
     np.add.at(state.sr.refcount, new_sr, 1)
     state.sh.mutations += 1
     state.sr.mutations += 1
     state.touch(assignments=True)
+    state.prefetch_host_index()
     return k
 
 

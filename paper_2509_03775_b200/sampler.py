@@ -210,14 +210,15 @@ def _apply_split_batch(state: ModelState, which: str, moves):
         return
     book, idx = _book_of(state, which)
     dev = book.device
-    g = torch.as_tensor(np.array([m[0] for m in moves], np.int64)).to(dev)
-    o = torch.as_tensor(np.array([m[1] for m in moves], np.int32)).to(dev)
-    nw = torch.as_tensor(np.array([m[2] for m in moves], np.int32)).to(dev)
-    u = torch.as_tensor(np.ascontiguousarray(np.stack([m[3] for m in moves]), np.float64)).to(dev)
+    g = nat.upload(np.array([m[0] for m in moves], np.int64), dev)
+    o = nat.upload(np.array([m[1] for m in moves], np.int32), dev)
+    nw = nat.upload(np.array([m[2] for m in moves], np.int32), dev)
+    u = nat.upload(np.stack([m[3] for m in moves]), dev, np.float64)
     nat.call("cgs_apply_splits", nat.ptr(book.rows), book.dim, nat.ptr(idx), nat.ptr(g), nat.ptr(o),
              nat.ptr(nw), nat.ptr(u), len(moves), nat.stream_handle(dev))
     book.mutations += 1
     state.touch(assignments=True)
+    state.prefetch_host_index(which)
 
 
 def apply_split(state: ModelState, proposal: SplitProposal) -> int:
@@ -245,7 +246,7 @@ def accept_split(state: ModelState, proposal: SplitProposal, lam: float, config:
 def _rows_host(book, rows: np.ndarray) -> np.ndarray:
     if len(rows) == 0:
         return np.zeros((0, book.dim), np.float32)
-    t = torch.as_tensor(rows.astype(np.int64)).to(book.device)
+    t = nat.upload(rows, book.device, np.int64)
     return book.rows.index_select(0, t).cpu().numpy()
 
 
@@ -295,10 +296,11 @@ def _apply_remap(state: ModelState, which: str, remap: dict):
     table = np.full(book.capacity, -1, np.int32)
     for c, p in remap.items():
         table[c] = p
-    t = torch.as_tensor(table).to(book.device)
+    t = nat.upload(table, book.device)
     nat.call("cgs_apply_remap", nat.ptr(idx), state.num_gaussians, nat.ptr(t), len(table),
              nat.stream_handle(book.device))
     state.touch(assignments=True)
+    state.prefetch_host_index(which)
 
 
 def apply_merge(state: ModelState, proposal: MergeProposal) -> None:
@@ -414,27 +416,24 @@ def clone_state(state: ModelState) -> ModelState:
 
 
 def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: TransitionRecord):
-    """Split branch of train_step (sampler.py:339-364): device eligibility compaction,
-    host accept loop over the Generator, one batched device apply."""
+    """Split branch of train_step (sampler.py:339-364): eligibility and the accept
+    loop on the host mirrors (assignments, refcounts) with the caller's
+    Generator, then one batched device apply -- no device synchronisation."""
     which = "sh" if rng.random() < 0.5 else "sr"
     rec.codebook = which
-    book, idx = _book_of(state, which)
+    book, _ = _book_of(state, which)
     n = state.num_gaussians
-    dev = state.device
-    elig = torch.empty((max(n, 1),), dtype=torch.int32, device=dev)
-    count = torch.zeros((1,), dtype=torch.int64, device=dev)
-    ws = torch.empty((nat.library().cgs_scan_workspace_bytes(max(n, 1)) + 1024,), dtype=torch.uint8,
-                     device=dev)
-    nat.call("cgs_split_eligible", nat.ptr(idx), n, nat.ptr(book.device_refcount()), nat.ptr(elig),
-             nat.ptr(count), nat.ptr(ws), ws.numel(), nat.stream_handle(dev))
-    n_elig = int(count.item())
+    # eligible = Gaussians whose row is shared (sampler.py:344), from the host
+    # mirrors of the assignments and refcounts: no device round trip
+    hidx = state.host_index(which)
+    elig = np.flatnonzero(book.refcount[hidx] >= 2)
+    n_elig = len(elig)
     n_cand = min(_candidate_count(config.split_fraction, n), n_elig)
     if n_cand <= 0:
         return
-    pos = rng.choice(n_elig, size=n_cand, replace=False)
-    cand_t = elig.index_select(0, torch.as_tensor(pos.astype(np.int64)).to(dev))
-    rows = idx.index_select(0, cand_t.long()).cpu().numpy()
-    cand = cand_t.cpu().numpy()
+    # rng.choice(eligible, ...) == eligible[rng.choice(len(eligible), ...)]
+    cand = elig[rng.choice(n_elig, size=n_cand, replace=False)]
+    rows = hidx[cand]
     lam = config.lambda_for(which)
     es, em = config.eps_for(which)
     moves = []
