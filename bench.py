@@ -387,7 +387,8 @@ def main():
                "frame": {"pairs": int(stats.n_pairs), "processed_pairs": P_x,
                          "touched": int(stats.n_touched), "onscreen": int(stats.n_onscreen)},
                "recon": tr.recon(), "mcmc_events": tr.mcmc_events,
-               "mcmc_ms": tr.mcmc_ms, "host_enqueue_ms_per_step": 1000.0 * host_s / args.steps,
+               "mcmc_ms": tr.mcmc_ms, "densify_ms": tr.densify_ms, "capture_ms": tr.capture_ms,
+               "host_enqueue_ms_per_step": 1000.0 * host_s / args.steps,
                "cuda_graphs": tr.use_graphs, "graph_captures": tr.captures}
         print(json.dumps(out))
     if world > 1:

@@ -62,7 +62,8 @@ struct __align__(16) SplatRec {
   double ca, cb, cc;    // conic [[A,B],[B,C]] (f64, render.py:176-181)
   float opac;           // sigmoid(logit) (computed in f64, render.py:200)
   float r, g, b;        // clamped colour (render.py:196-198)
-  uint16_t px0, px1, py0, py1;  // inclusive pixel rect (render.py:110-115)
+  uint16_t px0, px1, py0, py1;  // inclusive contribution box, inside the pixel rect of
+                                // render.py:110-115 (px0 = py0 = 0xffff when empty)
 };
 static_assert(sizeof(SplatRec) == 64, "SplatRec must be 64 bytes");
 

@@ -116,7 +116,10 @@ inline uint32_t* sorted_pair_vals(const FrameLayout& L) {
   return L.tile_key_bytes == 2 ? L.psort16.vals_alt : L.psort32.vals_alt;
 }
 
-// Raster launches (raster.cu).
+// Raster launches (raster.cu).  tile_order: CTA -> tile, longest work first
+// (work = list length when nproc is null, else the processed prefix).
+int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
+                      cudaStream_t st);
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
                       float* image, float* final_T, int32_t* counts, cudaStream_t st);
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,

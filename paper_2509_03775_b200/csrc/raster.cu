@@ -2,10 +2,11 @@
 //
 // Both kernels run one 128-thread CTA per 16x16 tile.  Warp w owns the 8x8
 // quadrant ((w & 1) * 8, (w >> 1) * 8) of the tile and each lane two pixels
-// (x, y) and (x, y + 4) of it.  A splat whose pixel rect (render.py:110-115)
-// misses a warp's quadrant is skipped by that warp without evaluating it:
-// outside the rect alpha < opacity / 255 < 1/255 by construction of the
-// footprint radius (render.py:32-34), so the skip changes no result.
+// (x, y) and (x, y + 4) of it.  A splat whose contribution box (projection:
+// the bounding box of its alpha >= 1/255 ellipse, inside the pixel rect of
+// render.py:110-115) misses a warp's quadrant is skipped by that warp without
+// evaluating it: outside the box the reference's float64 alpha is < 1/255,
+// so the skip changes no result.
 //
 // CTAs take tiles longest-work-first (tile_order_kernel): the block
 // scheduler hands out CTAs in blockIdx order as slots free up, so this is
@@ -22,8 +23,8 @@
 
 namespace cgs {
 
-// Tile-local inclusive pixel rect of a splat as 4 signed bytes (x0, x1, y0, y1),
-// clamped to [-1, 16].
+// Tile-local inclusive contribution box of a splat as 4 signed bytes
+// (x0, x1, y0, y1), clamped to [-1, 16] (an empty box has x0 = 16: no hit).
 __device__ __forceinline__ uint32_t local_rect(const SplatRec& r, int tx0, int ty0) {
   auto c = [](int v) { return static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(v < -1 ? -1 : (v > 16 ? 16 : v)))); };
   return c(r.px0 - tx0) | (c(r.px1 - tx0) << 8) | (c(r.py0 - ty0) << 16) | (c(r.py1 - ty0) << 24);
@@ -373,10 +374,16 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
 }
 
 // ---------------------------------------------------------------------------
+int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
+                      cudaStream_t st) {
+  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nproc, fd.total_tiles, L.tile_order);
+  CGS_CHECK_LAUNCH("tile_order_kernel");
+  return CGS_OK;
+}
+
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
                       float* image, float* final_T, int32_t* counts, cudaStream_t st) {
-  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nullptr, fd.total_tiles, L.tile_order);
-  CGS_CHECK_LAUNCH("tile_order_kernel");
+  // L.tile_order was computed from the list lengths before the depth sort
   CGS_PROFILED("raster_fwd_kernel", st,
                raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges, vals,
                                                                  L.recs, L.hdr,
@@ -388,8 +395,8 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, cudaStream_t st) {
-  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, L.tile_nproc, fd.total_tiles, L.tile_order);
-  CGS_CHECK_LAUNCH("tile_order_kernel");
+  int rc = launch_tile_order(fd, L, L.tile_nproc, st);
+  if (rc) return rc;
   CGS_PROFILED("raster_bwd_kernel", st,
                raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges,
                                                                  sorted_pair_vals(L),

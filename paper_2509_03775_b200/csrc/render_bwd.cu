@@ -92,6 +92,12 @@ struct GaussIn {
   const double* sr_cov;
 };
 
+__device__ __forceinline__ float ldg_volatile(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
 // Chain rule from screen space to model space for one (view, Gaussian)
 // splat (render.py:382-446).  acc = [d_color(3), d_opac, d_mean2d(2),
 // d_conic(A, B, C)].  Writes the per-splat pull-back record s.
@@ -101,6 +107,38 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   constexpr int NB = (DEG + 1) * (DEG + 1);
   constexpr int D = 3 * NB;
   const double px = g.pos[3 * gi + 0], py = g.pos[3 * gi + 1], pz = g.pos[3 * gi + 2];
+  // colour path first (render.py:415-429), so its registers are free before
+  // the geometric chain.
+  double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
+  const double len = sqrt((ox * ox + oy * oy) + oz * oz);
+  ox /= len;
+  oy /= len;
+  oz /= len;
+  double Bv[NB];
+  sh_basis<DEG>(ox, oy, oz, Bv);
+  // Two streaming passes over the row (the second re-reads L1; volatile loads
+  // keep the compiler from holding the row in registers): same sums, same order.
+  const float* row = g.sh_rows + static_cast<int64_t>(g.g2sh[gi]) * D;
+  double col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < D; ++e) col[e % 3] += Bv[e / 3] * static_cast<double>(__ldg(row + e));
+  const double draw[3] = {col[0] + 0.5 > 0.0 ? acc[0] : 0.0, col[1] + 0.5 > 0.0 ? acc[1] : 0.0,
+                          col[2] + 0.5 > 0.0 ? acc[2] : 0.0};
+  double dpc[3] = {0.0, 0.0, 0.0};
+  if constexpr (DEG >= 1) {
+    double wb[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      wb[b] = draw[0] * static_cast<double>(ldg_volatile(row + 3 * b + 0)) +
+              draw[1] * static_cast<double>(ldg_volatile(row + 3 * b + 1)) +
+              draw[2] * static_cast<double>(ldg_volatile(row + 3 * b + 2));
+    double dv[3];
+    sh_basis_grad_dot<DEG>(ox, oy, oz, wb, dv);
+    const double vd = ox * dv[0] + oy * dv[1] + oz * dv[2];
+    dpc[0] = (dv[0] - ox * vd) / len;
+    dpc[1] = (dv[1] - oy * vd) / len;
+    dpc[2] = (dv[2] - oz * vd) / len;
+  }
   const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
   const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
   const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
@@ -171,34 +209,9 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   double dp[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) dp[k] = dt[0] * cam.R[0 + k] + dt[1] * cam.R[3 + k] + dt[2] * cam.R[6 + k];
-  // colour path (render.py:415-429)
-  double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
-  const double len = sqrt((ox * ox + oy * oy) + oz * oz);
-  ox /= len;
-  oy /= len;
-  oz /= len;
-  double Bv[NB];
-  sh_basis<DEG>(ox, oy, oz, Bv);
-  const float* row = g.sh_rows + static_cast<int64_t>(g.g2sh[gi]) * D;
-  double cf[D];
-#pragma unroll
-  for (int e = 0; e < D; ++e) cf[e] = static_cast<double>(__ldg(row + e));
-  double col[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int e = 0; e < D; ++e) col[e % 3] += Bv[e / 3] * cf[e];
-  const double draw[3] = {col[0] + 0.5 > 0.0 ? acc[0] : 0.0, col[1] + 0.5 > 0.0 ? acc[1] : 0.0,
-                          col[2] + 0.5 > 0.0 ? acc[2] : 0.0};
   if constexpr (DEG >= 1) {
-    double wb[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b)
-      wb[b] = draw[0] * cf[3 * b + 0] + draw[1] * cf[3 * b + 1] + draw[2] * cf[3 * b + 2];
-    double dv[3];
-    sh_basis_grad_dot<DEG>(ox, oy, oz, wb, dv);
-    const double vd = ox * dv[0] + oy * dv[1] + oz * dv[2];
-    dp[0] += (dv[0] - ox * vd) / len;
-    dp[1] += (dv[1] - oy * vd) / len;
-    dp[2] += (dv[2] - oz * vd) / len;
+    for (int k = 0; k < 3; ++k) dp[k] += dpc[k];
   }
   const double o = 1.0 / (1.0 + exp(-static_cast<double>(g.logit[gi])));
   const double dlogit = acc[3] * o * (1.0 - o);  // render.py:446
@@ -302,7 +315,7 @@ __global__ void __launch_bounds__(256) splat_reduce_kernel(PairWalk pw, const Fr
 // Chain rule per touched splat (kept apart from the gather walk so the
 // latency-bound walk runs at full occupancy).
 template <int DEG>
-__global__ void __launch_bounds__(256) pull_back_kernel(const FrameHeader* __restrict__ fh,
+__global__ void __launch_bounds__(128, 4) pull_back_kernel(const FrameHeader* __restrict__ fh,
                                                         FrameDesc fd, int64_t n, int64_t vn,
                                                         GaussIn g, BwdLayout B) {
   if (fh->stats.overflow) return;
@@ -338,45 +351,65 @@ __global__ void __launch_bounds__(256) gauss_write_kernel(BwdLayout B, int64_t n
 }
 
 // SH row gradient = sum over members of basis(view) (x) d_raw (render.py:421,
-// 456).  One warp per codebook row, lane owns columns lane and lane + 32;
-// members in ascending Gaussian index, views ascending.  Writes every row.
-template <int DEG>
-__global__ void __launch_bounds__(256) sh_code_reduce_kernel(
-    const int32_t* __restrict__ off, const int32_t* __restrict__ mem, int64_t cap, int64_t n,
-    int n_views, BwdLayout B, float scale, float* __restrict__ gsh) {
+// 456).  One 128-thread CTA per codebook row: warp w owns the column group
+// [w*CPW, (w+1)*CPW) (warp-uniform, so the basis index of every column is a
+// compile-time constant after the switch on w) and its lanes take the row's
+// (member, view) splats round-robin; the 32 lane sums are combined by a fixed
+// xor tree.  Members ascend by Gaussian index, views ascend; every addition
+// has a fixed order, so the result is deterministic.  Writes every row.
+template <int DEG, int W>
+__device__ __forceinline__ void sh_row_columns(const int32_t* __restrict__ mem, int m0, int m1,
+                                               int64_t n, int n_views, const BwdLayout& B,
+                                               float scale, float* __restrict__ out) {
   constexpr int NB = (DEG + 1) * (DEG + 1);
   constexpr int D = 3 * NB;
+  constexpr int CPW = (D + 3) / 4;
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int c0 = lane, c1 = lane + 32;
-  const int b0 = c0 / 3, ch0 = c0 % 3, b1 = c1 / 3, ch1 = c1 % 3;
-  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < cap;
-       r += warps) {
-    const int m0 = off[r], m1 = off[r + 1];
-    double a0 = 0.0, a1 = 0.0;
-    for (int m = m0; m < m1; ++m) {
-      const int64_t i = mem[m];
-      for (int v = 0; v < n_views; ++v) {
-        const int64_t s = static_cast<int64_t>(v) * n + i;
-        if (!B.touched[s]) continue;
-        const float4 vd = B.s_view[s];
-        const float4 dr = B.s_draw[s];
-        float Bv[NB];
-        sh_basis_f<DEG>(vd.x, vd.y, vd.z, Bv);
-        float bv0 = 0.0f, bv1 = 0.0f;
+  const int items = (m1 - m0) * n_views;
+  double a[CPW];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          if (b == b0) bv0 = Bv[b];
-          if (b == b1) bv1 = Bv[b];
-        }
-        const float d0 = ch0 == 0 ? dr.x : (ch0 == 1 ? dr.y : dr.z);
-        const float d1 = ch1 == 0 ? dr.x : (ch1 == 1 ? dr.y : dr.z);
-        a0 += static_cast<double>(bv0 * d0);
-        a1 += static_cast<double>(bv1 * d1);
-      }
+  for (int c = 0; c < CPW; ++c) a[c] = 0.0;
+  for (int t = lane; t < items; t += 32) {
+    const int mi = t / n_views, v = t - mi * n_views;
+    const int64_t sp = static_cast<int64_t>(v) * n + mem[m0 + mi];
+    if (!B.touched[sp]) continue;
+    const float4 vd = B.s_view[sp];
+    const float4 dr = B.s_draw[sp];
+    float Bv[NB];
+    sh_basis_f<DEG>(vd.x, vd.y, vd.z, Bv);
+    const float d3[3] = {dr.x, dr.y, dr.z};
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      constexpr int base = W * CPW;
+      if (base + c < D) a[c] += static_cast<double>(Bv[(base + c) / 3] * d3[(base + c) % 3]);
     }
-    if (c0 < D) gsh[r * D + c0] = static_cast<float>(a0 * scale);
-    if (c1 < D) gsh[r * D + c1] = static_cast<float>(a1 * scale);
+  }
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) a[c] = warp_sum(a[c]);
+  if (lane < CPW && W * CPW + lane < D) {
+    double v = a[0];
+#pragma unroll
+    for (int c = 1; c < CPW; ++c)
+      if (lane == c) v = a[c];
+    out[W * CPW + lane] = static_cast<float>(v * scale);
+  }
+}
+
+template <int DEG>
+__global__ void __launch_bounds__(128) sh_code_reduce_kernel(
+    const int32_t* __restrict__ off, const int32_t* __restrict__ mem, int64_t cap, int64_t n,
+    int n_views, BwdLayout B, float scale, float* __restrict__ gsh) {
+  constexpr int D = 3 * (DEG + 1) * (DEG + 1);
+  const int w = threadIdx.x >> 5;
+  for (int64_t r = blockIdx.x; r < cap; r += gridDim.x) {
+    const int m0 = off[r], m1 = off[r + 1];
+    float* out = gsh + r * D;
+    switch (w) {
+      case 0: sh_row_columns<DEG, 0>(mem, m0, m1, n, n_views, B, scale, out); break;
+      case 1: sh_row_columns<DEG, 1>(mem, m0, m1, n, n_views, B, scale, out); break;
+      case 2: sh_row_columns<DEG, 2>(mem, m0, m1, n, n_views, B, scale, out); break;
+      default: sh_row_columns<DEG, 3>(mem, m0, m1, n, n_views, B, scale, out); break;
+    }
   }
 }
 
@@ -534,7 +567,7 @@ static void launch_splat_reduce(const PairWalk& pw, const FrameLayout& L, const 
                                                                                  L.vn, gi, B));
   note_launch();
   CGS_PROFILED("pull_back_kernel", st,
-               pull_back_kernel<DEG><<<grid_for(L.vn, 256, 8), 256, 0, st>>>(L.hdr, fd, L.n, L.vn,
+               pull_back_kernel<DEG><<<grid_for(L.vn, 128, 8), 128, 0, st>>>(L.hdr, fd, L.n, L.vn,
                                                                               gi, B));
 }
 
@@ -542,7 +575,7 @@ template <int DEG>
 static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap, int64_t n,
                              int nv, const BwdLayout& B, float scale, float* gsh, cudaStream_t st) {
   CGS_PROFILED("sh_code_reduce_kernel", st,
-               sh_code_reduce_kernel<DEG><<<grid_for(cap * 32, 256, 16), 256, 0, st>>>(
+               sh_code_reduce_kernel<DEG><<<grid_for(cap, 1, 16), 128, 0, st>>>(
                    off, mem, cap, n, nv, B, scale, gsh));
 }
 

@@ -163,14 +163,38 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
     rec.ca = c / det;  // conic = adj(Sigma2) / det (render.py:176-181)
     rec.cb = -b / det;
     rec.cc = a / det;
-    rec.opac = static_cast<float>(1.0 / (1.0 + exp(-static_cast<double>(in.logit[i]))));
+    const double opac = 1.0 / (1.0 + exp(-static_cast<double>(in.logit[i])));
+    rec.opac = static_cast<float>(opac);
     rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
     rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
     rec.b = static_cast<float>(fmax(col[2] + 0.5, 0.0));
-    rec.px0 = static_cast<uint16_t>(x0);
-    rec.px1 = static_cast<uint16_t>(x1);
-    rec.py0 = static_cast<uint16_t>(y0);
-    rec.py1 = static_cast<uint16_t>(y1);
+    // Contribution box for the raster's warp-level skip: pixels whose centre
+    // lies outside the bounding box of {d : o exp(-d^T conic d / 2) >= 1/255}
+    // have alpha < 1/255 in the reference's float64 arithmetic (render.py:
+    // 274-280), so they are never kept there and skipping them is exact.  The
+    // box half-widths are sqrt(t Sigma2_xx), sqrt(t Sigma2_yy) with
+    // t = 2 ln(255 o), widened by a relative 1e-7 for rounding; it lies inside
+    // the pixel rect (o < 1, Sigma2_xx <= lambda_max).  o < 1/255: no pixel.
+    {
+      const double t = 2.0 * log(255.0 * opac) * (1.0 + 1e-7) + 1e-12;
+      uint16_t bx0 = 0xffff, bx1 = 0, by0 = 0xffff, by1 = 0;
+      if (t > 0.0) {
+        const double hx = sqrt(t * a) * (1.0 + 1e-7) + 1e-7;
+        const double hy = sqrt(t * c) * (1.0 + 1e-7) + 1e-7;
+        const double cx0 = fmax(x0, ceil(mx - hx - 0.5)), cx1 = fmin(x1, floor(mx + hx - 0.5));
+        const double cy0 = fmax(y0, ceil(my - hy - 0.5)), cy1 = fmin(y1, floor(my + hy - 0.5));
+        if (cx0 <= cx1 && cy0 <= cy1) {
+          bx0 = static_cast<uint16_t>(cx0);
+          bx1 = static_cast<uint16_t>(cx1);
+          by0 = static_cast<uint16_t>(cy0);
+          by1 = static_cast<uint16_t>(cy1);
+        }
+      }
+      rec.px0 = bx0;  // empty box: px0 = py0 = 0xffff
+      rec.px1 = bx1;
+      rec.py0 = by0;
+      rec.py1 = by1;
+    }
     out.recs[s] = rec;
     out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
     out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
@@ -281,140 +305,177 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const KT* __restrict__
 // Per-tile depth order.  After the stable tile sort each tile's list holds
 // its splats in index order; a stable sort by depth then reproduces
 // np.lexsort((idx, tz)) restricted to the tile (render.py:203, 247-253).
-// Lists up to kTileSortCap are sorted in shared memory: a 4-pass stable LSD
-// radix on a 32-bit key (the fp64 depth rounded toward zero to fp32, which
-// is monotone), then runs of equal 32-bit keys -- rare -- are re-sorted by
-// the exact fp64 key with a stable insertion sort.  Longer lists take a
-// stable in-CTA 8-pass radix on the fp64 bits through global scratch.  The
-// kernel also records inv[emission index] = final position for the backward.
+//
+// Lists up to kTileSortCap: a bitonic sort held in registers (S = 256*E
+// slots, E = 1..16 per thread, thread-major, padded with +inf) on the
+// unique 64-bit key (fp32 depth rounded toward zero, which is monotone in
+// the fp64 depth) << 32 | splat id, so equal 32-bit depths fall back to index
+// order; strides below E are in-register compare-exchanges, strides below 32E
+// warp shuffles, the rest go through shared memory.  Runs of equal 32-bit
+// depth -- rare -- are then re-sorted by the exact fp64 key with a stable
+// insertion sort, which gives (fp64 depth, index) order.  Longer lists take a
+// stable in-CTA 8-pass radix on the fp64 bits through global scratch.  CTAs
+// take tiles longest-first (tile_order).  The kernel also records
+// inv[emission index] = final position for the backward.
 struct TileSortSmem {
-  uint32_t key[2][kTileSortCap];
-  uint32_t val[2][kTileSortCap];
-  uint32_t wcnt[8][256];  // (round tag << 16) | count
-  uint32_t base[256];
+  union {
+    uint64_t key[kTileSortCap];
+    struct {
+      uint32_t wcnt[8][256];
+      uint32_t base[256];
+    } radix;
+  };
 };
 
 __device__ __forceinline__ uint32_t depth_key32(uint64_t bits) {
   return __float_as_uint(__double2float_rz(__longlong_as_double(static_cast<long long>(bits))));
 }
 
-__global__ void __launch_bounds__(256) tile_depth_sort_kernel(
-    const uint2* __restrict__ ranges, uint32_t* __restrict__ vals,
-    const uint64_t* __restrict__ depth_key, const uint64_t* __restrict__ pair_off,
-    const uint64_t* __restrict__ rect, uint32_t* __restrict__ inv, uint32_t* __restrict__ scratch,
+// Slot x = tid * E + e lives in smem at x ^ ((x / E) & (E - 1)) (spreads a
+// warp's accesses over the banks).
+template <int E>
+__device__ __forceinline__ int swz(int x) {
+  return x ^ ((x / E) & (E - 1));
+}
+
+template <int NT, int E>
+__device__ __forceinline__ void bitonic_regs(uint64_t (&key)[E], uint64_t* sm, int tid) {
+  constexpr int S = NT * E;
+  for (int k = 2; k <= S; k <<= 1) {
+    int j = k >> 1;
+    for (; j >= 32 * E; j >>= 1) {  // across warps
+#pragma unroll
+      for (int e = 0; e < E; ++e) sm[swz<E>(tid * E + e)] = key[e];
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int x = tid * E + e;
+        const uint64_t o = sm[swz<E>(x ^ j)];
+        const bool keep_min = ((x & k) == 0) == ((x & j) == 0);
+        key[e] = keep_min ? (o < key[e] ? o : key[e]) : (o > key[e] ? o : key[e]);
+      }
+      __syncthreads();
+    }
+    for (; j >= E; j >>= 1) {  // across lanes
+      const int lm = j / E;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int x = tid * E + e;
+        const uint64_t o = __shfl_xor_sync(kFull, key[e], lm);
+        const bool keep_min = ((x & k) == 0) == ((x & j) == 0);
+        key[e] = keep_min ? (o < key[e] ? o : key[e]) : (o > key[e] ? o : key[e]);
+      }
+    }
+#pragma unroll
+    for (int jj = E / 2; jj > 0; jj >>= 1) {  // inside a thread
+      if (jj > j) continue;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & jj) continue;
+        const int p = e ^ jj;
+        const bool asc = ((tid * E + e) & k) == 0;
+        const uint64_t lo = key[e] < key[p] ? key[e] : key[p];
+        const uint64_t hi = key[e] < key[p] ? key[p] : key[e];
+        key[e] = asc ? lo : hi;
+        key[p] = asc ? hi : lo;
+      }
+    }
+  }
+}
+
+template <int NT, int E>
+__device__ __forceinline__ void sort_tile_short(TileSortSmem& S, uint32_t* seg, int len, int tile,
+                                                uint32_t first, const uint64_t* __restrict__ depth_key,
+                                                const uint64_t* __restrict__ pair_off,
+                                                const uint64_t* __restrict__ rect,
+                                                uint32_t* __restrict__ inv, const FrameDesc& fd,
+                                                int64_t n, int tid) {
+  uint64_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int x = tid * E + e;
+    if (x < len) {
+      const uint32_t sp = seg[x];
+      key[e] = (static_cast<uint64_t>(depth_key32(depth_key[sp])) << 32) | sp;
+    } else {
+      key[e] = ~0ULL;
+    }
+  }
+  bitonic_regs<NT, E>(key, S.key, tid);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) S.key[tid * E + e] = key[e];  // sorted position order
+  __syncthreads();
+  // exact order inside runs of equal 32-bit depth (stable insertion sort on fp64 bits)
+  for (int j = tid; j < len; j += NT) {
+    const uint32_t k = static_cast<uint32_t>(S.key[j] >> 32);
+    if ((j == 0 || static_cast<uint32_t>(S.key[j - 1] >> 32) != k) && j + 1 < len &&
+        static_cast<uint32_t>(S.key[j + 1] >> 32) == k) {
+      int e = j + 1;
+      while (e < len && static_cast<uint32_t>(S.key[e] >> 32) == k) ++e;
+      for (int a = j + 1; a < e; ++a) {
+        const uint64_t va = S.key[a];
+        const uint64_t ka = depth_key[static_cast<uint32_t>(va)];
+        int b = a - 1;
+        while (b >= j && depth_key[static_cast<uint32_t>(S.key[b])] > ka) {
+          S.key[b + 1] = S.key[b];
+          --b;
+        }
+        S.key[b + 1] = va;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < len; j += NT) {
+    const uint32_t sp = static_cast<uint32_t>(S.key[j]);
+    seg[j] = sp;
+    inv[emission_index(pair_off, rect, fd, n, sp, tile)] = first + j;
+  }
+}
+
+// Three launches over the longest-first tile order, one per list class:
+//   0: len <= 2048, 256 threads, E <= 8      1: 2048 < len <= 4096, 512 threads, E = 8
+//   2: len > 4096, stable 8-pass radix through global scratch (256 threads)
+// A CTA whose tile belongs to another class returns at once.
+template <int CLS>
+__global__ void __launch_bounds__(CLS == 1 ? 512 : 256) tile_depth_sort_kernel(
+    const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
+    uint32_t* __restrict__ vals, const uint64_t* __restrict__ depth_key,
+    const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect,
+    uint32_t* __restrict__ inv, uint32_t* __restrict__ scratch,
     const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSortSmem& S = *reinterpret_cast<TileSortSmem*>(smem_raw);
   if (hdr->stats.overflow) return;
-  const int tile = blockIdx.x;
+  const int tile = static_cast<int>(order[blockIdx.x]);
   const uint2 rg = ranges[tile];
   const int len = static_cast<int>(rg.y - rg.x);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   if (len <= 0) return;
   uint32_t* seg = vals + rg.x;
-  if (len <= kTileSortCap) {
-    for (int j = tid; j < len; j += 256) {
-      const uint32_t s = seg[j];
-      S.val[0][j] = s;
-      S.key[0][j] = depth_key32(depth_key[s]);
-    }
-    for (int q = tid; q < 8 * 256; q += 256) (&S.wcnt[0][0])[q] = 0xffff0000u;
-    int cur = 0;
-    uint32_t round = 0;
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 8 * pass;
-      S.base[tid] = 0;
-      __syncthreads();
-      // histogram with warp-aggregated shared atomics
-      for (int c0 = 0; c0 < len; c0 += 256) {
-        const int j = c0 + tid;
-        const unsigned d = j < len ? (S.key[cur][j] >> shift) & 255u : 256u + lane;
-        const unsigned peers = __match_any_sync(kFull, d);
-        if (j < len && lane == __ffs(peers) - 1) atomicAdd(&S.base[d], __popc(peers));
-      }
-      __syncthreads();
-      if (warp == 0) {  // exclusive scan of 256 counts, 8 per lane
-        uint32_t c[8], sum = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          c[k] = S.base[lane * 8 + k];
-          sum += c[k];
-        }
-        const uint32_t inc = warp_incl_scan(sum);
-        uint32_t run = inc - sum;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          S.base[lane * 8 + k] = run;
-          run += c[k];
-        }
-      }
-      __syncthreads();
-      for (int c0 = 0; c0 < len; c0 += 256, ++round) {
-        const int j = c0 + tid;
-        const bool ok = j < len;
-        const uint32_t key = ok ? S.key[cur][j] : 0u;
-        const uint32_t val = ok ? S.val[cur][j] : 0u;
-        const unsigned d = ok ? (key >> shift) & 255u : 256u + lane;
-        const unsigned peers = __match_any_sync(kFull, d);
-        const uint32_t rank = __popc(peers & lanemask_lt());
-        const uint32_t tag = round << 16;
-        if (ok && lane == __ffs(peers) - 1) S.wcnt[warp][d] = tag | __popc(peers);
-        __syncthreads();
-        if (ok) {
-          uint32_t before = 0;
-          for (int w2 = 0; w2 < warp; ++w2) {
-            const uint32_t v = S.wcnt[w2][d];
-            before += (v & 0xffff0000u) == tag ? (v & 0xffffu) : 0u;
-          }
-          const uint32_t pos = S.base[d] + before + rank;
-          S.key[cur ^ 1][pos] = key;
-          S.val[cur ^ 1][pos] = val;
-        }
-        __syncthreads();
-        {
-          uint32_t add = 0;
-#pragma unroll
-          for (int w2 = 0; w2 < 8; ++w2) {
-            const uint32_t v = S.wcnt[w2][tid];
-            add += (v & 0xffff0000u) == tag ? (v & 0xffffu) : 0u;
-          }
-          S.base[tid] += add;
-        }
-        __syncthreads();
-      }
-      cur ^= 1;
-    }
-    // exact order inside runs of equal 32-bit keys (stable insertion sort on fp64 bits)
-    for (int j = tid; j < len; j += 256) {
-      const uint32_t k = S.key[cur][j];
-      if ((j == 0 || S.key[cur][j - 1] != k) && j + 1 < len && S.key[cur][j + 1] == k) {
-        int e = j + 1;
-        while (e < len && S.key[cur][e] == k) ++e;
-        for (int a = j + 1; a < e; ++a) {
-          const uint32_t va = S.val[cur][a];
-          const uint64_t ka = depth_key[va];
-          int b = a - 1;
-          while (b >= j && depth_key[S.val[cur][b]] > ka) {
-            S.val[cur][b + 1] = S.val[cur][b];
-            --b;
-          }
-          S.val[cur][b + 1] = va;
-        }
-      }
-    }
-    __syncthreads();
-    for (int j = tid; j < len; j += 256) {
-      const uint32_t s = S.val[cur][j];
-      seg[j] = s;
-      inv[emission_index(pair_off, rect, fd, n, s, tile)] = rg.x + j;
-    }
+  if constexpr (CLS == 0) {
+    if (len > 2048) return;
+    if (len <= 256)
+      sort_tile_short<256, 1>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
+    else if (len <= 512)
+      sort_tile_short<256, 2>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
+    else if (len <= 1024)
+      sort_tile_short<256, 4>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
+    else
+      sort_tile_short<256, 8>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
+    return;
+  } else if constexpr (CLS == 1) {
+    if (len <= 2048 || len > kTileSortCap) return;
+    sort_tile_short<512, 8>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
     return;
   }
+  if (len <= kTileSortCap) return;
+  const int lane = tid & 31, warp = tid >> 5;
   // long list: stable LSD radix over the 64-bit depth key, ping-ponging
   // between the list and its scratch slice; 256-element chunks ranked with
   // warp match_any so equal digits keep their order.
-  uint32_t* cnt = S.base;
-  uint32_t* wcnt = &S.wcnt[0][0];
+  uint32_t* cnt = S.radix.base;
+  uint32_t* wcnt = &S.radix.wcnt[0][0];
   uint32_t* src = seg;
   uint32_t* dst = scratch + rg.x;
   for (int pass = 0; pass < 8; ++pass) {
@@ -525,16 +586,30 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
     static bool attr = false;
     const int smem = static_cast<int>(sizeof(TileSortSmem));
     if (!attr) {
-      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel,
+      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<0>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<2>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
     uint32_t* vals = sorted_pair_vals(L);
+    rc = launch_tile_order(fd, L, nullptr, st);
+    if (rc) return rc;
     CGS_PROFILED("tile_depth_sort_kernel", st,
-                 tile_depth_sort_kernel<<<fd.total_tiles, 256, smem, st>>>(
-                     L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr, fd,
-                     L.n));
+                 tile_depth_sort_kernel<0><<<fd.total_tiles, 256, 2048 * sizeof(uint64_t), st>>>(
+                     L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv,
+                     L.scratch, L.hdr, fd, L.n));
     CGS_CHECK_LAUNCH("tile_depth_sort_kernel");
+    tile_depth_sort_kernel<1><<<fd.total_tiles, 512, smem, st>>>(
+        L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr,
+        fd, L.n);
+    CGS_CHECK_LAUNCH("tile_depth_sort_kernel_mid");
+    tile_depth_sort_kernel<2><<<fd.total_tiles, 256, smem, st>>>(
+        L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr,
+        fd, L.n);
+    CGS_CHECK_LAUNCH("tile_depth_sort_kernel_long");
     rc = launch_raster_fwd(fd, L, vals, image, final_T, counts, st);
     if (rc) return rc;
   }

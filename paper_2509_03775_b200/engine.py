@@ -59,11 +59,15 @@ class Trainer:
         self.updates = 0
         self.mcmc_events = 0
         self.mcmc_ms = []
+        self.densify_ms = []
+        self.capture_ms = []
         self.last_loss = None
         self.use_graphs = use_graphs
         self.noise_ctr = torch.zeros((1,), dtype=torch.int64, device=self.dev)
         self._gkey = None
         self._g_fwd = self._g_sgld = None
+        self._pool = None
+        self._cap_stream = None
         self.captures = 0
         state.prefetch_host_index()  # the MCMC loop reads the assignments from the host
 
@@ -118,10 +122,23 @@ class Trainer:
                 st.sh.capacity, st.sr.capacity, sl.data_ptr(), sl.numel(), rl.data_ptr(), rl.numel())
 
     def _capture(self, fn):
-        torch.cuda.synchronize(self.dev)
+        """Capture fn into a CUDA graph on a side stream.  Unlike the
+        ``torch.cuda.graph`` context this skips the device synchronisation,
+        ``gc.collect()`` and ``empty_cache()`` (the latter forces fresh
+        cudaMallocs afterwards); all graphs share one memory pool."""
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+            self._cap_stream = torch.cuda.Stream(self.dev)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            fn()
+        cur = torch.cuda.current_stream(self.dev)
+        self._cap_stream.wait_stream(cur)
+        with torch.cuda.stream(self._cap_stream):
+            g.capture_begin(pool=self._pool)
+            try:
+                fn()
+            finally:
+                g.capture_end()
+        cur.wait_stream(self._cap_stream)
         return g
 
     def update(self):
@@ -132,6 +149,8 @@ class Trainer:
         if self.use_graphs:
             key = self._graph_key()
             if key != self._gkey:
+                import time
+                t0 = time.perf_counter()
                 self._enqueue_forward()
                 self._enqueue_backward()
                 self._enqueue_sgld()
@@ -139,6 +158,7 @@ class Trainer:
                 self._g_sgld = self._capture(self._enqueue_sgld)
                 self._gkey = key
                 self.captures += 1
+                self.capture_ms.append(1000.0 * (time.perf_counter() - t0))
             else:
                 self._g_fwd.replay()
                 self._enqueue_backward()
@@ -156,7 +176,10 @@ class Trainer:
         st.iteration += 1
         c = self.config
         if c.densify_every > 0 and st.iteration % c.densify_every == 0:
+            import time
+            t0 = time.perf_counter()
             densify(st, c.densify_growth, c.gaussian_cap, self.rng, jitter_sigma=c.densify_jitter)
+            self.densify_ms.append(1000.0 * (time.perf_counter() - t0))
 
     def mcmc(self):
         """One forced split and one forced merge transition (reference rules)."""
