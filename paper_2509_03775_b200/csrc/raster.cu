@@ -100,16 +100,47 @@ __device__ __forceinline__ void blend(PixState& p, float al, float cr, float cg,
   }
 }
 
+// 4-bit mask of the tile quadrants a tile-local contribution box overlaps
+// (bit w = quadrant ((w & 1) * 8, (w >> 1) * 8), the pixels of warp w).
+__device__ __forceinline__ uint32_t quad_mask(uint32_t rc) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+    if (quad_hit(rc, (w & 1) * 8, (w >> 1) * 8)) m |= 1u << w;
+  return m;
+}
+
+// Per-warp ordered list of the batch entries j < nb whose mask has bit
+// `warp`; returns the count.  (8 ballots per 256 entries instead of a
+// per-entry skip test in the blend loop.)
+template <int NB>
+__device__ __forceinline__ int warp_hit_list(const uint8_t* s_mask, int nb, int warp, int lane,
+                                             uint8_t* list) {
+  int cnt = 0;
+#pragma unroll
+  for (int c = 0; c < NB / 32; ++c) {
+    const int j = c * 32 + lane;
+    const bool hit = j < nb && ((s_mask[j] >> warp) & 1u);
+    const unsigned bal = __ballot_sync(kFull, hit);
+    if (hit) list[cnt + __popc(bal & lanemask_lt())] = static_cast<uint8_t>(j);
+    cnt += __popc(bal);
+  }
+  __syncwarp();
+  return cnt;
+}
+
 __global__ void __launch_bounds__(128) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
-    const FrameHeader* __restrict__ hdr, float* __restrict__ image, float* __restrict__ final_T, int32_t* __restrict__ counts,
-    uint32_t* __restrict__ px_last, uint32_t* __restrict__ tile_nproc) {
+    const FrameHeader* __restrict__ hdr, float* __restrict__ image,
+    float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
+    uint32_t* __restrict__ tile_nproc) {
   __shared__ __align__(128) SplatRec s_raw[256];
   __shared__ float4 s_a[256];
   __shared__ float4 s_b[256];
   __shared__ float s_c[256];
-  __shared__ uint32_t s_r[256];
+  __shared__ uint8_t s_mask[256];
+  __shared__ uint8_t s_list[4][256];
   __shared__ uint32_t s_max[4];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
@@ -129,6 +160,7 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
   const int n = static_cast<int>(rg.y - rg.x);
   const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
   const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+  uint8_t* my_list = s_list[warp];
 
   PixState p0{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in0};
   PixState p1{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in1};
@@ -153,7 +185,7 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
       s_a[k] = a;
       s_b[k] = b;
       s_c[k] = c;
-      s_r[k] = local_rect(s_raw[k], tx * kTile, ty * kTile);
+      s_mask[k] = static_cast<uint8_t>(quad_mask(local_rect(s_raw[k], tx * kTile, ty * kTile)));
     }
     __syncthreads();
     if (b0 + 256 < n) {
@@ -161,9 +193,10 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
       issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + 256, min(256, n - b0 - 256), tid, 128);
       pending = true;
     }
+    const int hits = warp_hit_list<256>(s_mask, nb, warp, lane, my_list);
     if (!(p0.done && p1.done)) {
-      for (int j = 0; j < nb; ++j) {
-        if (!quad_hit(s_r[j], qx, qy)) continue;  // warp-uniform, exact (see header)
+      for (int i = 0; i < hits; ++i) {  // splats whose box meets this warp's quadrant
+        const int j = my_list[i];
         const float4 a = s_a[j];
         const float4 b = s_b[j];
         const float dx = a.x + flx;
@@ -255,6 +288,13 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const
   return true;
 }
 
+// Batches of kBwdBatch splats, last batch first.  Staging writes, per
+// splat, the mask of warps that will process it (box meets the warp's
+// quadrant and k < the warp's last index); each warp walks its ordered hit
+// list backwards and stores its 9 reduced values per hit in its own s_red
+// slice; the combine sums the present warps in fixed order.
+constexpr int kBwdBatch = 128;
+
 __global__ void __launch_bounds__(128) raster_bwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
@@ -262,13 +302,16 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
     const float* __restrict__ final_T, const float* __restrict__ dL,
     float* __restrict__ partials) {
-  __shared__ __align__(128) SplatRec s_raw[256];
-  __shared__ float4 s_a[256];
-  __shared__ float4 s_b[256];
-  __shared__ float4 s_n[256];  // natural conic A, B, C and blue
-  __shared__ float s_io[256];  // 1 / opacity
-  __shared__ uint32_t s_r[256];
-  __shared__ float s_red[4][32][9];
+  constexpr int B = kBwdBatch;
+  __shared__ __align__(128) SplatRec s_raw[B];
+  __shared__ float4 s_a[B];
+  __shared__ float4 s_b[B];
+  __shared__ float4 s_n[B];  // natural conic A, B, C and blue
+  __shared__ float s_io[B];  // 1 / opacity
+  __shared__ uint8_t s_mask[B];
+  __shared__ uint8_t s_list[4][B];
+  __shared__ float s_red[4][B][9];
+  __shared__ uint32_t s_wlast[4];
   __shared__ __align__(8) uint64_t s_bar;
   if (fh->stats.overflow) return;
   const int tile = static_cast<int>(order[blockIdx.x]);
@@ -286,6 +329,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   const uint2 rg = ranges[tile];
   const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
   const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+  uint8_t* my_list = s_list[warp];
 
   PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
   PixBwd q1 = q0;
@@ -309,14 +353,15 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   uint32_t wlast = max(q0.last, q1.last);  // warp-uniform upper bound of k
 #pragma unroll
   for (int k = 16; k > 0; k >>= 1) wlast = max(wlast, __shfl_xor_sync(kFull, wlast, k));
+  if (lane == 0) s_wlast[warp] = wlast;
 
   if (tid == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   uint32_t phase = 0;
-  int b0 = ((nproc - 1) / 256) * 256;
-  issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(256, nproc - b0), tid, 128);
-  for (; b0 >= 0; b0 -= 256) {
-    const int nb = min(256, nproc - b0);
+  int b0 = ((nproc - 1) / B) * B;
+  issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(B, nproc - b0), tid, 128);
+  for (; b0 >= 0; b0 -= B) {
+    const int nb = min(B, nproc - b0);
     mbar_wait(&s_bar, phase);
     phase ^= 1;
     for (int k = tid; k < nb; k += 128) {
@@ -329,47 +374,51 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       s_n[k] = make_float4(static_cast<float>(r.ca), static_cast<float>(r.cb),
                            static_cast<float>(r.cc), c);
       s_io[k] = 1.0f / r.opac;
-      s_r[k] = local_rect(r, tx * kTile, ty * kTile);
+      uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);
+      s_mask[k] = static_cast<uint8_t>(m);
     }
     __syncthreads();
     if (b0 > 0) {
       fence_proxy_async_smem();
-      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - 256, 256, tid, 128);
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
     }
-    for (int se = nb; se > 0; se -= 32) {
-      const int ss = se > 32 ? se - 32 : 0;
-      for (int j = se - 1; j >= ss; --j) {
-        const uint32_t k = static_cast<uint32_t>(b0 + j);
-        float red = 0.0f;
-        if (k < wlast && quad_hit(s_r[j], qx, qy)) {  // warp-uniform skip
-          float o[9];
+    const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
+    for (int i = hits - 1; i >= 0; --i) {
+      const int j = my_list[i];
+      const uint32_t k = static_cast<uint32_t>(b0 + j);
+      float o[9];
 #pragma unroll
-          for (int u = 0; u < 9; ++u) o[u] = 0.0f;
-          const float4 a = s_a[j];
-          const float4 b = s_b[j];
-          const float4 nc = s_n[j];
-          const float io = s_io[j];
-          const float dx = a.x + flx;
-          const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
-          const float t0 = a.z * dx * dx, t1 = a.w * dx;
-          const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
-          const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
-          bool any = bwd_pixel(q0, k, al0, b, nc, io, dx, dy0, o);
-          any = bwd_pixel(q1, k, al1, b, nc, io, dx, dy1, o) || any;
-          // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
-          if (__any_sync(kFull, any)) red = warp_reduce9(o);
-        }
-        if (slot >= 0) s_red[warp][j - ss][slot] = red;
-      }
-      __syncthreads();
-      const int cnt = (se - ss) * 9;
-      for (int e = tid; e < cnt; e += 128) {
-        const int jj = e / 9, u = e - jj * 9;
-        const float acc = (s_red[0][jj][u] + s_red[1][jj][u]) + (s_red[2][jj][u] + s_red[3][jj][u]);
-        partials[(static_cast<int64_t>(rg.x) + b0 + ss + jj) * 9 + u] = acc;
-      }
-      __syncthreads();
+      for (int u = 0; u < 9; ++u) o[u] = 0.0f;
+      const float4 a = s_a[j];
+      const float4 b = s_b[j];
+      const float4 nc = s_n[j];
+      const float io = s_io[j];
+      const float dx = a.x + flx;
+      const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
+      const float t0 = a.z * dx * dx, t1 = a.w * dx;
+      const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
+      const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
+      bool any = bwd_pixel(q0, k, al0, b, nc, io, dx, dy0, o);
+      any = bwd_pixel(q1, k, al1, b, nc, io, dx, dy1, o) || any;
+      // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
+      float red = 0.0f;
+      if (__any_sync(kFull, any)) red = warp_reduce9(o);
+      if (slot >= 0) s_red[warp][j][slot] = red;
     }
+    __syncthreads();
+    for (int e = tid; e < nb * 9; e += 128) {
+      const int jj = e / 9, u = e - jj * 9;
+      const uint32_t m = s_mask[jj];
+      const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
+      const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
+      const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
+      const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
+      partials[(static_cast<int64_t>(rg.x) + b0 + jj) * 9 + u] = (r0 + r1) + (r2 + r3);
+    }
+    __syncthreads();
   }
 }
 
