@@ -6,24 +6,22 @@
 
 namespace cgs {
 
-// Tiles whose list is at most this long are depth-sorted in shared memory
-// (bitonic); longer lists take a stable in-CTA radix path through global
-// scratch.
-constexpr int kTileSortCap = 4096;
 
 struct FrameLayout {
   FrameHeader* hdr;
   SplatRec* recs;          // V*N
   uint64_t* depth_key;     // V*N (f64 bits of camera z)
+  uint32_t* dkey;          // V*N 32-bit depth sort keys
+  uint32_t* dval;          // V*N depth sort payload (splat ids); depth rank -> splat
+  SortWs<uint32_t> dsort;
   uint32_t* n_tiles;       // V*N
   uint64_t* rect;          // V*N packed tile rect
-  uint64_t* pair_off;      // V*N exclusive pair offsets (index order)
+  uint64_t* pair_off;      // V*N per splat: first emission index of its pairs
   void* pkeys;             // pair_cap tile keys (u16 or u32)
   uint32_t* pvals;         // pair_cap splat ids
   SortWs<uint16_t> psort16;
   SortWs<uint32_t> psort32;
   uint32_t* inv;           // pair_cap: emission index -> final pair position
-  uint32_t* scratch;       // pair_cap: long-tile radix scratch
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
   uint32_t* tile_nproc;    // total_tiles
@@ -85,6 +83,9 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.hdr = c.take<FrameHeader>(1);
   L.recs = c.take<SplatRec>(vn1);
   L.depth_key = c.take<uint64_t>(vn1);
+  L.dkey = c.take<uint32_t>(vn1);
+  L.dval = c.take<uint32_t>(vn1);
+  L.dsort = carve_sort<uint32_t>(c, vn1);
   L.n_tiles = c.take<uint32_t>(vn1);
   L.rect = c.take<uint64_t>(vn1);
   L.pair_off = c.take<uint64_t>(vn1);
@@ -97,7 +98,6 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   }
   L.pvals = c.take<uint32_t>(pc);
   L.inv = c.take<uint32_t>(pc);
-  L.scratch = c.take<uint32_t>(pc);
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
@@ -133,7 +133,7 @@ __device__ __forceinline__ uint64_t emission_index(const uint64_t* pair_off, con
   const uint64_t rc = rect[s];
   const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
   const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
-  const int v = static_cast<int>(s / static_cast<uint64_t>(n));
+  const int v = static_cast<int>(s / static_cast<uint32_t>(n));
   const int lt = tile - fd.cam[v].tile_base;
   const int ty = lt / fd.cam[v].ntx, tx = lt - ty * fd.cam[v].ntx;
   return pair_off[s] + static_cast<uint64_t>((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));

@@ -2,14 +2,18 @@
 //
 //   sr_precompute   Sigma3 per SR codebook row (render.py:85-91, 168-169)
 //   project         per (view, Gaussian): fp64 EWA projection, codebook gather,
-//                   SH colour, pixel/tile rect, depth key (render.py:145-203,110-115)
-//   pair offsets    one decoupled-lookback scan over the splats' tile counts
-//   emit + sort     (tile, splat) pairs in splat index order, stable onesweep
-//                   radix sort by tile id
-//   tile sort       per tile, stable sort by fp64 camera depth -- together with
-//                   the stable tile sort this is exactly the per-tile append
-//                   order of _bin_tiles over np.lexsort((idx, tz))
-//                   (render.py:203, 240-254)
+//                   SH colour, pixel/tile rect, depth keys (render.py:145-203,110-115)
+//   depth order     all splats of the frame, one stable LSD onesweep on the
+//                   fp32-rounded-toward-zero depth (monotone in the fp64 depth),
+//                   input in splat index order; runs of equal 32-bit keys are
+//                   re-sorted by the exact fp64 depth (stable insertion sort).
+//                   = np.lexsort((idx, tz)) (render.py:203), per view
+//   pair offsets    one decoupled-lookback scan over the splats' tile counts in
+//                   depth order
+//   emit + sort     (tile, splat) pairs in depth order, stable onesweep radix
+//                   sort by tile id: the per-tile append order of _bin_tiles
+//                   (render.py:240-254)
+//   inverse map     emission index -> final pair position (for the backward)
 //   raster_fwd      raster.cu
 #include <cmath>
 
@@ -65,6 +69,8 @@ struct ProjIn {
 struct ProjOut {
   SplatRec* recs;
   uint64_t* depth_key;
+  uint32_t* dkey;  // 32-bit depth sort key (~0 for splats without tiles)
+  uint32_t* dval;  // splat id (sort payload)
   uint32_t* n_tiles;
   uint64_t* rect;
   FrameHeader* hdr;
@@ -85,6 +91,8 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
     const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
     const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
     const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
+    out.dval[s] = static_cast<uint32_t>(s);
+    out.dkey[s] = 0xffffffffu;
     if (!(tz > kNear)) {  // near-plane cull, render.py:149
       out.n_tiles[s] = 0;
       continue;
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
     }
     out.recs[s] = rec;
     out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
+    out.dkey[s] = __float_as_uint(__double2float_rz(tz));  // tz > 0: monotone bits
     out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
     out.rect[s] = static_cast<uint64_t>(tx0) | (static_cast<uint64_t>(tx1) << 16) |
                   (static_cast<uint64_t>(ty0) << 32) | (static_cast<uint64_t>(ty1) << 48);
@@ -204,16 +213,48 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
 }
 
 // ---------------------------------------------------------------------------
-// Pair offsets in splat index order.  One scan carries both the pair count
-// (low 40 bits) and the on-screen splat count (high bits).
+// Exact order inside runs of equal 32-bit depth keys: a stable insertion sort
+// of the run by the fp64 depth bits (positive doubles order as integers), so
+// ties of the fp64 depth keep splat index order.  Runs are short (a handful
+// of splats even at 4M Gaussians).  Splats without tiles (key ~0) are last
+// and untouched.
+__global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __restrict__ key,
+                                                            uint32_t* __restrict__ val,
+                                                            const uint64_t* __restrict__ depth_key,
+                                                            int64_t vn) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i + 1 < vn;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = key[i];
+    if (k == 0xffffffffu || key[i + 1] != k || (i > 0 && key[i - 1] == k)) continue;
+    int64_t e = i + 1;
+    while (e < vn && key[e] == k) ++e;
+    for (int64_t a = i + 1; a < e; ++a) {
+      const uint32_t va = val[a];
+      const uint64_t ka = depth_key[va];
+      int64_t b = a - 1;
+      while (b >= i && depth_key[val[b]] > ka) {
+        val[b + 1] = val[b];
+        --b;
+      }
+      val[b + 1] = va;
+    }
+  }
+}
+
+// Pair offsets in depth order (perm = depth rank -> splat), stored per splat.
+// One scan carries both the pair count (low 40 bits) and the on-screen splat
+// count (high bits).
 struct PairOffsets {
+  const uint32_t* perm;
   const uint32_t* n_tiles;
   uint64_t* off;
-  __device__ uint64_t load(int64_t s) const {
-    const uint64_t c = n_tiles[s];
+  __device__ uint64_t load(int64_t r) const {
+    const uint64_t c = n_tiles[perm[r]];
     return c | (c ? (1ULL << 40) : 0ULL);
   }
-  __device__ void store(int64_t s, uint64_t ex, uint64_t) const { off[s] = ex & ((1ULL << 40) - 1); }
+  __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
+    if (v) off[perm[r]] = ex & ((1ULL << 40) - 1);
+  }
 };
 
 __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views) {
@@ -230,22 +271,26 @@ __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n
   hdr->stats.n_views = n_views;
 }
 
-// Warp-cooperative pair emission in splat index order: a warp takes 32
-// consecutive splats and writes their concatenated pair range with all 32
-// lanes (a near-plane splat covering every tile does not serialise a thread).
-// Within one splat, tiles are emitted row-major over its tile rect.
+// Warp-cooperative pair emission in depth order: a warp takes 32
+// consecutive depth ranks (whose pair ranges are contiguous) and writes their
+// concatenated pair range with all 32 lanes (a near-plane splat covering
+// every tile does not serialise a thread).  Within one splat, tiles are
+// emitted row-major over its tile rect.
 template <typename KT>
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
-    const uint64_t* __restrict__ off, const uint32_t* __restrict__ n_tiles,
-    const uint64_t* __restrict__ rect, const FrameHeader* __restrict__ hdr, FrameDesc fd,
-    int64_t n, int64_t vn, KT* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
+    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
+    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, int64_t vn,
+    KT* __restrict__ keys, uint32_t* __restrict__ vals) {
   if (hdr->stats.overflow) return;
   const int lane = threadIdx.x & 31;
+  const int64_t ns = static_cast<int64_t>(hdr->n_onscreen);  // ranks with tiles come first
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w * 32 < vn;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w * 32 < ns;
        w += warps) {
-    const int64_t s = w * 32 + lane;
-    const bool ok = s < vn;
+    const int64_t r = w * 32 + lane;
+    const bool ok = r < ns;
+    const uint32_t s = ok ? perm[r] : 0u;
     const uint64_t cnt = ok ? n_tiles[s] : 0ULL;
     const uint64_t o = ok ? off[s] : ~0ULL;
     uint64_t e = ok ? o + cnt : 0ULL;
@@ -255,9 +300,9 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
       e = t > e ? t : e;
     }
     const uint64_t start = __shfl_sync(kFull, o, 0);
-    if (start >= e) continue;  // no pairs in this group of splats
-    const uint64_t rc = (ok && cnt) ? rect[s] : 0ULL;
-    const int v = ok ? static_cast<int>(s / n) : 0;
+    if (start >= e) continue;
+    const uint64_t rc = ok ? rect[s] : 0ULL;
+    const int v = ok ? static_cast<int>(s / static_cast<uint32_t>(n)) : 0;
     const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
     const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
     const int span = tx1 - tx0 + 1;
@@ -278,11 +323,12 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
       const int by = __shfl_sync(kFull, ty0, owner);
       const int nt = __shfl_sync(kFull, ntx, owner);
       const int tb = __shfl_sync(kFull, tbase, owner);
+      const uint32_t so = __shfl_sync(kFull, s, owner);
       if (p < e) {
         const int k = static_cast<int>(p - oo);
         const int ty = by + k / sp, tx = bx + k % sp;
         keys[p] = static_cast<KT>(tb + ty * nt + tx);
-        vals[p] = static_cast<uint32_t>(w * 32 + owner);
+        vals[p] = so;
       }
     }
   }
@@ -302,228 +348,18 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const KT* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// Per-tile depth order.  After the stable tile sort each tile's list holds
-// its splats in index order; a stable sort by depth then reproduces
-// np.lexsort((idx, tz)) restricted to the tile (render.py:203, 247-253).
-//
-// Lists up to kTileSortCap: a bitonic sort held in registers (S = 256*E
-// slots, E = 1..16 per thread, thread-major, padded with +inf) on the
-// unique 64-bit key (fp32 depth rounded toward zero, which is monotone in
-// the fp64 depth) << 32 | splat id, so equal 32-bit depths fall back to index
-// order; strides below E are in-register compare-exchanges, strides below 32E
-// warp shuffles, the rest go through shared memory.  Runs of equal 32-bit
-// depth -- rare -- are then re-sorted by the exact fp64 key with a stable
-// insertion sort, which gives (fp64 depth, index) order.  Longer lists take a
-// stable in-CTA 8-pass radix on the fp64 bits through global scratch.  CTAs
-// take tiles longest-first (tile_order).  The kernel also records
-// inv[emission index] = final position for the backward.
-struct TileSortSmem {
-  union {
-    uint64_t key[kTileSortCap];
-    struct {
-      uint32_t wcnt[8][256];
-      uint32_t base[256];
-    } radix;
-  };
-};
-
-__device__ __forceinline__ uint32_t depth_key32(uint64_t bits) {
-  return __float_as_uint(__double2float_rz(__longlong_as_double(static_cast<long long>(bits))));
-}
-
-// Slot x = tid * E + e lives in smem at x ^ ((x / E) & (E - 1)) (spreads a
-// warp's accesses over the banks).
-template <int E>
-__device__ __forceinline__ int swz(int x) {
-  return x ^ ((x / E) & (E - 1));
-}
-
-template <int NT, int E>
-__device__ __forceinline__ void bitonic_regs(uint64_t (&key)[E], uint64_t* sm, int tid) {
-  constexpr int S = NT * E;
-  for (int k = 2; k <= S; k <<= 1) {
-    int j = k >> 1;
-    for (; j >= 32 * E; j >>= 1) {  // across warps
-#pragma unroll
-      for (int e = 0; e < E; ++e) sm[swz<E>(tid * E + e)] = key[e];
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int x = tid * E + e;
-        const uint64_t o = sm[swz<E>(x ^ j)];
-        const bool keep_min = ((x & k) == 0) == ((x & j) == 0);
-        key[e] = keep_min ? (o < key[e] ? o : key[e]) : (o > key[e] ? o : key[e]);
-      }
-      __syncthreads();
-    }
-    for (; j >= E; j >>= 1) {  // across lanes
-      const int lm = j / E;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int x = tid * E + e;
-        const uint64_t o = __shfl_xor_sync(kFull, key[e], lm);
-        const bool keep_min = ((x & k) == 0) == ((x & j) == 0);
-        key[e] = keep_min ? (o < key[e] ? o : key[e]) : (o > key[e] ? o : key[e]);
-      }
-    }
-#pragma unroll
-    for (int jj = E / 2; jj > 0; jj >>= 1) {  // inside a thread
-      if (jj > j) continue;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (e & jj) continue;
-        const int p = e ^ jj;
-        const bool asc = ((tid * E + e) & k) == 0;
-        const uint64_t lo = key[e] < key[p] ? key[e] : key[p];
-        const uint64_t hi = key[e] < key[p] ? key[p] : key[e];
-        key[e] = asc ? lo : hi;
-        key[p] = asc ? hi : lo;
-      }
-    }
-  }
-}
-
-template <int NT, int E>
-__device__ __forceinline__ void sort_tile_short(TileSortSmem& S, uint32_t* seg, int len, int tile,
-                                                uint32_t first, const uint64_t* __restrict__ depth_key,
-                                                const uint64_t* __restrict__ pair_off,
-                                                const uint64_t* __restrict__ rect,
-                                                uint32_t* __restrict__ inv, const FrameDesc& fd,
-                                                int64_t n, int tid) {
-  uint64_t key[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int x = tid * E + e;
-    if (x < len) {
-      const uint32_t sp = seg[x];
-      key[e] = (static_cast<uint64_t>(depth_key32(depth_key[sp])) << 32) | sp;
-    } else {
-      key[e] = ~0ULL;
-    }
-  }
-  bitonic_regs<NT, E>(key, S.key, tid);
-  __syncthreads();
-#pragma unroll
-  for (int e = 0; e < E; ++e) S.key[tid * E + e] = key[e];  // sorted position order
-  __syncthreads();
-  // exact order inside runs of equal 32-bit depth (stable insertion sort on fp64 bits)
-  for (int j = tid; j < len; j += NT) {
-    const uint32_t k = static_cast<uint32_t>(S.key[j] >> 32);
-    if ((j == 0 || static_cast<uint32_t>(S.key[j - 1] >> 32) != k) && j + 1 < len &&
-        static_cast<uint32_t>(S.key[j + 1] >> 32) == k) {
-      int e = j + 1;
-      while (e < len && static_cast<uint32_t>(S.key[e] >> 32) == k) ++e;
-      for (int a = j + 1; a < e; ++a) {
-        const uint64_t va = S.key[a];
-        const uint64_t ka = depth_key[static_cast<uint32_t>(va)];
-        int b = a - 1;
-        while (b >= j && depth_key[static_cast<uint32_t>(S.key[b])] > ka) {
-          S.key[b + 1] = S.key[b];
-          --b;
-        }
-        S.key[b + 1] = va;
-      }
-    }
-  }
-  __syncthreads();
-  for (int j = tid; j < len; j += NT) {
-    const uint32_t sp = static_cast<uint32_t>(S.key[j]);
-    seg[j] = sp;
-    inv[emission_index(pair_off, rect, fd, n, sp, tile)] = first + j;
-  }
-}
-
-// Three launches over the longest-first tile order, one per list class:
-//   0: len <= 2048, 256 threads, E <= 8      1: 2048 < len <= 4096, 512 threads, E = 8
-//   2: len > 4096, stable 8-pass radix through global scratch (256 threads)
-// A CTA whose tile belongs to another class returns at once.
-template <int CLS>
-__global__ void __launch_bounds__(CLS == 1 ? 512 : 256) tile_depth_sort_kernel(
-    const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
-    uint32_t* __restrict__ vals, const uint64_t* __restrict__ depth_key,
+// inv[emission index of pair (splat, tile)] = final pair position; the
+// backward walks each splat's pairs in emission order through it.
+template <typename KT>
+__global__ void __launch_bounds__(256) pair_inverse_kernel(
+    const KT* __restrict__ keys, const uint32_t* __restrict__ vals,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect,
-    uint32_t* __restrict__ inv, uint32_t* __restrict__ scratch,
-    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSortSmem& S = *reinterpret_cast<TileSortSmem*>(smem_raw);
-  if (hdr->stats.overflow) return;
-  const int tile = static_cast<int>(order[blockIdx.x]);
-  const uint2 rg = ranges[tile];
-  const int len = static_cast<int>(rg.y - rg.x);
-  const int tid = threadIdx.x;
-  if (len <= 0) return;
-  uint32_t* seg = vals + rg.x;
-  if constexpr (CLS == 0) {
-    if (len > 2048) return;
-    if (len <= 256)
-      sort_tile_short<256, 1>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
-    else if (len <= 512)
-      sort_tile_short<256, 2>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
-    else if (len <= 1024)
-      sort_tile_short<256, 4>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
-    else
-      sort_tile_short<256, 8>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
-    return;
-  } else if constexpr (CLS == 1) {
-    if (len <= 2048 || len > kTileSortCap) return;
-    sort_tile_short<512, 8>(S, seg, len, tile, rg.x, depth_key, pair_off, rect, inv, fd, n, tid);
-    return;
-  }
-  if (len <= kTileSortCap) return;
-  const int lane = tid & 31, warp = tid >> 5;
-  // long list: stable LSD radix over the 64-bit depth key, ping-ponging
-  // between the list and its scratch slice; 256-element chunks ranked with
-  // warp match_any so equal digits keep their order.
-  uint32_t* cnt = S.radix.base;
-  uint32_t* wcnt = &S.radix.wcnt[0][0];
-  uint32_t* src = seg;
-  uint32_t* dst = scratch + rg.x;
-  for (int pass = 0; pass < 8; ++pass) {
-    const int shift = 8 * pass;
-    cnt[tid] = 0;
-    __syncthreads();
-    for (int j = tid; j < len; j += 256) atomicAdd(&cnt[(depth_key[src[j]] >> shift) & 255u], 1u);
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t run = 0;
-      for (int d = 0; d < 256; ++d) {
-        const uint32_t c = cnt[d];
-        cnt[d] = run;
-        run += c;
-      }
-    }
-    __syncthreads();
-    for (int c0 = 0; c0 < len; c0 += 256) {
-      const int j = c0 + tid;
-      const bool ok = j < len;
-      const uint32_t s = ok ? src[j] : 0u;
-      const unsigned d = ok ? static_cast<unsigned>((depth_key[s] >> shift) & 255u) : 256u + lane;
-      for (int q = tid; q < 8 * 256; q += 256) wcnt[q] = 0;
-      __syncthreads();
-      const unsigned peers = __match_any_sync(kFull, d);
-      const uint32_t rank = __popc(peers & lanemask_lt());
-      if (ok && lane == __ffs(peers) - 1) wcnt[warp * 256 + d] = __popc(peers);
-      __syncthreads();
-      if (ok) {
-        uint32_t before = 0;
-        for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2 * 256 + d];
-        dst[cnt[d] + before + rank] = s;
-      }
-      __syncthreads();
-      {
-        uint32_t add = 0;
-        for (int w2 = 0; w2 < 8; ++w2) add += wcnt[w2 * 256 + tid];
-        cnt[tid] += add;
-      }
-      __syncthreads();
-    }
-    uint32_t* t = src;
-    src = dst;
-    dst = t;
-  }
-  // 8 passes: the result is back in seg
-  for (int j = tid; j < len; j += 256)
-    inv[emission_index(pair_off, rect, fd, n, seg[j], tile)] = rg.x + j;
+    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ inv) {
+  const int64_t np = static_cast<int64_t>(hdr->n_pairs);
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < np;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    inv[emission_index(pair_off, rect, fd, n, vals[p], static_cast<int>(keys[p]))] =
+        static_cast<uint32_t>(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -535,13 +371,14 @@ static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut&
 }
 
 template <typename KT>
-static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws, cudaStream_t st) {
+static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
+                           const uint32_t* perm, cudaStream_t st) {
   KT* kres;
   uint32_t* vres;
   const int eg = grid_for(L.vn, 256, 16);
   CGS_PROFILED("emit_pairs_kernel", st,
-               emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(L.pair_off, L.n_tiles, L.rect, L.hdr, fd,
-                                                          L.n, L.vn, static_cast<KT*>(L.pkeys),
+               emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.pair_off, L.n_tiles, L.rect, L.hdr,
+                                                          fd, L.n, L.vn, static_cast<KT*>(L.pkeys),
                                                           L.pvals));
   CGS_CHECK_LAUNCH("emit_pairs_kernel");
   int rc = launch_radix_sort<KT>(static_cast<KT*>(L.pkeys), L.pvals, &L.hdr->n_pairs, 0,
@@ -550,6 +387,9 @@ static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws, 
   CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * (fd.total_tiles > 0 ? fd.total_tiles : 1), st));
   tile_ranges_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(kres, L.hdr, L.ranges);
   CGS_CHECK_LAUNCH("tile_ranges_kernel");
+  pair_inverse_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(
+      kres, vres, L.pair_off, L.rect, L.hdr, fd, L.n, L.inv);
+  CGS_CHECK_LAUNCH("pair_inverse_kernel");
   return CGS_OK;
 }
 
@@ -565,7 +405,7 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   }
   if (vn > 0) {
     ProjIn in{sc->n, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, sr_cov};
-    ProjOut out{L.recs, L.depth_key, L.n_tiles, L.rect, L.hdr};
+    ProjOut out{L.recs, L.depth_key, L.dkey, L.dval, L.n_tiles, L.rect, L.hdr};
     switch (sc->sh_degree) {
       case 0: launch_project<0>(in, fd, out, vn, st); break;
       case 1: launch_project<1>(in, fd, out, vn, st); break;
@@ -574,43 +414,31 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
     }
     CGS_CHECK_LAUNCH("project_kernel");
   }
-  int rc = launch_scan(PairOffsets{L.n_tiles, L.pair_off}, nullptr, vn, vn, L.scan,
+  // depth order of every splat of the frame (all views; the tile sort below
+  // separates the views again)
+  uint32_t* perm = L.dval;
+  if (vn > 0) {
+    uint32_t* kres;
+    int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, nullptr, vn, vn, 32, L.dsort, &kres, &perm,
+                                         st);
+    if (rc) return rc;
+    CGS_PROFILED("depth_tie_fix_kernel", st,
+                 depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(kres, perm,
+                                                                           L.depth_key, vn));
+    CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
+  }
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off}, nullptr, vn, vn, L.scan,
                        &L.hdr->scratch[0], st);
   if (rc) return rc;
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
-  rc = L.tile_key_bytes == 2 ? emit_sort_range<uint16_t>(L, fd, L.psort16, st)
-                             : emit_sort_range<uint32_t>(L, fd, L.psort32, st);
+  rc = L.tile_key_bytes == 2 ? emit_sort_range<uint16_t>(L, fd, L.psort16, perm, st)
+                             : emit_sort_range<uint32_t>(L, fd, L.psort32, perm, st);
   if (rc) return rc;
   if (fd.total_tiles > 0) {
-    static bool attr = false;
-    const int smem = static_cast<int>(sizeof(TileSortSmem));
-    if (!attr) {
-      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<0>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      CGS_CUDA(cudaFuncSetAttribute(tile_depth_sort_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    uint32_t* vals = sorted_pair_vals(L);
     rc = launch_tile_order(fd, L, nullptr, st);
     if (rc) return rc;
-    CGS_PROFILED("tile_depth_sort_kernel", st,
-                 tile_depth_sort_kernel<0><<<fd.total_tiles, 256, 2048 * sizeof(uint64_t), st>>>(
-                     L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv,
-                     L.scratch, L.hdr, fd, L.n));
-    CGS_CHECK_LAUNCH("tile_depth_sort_kernel");
-    tile_depth_sort_kernel<1><<<fd.total_tiles, 512, smem, st>>>(
-        L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr,
-        fd, L.n);
-    CGS_CHECK_LAUNCH("tile_depth_sort_kernel_mid");
-    tile_depth_sort_kernel<2><<<fd.total_tiles, 256, smem, st>>>(
-        L.tile_order, L.ranges, vals, L.depth_key, L.pair_off, L.rect, L.inv, L.scratch, L.hdr,
-        fd, L.n);
-    CGS_CHECK_LAUNCH("tile_depth_sort_kernel_long");
-    rc = launch_raster_fwd(fd, L, vals, image, final_T, counts, st);
+    rc = launch_raster_fwd(fd, L, sorted_pair_vals(L), image, final_T, counts, st);
     if (rc) return rc;
   }
   return CGS_OK;

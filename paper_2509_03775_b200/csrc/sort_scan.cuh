@@ -223,7 +223,14 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ ke
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t k = static_cast<uint64_t>(keys[i]);
-    for (int p = 0; p < passes; ++p) atomicAdd(&s_h[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
+    // warp-aggregated: skewed digits (e.g. the exponent byte of depths) would
+    // otherwise serialise 32 lanes on one shared-memory counter
+    const unsigned active = __activemask();
+    for (int p = 0; p < passes; ++p) {
+      const unsigned d = static_cast<unsigned>((k >> (8 * p)) & 255u);
+      const unsigned peers = __match_any_sync(active, d);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
@@ -320,17 +327,21 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     st_volatile(st, kSortPre | agg);
   } else {
     st_volatile(st, kSortAgg | agg);
-    // Windowed lookback: 8 independent status loads per round trip, consumed
-    // in order until an inclusive prefix is found (an unpublished slot makes
-    // the next window start there).
+    // Windowed lookback: kLookback independent status loads per round trip,
+    // consumed in order until an inclusive prefix is found (an unpublished
+    // slot makes the next window start there).  All partitions start
+    // together, so partition p typically walks back ~p slots before it meets
+    // an inclusive prefix: the window width sets the number of L2 round trips.
+    constexpr int kLookback = 32;
     int64_t p = part - 1;
     bool done = false;
     while (!done) {
-      uint32_t s[8];
+      uint32_t s[kLookback];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s[k] = (p - k >= 0) ? ld_volatile(status + (p - k) * 256 + d) : kSortPre;
+      for (int k = 0; k < kLookback; ++k)
+        s[k] = (p - k >= 0) ? ld_volatile(status + (p - k) * 256 + d) : kSortPre;
       int k = 0;
-      for (; k < 8; ++k) {
+      for (; k < kLookback; ++k) {
         const uint32_t flag = s[k] >> 30;
         if (flag == 0) break;
         excl += s[k] & kSortVal;
