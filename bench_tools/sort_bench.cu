@@ -1,0 +1,77 @@
+// Standalone timing of the radix sort / scan primitives (sort_scan.cuh) at
+// the sizes of the frame pipeline.  nvcc -gencode arch=compute_100a,code=sm_100a
+//   -O3 -I include bench_tools/sort_bench.cu -o bench_tools/sort_bench
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "../paper_2509_03775_b200/csrc/sort_scan.cuh"
+
+namespace cgs {
+void set_error(const std::string& m) { fprintf(stderr, "%s\n", m.c_str()); }
+int cuda_status(cudaError_t e, const char* w) {
+  fprintf(stderr, "%s: %s\n", w, cudaGetErrorString(e));
+  return 2;
+}
+void note_launch() {}
+ProfScope::ProfScope(const char*, cudaStream_t s) : on(false), st(s) {}
+ProfScope::~ProfScope() {}
+}  // namespace cgs
+
+template <typename K>
+static void run(int64_t n, int bits, int reps) {
+  using namespace cgs;
+  std::vector<K> hk(n);
+  std::vector<uint32_t> hv(n);
+  uint64_t x = 88172645463325252ULL;
+  for (int64_t i = 0; i < n; ++i) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    hk[i] = static_cast<K>(x & ((bits >= 64) ? ~0ULL : ((1ULL << bits) - 1)));
+    hv[i] = static_cast<uint32_t>(i);
+  }
+  K* dk; uint32_t* dv; K* k0; uint32_t* v0;
+  cudaMalloc(&dk, n * sizeof(K)); cudaMalloc(&dv, n * 4);
+  cudaMalloc(&k0, n * sizeof(K)); cudaMalloc(&v0, n * 4);
+  cudaMemcpy(k0, hk.data(), n * sizeof(K), cudaMemcpyHostToDevice);
+  cudaMemcpy(v0, hv.data(), n * 4, cudaMemcpyHostToDevice);
+  size_t wsb = sort_ws_bytes<K>(n) + 4096;
+  void* ws; cudaMalloc(&ws, wsb);
+  Carver c(ws, wsb);
+  SortWs<K> w = carve_sort<K>(c, n);
+  cudaStream_t st; cudaStreamCreate(&st);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  K* ko; uint32_t* vo;
+  float best = 1e9;
+  for (int r = 0; r < reps; ++r) {
+    cudaMemcpyAsync(dk, k0, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dv, v0, n * 4, cudaMemcpyDeviceToDevice, st);
+    cudaEventRecord(a, st);
+    launch_radix_sort<K>(dk, dv, nullptr, n, n, bits, w, &ko, &vo, st);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    if (r > 0 && ms < best) best = ms;
+  }
+  std::vector<K> rk(n); std::vector<uint32_t> rv(n);
+  cudaMemcpy(rk.data(), ko, n * sizeof(K), cudaMemcpyDeviceToHost);
+  cudaMemcpy(rv.data(), vo, n * 4, cudaMemcpyDeviceToHost);
+  bool ok = true;
+  for (int64_t i = 1; i < n; ++i)
+    if (rk[i - 1] > rk[i] || (rk[i - 1] == rk[i] && rv[i - 1] > rv[i])) { ok = false; break; }
+  printf("n=%9lld key=%zuB bits=%2d passes=%d  %8.1f us  (%.1f us/pass) %s\n", (long long)n,
+         sizeof(K), bits, (bits + 7) / 8, best * 1000, best * 1000 / ((bits + 7) / 8),
+         ok ? "sorted+stable" : "WRONG");
+  cudaFree(dk); cudaFree(dv); cudaFree(k0); cudaFree(v0); cudaFree(ws);
+}
+
+int main(int argc, char** argv) {
+  const int only = argc > 1 ? atoi(argv[1]) : -1;
+  if (only < 0 || only == 0) run<uint32_t>(100000, 32, 20);
+  if (only < 0 || only == 1) run<uint32_t>(400000, 32, 20);
+  if (only < 0 || only == 2) run<uint32_t>(4000000, 32, 10);
+  if (only < 0 || only == 3) run<uint16_t>(1100000, 10, 20);
+  if (only < 0 || only == 4) run<uint16_t>(1600000, 16, 20);
+  if (only < 0 || only == 5) run<uint32_t>(12000000, 14, 10);
+  return 0;
+}
