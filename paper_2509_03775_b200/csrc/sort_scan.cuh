@@ -34,6 +34,19 @@ __device__ __forceinline__ int64_t dev_count(const unsigned long long* n_dev, in
   return n_dev ? static_cast<int64_t>(ld_volatile(n_dev)) : n_host;
 }
 
+// Lanes of the warp whose 8-bit digit equals this lane's (all 32 lanes must
+// call it).  Eight ballots instead of one match.any, which issues far slower.
+__device__ __forceinline__ unsigned warp_peers8(unsigned d) {
+  unsigned peers = kFull;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(kFull, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
   const int lane = threadIdx.x & 31;
@@ -168,12 +181,15 @@ int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t 
 
 // ===========================================================================
 // Onesweep LSD radix sort, 8-bit digits.  One histogram kernel for all
-// passes, then one kernel per pass: per-warp match_any ranking (stable),
+// passes, then one kernel per pass: per-warp ballot ranking (stable),
 // per-digit decoupled lookback across partitions, smem reorder, coalesced
 // scatter.  Status words: 30-bit count, flag in bits 30..31.
 // ===========================================================================
 constexpr int kSortWarps = 8;
-constexpr int kSortItems = 16;
+#ifndef CGS_SORT_ITEMS
+#define CGS_SORT_ITEMS 16
+#endif
+constexpr int kSortItems = CGS_SORT_ITEMS;
 constexpr int kSortTile = kSortWarps * 32 * kSortItems;  // 4096
 constexpr unsigned kSortAgg = 1u << 30;
 constexpr unsigned kSortPre = 2u << 30;
@@ -220,16 +236,18 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ ke
   for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
   const int64_t n = dev_count(n_dev, n_host);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = static_cast<uint64_t>(keys[i]);
-    // warp-aggregated: skewed digits (e.g. the exponent byte of depths) would
-    // otherwise serialise 32 lanes on one shared-memory counter
-    const unsigned active = __activemask();
+  // warp-aggregated (ballot peers): skewed digits, e.g. the exponent byte of
+  // depths, would otherwise serialise 32 lanes on one shared counter
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x); b < n;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = b + threadIdx.x;
+    const bool ok = i < n;
+    const uint64_t k = ok ? static_cast<uint64_t>(keys[i]) : 0ULL;
+    const unsigned valid = __ballot_sync(kFull, ok);
     for (int p = 0; p < passes; ++p) {
       const unsigned d = static_cast<unsigned>((k >> (8 * p)) & 255u);
-      const unsigned peers = __match_any_sync(active, d);
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
+      const unsigned peers = warp_peers8(d) & valid;
+      if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
     }
   }
   __syncthreads();
@@ -281,7 +299,7 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & 255u);
-    const unsigned peers = __match_any_sync(kFull, d);
+    const unsigned peers = warp_peers8(d);
     const unsigned before = wc[d];
     rank[j] = before + __popc(peers & lanemask_lt());
     __syncwarp();
@@ -332,7 +350,10 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     // slot makes the next window start there).  All partitions start
     // together, so partition p typically walks back ~p slots before it meets
     // an inclusive prefix: the window width sets the number of L2 round trips.
-    constexpr int kLookback = 32;
+#ifndef CGS_SORT_LOOKBACK
+#define CGS_SORT_LOOKBACK 32
+#endif
+    constexpr int kLookback = CGS_SORT_LOOKBACK;
     int64_t p = part - 1;
     bool done = false;
     while (!done) {
