@@ -321,12 +321,27 @@ def main():
         alg = 0
     avg_s = (prof_ms.value / max(prof_n.value, 1)) / 1000.0
     achieved = alg / avg_s / 1e9 if avg_s > 0 else 0.0
+    # DRAM bytes per launch of the same kernel from the committed ncu --set full
+    # capture (profiles/ncu_traffic.json, written by scripts/ncu_summary.py)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            t = json.load(open(tpath)).get(name)
+            if t:
+                traffic = float(t["bytes_per_launch"])
+                traffic_src = f"profiles/ncu_traffic.json ({t.get('source')}, ncu --set full)"
+        except Exception:
+            pass
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
+                "traffic": traffic, "traffic_source": traffic_src,
+                "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
                 "alg_bytes_per_launch": alg, "P_x": P_x, "pixels": px,
-                "note": "raster kernels are FP32/MUFU-bound at config 1; HBM fraction uses "
-                        "processed-prefix bytes only (SURVEY.md §8(d))"}
+                "note": "the raster kernels are instruction-issue bound (ncu: ~73% issue slots "
+                        "busy, FMA+ALU pipes, see profiles/r1_ncu_raster_bwd_config1.txt), not "
+                        "HBM bound; achieved uses processed-prefix algorithmic bytes only "
+                        "(SURVEY.md §8(d)), traffic is the ncu DRAM bytes of one launch"}
 
     # e2e: same step through the public API with host buffers (pinned H2D of the
     # step's target images, D2H of the recon loss) inside the timed region

@@ -7,6 +7,11 @@
 namespace cgs {
 
 
+// Splats with more tile pairs than this (near-plane giants cover every tile)
+// are emitted and reduced by a whole CTA each, from a list built during
+// emission, instead of by the warp that owns their depth rank.
+constexpr uint32_t kLongSplat = 256;
+
 struct FrameLayout {
   FrameHeader* hdr;
   SplatRec* recs;          // V*N
@@ -22,6 +27,7 @@ struct FrameLayout {
   SortWs<uint16_t> psort16;
   SortWs<uint32_t> psort32;
   uint32_t* inv;           // pair_cap: emission index -> final pair position
+  uint32_t* long_list;     // V*N: splats with more than kLongSplat pairs (count: hdr->scratch[2])
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
   uint32_t* tile_nproc;    // total_tiles
@@ -98,6 +104,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   }
   L.pvals = c.take<uint32_t>(pc);
   L.inv = c.take<uint32_t>(pc);
+  L.long_list = c.take<uint32_t>(vn1);
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);

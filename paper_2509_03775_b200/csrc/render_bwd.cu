@@ -279,8 +279,9 @@ __global__ void __launch_bounds__(256) splat_reduce_kernel(PairWalk pw, const Fr
 #pragma unroll
     for (int u = 0; u < 9; ++u) acc[u] = 0.0;
     bool touched = false;
-    const bool lng = cnt > 32;
-    if (cnt > 0 && !lng) touched = walk_pairs(pw, fd, n, s, cnt, 0, 1, acc);
+    const bool huge = cnt > kLongSplat;  // splat_reduce_long_kernel's (one CTA each)
+    const bool lng = cnt > 32 && !huge;
+    if (cnt > 0 && !lng && !huge) touched = walk_pairs(pw, fd, n, s, cnt, 0, 1, acc);
     unsigned mask = __ballot_sync(kFull, lng);
     while (mask) {
       const int l = __ffs(mask) - 1;
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(256) splat_reduce_kernel(PairWalk pw, const Fr
     }
     const unsigned tm = __ballot_sync(kFull, ok && touched);
     if (lane == 0 && tm) atomicAdd(&B.hdr->n_touched, static_cast<unsigned long long>(__popc(tm)));
-    if (!ok) continue;
+    if (!ok || huge) continue;
     B.touched[s] = touched ? 1 : 0;
     if (!touched) continue;
     B.acc0[s] = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
@@ -309,6 +310,48 @@ __global__ void __launch_bounds__(256) splat_reduce_kernel(PairWalk pw, const Fr
     B.acc1[s] = make_float4(static_cast<float>(acc[4]), static_cast<float>(acc[5]),
                             static_cast<float>(acc[6]), static_cast<float>(acc[7]));
     B.acc2[s] = static_cast<float>(acc[8]);
+  }
+}
+
+// Splats with more than kLongSplat pairs (listed during emission): one CTA
+// each walks the pairs with a 256 stride, then a fixed-order block reduction.
+__global__ void __launch_bounds__(256) splat_reduce_long_kernel(PairWalk pw,
+                                                                const FrameHeader* __restrict__ fh,
+                                                                const uint32_t* __restrict__ list,
+                                                                FrameDesc fd, int64_t n,
+                                                                BwdLayout B) {
+  __shared__ double s_w[8][9];
+  if (fh->stats.overflow) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nl = static_cast<int64_t>(fh->scratch[2]);
+  for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
+    const uint32_t s = list[e];
+    double acc[9];
+#pragma unroll
+    for (int u = 0; u < 9; ++u) acc[u] = 0.0;
+    const bool any = walk_pairs(pw, fd, n, s, pw.n_tiles[s], tid, 256, acc);
+#pragma unroll
+    for (int u = 0; u < 9; ++u) acc[u] = warp_sum(acc[u]);
+    if (lane == 0)
+#pragma unroll
+      for (int u = 0; u < 9; ++u) s_w[warp][u] = acc[u];
+    const bool touched = __syncthreads_or(any);
+    if (tid == 0 && touched) {
+      double t[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        t[u] = s_w[0][u];
+        for (int w = 1; w < 8; ++w) t[u] += s_w[w][u];
+      }
+      B.touched[s] = 1;
+      B.acc0[s] = make_float4(static_cast<float>(t[0]), static_cast<float>(t[1]),
+                              static_cast<float>(t[2]), static_cast<float>(t[3]));
+      B.acc1[s] = make_float4(static_cast<float>(t[4]), static_cast<float>(t[5]),
+                              static_cast<float>(t[6]), static_cast<float>(t[7]));
+      B.acc2[s] = static_cast<float>(t[8]);
+      atomicAdd(&B.hdr->n_touched, 1ULL);
+    }
+    __syncthreads();
   }
 }
 
@@ -565,6 +608,8 @@ static void launch_splat_reduce(const PairWalk& pw, const FrameLayout& L, const 
   CGS_PROFILED("splat_reduce_kernel", st,
                splat_reduce_kernel<DEG><<<grid_for(L.vn, 256, 8), 256, 0, st>>>(pw, L.hdr, fd, L.n,
                                                                                  L.vn, gi, B));
+  note_launch();
+  splat_reduce_long_kernel<<<148 * 4, 256, 0, st>>>(pw, L.hdr, L.long_list, fd, L.n, B);
   note_launch();
   CGS_PROFILED("pull_back_kernel", st,
                pull_back_kernel<DEG><<<grid_for(L.vn, 128, 8), 128, 0, st>>>(L.hdr, fd, L.n, L.vn,

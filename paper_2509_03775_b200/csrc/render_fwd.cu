@@ -272,15 +272,27 @@ __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n
 }
 
 // Warp-cooperative pair emission in depth order: a warp takes 32
-// consecutive depth ranks (whose pair ranges are contiguous) and writes their
-// concatenated pair range with all 32 lanes (a near-plane splat covering
-// every tile does not serialise a thread).  Within one splat, tiles are
-// emitted row-major over its tile rect.
+// consecutive depth ranks and writes the pairs of those with at most
+// kLongSplat tiles with all 32 lanes (warp-local offsets from a shuffle scan).
+// Longer splats -- near-plane giants covering every tile sit together at the
+// front of the depth order -- are appended to long_list and emitted by
+// emit_long_pairs_kernel, one CTA per splat, so no warp serialises on them.
+// Within one splat, tiles are emitted row-major over its tile rect.
+template <typename KT>
+__device__ __forceinline__ void emit_one(uint64_t p, int k, uint64_t rc, int ntx, int tbase,
+                                         uint32_t s, KT* keys, uint32_t* vals) {
+  const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
+  const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
+  const int span = tx1 - tx0 + 1;
+  keys[p] = static_cast<KT>(tbase + (ty0 + k / span) * ntx + tx0 + k % span);
+  vals[p] = s;
+}
+
 template <typename KT>
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
-    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, int64_t vn,
+    FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ long_list,
     KT* __restrict__ keys, uint32_t* __restrict__ vals) {
   if (hdr->stats.overflow) return;
   const int lane = threadIdx.x & 31;
@@ -291,46 +303,59 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
     const int64_t r = w * 32 + lane;
     const bool ok = r < ns;
     const uint32_t s = ok ? perm[r] : 0u;
-    const uint64_t cnt = ok ? n_tiles[s] : 0ULL;
-    const uint64_t o = ok ? off[s] : ~0ULL;
-    uint64_t e = ok ? o + cnt : 0ULL;
-#pragma unroll
-    for (int k = 16; k > 0; k >>= 1) {
-      const uint64_t t = __shfl_xor_sync(kFull, e, k);
-      e = t > e ? t : e;
-    }
-    const uint64_t start = __shfl_sync(kFull, o, 0);
-    if (start >= e) continue;
-    const uint64_t rc = ok ? rect[s] : 0ULL;
+    const uint32_t cnt = ok ? n_tiles[s] : 0u;
+    const bool lng = cnt > kLongSplat;
+    if (lng) long_list[atomicAdd(&hdr->scratch[2], 1ULL)] = s;
+    const uint32_t c = lng ? 0u : cnt;  // pairs this warp emits for lane's splat
+    const uint32_t inc = warp_incl_scan(c);
+    const uint32_t loc = inc - c;        // warp-local offset of lane's pairs
+    const uint32_t total = __shfl_sync(kFull, inc, 31);
+    if (total == 0) continue;
+    const uint64_t o = c ? off[s] : 0ULL;
+    const uint64_t rc = c ? rect[s] : 0ULL;
     const int v = ok ? static_cast<int>(s / static_cast<uint32_t>(n)) : 0;
-    const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
-    const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
-    const int span = tx1 - tx0 + 1;
     const int ntx = fd.cam[v].ntx;
     const int tbase = fd.cam[v].tile_base;
-    for (uint64_t p0 = start; p0 < e; p0 += 32) {
-      const uint64_t p = p0 + lane;
-      int owner = 0;
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const uint32_t end = loc + c;
+      int own = 0;  // first lane whose pair range ends after q (ends are nondecreasing)
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1) {
-        const int cand = owner + step;
-        const uint64_t oc = __shfl_sync(kFull, o, cand & 31);
-        if (cand < 32 && oc <= p) owner = cand;
+        const int cand = own + step;
+        if (__shfl_sync(kFull, end, (cand - 1) & 31) <= q && cand < 32) own = cand;
       }
-      const uint64_t oo = __shfl_sync(kFull, o, owner);
-      const int sp = __shfl_sync(kFull, span, owner);
-      const int bx = __shfl_sync(kFull, tx0, owner);
-      const int by = __shfl_sync(kFull, ty0, owner);
-      const int nt = __shfl_sync(kFull, ntx, owner);
-      const int tb = __shfl_sync(kFull, tbase, owner);
-      const uint32_t so = __shfl_sync(kFull, s, owner);
-      if (p < e) {
-        const int k = static_cast<int>(p - oo);
-        const int ty = by + k / sp, tx = bx + k % sp;
-        keys[p] = static_cast<KT>(tb + ty * nt + tx);
-        vals[p] = so;
+      const uint64_t oo = __shfl_sync(kFull, o, own);
+      const uint32_t lo2 = __shfl_sync(kFull, loc, own);
+      const uint64_t rco = __shfl_sync(kFull, rc, own);
+      const int nt = __shfl_sync(kFull, ntx, own);
+      const int tb = __shfl_sync(kFull, tbase, own);
+      const uint32_t so = __shfl_sync(kFull, s, own);
+      if (q < total) {
+        const int k = static_cast<int>(q - lo2);
+        emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
       }
     }
+  }
+}
+
+// One CTA per long splat (near-plane giants): its pair range is contiguous.
+template <typename KT>
+__global__ void __launch_bounds__(256) emit_long_pairs_kernel(
+    const uint32_t* __restrict__ long_list, const uint64_t* __restrict__ off,
+    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
+    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, KT* __restrict__ keys,
+    uint32_t* __restrict__ vals) {
+  if (hdr->stats.overflow) return;
+  const int64_t nl = static_cast<int64_t>(hdr->scratch[2]);
+  for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
+    const uint32_t s = long_list[e];
+    const uint64_t o = off[s];
+    const int cnt = static_cast<int>(n_tiles[s]);
+    const uint64_t rc = rect[s];
+    const int v = static_cast<int>(s / static_cast<uint32_t>(n));
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x)
+      emit_one<KT>(o + k, k, rc, fd.cam[v].ntx, fd.cam[v].tile_base, s, keys, vals);
   }
 }
 
@@ -378,9 +403,13 @@ static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
   const int eg = grid_for(L.vn, 256, 16);
   CGS_PROFILED("emit_pairs_kernel", st,
                emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.pair_off, L.n_tiles, L.rect, L.hdr,
-                                                          fd, L.n, L.vn, static_cast<KT*>(L.pkeys),
-                                                          L.pvals));
+                                                          fd, L.n, L.long_list,
+                                                          static_cast<KT*>(L.pkeys), L.pvals));
   CGS_CHECK_LAUNCH("emit_pairs_kernel");
+  emit_long_pairs_kernel<KT><<<148 * 4, 256, 0, st>>>(L.long_list, L.pair_off, L.n_tiles, L.rect,
+                                                       L.hdr, fd, L.n, static_cast<KT*>(L.pkeys),
+                                                       L.pvals);
+  CGS_CHECK_LAUNCH("emit_long_pairs_kernel");
   int rc = launch_radix_sort<KT>(static_cast<KT*>(L.pkeys), L.pvals, &L.hdr->n_pairs, 0,
                                  L.pair_cap, L.tile_key_bits, ws, &kres, &vres, st);
   if (rc) return rc;

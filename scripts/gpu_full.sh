@@ -11,5 +11,5 @@ timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 tail -2 gpurun_out/bench_$TAG.err
 CMD="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline"
 timeout 300 $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${KERN:-raster_bwd}" -s 6 -c 1 -o gpurun_out/full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"

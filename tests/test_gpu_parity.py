@@ -343,3 +343,44 @@ def test_full_size_tile_lists_bit_exact(cg, make):
     assert np.array_equal(ids, rids)
     if make is _crowded_scene:  # the three sort classes were exercised
         assert lens.max() > 4096 and np.any((lens > 2048) & (lens <= 4096)) and np.any(lens <= 2048)
+
+
+def _giant_scene(seed=5, n=240, giants=6, size=320):
+    """A few near-plane Gaussians covering every one of 400 tiles (> kLongSplat
+    pairs: CTA-per-splat emission and reduction) among ordinary ones."""
+    from paper_2509_03775_b200 import camera, scenes
+    a = scenes.config0(seed)
+    rng = np.random.default_rng(seed)
+    cam = camera.ring_cameras(1, (0.0, 0.0, 0.0), 3.0, 0.0, float(size), size, size)[0]
+    pos = rng.uniform(-0.8, 0.8, size=(n, 3)).astype(np.float32)
+    eye = -cam.rotation.T @ cam.translation
+    fwd = cam.rotation[2]
+    for k in range(giants):  # just beyond the near plane, in front of the eye
+        pos[k] = (eye + fwd * (0.05 + 0.02 * k) + rng.normal(0, 0.01, 3)).astype(np.float32)
+    idx = rng.integers(0, a.sr_rows.shape[0], n).astype(np.int32)
+    sr = a.sr_rows.copy()
+    sr[idx[:giants], 0:3] = -1.0  # large scales for the giants' rows
+    logit = rng.normal(-1.0, 0.5, n).astype(np.float32)
+    return pos, logit, idx, idx, a.sh_rows, sr, cam
+
+
+def test_near_plane_giants_match_oracle(cg):
+    from gpu_helpers import group_rel
+    from oracle import cgs_oracle as O
+    pos, logit, g2sh, g2sr, sh, sr, cam = _giant_scene()
+    st = cg.ModelState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    art = cg.rasterize_forward(st, cam)
+    ost = O.OState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    ocam = O.cam_from_any(cam)
+    fw = O.raster_forward(ost, ocam)
+    offs, ids = art.frame.tile_lists()
+    assert np.array_equal(offs, fw["tile_offsets"]) and np.array_equal(ids, fw["tile_ids"])
+    assert np.diff(offs).min() > 0 and (np.bincount(ids) > 256).sum() >= 3  # giants in every tile
+    img = art.image.cpu().numpy()
+    assert np.allclose(img, fw["image"], rtol=RTOL, atol=ATOL), np.abs(img - fw["image"]).max()
+    dL = np.random.default_rng(1).normal(0, 1e-3, img.shape)
+    g = cg.rasterize_backward(st, cam, art, dL).numpy()
+    og = O.raster_backward(ost, ocam, dL)
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        assert group_rel(g[k], og[k]) <= 1e-4, (k, group_rel(g[k], og[k]))
+        assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
