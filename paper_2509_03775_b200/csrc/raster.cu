@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
-    uint32_t* __restrict__ tile_nproc) {
+    uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
+    uint32_t* __restrict__ last_rank) {
   __shared__ __align__(128) SplatRec s_raw[256];
   __shared__ float4 s_a[256];
   __shared__ float4 s_b[256];
@@ -240,7 +241,13 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
   for (int k = 16; k > 0; k >>= 1) m = max(m, __shfl_xor_sync(kFull, m, k));
   if (lane == 0) s_max[warp] = m;
   __syncthreads();
-  if (tid == 0) tile_nproc[tile] = max(max(s_max[0], s_max[1]), max(s_max[2], s_max[3]));
+  if (tid == 0) {
+    const uint32_t np = max(max(s_max[0], s_max[1]), max(s_max[2], s_max[3]));
+    tile_nproc[tile] = np;
+    // the list is in increasing depth rank, so pair (s, tile) was processed
+    // iff rank_of[s] < last_rank[tile] (the backward's test, no inverse map)
+    last_rank[tile] = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -301,6 +308,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const FrameHeader* __restrict__ fh,
     const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
     const float* __restrict__ final_T, const float* __restrict__ dL,
+    const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect, int64_t n,
     float* __restrict__ partials) {
   constexpr int B = kBwdBatch;
   __shared__ __align__(128) SplatRec s_raw[B];
@@ -310,6 +318,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   __shared__ float s_io[B];  // 1 / opacity
   __shared__ uint8_t s_mask[B];
   __shared__ uint8_t s_list[4][B];
+  __shared__ uint32_t s_eidx[B];  // emission index of each staged pair
   __shared__ float s_red[4][B][9];
   __shared__ uint32_t s_wlast[4];
   __shared__ __align__(8) uint64_t s_bar;
@@ -374,6 +383,8 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       s_n[k] = make_float4(static_cast<float>(r.ca), static_cast<float>(r.cb),
                            static_cast<float>(r.cc), c);
       s_io[k] = 1.0f / r.opac;
+      s_eidx[k] = static_cast<uint32_t>(
+          emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
       uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
 #pragma unroll
       for (int w = 0; w < 4; ++w)
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
       const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
       const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
-      partials[(static_cast<int64_t>(rg.x) + b0 + jj) * 9 + u] = (r0 + r1) + (r2 + r3);
+      partials[static_cast<int64_t>(s_eidx[jj]) * 9 + u] = (r0 + r1) + (r2 + r3);
     }
     __syncthreads();
   }
@@ -437,7 +448,8 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges, vals,
                                                                  L.recs, L.hdr,
                                                                  image, final_T, counts, L.px_last,
-                                                                 L.tile_nproc));
+                                                                 L.tile_nproc, L.rank_of,
+                                                                 L.last_rank));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
   return CGS_OK;
 }
@@ -450,7 +462,9 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
                raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges,
                                                                  sorted_pair_vals(L),
                                                                  L.recs, L.hdr, L.px_last,
-                                                                 L.tile_nproc, final_T, dL, partials));
+                                                                 L.tile_nproc, final_T, dL,
+                                                                 L.pair_off, L.rect, L.n,
+                                                                 partials));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   return CGS_OK;
 }

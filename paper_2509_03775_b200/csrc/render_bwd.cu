@@ -1,11 +1,13 @@
 // Backward render path (reference render.py:318-459) for sm_100a.
 //
 //   raster_bwd      raster.cu: one CTA per tile, reverse traversal, one
-//                   9-float partial per processed pair (render.py:343-377)
+//                   9-float partial per processed pair, stored at the pair's
+//                   emission index (render.py:343-377)
 //   splat_reduce    per (view, Gaussian) splat: walk its pairs in emission
 //                   order (= row-major tile order, the order of np.add.at over
-//                   the reference's tile dict), look each up through the
-//                   inverse pair map, sum the processed partials in fp64 and
+//                   the reference's tile dict) -- contiguous partials -- keep
+//                   those inside each tile's processed prefix (depth rank <
+//                   the tile's last processed rank), sum them in fp64 and
 //                   apply the chain rule to model space (render.py:382-446)
 //   gauss_write     per Gaussian: sum over views -> position / logit gradients
 //   code reduces    per codebook row through a code -> members CSR (rebuilt
@@ -27,7 +29,7 @@ struct BwdHeader {
 
 struct BwdLayout {
   BwdHeader* hdr;
-  float* partials;     // pair_cap * 9, indexed by final pair position
+  float* partials;     // pair_cap * 9, indexed by emission index
   uint8_t* touched;    // V*N
   float4* s_posl;      // V*N: d_pos xyz, d_logit
   float4* s_view;      // V*N: view direction
@@ -229,10 +231,9 @@ struct PairWalk {
   const uint64_t* pair_off;
   const uint32_t* n_tiles;
   const uint64_t* rect;
-  const uint32_t* inv;
-  const uint2* ranges;
-  const uint32_t* tile_nproc;
-  const float* partials;
+  const uint32_t* rank_of;
+  const uint32_t* last_rank;
+  const float* partials;  // by emission index
 };
 
 // Adds the partials of splat s's processed pairs k = k0, k0+kstep, ... (in
@@ -247,13 +248,13 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
   const int span = tx1 - tx0 + 1;
   const int v = static_cast<int>(s / n);
   const int tb = fd.cam[v].tile_base, ntx = fd.cam[v].ntx;
+  const uint32_t r = w.rank_of[s];
   bool any = false;
   for (uint32_t k = k0; k < cnt; k += kstep) {
     const int t = tb + (ty0 + static_cast<int>(k) / span) * ntx + tx0 + static_cast<int>(k) % span;
-    const uint32_t p = w.inv[o + k];
-    if (p - w.ranges[t].x < w.tile_nproc[t]) {
+    if (r < w.last_rank[t]) {  // inside the tile's processed prefix
       any = true;
-      const float* pp = w.partials + static_cast<int64_t>(p) * 9;
+      const float* pp = w.partials + static_cast<int64_t>(o + k) * 9;
 #pragma unroll
       for (int u = 0; u < 9; ++u) acc[u] += static_cast<double>(pp[u]);
     }
@@ -653,7 +654,7 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
     if (rc) return rc;
     rc = launch_raster_bwd(fd, L, final_T, dL, B.partials, st);
     if (rc) return rc;
-    PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.inv, L.ranges, L.tile_nproc, B.partials};
+    PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials};
     GaussIn gi{sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
       case 0: launch_splat_reduce<0>(pw, L, fd, gi, B, st); break;

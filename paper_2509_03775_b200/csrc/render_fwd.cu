@@ -13,7 +13,6 @@
 //   emit + sort     (tile, splat) pairs in depth order, stable onesweep radix
 //                   sort by tile id: the per-tile append order of _bin_tiles
 //                   (render.py:240-254)
-//   inverse map     emission index -> final pair position (for the backward)
 //   raster_fwd      raster.cu
 #include <cmath>
 
@@ -248,12 +247,16 @@ struct PairOffsets {
   const uint32_t* perm;
   const uint32_t* n_tiles;
   uint64_t* off;
+  uint32_t* rank_of;
   __device__ uint64_t load(int64_t r) const {
     const uint64_t c = n_tiles[perm[r]];
     return c | (c ? (1ULL << 40) : 0ULL);
   }
   __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
-    if (v) off[perm[r]] = ex & ((1ULL << 40) - 1);
+    if (!v) return;
+    const uint32_t s = perm[r];
+    off[s] = ex & ((1ULL << 40) - 1);
+    rank_of[s] = static_cast<uint32_t>(r);
   }
 };
 
@@ -373,21 +376,6 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const KT* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// inv[emission index of pair (splat, tile)] = final pair position; the
-// backward walks each splat's pairs in emission order through it.
-template <typename KT>
-__global__ void __launch_bounds__(256) pair_inverse_kernel(
-    const KT* __restrict__ keys, const uint32_t* __restrict__ vals,
-    const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect,
-    const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ inv) {
-  const int64_t np = static_cast<int64_t>(hdr->n_pairs);
-  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < np;
-       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    inv[emission_index(pair_off, rect, fd, n, vals[p], static_cast<int>(keys[p]))] =
-        static_cast<uint32_t>(p);
-}
-
-// ---------------------------------------------------------------------------
 template <int DEG>
 static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut& out,
                            int64_t vn, cudaStream_t st) {
@@ -416,9 +404,6 @@ static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
   CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * (fd.total_tiles > 0 ? fd.total_tiles : 1), st));
   tile_ranges_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(kres, L.hdr, L.ranges);
   CGS_CHECK_LAUNCH("tile_ranges_kernel");
-  pair_inverse_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(
-      kres, vres, L.pair_off, L.rect, L.hdr, fd, L.n, L.inv);
-  CGS_CHECK_LAUNCH("pair_inverse_kernel");
   return CGS_OK;
 }
 
@@ -456,7 +441,7 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
                                                                            L.depth_key, vn));
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
   }
-  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off}, nullptr, vn, vn, L.scan,
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.rank_of}, nullptr, vn, vn, L.scan,
                        &L.hdr->scratch[0], st);
   if (rc) return rc;
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
