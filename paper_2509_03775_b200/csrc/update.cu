@@ -35,6 +35,24 @@ __device__ __forceinline__ double philox_normal(uint64_t seed, uint64_t offset, 
   return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
+// Four normals from one Philox call (two fp32 Box-Muller pairs): normal
+// 4c + q of a stream.  Throughput mode only; parity mode takes the host
+// Generator's draws.
+__device__ __forceinline__ float4 philox_normal4(uint64_t seed, uint64_t offset, uint32_t stream,
+                                                 uint64_t chunk) {
+  const uint4 c = philox(make_uint4(static_cast<unsigned>(chunk), static_cast<unsigned>(chunk >> 32),
+                                    stream | 0x80000000u, static_cast<unsigned>(offset)),
+                         make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32)));
+  const float k = 0x1.0p-32f;
+  const float u0 = (static_cast<float>(c.x) + 0.5f) * k, u1 = static_cast<float>(c.y) * k;
+  const float u2 = (static_cast<float>(c.z) + 0.5f) * k, u3 = static_cast<float>(c.w) * k;
+  const float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
 struct SgldDev {
   double c_pos, c_op, c_sh, c_sr;  // 0.5 * eps per group
   double k_pos, k_op, k_sh, k_sr;  // mult * sqrt(eps) (0 = no noise)
@@ -93,8 +111,34 @@ __global__ void __launch_bounds__(256) sgld_kernel(
   const int64_t c = p.on_sh ? n_sh * D : 0;
   const int64_t d = p.on_sr ? n_sr : 0;
   const int64_t tot = a + b + c + d;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  // device noise on positions / logits: 4 elements per Philox call
+  const bool chunked = p.noise_src != 1;
+  const int64_t ca = chunked ? (a + 3) / 4 : 0, cb = chunked ? (b + 3) / 4 : 0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ca + cb;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const bool isp = t < ca;
+    const int64_t ch = isp ? t : t - ca;
+    float* v = isp ? pos : logit;
+    const float* g = isp ? gpos : glogit;
+    const int64_t m = isp ? a : b;
+    const double cc = isp ? p.c_pos : p.c_op, kk = isp ? p.k_pos : p.k_op;
+    float4 eta4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kk != 0.0) eta4 = philox_normal4(p.seed, offset, isp ? 0u : 1u, static_cast<uint64_t>(ch));
+    const float eta[4] = {eta4.x, eta4.y, eta4.z, eta4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = 4 * ch + q;
+      if (j >= m) break;
+      double gg = static_cast<double>(g[j]);
+      if (p.gscale != 1.0) gg = __dmul_rn(gg, p.gscale);
+      double nv = __dsub_rn(static_cast<double>(v[j]), __dmul_rn(cc, gg));
+      if (kk != 0.0) nv = __dadd_rn(nv, __dmul_rn(kk, static_cast<double>(eta[q])));
+      v[j] = __double2float_rn(nv);
+    }
+  }
+  for (int64_t i = (chunked ? a + b : 0) + blockIdx.x * static_cast<int64_t>(blockDim.x) +
+                   threadIdx.x;
+       i < tot; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (i < a) {
       pos[i] = sgld_one(pos[i], gpos[i], p.c_pos, p.k_pos, p.gscale, npos, i, p.noise_src, p.seed,
                         offset, 0);

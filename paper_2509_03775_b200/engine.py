@@ -72,6 +72,26 @@ class Trainer:
         state.prefetch_host_index()  # the MCMC loop reads the assignments from the host
 
     # -- buffers ---------------------------------------------------------------
+    def _capacity_buffers(self):
+        """Frame, backward and gradient buffers sized for the Gaussian capacity
+        (densify grows N inside it without a reallocation; only the graphs are
+        re-captured)."""
+        st = self.state
+        lib = nat.library()
+        ncap = max(st.gaussians.capacity, st.num_gaussians)
+        key = (ncap, st.sh.capacity, st.sr.capacity, self.pair_cap)
+        if getattr(self, "_cap_key", None) == key:
+            return
+        cams = nat.cams_array(self.cams)
+        fb = lib.cgs_frame_workspace_bytes(ncap, cams, self.V, self.pair_cap, st.sr.capacity)
+        bb = lib.cgs_backward_workspace_bytes(ncap, cams, self.V, self.pair_cap, st.sh.capacity,
+                                              st.sr.capacity)
+        self._frame_ws = torch.empty((fb,), dtype=torch.uint8, device=self.dev)
+        self.bws = torch.empty((bb,), dtype=torch.uint8, device=self.dev)
+        self._grad_buf = torch.empty((4 * ncap + st.sh.capacity * st.sh.dim + 7 * st.sr.capacity,),
+                                     dtype=torch.float32, device=self.dev)
+        self._cap_key = key
+
     def _prepare(self):
         st = self.state
         fr = self.frame
@@ -79,15 +99,18 @@ class Trainer:
             if self.pair_cap is None:
                 probe = Frame(st, self.cams).run_checked()
                 self.pair_cap = int(probe.stats().n_pairs * self.headroom) + 4096
-            self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap)
-            self.dL = torch.empty_like(self.frame.image)
+            self._capacity_buffers()
+            self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap, ws=self._frame_ws)
+            if self.dL is None or self.dL.shape != self.frame.image.shape:
+                self.dL = torch.empty_like(self.frame.image)
         nb = backward_workspace_bytes(st, self.frame)
         if self.bws is None or self.bws.numel() < nb:
             self.bws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
         g = self.grads
         if (g is None or g.positions.shape[0] != st.num_gaussians
                 or g.sh_rows.shape[0] != st.sh.capacity or g.sr_rows.shape[0] != st.sr.capacity):
-            self.grads = GradientSet.empty(st)
+            self._capacity_buffers()
+            self.grads = GradientSet.empty(st, self._grad_buf)
 
     # -- transitions -------------------------------------------------------------
     # The update is enqueued in three parts: forward + loss, backward, SGLD.

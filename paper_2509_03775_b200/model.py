@@ -287,6 +287,11 @@ class GaussianArrays:
     def count(self) -> int:
         return self._n
 
+    @property
+    def capacity(self) -> int:
+        """Rows allocated in the backing buffers (N can grow to this in place)."""
+        return int(self._pos.shape[0])
+
     def opacities(self) -> np.ndarray:
         """sigmoid(logit) in float64 on the host (model.py:134-135)."""
         lg = self.opacity_logits.detach().cpu().numpy().astype(np.float64)

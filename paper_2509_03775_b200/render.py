@@ -62,7 +62,8 @@ def _initial_pair_capacity(n: int, cams) -> int:
 class Frame:
     """One batched forward render of ``cams`` (<= 16 views) and its workspace."""
 
-    def __init__(self, state: ModelState, cams, pair_capacity: Optional[int] = None):
+    def __init__(self, state: ModelState, cams, pair_capacity: Optional[int] = None,
+                 ws: Optional[torch.Tensor] = None):
         if not 1 <= len(cams) <= nat.MAX_VIEWS:
             raise ValueError(f"a frame holds 1..{nat.MAX_VIEWS} views")
         self.state = state
@@ -76,16 +77,22 @@ class Frame:
         self.image = torch.empty((self.pixels * 3,), dtype=torch.float32, device=self.device)
         self.final_T = torch.empty((self.pixels,), dtype=torch.float32, device=self.device)
         self.counts = torch.empty((self.pixels,), dtype=torch.int32, device=self.device)
-        self._alloc_ws()
+        self._alloc_ws(ws)
         self.token = None
         self._stats = None
 
-    def _alloc_ws(self):
+    def _alloc_ws(self, ws: Optional[torch.Tensor] = None):
+        """Frame workspace; a caller buffer that is large enough is used in place
+        (the trainer sizes one for the Gaussian capacity, so densify does not
+        reallocate)."""
         nb = nat.library().cgs_frame_workspace_bytes(self.n, self.c_cams, len(self.cams),
                                                      self.pair_cap, self.sr_cap)
         if nb == 0:
             raise ValueError(nat.last_error())
-        self.ws = torch.empty((nb,), dtype=torch.uint8, device=self.device)
+        if ws is not None and ws.numel() >= nb:
+            self.ws = ws[:nb]
+        else:
+            self.ws = torch.empty((nb,), dtype=torch.uint8, device=self.device)
 
     def run(self):
         self.scene = scene_struct(self.state)
@@ -206,11 +213,15 @@ class GradientSet:
     flat: Optional[torch.Tensor] = field(default=None, repr=False)
 
     @classmethod
-    def empty(cls, state: ModelState) -> "GradientSet":
-        """One flat buffer [pos | logit | sh | sr] (a single allreduce over NVLink)."""
+    def empty(cls, state: ModelState, buf: Optional[torch.Tensor] = None) -> "GradientSet":
+        """One flat buffer [pos | logit | sh | sr] (a single allreduce over NVLink),
+        carved from ``buf`` when it is large enough."""
         n, ksh, d, ksr = state.num_gaussians, state.sh.capacity, state.sh.dim, state.sr.capacity
         sizes = [3 * n, n, ksh * d, 7 * ksr]
-        flat = torch.empty((sum(sizes),), dtype=torch.float32, device=state.device)
+        if buf is not None and buf.numel() >= sum(sizes):
+            flat = buf[: sum(sizes)]
+        else:
+            flat = torch.empty((sum(sizes),), dtype=torch.float32, device=state.device)
         parts = torch.split(flat, sizes)
         return cls(positions=parts[0].view(n, 3), opacity_logits=parts[1],
                    sh_rows=parts[2].view(ksh, d), sr_rows=parts[3].view(ksr, 7), flat=flat)

@@ -384,3 +384,44 @@ def test_near_plane_giants_match_oracle(cg):
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
         assert group_rel(g[k], og[k]) <= 1e-4, (k, group_rel(g[k], og[k]))
         assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
+
+
+def test_sgld_device_noise_statistics(cg):
+    """Throughput mode (device Philox noise): with zero gradients the update is
+    exactly k * eta per coordinate, eta ~ N(0, 1) i.i.d.; fresh draws per
+    update, deterministic for a given (seed, offset)."""
+    n = 200_003  # not a multiple of 4: exercises the ragged last chunk
+    rng = np.random.default_rng(0)
+    pos = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    logit = np.zeros(n, np.float32)
+    idx = np.zeros(n, np.int32)
+    sh = np.zeros((1, 12), np.float32)
+    sr = np.array([[-3, -3, -3, 1, 0, 0, 0]], np.float32)
+
+    def run(seed, updates):
+        st = cg.ModelState.from_arrays(pos, logit, idx, idx, sh, sr)
+        grads = cg.GradientSet.empty(st)
+        grads.flat.zero_()
+        cfg = cg.SamplerConfig(device_noise=True, seed=seed, noise_pos=1.0, noise_opacity=1.0,
+                               step_pos=0.25, step_opacity=0.04)
+        ctr = torch.zeros((1,), dtype=torch.int64, device=st.device)
+        outs = []
+        for _ in range(updates):
+            cg.sgld_update(st, grads, cfg, rng, offset_dev=ctr)
+            outs.append((st.gaussians.positions.double().cpu().numpy(),
+                         st.gaussians.opacity_logits.double().cpu().numpy()))
+        return outs
+
+    a = run(7, 2)
+    b = run(7, 2)
+    for (pa, la), (pb, lb) in zip(a, b):
+        assert np.array_equal(pa, pb) and np.array_equal(la, lb)  # deterministic
+    eta_p = (a[0][0] - pos.astype(np.float64)) / (1.0 * np.sqrt(0.25))
+    eta_l = (a[0][1] - 0.0) / (1.0 * np.sqrt(0.04))
+    eta_p2 = (a[1][0] - a[0][0]) / np.sqrt(0.25)
+    for e in (eta_p.ravel(), eta_l, eta_p2.ravel()):
+        m = e.size
+        assert abs(e.mean()) < 5.0 / np.sqrt(m)
+        assert abs(e.std() - 1.0) < 0.01
+        assert abs(np.mean(e ** 4) - 3.0) < 0.1  # Gaussian kurtosis
+    assert abs(np.corrcoef(eta_p.ravel(), eta_p2.ravel())[0, 1]) < 0.01  # fresh per update
