@@ -2,10 +2,10 @@
 //
 // L = (1-lam) mean|a-b| + lam (1 - SSIM), SSIM over an 11x11 Gaussian window
 // (sigma 1.5), valid positions only, mean over channels.  Two tiled kernels:
-//   ssim_stats  16x16 valid positions per CTA from a 26x26 smem halo: the five
+//   ssim_stats  32x32 valid positions per CTA from a 42x42 smem halo: the five
 //               windowed moments (separable, fp64), SSIM map partial sums, and
 //               the three adjoint seeds d_mx, d_ex2, d_exy (metrics.py:96-109)
-//   ssim_grad   16x16 pixels per CTA: adjoint filtering of the seeds
+//   ssim_grad   32x32 pixels per CTA: adjoint filtering of the seeds
 //               (metrics.py:40-45) fused with the L1 sign term -> dL/dimage
 // Per-CTA partial sums are reduced in fixed order (deterministic).
 #include <cmath>
@@ -27,8 +27,8 @@ static inline int64_t valid_n(int h, int w) {
   return (h >= 11 && w >= 11) ? static_cast<int64_t>(h - 10) * (w - 10) : 0;
 }
 
-static inline int blocks_x(int w) { return (w + 15) / 16; }
-static inline int blocks_y(int h) { return (h + 15) / 16; }
+static inline int blocks_x(int w) { return (w + 31) / 32; }
+static inline int blocks_y(int h) { return (h + 31) / 32; }
 
 static LossLayout plan_loss(void* base, size_t cap, int nv, int h, int w) {
   LossLayout L{};
@@ -42,77 +42,133 @@ static LossLayout plan_loss(void* base, size_t cap, int nv, int h, int w) {
   return L;
 }
 
-// grid: (bx, by, view*3 + channel); block 256.
+// Both kernels tile 32x32 outputs per CTA (256 threads) and run the separable
+// 11-tap window as two register-blocked passes: each thread slides the window
+// over 4 adjacent outputs (14 loads feed 44 taps per moment), so the passes
+// are fp64-FMA bound rather than shared-memory bound.
+constexpr int kLT = 32;            // outputs per CTA side
+constexpr int kLH = kLT + 10;      // halo side (42)
+constexpr int kLP = kLH + 1;       // padded smem row (floats)
+
+struct StatsSmem {
+  float sa[kLH][kLP];
+  float sb[kLH][kLP];
+  double hm[5][kLH][kLT];
+  double red_s[8], red_l[8];
+};
+
+struct GradSmem {
+  float sd[3][kLH][kLP];
+  double hv[3][kLH][kLT];
+};
+
+// grid: (ceil(W/32), ceil(H/32), view*3 + channel); block 256.
 __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict__ img,
                                                          const float* __restrict__ gt, int H, int W,
                                                          int do_ssim, LossLayout L) {
-  __shared__ double sx[26][26], sy[26][26];
-  __shared__ double hm[5][26][16];
-  __shared__ double red_s[8], red_l[8];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  StatsSmem& S = *reinterpret_cast<StatsSmem*>(smem_raw);
   const int vc = blockIdx.z;
   const int v = vc / 3, ch = vc - 3 * (vc / 3);
-  const int tid = threadIdx.x, lx = tid & 15, ly = tid >> 4;
-  const int x0 = blockIdx.x * 16, y0 = blockIdx.y * 16;
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
   const float* A = img + static_cast<int64_t>(v) * H * W * 3;
   const float* Bm = gt + static_cast<int64_t>(v) * H * W * 3;
-  // L1 partial over this block's 16x16 pixels of channel ch
+  // L1 partial over this block's 32x32 pixels of channel ch (4 per thread)
   double l1 = 0.0;
-  {
-    const int px = x0 + lx, py = y0 + ly;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int px = x0 + (tid & 31), py = y0 + (tid >> 5) + 8 * k;
     if (px < W && py < H) {
       const int64_t o = (static_cast<int64_t>(py) * W + px) * 3 + ch;
-      l1 = fabs(static_cast<double>(A[o]) - static_cast<double>(Bm[o]));
+      l1 += fabs(static_cast<double>(A[o]) - static_cast<double>(Bm[o]));
     }
   }
   double s_acc = 0.0;
   const int Hv = H - 10, Wv = W - 10;
   if (do_ssim && Hv > 0 && Wv > 0 && x0 < Wv && y0 < Hv) {
-    for (int e = tid; e < 26 * 26; e += 256) {
-      const int yy = e / 26, xx = e - yy * 26;
+    // all of a thread's halo loads are issued before any is stored (7 per
+    // array in flight instead of one)
+    constexpr int kPer = (kLH * kLH + 255) / 256;
+    float la[kPer], lb[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = tid + 256 * q;
+      const int yy = e / kLH, xx = e - yy * kLH;
       const int gx = x0 + xx, gy = y0 + yy;
-      double a = 0.0, b = 0.0;
-      if (gx < W && gy < H) {
+      la[q] = lb[q] = 0.0f;
+      if (e < kLH * kLH && gx < W && gy < H) {
         const int64_t o = (static_cast<int64_t>(gy) * W + gx) * 3 + ch;
-        a = A[o];
-        b = Bm[o];
+        la[q] = __ldg(A + o);
+        lb[q] = __ldg(Bm + o);
       }
-      sx[yy][xx] = a;
-      sy[yy][xx] = b;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = tid + 256 * q;
+      if (e < kLH * kLH) {
+        const int yy = e / kLH, xx = e - yy * kLH;
+        S.sa[yy][xx] = la[q];
+        S.sb[yy][xx] = lb[q];
+      }
     }
     __syncthreads();
-    for (int e = tid; e < 26 * 16; e += 256) {
-      const int yy = e / 16, xx = e - yy * 16;
-      double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+    // horizontal: 42 rows x 8 segments of 4 outputs
+    for (int it = tid; it < kLH * 8; it += 256) {
+      const int row = it >> 3, c0 = (it & 7) * 4;
+      double av[14], bv[14];
 #pragma unroll
-      for (int j = 0; j < 11; ++j) {
-        const double a = sx[yy][xx + j], b = sy[yy][xx + j], k = c_win[j];
-        m0 += k * a; m1 += k * b; m2 += k * a * a; m3 += k * b * b; m4 += k * a * b;
+      for (int i = 0; i < 14; ++i) {
+        av[i] = S.sa[row][c0 + i];
+        bv[i] = S.sb[row][c0 + i];
       }
-      hm[0][yy][xx] = m0; hm[1][yy][xx] = m1; hm[2][yy][xx] = m2; hm[3][yy][xx] = m3; hm[4][yy][xx] = m4;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+#pragma unroll
+        for (int j = 0; j < 11; ++j) {
+          const double a = av[o + j], b = bv[o + j], k = c_win[j];
+          m0 += k * a; m1 += k * b; m2 += k * a * a; m3 += k * b * b; m4 += k * a * b;
+        }
+        S.hm[0][row][c0 + o] = m0; S.hm[1][row][c0 + o] = m1; S.hm[2][row][c0 + o] = m2;
+        S.hm[3][row][c0 + o] = m3; S.hm[4][row][c0 + o] = m4;
+      }
     }
     __syncthreads();
-    const int ux = x0 + lx, uy = y0 + ly;
-    if (ux < Wv && uy < Hv) {
-      double m[5] = {0, 0, 0, 0, 0};
+    // vertical: 32 columns x 8 segments of 4 outputs (one item per thread)
+    const int col = tid & 31, r0 = (tid >> 5) * 4;
+    double m[5][4];
 #pragma unroll
-      for (int j = 0; j < 11; ++j) {
-        const double k = c_win[j];
+    for (int q = 0; q < 5; ++q) {
+      double hv[14];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) m[q] += k * hm[q][ly + j][lx];
+      for (int i = 0; i < 14; ++i) hv[i] = S.hm[q][r0 + i][col];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 11; ++j) acc += c_win[j] * hv[o + j];
+        m[q][o] = acc;
       }
-      const double mx = m[0], my = m[1];
-      const double vx = m[2] - mx * mx, vy = m[3] - my * my, cxy = m[4] - mx * my;
+    }
+    const int ux = x0 + col;
+    const int64_t vn = static_cast<int64_t>(Hv) * Wv;
+    float* sd = L.seeds + (static_cast<int64_t>(v) * 3 + ch) * 3 * vn;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int uy = y0 + r0 + o;
+      if (ux >= Wv || uy >= Hv) continue;
+      const double mx = m[0][o], my = m[1][o];
+      const double vx = m[2][o] - mx * mx, vy = m[3][o] - my * my, cxy = m[4][o] - mx * my;
       const double C1 = 1e-4, C2 = 9e-4;
       const double A1 = 2 * mx * my + C1, A2 = 2 * cxy + C2;
       const double B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
       const double F = 1.0 / (B1 * B2);
-      const double s = A1 * A2 * F;
-      s_acc = s;
-      const double d_mx = 2 * my * F * (A2 - A1) - 2 * mx * s * (1.0 / B1 - 1.0 / B2);
-      const double d_ex2 = -s / B2;
+      const double sv = A1 * A2 * F;
+      s_acc += sv;
+      const double d_mx = 2 * my * F * (A2 - A1) - 2 * mx * sv * (1.0 / B1 - 1.0 / B2);
+      const double d_ex2 = -sv / B2;
       const double d_exy = 2 * A1 * F;
-      const int64_t vn = static_cast<int64_t>(Hv) * Wv;
-      float* sd = L.seeds + (static_cast<int64_t>(v) * 3 + ch) * 3 * vn;
       const int64_t pos = static_cast<int64_t>(uy) * Wv + ux;
       sd[pos] = static_cast<float>(d_mx);
       sd[vn + pos] = static_cast<float>(d_ex2);
@@ -127,13 +183,13 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
     b += __shfl_xor_sync(0xffffffffu, b, o);
   }
   if ((tid & 31) == 0) {
-    red_s[tid >> 5] = a;
-    red_l[tid >> 5] = b;
+    S.red_s[tid >> 5] = a;
+    S.red_l[tid >> 5] = b;
   }
   __syncthreads();
   if (tid == 0) {
     double ts = 0, tl = 0;
-    for (int w = 0; w < 8; ++w) { ts += red_s[w]; tl += red_l[w]; }
+    for (int w = 0; w < 8; ++w) { ts += S.red_s[w]; tl += S.red_l[w]; }
     const int64_t nb = static_cast<int64_t>(gridDim.x) * gridDim.y * 3;
     const int64_t bi = (static_cast<int64_t>(ch) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     L.part_s[v * nb + bi] = ts;
@@ -141,69 +197,97 @@ __global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict
   }
 }
 
+// dL/dimage: adjoint filtering of the three seed maps (metrics.py:40-45, the
+// window is symmetric) fused with the L1 sign term; 32x32 pixels per CTA.
 __global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict__ img,
                                                         const float* __restrict__ gt, int H, int W,
                                                         double lam, double inv_size,
                                                         double inv_count, float grad_scale,
                                                         int do_ssim, LossLayout L,
                                                         float* __restrict__ dL) {
-  __shared__ float sd[3][26][26];
-  __shared__ double hv[3][26][16];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GradSmem& S = *reinterpret_cast<GradSmem*>(smem_raw);
   const int vc = blockIdx.z;
   const int v = vc / 3, ch = vc - 3 * (vc / 3);
-  const int tid = threadIdx.x, lx = tid & 15, ly = tid >> 4;
-  const int x0 = blockIdx.x * 16, y0 = blockIdx.y * 16;
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * kLT, y0 = blockIdx.y * kLT;
   const int Hv = H - 10, Wv = W - 10;
-  double gs = 0.0;
   const bool ssim_on = do_ssim && Hv > 0 && Wv > 0;
+  const int col = tid & 31, r0 = (tid >> 5) * 4;
+  double r[3][4] = {};
   if (ssim_on) {
     const int64_t vn = static_cast<int64_t>(Hv) * Wv;
     const float* seeds = L.seeds + (static_cast<int64_t>(v) * 3 + ch) * 3 * vn;
-    // window rows/cols [y0-10, y0+15], zero outside the valid seed range
-    for (int e = tid; e < 26 * 26; e += 256) {
-      const int yy = e / 26, xx = e - yy * 26;
+    // seed window rows/cols [y0-10, y0+31], zero outside the valid range
+    constexpr int kPer = (kLH * kLH + 255) / 256;
+    float ls[3][kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = tid + 256 * i;
+      const int yy = e / kLH, xx = e - yy * kLH;
       const int uy = y0 - 10 + yy, ux = x0 - 10 + xx;
-      const bool ok = uy >= 0 && uy < Hv && ux >= 0 && ux < Wv;
+      const bool ok = e < kLH * kLH && uy >= 0 && uy < Hv && ux >= 0 && ux < Wv;
       const int64_t pos = static_cast<int64_t>(uy) * Wv + ux;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) sd[q][yy][xx] = ok ? seeds[q * vn + pos] : 0.0f;
+      for (int q = 0; q < 3; ++q) ls[q][i] = ok ? __ldg(seeds + q * vn + pos) : 0.0f;
     }
-    __syncthreads();
-    for (int e = tid; e < 26 * 16; e += 256) {
-      const int yy = e / 16, xx = e - yy * 16;
-      double a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
-      for (int j = 0; j < 11; ++j) {
-        const double k = c_win[j];
-        a0 += k * sd[0][yy][xx + j];
-        a1 += k * sd[1][yy][xx + j];
-        a2 += k * sd[2][yy][xx + j];
+    for (int i = 0; i < kPer; ++i) {
+      const int e = tid + 256 * i;
+      if (e < kLH * kLH) {
+        const int yy = e / kLH, xx = e - yy * kLH;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) S.sd[q][yy][xx] = ls[q][i];
       }
-      hv[0][yy][xx] = a0; hv[1][yy][xx] = a1; hv[2][yy][xx] = a2;
     }
     __syncthreads();
+    for (int it = tid; it < kLH * 8; it += 256) {
+      const int row = it >> 3, c0 = (it & 7) * 4;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double sv[14];
+#pragma unroll
+        for (int i = 0; i < 14; ++i) sv[i] = S.sd[q][row][c0 + i];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < 11; ++j) acc += c_win[j] * sv[o + j];
+          S.hv[q][row][c0 + o] = acc;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double hv[14];
+#pragma unroll
+      for (int i = 0; i < 14; ++i) hv[i] = S.hv[q][r0 + i][col];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 11; ++j) acc += c_win[j] * hv[o + j];
+        r[q][o] = acc;
+      }
+    }
   }
-  const int px = x0 + lx, py = y0 + ly;
-  if (px >= W || py >= H) return;
   const float* A = img + static_cast<int64_t>(v) * H * W * 3;
   const float* Bm = gt + static_cast<int64_t>(v) * H * W * 3;
-  const int64_t o = (static_cast<int64_t>(py) * W + px) * 3 + ch;
-  const double a = A[o], b = Bm[o];
-  if (ssim_on) {
-    double r0 = 0, r1 = 0, r2 = 0;
+  const int px = x0 + col;
 #pragma unroll
-    for (int j = 0; j < 11; ++j) {
-      const double k = c_win[j];
-      r0 += k * hv[0][ly + j][lx];
-      r1 += k * hv[1][ly + j][lx];
-      r2 += k * hv[2][ly + j][lx];
-    }
-    gs = (r0 + 2.0 * a * r1 + b * r2) * inv_count;
+  for (int o = 0; o < 4; ++o) {
+    const int py = y0 + r0 + o;
+    if (px >= W || py >= H) continue;
+    const int64_t off = (static_cast<int64_t>(py) * W + px) * 3 + ch;
+    const double a = A[off], b = Bm[off];
+    double gs = 0.0;
+    if (ssim_on) gs = (r[0][o] + 2.0 * a * r[1][o] + b * r[2][o]) * inv_count;
+    const double sgn = a > b ? 1.0 : (a < b ? -1.0 : 0.0);
+    double g = (1.0 - lam) * sgn * inv_size;
+    if (lam != 0.0) g -= lam * gs;
+    dL[static_cast<int64_t>(v) * H * W * 3 + off] = static_cast<float>(g * grad_scale);
   }
-  const double sgn = a > b ? 1.0 : (a < b ? -1.0 : 0.0);
-  double g = (1.0 - lam) * sgn * inv_size;
-  if (lam != 0.0) g -= lam * gs;
-  dL[static_cast<int64_t>(v) * H * W * 3 + o] = static_cast<float>(g * grad_scale);
 }
 
 // One CTA per view: strided fixed-order partial sums, then a fixed tree.
@@ -272,12 +356,20 @@ int recon_loss(const float* img, const float* gt, int nv, int H, int W, double l
   }
   const bool has_ssim = (H >= 11 && W >= 11) && (lam != 0.0 || want_ssim);
   const dim3 grid(blocks_x(W), blocks_y(H), 3 * nv);
-  CGS_PROFILED("ssim_stats_kernel", st, ssim_stats_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, has_ssim ? 1 : 0, L));
+  static bool attr = false;
+  if (!attr) {
+    CGS_CUDA(cudaFuncSetAttribute(ssim_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(StatsSmem))));
+    CGS_CUDA(cudaFuncSetAttribute(ssim_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(GradSmem))));
+    attr = true;
+  }
+  CGS_PROFILED("ssim_stats_kernel", st, ssim_stats_kernel<<<grid, 256, sizeof(StatsSmem), st>>>(img, gt, H, W, has_ssim ? 1 : 0, L));
   CGS_CHECK_LAUNCH("ssim_stats_kernel");
   const double inv_size = 1.0 / (3.0 * H * W);
   const double inv_count = has_ssim ? 1.0 / (3.0 * (H - 10.0) * (W - 10.0)) : 0.0;
   if (dL) {
-    CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, 0, st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
+    CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, sizeof(GradSmem), st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
                                            (has_ssim && lam != 0.0) ? 1 : 0, L, dL));
     CGS_CHECK_LAUNCH("ssim_grad_kernel");
   }

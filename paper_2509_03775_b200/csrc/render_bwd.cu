@@ -86,6 +86,7 @@ struct TileProcCount {
 };
 
 struct GaussIn {
+  const SplatRec* recs;  // projection records of the frame (conic, clamped colour)
   const float* pos;
   const float* logit;
   const int32_t* g2sh;
@@ -93,12 +94,6 @@ struct GaussIn {
   const float* sh_rows;
   const double* sr_cov;
 };
-
-__device__ __forceinline__ float ldg_volatile(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-}
 
 // Chain rule from screen space to model space for one (view, Gaussian)
 // splat (render.py:382-446).  acc = [d_color(3), d_opac, d_mean2d(2),
@@ -116,24 +111,20 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   ox /= len;
   oy /= len;
   oz /= len;
-  double Bv[NB];
-  sh_basis<DEG>(ox, oy, oz, Bv);
-  // Two streaming passes over the row (the second re-reads L1; volatile loads
-  // keep the compiler from holding the row in registers): same sums, same order.
-  const float* row = g.sh_rows + static_cast<int64_t>(g.g2sh[gi]) * D;
-  double col[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int e = 0; e < D; ++e) col[e % 3] += Bv[e / 3] * static_cast<double>(__ldg(row + e));
-  const double draw[3] = {col[0] + 0.5 > 0.0 ? acc[0] : 0.0, col[1] + 0.5 > 0.0 ? acc[1] : 0.0,
-                          col[2] + 0.5 > 0.0 ? acc[2] : 0.0};
+  const SplatRec& rec = g.recs[s];
+  // colour gate raw > 0 (render.py:418-419): the projection stored
+  // max(raw, 0) in fp32, which is > 0 exactly when raw > 0 (fp64 decision)
+  const double draw[3] = {rec.r > 0.0f ? acc[0] : 0.0, rec.g > 0.0f ? acc[1] : 0.0,
+                          rec.b > 0.0f ? acc[2] : 0.0};
   double dpc[3] = {0.0, 0.0, 0.0};
   if constexpr (DEG >= 1) {
+    const float* row = g.sh_rows + static_cast<int64_t>(g.g2sh[gi]) * D;
     double wb[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b)
-      wb[b] = draw[0] * static_cast<double>(ldg_volatile(row + 3 * b + 0)) +
-              draw[1] * static_cast<double>(ldg_volatile(row + 3 * b + 1)) +
-              draw[2] * static_cast<double>(ldg_volatile(row + 3 * b + 2));
+      wb[b] = draw[0] * static_cast<double>(__ldg(row + 3 * b + 0)) +
+              draw[1] * static_cast<double>(__ldg(row + 3 * b + 1)) +
+              draw[2] * static_cast<double>(__ldg(row + 3 * b + 2));
     double dv[3];
     sh_basis_grad_dot<DEG>(ox, oy, oz, wb, dv);
     const double vd = ox * dv[0] + oy * dv[1] + oz * dv[2];
@@ -155,16 +146,9 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   }
   const double* cv = g.sr_cov + static_cast<int64_t>(g.g2sr[gi]) * 8;
   const double S[3][3] = {{cv[0], cv[1], cv[2]}, {cv[1], cv[3], cv[4]}, {cv[2], cv[4], cv[5]}};
-  double SM[3][2];  // S M^T
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) SM[a][b] = S[a][0] * M[b][0] + S[a][1] * M[b][1] + S[a][2] * M[b][2];
-  const double c00 = M[0][0] * SM[0][0] + M[0][1] * SM[1][0] + M[0][2] * SM[2][0] + kBlur;
-  const double c01 = M[0][0] * SM[0][1] + M[0][1] * SM[1][1] + M[0][2] * SM[2][1];
-  const double c11 = M[1][0] * SM[0][1] + M[1][1] * SM[1][1] + M[1][2] * SM[2][1] + kBlur;
-  const double det = c00 * c11 - c01 * c01;
-  const double Q[2][2] = {{c11 / det, -c01 / det}, {-c01 / det, c00 / det}};
+  // the forward's conic (render.py:176-181; the reference's pull-back reuses
+  // _Projection's conic the same way)
+  const double Q[2][2] = {{rec.ca, rec.cb}, {rec.cb, rec.cc}};
   // dConic (render.py:391-394) and dSigma2 = -Q dQ Q (render.py:396-397)
   const double dQ[2][2] = {{acc[6], 0.5 * acc[7]}, {0.5 * acc[7], acc[8]}};
   double QdQ[2][2], dS2[2][2];
@@ -655,7 +639,7 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
     rc = launch_raster_bwd(fd, L, final_T, dL, B.partials, st);
     if (rc) return rc;
     PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials};
-    GaussIn gi{sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
+    GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
       case 0: launch_splat_reduce<0>(pw, L, fd, gi, B, st); break;
       case 1: launch_splat_reduce<1>(pw, L, fd, gi, B, st); break;
