@@ -264,6 +264,7 @@ def main():
     lib.cgs_profile_kernel(args.profile_kernel.encode())
     clocks = ClockSampler(local)
     launches0 = lib.cgs_launch_count()
+    cap0, rep0 = tr.capture_counted, tr.replayed_kernels
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     views_done = 0
@@ -283,7 +284,10 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    launches = int(lib.cgs_launch_count() - launches0)
+    # ABI launch calls + kernels executed by graph replays - calls recorded
+    # (not executed) while capturing
+    launches = int(lib.cgs_launch_count() - launches0) + (tr.replayed_kernels - rep0) - (
+        tr.capture_counted - cap0)
     tr.check()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)

@@ -66,6 +66,12 @@ class Trainer:
         self.noise_ctr = torch.zeros((1,), dtype=torch.int64, device=self.dev)
         self._gkey = None
         self._g_fwd = self._g_sgld = None
+        # kernel accounting: the C ABI counts every launch call, including the
+        # ones recorded while capturing (not executed); replays execute the
+        # recorded kernels without calling the ABI
+        self._g_kernels = {}
+        self.capture_counted = 0
+        self.replayed_kernels = 0
         self._pool = None
         self._cap_stream = None
         self.captures = 0
@@ -153,6 +159,7 @@ class Trainer:
             self._pool = torch.cuda.graph_pool_handle()
             self._cap_stream = torch.cuda.Stream(self.dev)
         g = torch.cuda.CUDAGraph()
+        c0 = nat.library().cgs_launch_count()
         cur = torch.cuda.current_stream(self.dev)
         self._cap_stream.wait_stream(cur)
         with torch.cuda.stream(self._cap_stream):
@@ -162,7 +169,14 @@ class Trainer:
             finally:
                 g.capture_end()
         cur.wait_stream(self._cap_stream)
+        k = int(nat.library().cgs_launch_count() - c0)
+        self.capture_counted += k
+        self._g_kernels[id(g)] = k
         return g
+
+    def _replay(self, g):
+        g.replay()
+        self.replayed_kernels += self._g_kernels.get(id(g), 0)
 
     def update(self):
         """SGLD update over the view batch (device only, no host synchronisation)."""
@@ -183,9 +197,9 @@ class Trainer:
                 self.captures += 1
                 self.capture_ms.append(1000.0 * (time.perf_counter() - t0))
             else:
-                self._g_fwd.replay()
+                self._replay(self._g_fwd)
                 self._enqueue_backward()
-                self._g_sgld.replay()
+                self._replay(self._g_sgld)
         else:
             self._enqueue_forward()
             self._enqueue_backward()
