@@ -8,6 +8,8 @@ hand-written sm_100a kernels of ``libcgs_b200.so`` through its C ABI
 
 from .camera import Camera, look_at, ring_cameras
 from .metrics import LossTerms, psnr, recon_loss, recon_loss_grad, ssim, total_loss
+from .modelio import (ModelFormatError, deserialize_model, load_model, save_model,
+                      serialize_model, write_metrics_csv)
 from .model import (Codebook, GaussianArrays, ModelState, densify, init_one_to_one, lookup,
                     model_bytes, remap_gaussian, sh_dim, validate_state)
 from .render import (Frame, GradientSet, ProjectedSplat, RenderArtifacts, build_covariance,

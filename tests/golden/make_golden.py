@@ -345,13 +345,59 @@ def make_mcmc():
     print("mcmc:", names)
 
 
+def ref_state_from(d, p) -> ModelState:
+    """Reference ModelState from a state_arrays snapshot."""
+    sh = Codebook(d[p + "sh_rows"].copy())
+    sr = Codebook(d[p + "sr_rows"].copy())
+    for book, name in ((sh, "sh"), (sr, "sr")):
+        book.refcount[:] = d[p + name + "_refcount"]
+        book.parent[:] = d[p + name + "_parent"]
+        book._free = [int(r) for r in d[p + name + "_free"]]
+        heapq.heapify(book._free)
+    g = GaussianArrays(positions=d[p + "positions"].copy(),
+                       opacity_logits=d[p + "opacity_logits"].copy(),
+                       g2sh=d[p + "g2sh"].copy(), g2sr=d[p + "g2sr"].copy())
+    st = ModelState(gaussians=g, sh=sh, sr=sr)
+    contrags.validate_state(st)
+    return st
+
+
+def make_modelio():
+    """serialize_model / deserialize_model (modelio.py:58-127) on MCMC-chain states
+    with freed and appended rows, plus the reference's errors on corrupt files."""
+    d = dict(np.load(os.path.join(OUT, "mcmc.npz"), allow_pickle=False))
+    out = {}
+    cases = []
+    for chain in [str(n) for n in d["names"]]:
+        for step in (0, 6, 12):
+            p = f"{chain}_s{step}_"
+            data = rmodelio.serialize_model(ref_state_from(d, p))
+            out[f"{chain}_s{step}_bytes"] = np.frombuffer(data, dtype=np.uint8).copy()
+            cases.append(f"{chain}_s{step}")
+    good = rmodelio.serialize_model(ref_state_from(d, "always_s12_"))
+    bad = {"truncated": good[:-5], "magic": b"CGSX" + good[4:], "trailing": good + b"\0\0",
+           "version": good[:4] + (2).to_bytes(4, "little") + good[8:]}
+    for name, blob in bad.items():
+        try:
+            rmodelio.deserialize_model(blob)
+            msg = ""
+        except rmodelio.ModelFormatError as e:
+            msg = str(e)
+        out[f"bad_{name}_bytes"] = np.frombuffer(blob, dtype=np.uint8).copy()
+        out[f"bad_{name}_msg"] = np.array(msg)
+    out["cases"] = np.array(cases)
+    out["bad"] = np.array(list(bad))
+    np.savez_compressed(os.path.join(OUT, "modelio.npz"), **out)
+    print("modelio:", cases)
+
+
+MAKERS = {"loss_sh": make_loss_sh, "sgld": make_sgld, "mcmc": make_mcmc, "render": make_render,
+          "gradcheck": make_gradcheck, "modelio": make_modelio}
+
 if __name__ == "__main__":
     print("numpy", np.__version__)
-    make_loss_sh()
-    make_sgld()
-    make_mcmc()
-    make_render()
-    make_gradcheck()
+    for name in (sys.argv[1:] or list(MAKERS)):
+        MAKERS[name]()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))
