@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--views-per-frame", type=int, default=1,
+                    help="config 4: poses rendered per batched frame")
     return ap.parse_args()
 
 
@@ -72,7 +74,8 @@ def workload_name(config):
     return {0: "config0: N=4096 SH-1 K=256, 1x64^2 view, L1",
             1: "config1: N=100k, SR K=4096, SH-3 K=4096, 4x256^2 views/GPU, L1+SSIM, MCMC every 25",
             2: "config2: N=1M clustered, SR 8192, SH-3 16384, 1x1280x720 view/GPU",
-            3: "config3: N=4M outdoor, SR 16384, SH-3 65536, 1x1960x1088 view/GPU"}[config]
+            3: "config3: N=4M outdoor, SR 16384, SH-3 65536, 1x1960x1088 view/GPU",
+            4: "config4: render-only, N=6M, K=65536 both, 64 poses 1920x1080 sharded over GPUs"}[config]
 
 
 class ClockSampler:
@@ -205,6 +208,128 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def _oracle_render_mpix(a, cam, crop=(480, 270)):
+    """Reference forward (numpy oracle port) of a crop window of one pose: the
+    full scene is projected and the crop's pixels rasterized.  Returns
+    (Mpix/s, seconds, sample description)."""
+    from oracle import cgs_oracle as O
+    cw, ch = crop
+    c = O.cam_from_any(cam)
+    c = O.OCam(R=c.R, t=c.t, fx=c.fx, fy=c.fy, cx=c.cx - (c.width - cw) / 2.0,
+               cy=c.cy - (c.height - ch) / 2.0, width=cw, height=ch)
+    st = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    t0 = time.perf_counter()
+    O.raster_forward(st, c)
+    secs = time.perf_counter() - t0
+    return (cw * ch / secs / 1e6, secs,
+            f"oracle forward of the central {cw}x{ch} window of pose 0 (all {a.n} Gaussians "
+            "projected), 1 process")
+
+
+def run_render(args, world, rank, local):
+    """--config 4: render-only throughput.  A step renders all 64 poses of the
+    job (strong scaling: poses sharded round-robin over ranks), forward only,
+    in batched frames of --views-per-frame poses; value = rendered Mpix/s of
+    the whole job.  e2e adds the D2H copy of every image to pinned memory."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2509_03775_b200 as cg
+    from paper_2509_03775_b200 import _native as nat
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config4(args.seed)
+    dev = torch.device("cuda", local)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows, device=dev)
+    mine = a.cameras[rank::world]
+    B = max(1, min(args.views_per_frame, nat.MAX_VIEWS))
+    groups = [mine[i:i + B] for i in range(0, len(mine), B)]
+    frames = [cg.Frame(st, g).run_checked() for g in groups]  # sizes the pair buffers
+    flush = torch.empty((64 * 1024 * 1024,), dtype=torch.float32, device=dev)
+    lib = nat.library()
+
+    def step():
+        for f in frames:
+            f.run()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if any(f.stats().overflow for f in frames):
+        raise RuntimeError("pair capacity overflow")
+    clocks = ClockSampler(local)
+    l0 = lib.cgs_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = int(lib.cgs_launch_count() - l0)
+    ms = [s.elapsed_time(e) for s, e in ev]
+    tot = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    px_job = sum(c.width * c.height for c in a.cameras)
+    value = args.steps * px_job / (tot / 1000.0) / 1e6
+    # e2e: the same renders plus the D2H copy of every image into pinned memory
+    hosts = [torch.empty(f.image.shape, dtype=torch.float32).pin_memory() for f in frames]
+    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        e_ev[k][0].record()
+        for f, h in zip(frames, hosts):
+            f.run()
+            h.copy_(f.image, non_blocking=True)
+        e_ev[k][1].record()
+    torch.cuda.synchronize()
+    e_tot = sum(s.elapsed_time(e) for s, e in e_ev)
+    if world > 1:
+        t = torch.tensor([e_tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_tot = float(t.item())
+    stats = [f.stats() for f in frames]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, secs, sample = _oracle_render_mpix(a, a.cameras[0])
+        cpu = {"value": v, "unit": "Mpix/s", "cores": 1, "kind": "port", "sample": sample,
+               "seconds": secs}
+    if rank == 0:
+        out = {"metric": "rendered Mpix/s", "value": value, "unit": "Mpix/s", "n_gpus": world,
+               "steps": args.steps, "warmup": max(3, args.warmup),
+               "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32 (fp64 projection geometry)",
+               "data": "synthetic (seeded scene, SURVEY.md §8(d)); random-init codebooks",
+               "config": {"workload": workload_name(4), "views_per_frame": B,
+                          "poses_per_gpu": len(mine), "gaussians": a.n,
+                          "l2": "flushed (256 MB write) between timed iterations",
+                          "parallelism": f"dp{world} (poses sharded, no collective)"},
+               "gpu_launches": launches, "clocks": clk,
+               "e2e": {"value": args.steps * px_job / (e_tot / 1000.0) / 1e6, "unit": "Mpix/s",
+                       "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hosts)) * world},
+               "cpu_baseline": cpu,
+               "frame": {"pairs": int(sum(x.n_pairs for x in stats)),
+                         "onscreen": int(sum(x.n_onscreen for x in stats))}}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -212,6 +337,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 4:
+        return run_render(args, world, rank, local)
 
     import torch
     import torch.distributed as dist

@@ -241,29 +241,26 @@ __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __re
 }
 
 // Pair offsets in depth order (perm = depth rank -> splat), stored per splat.
-// One scan carries both the pair count (low 40 bits) and the on-screen splat
-// count (high bits).
 struct PairOffsets {
   const uint32_t* perm;
   const uint32_t* n_tiles;
   uint64_t* off;
   uint32_t* rank_of;
-  __device__ uint64_t load(int64_t r) const {
-    const uint64_t c = n_tiles[perm[r]];
-    return c | (c ? (1ULL << 40) : 0ULL);
-  }
+  __device__ uint64_t load(int64_t r) const { return n_tiles[perm[r]]; }
   __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
     if (!v) return;
     const uint32_t s = perm[r];
-    off[s] = ex & ((1ULL << 40) - 1);
+    off[s] = ex;
     rank_of[s] = static_cast<uint32_t>(r);
   }
 };
 
-__global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views) {
-  const unsigned long long packed = hdr->scratch[0];
-  const unsigned long long raw = packed & ((1ULL << 40) - 1);
-  hdr->n_onscreen = packed >> 40;
+// hist_top: the depth sort's histogram of the key's top byte; splats without
+// tiles carry key ~0, so their count is hist_top[255].
+__global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views,
+                                       const uint32_t* hist_top, int64_t vn) {
+  const unsigned long long raw = hdr->scratch[0];
+  hdr->n_onscreen = static_cast<unsigned long long>(vn) - (hist_top ? hist_top[255] : 0u);
   hdr->n_pairs_raw = raw;
   const bool over = raw > static_cast<unsigned long long>(pair_cap);
   hdr->n_pairs = over ? 0ULL : raw;
@@ -444,7 +441,8 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.rank_of}, nullptr, vn, vn, L.scan,
                        &L.hdr->scratch[0], st);
   if (rc) return rc;
-  finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
+  finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views,
+                                          vn > 0 ? L.dsort.hist + 3 * 256 : nullptr, vn);
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
   rc = L.tile_key_bytes == 2 ? emit_sort_range<uint16_t>(L, fd, L.psort16, perm, st)
                              : emit_sort_range<uint32_t>(L, fd, L.psort32, perm, st);
