@@ -263,12 +263,21 @@ struct PixBwd {
   uint32_t last;
 };
 
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Adds pixel p's contribution of splat k to o[9]; returns whether it had one.
+// o = [sum w g (3), sum dp, sum dp dx, sum dp dy, sum dp dx^2, sum dp dx dy,
+// sum dp dy^2] with dp = dL/dalpha * alpha: the per-splat gradient is a
+// linear map of these moments (moments_to_grad), applied once per splat
+// after the pixel sums instead of per pixel.
 __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const float4& b,
-                                          const float4& nc, float io, float dx, float dy,
-                                          float* o) {
+                                          const float4& nc, float dx, float dy, float* o) {
   if (!(k < p.last) || !(al >= kAlphaSkipF)) return false;
-  const float iom = __frcp_rn(1.0f - al);
+  const float iom = fast_rcp(1.0f - al);  // 1 - alpha >= 0.01
   const float Tb = p.T * iom;
   const float w = al * Tb;
   o[0] = fmaf(w, p.gr, o[0]);  // d colour += weight * dL (render.py:351-352)
@@ -285,14 +294,31 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const
   p.T = Tb;
   if (al < kAlphaClampVal) {  // no gradient through the clamp (render.py:361)
     const float dp = da * al;
-    o[3] = fmaf(dp, io, o[3]);                               // d opacity
-    o[4] = fmaf(dp, fmaf(nc.x, dx, nc.y * dy), o[4]);        // d mean2d
-    o[5] = fmaf(dp, fmaf(nc.y, dx, nc.z * dy), o[5]);
-    o[6] = fmaf(dp, -0.5f * dx * dx, o[6]);                  // d conic (A, B, C)
-    o[7] = fmaf(dp, -dx * dy, o[7]);
-    o[8] = fmaf(dp, -0.5f * dy * dy, o[8]);
+    const float tx = dp * dx, ty = dp * dy;
+    o[3] += dp;
+    o[4] += tx;
+    o[5] += ty;
+    o[6] = fmaf(tx, dx, o[6]);
+    o[7] = fmaf(tx, dy, o[7]);
+    o[8] = fmaf(ty, dy, o[8]);
   }
   return true;
+}
+
+// Moments -> [d colour (3), d opacity, d mean2d (2), d conic (A, B, C)]
+// (render.py:364-377: d_opac = sum dp / o, d_mean = conic * sum dp d,
+// d_conic = -(1/2 dx^2, dx dy, 1/2 dy^2) summed with weight dp).
+__device__ __forceinline__ void moments_to_grad(const float* m, const float4& nc, float io,
+                                                float* g) {
+  g[0] = m[0];
+  g[1] = m[1];
+  g[2] = m[2];
+  g[3] = m[3] * io;
+  g[4] = fmaf(nc.x, m[4], nc.y * m[5]);
+  g[5] = fmaf(nc.y, m[4], nc.z * m[5]);
+  g[6] = -0.5f * m[6];
+  g[7] = -m[7];
+  g[8] = -0.5f * m[8];
 }
 
 // Batches of kBwdBatch splats, last batch first.  Staging writes, per
@@ -406,28 +432,34 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       const float4 a = s_a[j];
       const float4 b = s_b[j];
       const float4 nc = s_n[j];
-      const float io = s_io[j];
       const float dx = a.x + flx;
       const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
       const float t0 = a.z * dx * dx, t1 = a.w * dx;
       const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
       const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
-      bool any = bwd_pixel(q0, k, al0, b, nc, io, dx, dy0, o);
-      any = bwd_pixel(q1, k, al1, b, nc, io, dx, dy1, o) || any;
+      bool any = bwd_pixel(q0, k, al0, b, nc, dx, dy0, o);
+      any = bwd_pixel(q1, k, al1, b, nc, dx, dy1, o) || any;
       // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
       float red = 0.0f;
       if (__any_sync(kFull, any)) red = warp_reduce9(o);
       if (slot >= 0) s_red[warp][j][slot] = red;
     }
     __syncthreads();
-    for (int e = tid; e < nb * 9; e += 128) {
-      const int jj = e / 9, u = e - jj * 9;
+    for (int jj = tid; jj < nb; jj += 128) {  // one splat per thread, warps in fixed order
       const uint32_t m = s_mask[jj];
-      const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
-      const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
-      const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
-      const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
-      partials[static_cast<int64_t>(s_eidx[jj]) * 9 + u] = (r0 + r1) + (r2 + r3);
+      float mom[9], g[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
+        const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
+        const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
+        const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
+        mom[u] = (r0 + r1) + (r2 + r3);
+      }
+      moments_to_grad(mom, s_n[jj], s_io[jj], g);
+      float* out = partials + static_cast<int64_t>(s_eidx[jj]) * 9;
+#pragma unroll
+      for (int u = 0; u < 9; ++u) out[u] = g[u];
     }
     __syncthreads();
   }
