@@ -1,6 +1,7 @@
 // Standalone timing of the radix sort / scan primitives (sort_scan.cuh) at
 // the sizes of the frame pipeline.  nvcc -gencode arch=compute_100a,code=sm_100a
 //   -O3 -I include bench_tools/sort_bench.cu -o bench_tools/sort_bench
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -53,6 +54,38 @@ static void run(int64_t n, int bits, int reps) {
     float ms; cudaEventElapsedTime(&ms, a, b);
     if (r > 0 && ms < best) best = ms;
   }
+#ifdef CGS_SORT_TRACE
+  {
+    const int64_t parts = ceil_div(n, kSortTile);
+    unsigned long long* tr;
+    cudaMalloc(&tr, parts * 5 * sizeof(unsigned long long));
+    cudaMemset(tr, 0, parts * 5 * sizeof(unsigned long long));
+    cudaMemcpyToSymbol(g_sort_trace, &tr, sizeof(tr));
+    cudaMemcpyAsync(dk, k0, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dv, v0, n * 4, cudaMemcpyDeviceToDevice, st);
+    launch_radix_sort<K>(dk, dv, nullptr, n, n, bits, w, &ko, &vo, st);  // last pass traced
+    cudaStreamSynchronize(st);
+    std::vector<unsigned long long> h(parts * 5);
+    cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ULL, t4 = 0;
+    double ph[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+    for (int64_t p = 0; p < parts; ++p) {
+      t0 = std::min(t0, h[p * 5]);
+      t4 = std::max(t4, h[p * 5 + 4]);
+      for (int q = 0; q < 4; ++q) {
+        const double d = double(h[p * 5 + q + 1] - h[p * 5 + q]);
+        ph[q] += d / parts;
+        mx[q] = std::max(mx[q], d);
+      }
+    }
+    printf("  trace (last pass, ns): span %.0f; load %.0f/%.0f rank %.0f/%.0f scan+lookback %.0f/%.0f "
+           "scatter %.0f/%.0f (mean/max)\n", double(t4 - t0), ph[0], mx[0], ph[1], mx[1], ph[2],
+           mx[2], ph[3], mx[3]);
+    unsigned long long* z = nullptr;
+    cudaMemcpyToSymbol(g_sort_trace, &z, sizeof(z));
+    cudaFree(tr);
+  }
+#endif
   std::vector<K> rk(n); std::vector<uint32_t> rv(n);
   cudaMemcpy(rk.data(), ko, n * sizeof(K), cudaMemcpyDeviceToHost);
   cudaMemcpy(rv.data(), vo, n * 4, cudaMemcpyDeviceToHost);
