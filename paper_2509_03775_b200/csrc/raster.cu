@@ -1,12 +1,14 @@
 // Tile rasterizer kernels, forward and backward (reference render.py:265-377).
 //
-// Both kernels run one 128-thread CTA per 16x16 tile.  Warp w owns the 8x8
-// quadrant ((w & 1) * 8, (w >> 1) * 8) of the tile and each lane two pixels
-// (x, y) and (x, y + 4) of it.  A splat whose contribution box (projection:
-// the bounding box of its alpha >= 1/255 ellipse, inside the pixel rect of
-// render.py:110-115) misses a warp's quadrant is skipped by that warp without
-// evaluating it: outside the box the reference's float64 alpha is < 1/255,
-// so the skip changes no result.
+// One CTA per 16x16 tile.  The forward runs 256 threads, one pixel each,
+// warp w on the 8x4 block ((w & 1) * 8, (w >> 1) * 4); the backward runs 128
+// threads, warp w on the 8x8 quadrant ((w & 1) * 8, (w >> 1) * 8), each lane
+// on pixels (x, y) and (x, y + 4) (two pixels per lane amortise its per-splat
+// warp reduction).  A splat whose contribution box (projection: the bounding
+// box of its alpha >= 1/255 ellipse, inside the pixel rect of
+// render.py:110-115) misses a warp's pixel block is skipped by that warp
+// without evaluating it: outside the box the reference's float64 alpha is
+// < 1/255, so the skip changes no result.
 //
 // CTAs take tiles longest-work-first (tile_order_kernel): the block
 // scheduler hands out CTAs in blockIdx order as slots free up, so this is
@@ -129,7 +131,24 @@ __device__ __forceinline__ int warp_hit_list(const uint8_t* s_mask, int nb, int 
   return cnt;
 }
 
-__global__ void __launch_bounds__(128) raster_fwd_kernel(
+// Forward: 256 threads, one pixel each; warp w owns the 8x4 block
+// ((w & 1) * 8, (w >> 1) * 4) of the tile and walks only the splats whose
+// contribution box meets it (8-bit block masks, per-warp hit lists).  Finer
+// blocks than the backward's quadrants skip more splats, and 8 warps per tile
+// hide more latency (no per-splat reduction here to amortise).
+__device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
+  const int x0 = static_cast<int8_t>(rc & 0xff), x1 = static_cast<int8_t>((rc >> 8) & 0xff);
+  const int y0 = static_cast<int8_t>((rc >> 16) & 0xff), y1 = static_cast<int8_t>(rc >> 24);
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int bx = (w & 1) * 8, by = (w >> 1) * 4;
+    if (x1 >= bx && x0 <= bx + 7 && y1 >= by && y0 <= by + 3) m |= 1u << w;
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(256) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
@@ -141,8 +160,8 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
   __shared__ float4 s_b[256];
   __shared__ float s_c[256];
   __shared__ uint8_t s_mask[256];
-  __shared__ uint8_t s_list[4][256];
-  __shared__ uint32_t s_max[4];
+  __shared__ uint8_t s_list[8][256];
+  __shared__ uint32_t s_max[8];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
   const int tile = static_cast<int>(order[blockIdx.x]);
@@ -152,26 +171,22 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
   const int lt = tile - cam.tile_base;
   const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int qx = (warp & 1) * 8, qy = (warp >> 1) * 8;
-  const int lx = qx + (lane & 7), ly = qy + (lane >> 3);  // pixels (lx, ly), (lx, ly + 4)
-  const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
-  const bool in0 = px < cam.width && py0 < cam.height;
-  const bool in1 = px < cam.width && py1 < cam.height;
+  const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+  const int px = tx * kTile + lx, py = ty * kTile + ly;
+  const bool in = px < cam.width && py < cam.height;
   const uint2 rg = ranges[tile];
   const int n = static_cast<int>(rg.y - rg.x);
   const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
   const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
   uint8_t* my_list = s_list[warp];
-
-  PixState p0{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in0};
-  PixState p1{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in1};
+  PixState p{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in};
 
   if (tid == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   bool pending = false;
   if (n > 0) {
-    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(256, n), tid, 128);
+    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(256, n), tid, 256);
     pending = true;
   }
   for (int b0 = 0; b0 < n; b0 += 256) {
@@ -179,73 +194,59 @@ __global__ void __launch_bounds__(128) raster_fwd_kernel(
     mbar_wait(&s_bar, phase);
     phase ^= 1;
     pending = false;
-    for (int k = tid; k < nb; k += 128) {
+    if (tid < nb) {
       float4 a, b;
       float c;
-      stage_splat(s_raw[k], ox, oy, a, b, c);
-      s_a[k] = a;
-      s_b[k] = b;
-      s_c[k] = c;
-      s_mask[k] = static_cast<uint8_t>(quad_mask(local_rect(s_raw[k], tx * kTile, ty * kTile)));
+      stage_splat(s_raw[tid], ox, oy, a, b, c);
+      s_a[tid] = a;
+      s_b[tid] = b;
+      s_c[tid] = c;
+      s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
     }
     __syncthreads();
     if (b0 + 256 < n) {
       fence_proxy_async_smem();
-      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + 256, min(256, n - b0 - 256), tid, 128);
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + 256, min(256, n - b0 - 256), tid, 256);
       pending = true;
     }
     const int hits = warp_hit_list<256>(s_mask, nb, warp, lane, my_list);
-    if (!(p0.done && p1.done)) {
-      for (int i = 0; i < hits; ++i) {  // splats whose box meets this warp's quadrant
+    if (!p.done) {
+      for (int i = 0; i < hits; ++i) {
         const int j = my_list[i];
         const float4 a = s_a[j];
         const float4 b = s_b[j];
-        const float dx = a.x + flx;
-        const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
-        const float t0 = a.z * dx * dx, t1 = a.w * dx;
-        const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
-        const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
-        if (al0 >= kAlphaSkipF || al1 >= kAlphaSkipF) {
-          const float cb = s_c[j];
-          blend(p0, al0, b.z, b.w, cb, static_cast<uint32_t>(b0 + j));
-          blend(p1, al1, b.z, b.w, cb, static_cast<uint32_t>(b0 + j));
-          if (p0.done && p1.done) break;
+        const float dx = a.x + flx, dy = a.y + fly;
+        const float al = fminf(b.y * fast_exp2(fmaf(a.w * dx, dy, fmaf(b.x * dy, dy, a.z * dx * dx))),
+                               kAlphaClampVal);
+        if (al >= kAlphaSkipF) {
+          blend(p, al, b.z, b.w, s_c[j], static_cast<uint32_t>(b0 + j));
+          if (p.done) break;
         }
       }
     }
-    if (__syncthreads_count(p0.done && p1.done) == 128) break;
+    if (__syncthreads_count(p.done) == 256) break;
   }
-  if (pending) mbar_wait(&s_bar, phase);  // never exit with copies in flight
-  if (in0 && !p0.done) p0.last = static_cast<uint32_t>(n);
-  if (in1 && !p1.done) p1.last = static_cast<uint32_t>(n);
-  if (in0) {
-    const int64_t pix = cam.pix_base + static_cast<int64_t>(py0) * cam.width + px;
-    image[3 * pix + 0] = p0.r;
-    image[3 * pix + 1] = p0.g;
-    image[3 * pix + 2] = p0.b;
-    final_T[pix] = p0.T;
-    counts[pix] = p0.cnt;
-    px_last[pix] = p0.last;
+  if (pending) mbar_wait(&s_bar, phase);
+  if (in && !p.done) p.last = static_cast<uint32_t>(n);
+  if (in) {
+    const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
+    image[3 * pix + 0] = p.r;
+    image[3 * pix + 1] = p.g;
+    image[3 * pix + 2] = p.b;
+    final_T[pix] = p.T;
+    counts[pix] = p.cnt;
+    px_last[pix] = p.last;
   }
-  if (in1) {
-    const int64_t pix = cam.pix_base + static_cast<int64_t>(py1) * cam.width + px;
-    image[3 * pix + 0] = p1.r;
-    image[3 * pix + 1] = p1.g;
-    image[3 * pix + 2] = p1.b;
-    final_T[pix] = p1.T;
-    counts[pix] = p1.cnt;
-    px_last[pix] = p1.last;
-  }
-  uint32_t m = max(in0 ? p0.last : 0u, in1 ? p1.last : 0u);
+  uint32_t m = in ? p.last : 0u;
 #pragma unroll
   for (int k = 16; k > 0; k >>= 1) m = max(m, __shfl_xor_sync(kFull, m, k));
   if (lane == 0) s_max[warp] = m;
   __syncthreads();
   if (tid == 0) {
-    const uint32_t np = max(max(s_max[0], s_max[1]), max(s_max[2], s_max[3]));
+    uint32_t np = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) np = max(np, s_max[w]);
     tile_nproc[tile] = np;
-    // the list is in increasing depth rank, so pair (s, tile) was processed
-    // iff rank_of[s] < last_rank[tile] (the backward's test, no inverse map)
     last_rank[tile] = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;
   }
 }
@@ -477,7 +478,7 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       float* image, float* final_T, int32_t* counts, cudaStream_t st) {
   // L.tile_order was computed from the list lengths before the depth sort
   CGS_PROFILED("raster_fwd_kernel", st,
-               raster_fwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges, vals,
+               raster_fwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.tile_order, L.ranges, vals,
                                                                  L.recs, L.hdr,
                                                                  image, final_T, counts, L.px_last,
                                                                  L.tile_nproc, L.rank_of,
