@@ -391,8 +391,58 @@ def make_modelio():
     print("modelio:", cases)
 
 
+def make_exact():
+    """train_step with exact_ratio=True (sampler.py:309-317): every split/merge
+    candidate renders the view before and after the trial move.  Small scene
+    (600 Gaussians sharing 48 rows, 48x48 view) so the reference finishes in
+    seconds; lambda small enough that the rendered ratio decides acceptance."""
+    rng0 = np.random.default_rng(11)
+    n, k = 600, 48
+    a = scenes.config0(3)
+    pos = rng0.uniform(-0.8, 0.8, (n, 3)).astype(np.float32)
+    idx = rng0.integers(0, k, n).astype(np.int32)
+    sr = a.sr_rows[:k].copy()
+    sr[:, 0:3] += 2.0  # larger splats so moves change the image
+    sh = a.sh_rows[:k].copy()
+    logit = rng0.normal(0.5, 1.0, n).astype(np.float32)
+    arrays = scenes.SceneArrays(pos, logit, idx, idx, sh, sr, 1)
+    gt_arrays = scenes.SceneArrays(rng0.uniform(-0.8, 0.8, (n, 3)).astype(np.float32), logit, idx,
+                                   idx, sh, sr, 1)
+    cam = scenes.ring_cameras(1, (0.0, 0.0, 0.0), 3.0, 0.0, 48.0, 48, 48)[0]
+    rcam = to_rcam(cam)
+    gt = rrender.rasterize_forward(ref_state(gt_arrays), rcam).image
+    cfg = rsampler.SamplerConfig(lambda_sh=1e-3, lambda_sr=1e-3, eps_split_sh=0.05,
+                                 eps_merge_sh=0.05, eps_split_sr=0.05, eps_merge_sr=0.05,
+                                 split_fraction=0.02, exact_ratio=True, lambda_ssim=0.0,
+                                 densify_every=0)
+    st = ref_state(arrays)
+    out = {}
+    state_arrays(st, "s0_", out)
+    cam_arrays(cam, "cam_", out)
+    out["gt"] = gt
+    for kk, v in _cfg_arrays(cfg).items():
+        out[f"cfg_{kk}"] = np.asarray(v)
+    rng = np.random.default_rng(2024)
+    schedule = ["split", "split", "merge", "split", "merge"]
+    for step, kind in enumerate(schedule):
+        c = copy.deepcopy(cfg)
+        c.p_update, c.p_split, c.p_merge = ((0.0, 1.0, 0.0) if kind == "split" else (0.0, 0.0, 1.0))
+        rec = rsampler.train_step(st, [(rcam, gt)], c, rng)
+        contrags.validate_state(st)
+        p = f"s{step + 1}_"
+        state_arrays(st, p, out)
+        out[p + "kind"] = np.array(kind)
+        out[p + "rec"] = np.array([rec.attempts, rec.accepts, rec.live_sh, rec.live_sr])
+        out[p + "accept_probs"] = np.array(rec.accept_probs, dtype=np.float64)
+    out["steps"] = np.int64(len(schedule))
+    out["rng_after"] = np.asarray(rng.random(4))
+    np.savez_compressed(os.path.join(OUT, "exact.npz"), **out)
+    print("exact: accepts", [int(out[f"s{i + 1}_rec"][1]) for i in range(len(schedule))],
+          "attempts", [int(out[f"s{i + 1}_rec"][0]) for i in range(len(schedule))])
+
+
 MAKERS = {"loss_sh": make_loss_sh, "sgld": make_sgld, "mcmc": make_mcmc, "render": make_render,
-          "gradcheck": make_gradcheck, "modelio": make_modelio}
+          "gradcheck": make_gradcheck, "modelio": make_modelio, "exact": make_exact}
 
 if __name__ == "__main__":
     print("numpy", np.__version__)

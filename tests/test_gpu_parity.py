@@ -425,3 +425,26 @@ def test_sgld_device_noise_statistics(cg):
         assert abs(e.std() - 1.0) < 0.01
         assert abs(np.mean(e ** 4) - 3.0) < 0.1  # Gaussian kurtosis
     assert abs(np.corrcoef(eta_p.ravel(), eta_p2.ravel())[0, 1]) < 0.01  # fresh per update
+
+
+def test_exact_ratio_chain_matches_reference(cg):
+    """train_step with exact_ratio=True (sampler.py:309-317): each candidate's
+    acceptance uses the rendered loss before/after the trial move; decisions,
+    states and the Generator stream match the reference, probabilities to 1e-6."""
+    from gpu_helpers import assert_state_equal, cam_from, state_from
+    d = golden("exact")
+    st = state_from(d, "s0_")
+    cam = cam_from(d, "cam_")
+    kw = {k[4:]: (v.item() if v.shape == () else v) for k, v in d.items() if k.startswith("cfg_")}
+    rng = np.random.default_rng(2024)
+    for step in range(1, int(d["steps"]) + 1):
+        p = f"s{step}_"
+        kind = str(d[p + "kind"])
+        mix = (0.0, 1.0, 0.0) if kind == "split" else (0.0, 0.0, 1.0)
+        cfg = cg.SamplerConfig(**{**kw, "p_update": mix[0], "p_split": mix[1], "p_merge": mix[2]})
+        rec = cg.train_step(st, [(cam, d["gt"])], cfg, rng)
+        cg.validate_state(st)
+        assert [rec.attempts, rec.accepts, rec.live_sh, rec.live_sr] == d[p + "rec"].tolist()
+        assert np.allclose(rec.accept_probs, d[p + "accept_probs"], rtol=1e-6, atol=0)
+        assert_state_equal(st, d, p)
+    assert np.array_equal(rng.random(4), d["rng_after"])
