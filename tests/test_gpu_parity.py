@@ -448,3 +448,50 @@ def test_exact_ratio_chain_matches_reference(cg):
         assert np.allclose(rec.accept_probs, d[p + "accept_probs"], rtol=1e-6, atol=0)
         assert_state_equal(st, d, p)
     assert np.array_equal(rng.random(4), d["rng_after"])
+
+
+def test_config1_full_size_matches_oracle(cg):
+    """BASELINE config 1 at full size (100k Gaussians, SH-3, 256x256, two views
+    rendered as one batched frame) against the oracle (~6 s of numpy per view).
+
+    The raster computes alpha and T in fp32; the reference in fp64.  At this
+    size a handful of pixels per view sit on a knife edge -- T_before within
+    ~1e-6 relative of the 1e-4 termination threshold (or alpha of 1/255) --
+    where the two precisions take different discrete decisions (SURVEY.md
+    section 7, hard part 1).  Those pixels are identified by their
+    contribution count differing by exactly one; everything else must match:
+    counts bit-exact, images / transmittance within rtol 1e-4, atol 1e-6, and
+    gradients within the same tolerance elementwise with the knife-edge pixels
+    removed from dL/dimage."""
+    from oracle import cgs_oracle as O
+    from paper_2509_03775_b200 import scenes
+    a, g = scenes.config1(0), scenes.config1(1)
+    cams = a.cameras[1:3]  # views with knife-edge pixels
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows,
+                                    g.sr_rows)
+    fr = cg.render_frame(st, cams)
+    gfr = cg.render_frame(gst, cams)
+    ost = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    dls, refs = [], []
+    for v, cam in enumerate(cams):
+        ocam = O.cam_from_any(cam)
+        fw = O.raster_forward(ost, ocam)
+        cnt = fr.view_counts(v).cpu().numpy()
+        knife = cnt != fw["counts"]
+        assert knife.sum() <= 16 and np.all(np.abs(cnt[knife] - fw["counts"][knife]) == 1)
+        ok = ~knife
+        img = fr.view_image(v).cpu().numpy()
+        T = fr.view_T(v).cpu().numpy()
+        assert np.allclose(img[ok], fw["image"][ok], rtol=RTOL, atol=ATOL)
+        assert np.allclose(T[ok], fw["final_T"][ok], rtol=RTOL, atol=ATOL)
+        dL = O.recon_loss_grad(fw["image"], gfr.view_image(v).cpu().numpy().astype(np.float64), 0.2)
+        dL[knife] = 0.0
+        dls.append(dL)
+        refs.append(O.raster_backward(ost, ocam, dL))
+    dl = torch.as_tensor(np.concatenate([x.reshape(-1) for x in dls]).astype(np.float32)).cuda()
+    gr = fr.backward(dl).numpy()
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        ref = refs[0][k] + refs[1][k]
+        assert np.allclose(gr[k], ref, rtol=RTOL, atol=ATOL), (k, np.abs(gr[k] - ref).max())
