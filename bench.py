@@ -131,29 +131,62 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def _oracle_view(args):
-    """One config view: oracle forward + L1/SSIM loss + backward (worker process)."""
-    from oracle import cgs_oracle as O
-    arrays, gt_arrays, cam, lam = args
-    st = O.OState.from_arrays(*arrays)
-    t0 = time.perf_counter()
-    fw = O.raster_forward(st, cam)
-    dL = O.recon_loss_grad(fw["image"], gt_arrays, lam)
-    g = O.raster_backward(st, cam, dL)
-    return time.perf_counter() - t0, g
+_W = {}
 
 
-def _oracle_iteration(a, gts, cams, lam, pool):
-    """One full reference update iteration on host cores: the views' forward /
-    loss / backward in parallel worker processes, then the mean gradient and
-    the SGLD update (reference sampler.py:320-338, 262-300)."""
+def _worker_init(arrays):
+    """Pool initializer: each worker builds the oracle state once."""
     from oracle import cgs_oracle as O
-    arrays = (a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
-    jobs = [(arrays, gts[k], O.cam_from_any(c), lam) for k, c in enumerate(cams)]
+    _W["st"] = O.OState.from_arrays(*arrays)
+
+
+def _strip_cam(cam, y0, y1):
+    """Rows [y0, y1) of a view as a camera of its own (principal point shifted).
+    Every pixel's compositing and gradient depend only on that pixel, so the
+    strips' images concatenate to the view's image and their gradients sum to
+    the view's gradient."""
+    from oracle import cgs_oracle as O
+    return O.OCam(R=cam.R, t=cam.t, fx=cam.fx, fy=cam.fy, cx=cam.cx, cy=cam.cy - y0,
+                  width=cam.width, height=y1 - y0)
+
+
+def _job_fwd(cam):
+    from oracle import cgs_oracle as O
+    return O.raster_forward(_W["st"], cam)["image"]
+
+
+def _job_loss(args):
+    from oracle import cgs_oracle as O
+    img, gt, lam = args
+    return O.recon_loss_grad(img, gt, lam)
+
+
+def _job_bwd(args):
+    from oracle import cgs_oracle as O
+    cam, dL = args
+    return O.raster_backward(_W["st"], cam, dL)
+
+
+def _oracle_iteration(a, gts, cams, lam, pool, strips):
+    """One full reference update iteration on host cores: forward, L1/SSIM loss
+    gradient and backward of every view, split into row strips so all worker
+    processes are busy, then the mean gradient and the SGLD update (reference
+    sampler.py:320-338, 262-300)."""
+    from oracle import cgs_oracle as O
+    ocams = [O.cam_from_any(c) for c in cams]
+    parts = []
+    for v, c in enumerate(ocams):
+        rows = max(16, ((c.height + strips - 1) // strips + 15) // 16 * 16)
+        for y0 in range(0, c.height, rows):
+            parts.append((v, y0, min(c.height, y0 + rows)))
     t0 = time.perf_counter()
-    res = pool.map(_oracle_view, jobs)
-    grads = {k: sum(r[1][k] for r in res) / len(res) for k in res[0][1]}
-    st = O.OState.from_arrays(*arrays)
+    imgs = pool.map(_job_fwd, [_strip_cam(ocams[v], y0, y1) for v, y0, y1 in parts])
+    full = [np.concatenate([im for (v2, _, _), im in zip(parts, imgs) if v2 == v], axis=0)
+            for v in range(len(ocams))]
+    dls = pool.map(_job_loss, [(full[v], gts[v], lam) for v in range(len(ocams))])
+    res = pool.map(_job_bwd, [(_strip_cam(ocams[v], y0, y1), dls[v][y0:y1]) for v, y0, y1 in parts])
+    grads = {k: sum(r[k] for r in res) / len(ocams) for k in res[0]}
+    st = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
     O.sgld_update(st, grads, O.config(), np.random.default_rng(0))
     return time.perf_counter() - t0
 
@@ -165,20 +198,22 @@ def _oracle_gts(g, cams):
 
 
 def cpu_iteration_timer(config, seed):
-    """Returns (fn() -> seconds per iteration, cores, sample description)."""
+    """Returns (fn() -> seconds per iteration, cores, sample description, pool)."""
     a, g, cams = make_scene(config, seed, 0, 1)
     gts = _oracle_gts(g, cams)
-    cores = max(1, min(len(cams), os.cpu_count() or 1))
-    ctx = mp.get_context("fork")
-    pool = ctx.Pool(cores)
+    cores = max(1, os.cpu_count() or 1)
+    strips = max(1, cores // len(cams))
+    arrays = (a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    pool = mp.get_context("fork").Pool(cores, initializer=_worker_init, initargs=(arrays,))
     lam = 0.0 if config == 0 else 0.2
 
     def run():
-        return _oracle_iteration(a, gts, cams, lam, pool)
+        return _oracle_iteration(a, gts, cams, lam, pool, strips)
 
     sample = (f"one full {workload_name(config).split(':')[0]} update iteration "
-              f"({len(cams)} views fwd+L1/SSIM+bwd in {cores} worker processes, mean grad, SGLD) "
-              "through the numpy oracle port (oracle/cgs_oracle.py) of the reference")
+              f"({len(cams)} views x {strips} row strips fwd + L1/SSIM grad + bwd in {cores} "
+              "worker processes, mean grad, SGLD) through the numpy oracle port "
+              "(oracle/cgs_oracle.py) of the reference")
     return run, cores, sample, pool
 
 

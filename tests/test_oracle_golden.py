@@ -6,6 +6,7 @@ container); known answers are the reference's own tests
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -241,3 +242,28 @@ def test_acceptance_known_answers():
     assert math.isclose(O.q_sm(u, 0.1, 0.05), math.exp(1.5), rel_tol=1e-12)
     assert math.isclose(O.accept_prob("split", np.zeros(3), 2.3, 0.1, 0.05), math.exp(-2.3), rel_tol=1e-12)
     assert O.accept_prob("merge", np.zeros(3), 2.3, 0.1, 0.05) == 1.0
+
+
+def test_row_strips_compose_to_the_view():
+    """bench.py's CPU baseline splits each view into row strips (one camera each,
+    principal point shifted): images concatenate and gradients sum to the
+    full view's, since every pixel's compositing depends only on that pixel."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import _strip_cam
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config0(0)
+    st = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    cam = O.cam_from_any(a.cameras[0])
+    full = O.raster_forward(st, cam)
+    dL = np.random.default_rng(0).normal(0, 1e-3, full["image"].shape)
+    gfull = O.raster_backward(st, cam, dL)
+    imgs, gsum = [], None
+    for y0 in range(0, cam.height, 16):
+        c = _strip_cam(cam, y0, min(cam.height, y0 + 16))
+        imgs.append(O.raster_forward(st, c)["image"])
+        g = O.raster_backward(st, c, dL[y0:y0 + 16])
+        gsum = g if gsum is None else {k: gsum[k] + g[k] for k in g}
+    assert np.allclose(np.concatenate(imgs, 0), full["image"], rtol=1e-12, atol=1e-15)
+    for k in gfull:
+        assert np.allclose(gsum[k], gfull[k], rtol=1e-9, atol=1e-15), k
