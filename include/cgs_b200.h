@@ -240,6 +240,15 @@ CGS_API int cgs_densify_append(float* positions, float* opacity_logits, int32_t*
                        int64_t n, const int64_t* src, const double* jitter, int64_t k,
                        cgs_stream_t stream);
 
+/* densify sources on the device (throughput mode; replaces the host
+ * rng.choice(n, k, p=sigmoid(logit)/sum) of model.py:256 with the same
+ * host-drawn uniforms, see update.cu): src[j] = first i with
+ * cumsum(sigmoid(logit))[i] > uniforms[j] * total (fixed point 2^-40). */
+CGS_API size_t cgs_densify_select_workspace_bytes(int64_t n);
+CGS_API int cgs_densify_select(const float* opacity_logits, int64_t n, const double* uniforms,
+                               int64_t k, int64_t* src, void* ws, size_t ws_bytes,
+                               cgs_stream_t stream);
+
 /* counts[r] = #{i : idx[i] == r} (validate_state, model.py:297). */
 CGS_API int cgs_refcount_histogram(const int32_t* idx, int64_t n, int32_t* counts, int64_t capacity,
                            cgs_stream_t stream);

@@ -95,6 +95,8 @@ SIGNATURES = {
     "cgs_apply_splits": (I32, [P, I32, P, P, P, P, P, I64, P]),
     "cgs_apply_remap": (I32, [P, I64, P, I64, P]),
     "cgs_densify_append": (I32, [P, P, P, P, I64, P, P, I64, P]),
+    "cgs_densify_select_workspace_bytes": (SZ, [I64]),
+    "cgs_densify_select": (I32, [P, I64, P, I64, P, P, SZ, P]),
     "cgs_refcount_histogram": (I32, [P, I64, P, I64, P]),
     "cgs_scan_workspace_bytes": (SZ, [I64]),
     "cgs_exclusive_scan_u32": (I32, [P, P, I64, P, P, SZ, P]),

@@ -90,6 +90,9 @@ int apply_splits(float* rows, int dim, int32_t* idx, const int64_t* gauss, const
 int apply_remap(int32_t* idx, int64_t n, const int32_t* remap, int64_t len, cudaStream_t st);
 int densify_append(float* pos, float* logit, int32_t* g2sh, int32_t* g2sr, int64_t n,
                    const int64_t* src, const double* jit, int64_t k, cudaStream_t st);
+size_t densify_select_ws_bytes(int64_t n);
+int densify_select(const float* logit, int64_t n, const double* u, int64_t k, int64_t* src,
+                   void* ws, size_t ws_bytes, cudaStream_t st);
 int refcount_histogram(const int32_t* idx, int64_t n, int32_t* counts, int64_t cap,
                        cudaStream_t st);
 
@@ -422,6 +425,14 @@ int cgs_densify_append(float* positions, float* opacity_logits, int32_t* g2sh, i
                        int64_t n, const int64_t* src, const double* jitter, int64_t k,
                        cgs_stream_t stream) {
   return densify_append(positions, opacity_logits, g2sh, g2sr, n, src, jitter, k,
+                        static_cast<cudaStream_t>(stream));
+}
+
+size_t cgs_densify_select_workspace_bytes(int64_t n) { return densify_select_ws_bytes(n); }
+
+int cgs_densify_select(const float* opacity_logits, int64_t n, const double* uniforms, int64_t k,
+                       int64_t* src, void* ws, size_t ws_bytes, cgs_stream_t stream) {
+  return densify_select(opacity_logits, n, uniforms, k, src, ws, ws_bytes,
                         static_cast<cudaStream_t>(stream));
 }
 

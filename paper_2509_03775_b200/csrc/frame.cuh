@@ -132,7 +132,8 @@ int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
                       float* image, float* final_T, int32_t* counts, cudaStream_t st);
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
-                      const float* dL, float* partials, cudaStream_t st);
+                      const float* dL, float* partials, unsigned long long* n_processed,
+                      cudaStream_t st);
 
 // Emission index of pair (splat s, tile t): pairs of a splat are emitted in
 // row-major order over its tile rect starting at pair_off[s].

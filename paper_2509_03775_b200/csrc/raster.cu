@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
     const float* __restrict__ final_T, const float* __restrict__ dL,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect, int64_t n,
-    float* __restrict__ partials) {
+    float* __restrict__ partials, unsigned long long* __restrict__ n_processed) {
   constexpr int B = kBwdBatch;
   __shared__ __align__(128) SplatRec s_raw[B];
   __shared__ float4 s_a[B];
@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   const int tile = static_cast<int>(order[blockIdx.x]);
   const int nproc = static_cast<int>(tile_nproc[tile]);
   if (nproc == 0) return;
+  if (threadIdx.x == 0) atomicAdd(n_processed, static_cast<unsigned long long>(nproc));  // P_x
   int v = 0;
   while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
   const CamDev& cam = fd.cam[v];
@@ -488,7 +489,8 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 }
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
-                      const float* dL, float* partials, cudaStream_t st) {
+                      const float* dL, float* partials, unsigned long long* n_processed,
+                      cudaStream_t st) {
   int rc = launch_tile_order(fd, L, L.tile_nproc, st);
   if (rc) return rc;
   CGS_PROFILED("raster_bwd_kernel", st,
@@ -497,7 +499,7 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
                                                                  L.recs, L.hdr, L.px_last,
                                                                  L.tile_nproc, final_T, dL,
                                                                  L.pair_off, L.rect, L.n,
-                                                                 partials));
+                                                                 partials, n_processed));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   return CGS_OK;
 }

@@ -79,11 +79,6 @@ inline BwdLayout plan_bwd(void* base, size_t cap, int64_t n, int n_views, int to
 }
 
 // ---------------------------------------------------------------------------
-struct TileProcCount {
-  const uint32_t* nproc;
-  __device__ uint64_t load(int64_t t) const { return nproc[t]; }
-  __device__ void store(int64_t, uint64_t, uint64_t) const {}
-};
 
 struct GaussIn {
   const SplatRec* recs;  // projection records of the frame (conic, clamped colour)
@@ -633,10 +628,7 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
     }
   }
   if (fd.total_tiles > 0 && L.vn > 0) {
-    int rc = launch_scan(TileProcCount{L.tile_nproc}, nullptr, fd.total_tiles, fd.total_tiles,
-                         B.scan, &B.hdr->n_processed, st);
-    if (rc) return rc;
-    rc = launch_raster_bwd(fd, L, final_T, dL, B.partials, st);
+    int rc = launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed, st);
     if (rc) return rc;
     PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};

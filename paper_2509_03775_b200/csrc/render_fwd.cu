@@ -70,145 +70,174 @@ struct ProjOut {
   uint64_t* depth_key;
   uint32_t* dkey;  // 32-bit depth sort key (~0 for splats without tiles)
   uint32_t* dval;  // splat id (sort payload)
+  uint32_t* hist;  // 4 x 256 digit histogram of dkey (depth sort)
   uint32_t* n_tiles;
   uint64_t* rect;
   FrameHeader* hdr;
 };
 
+// One (view, Gaussian) splat; returns its 32-bit depth sort key (~0: no tiles).
 template <int DEG>
-__global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
+__device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDesc& fd,
+                                                const ProjOut& out, int64_t s) {
   constexpr int NB = (DEG + 1) * (DEG + 1);
   constexpr int D = 3 * NB;
-  const int64_t vn = in.n * fd.n_views;
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < vn;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int v = static_cast<int>(s / in.n);
-    const int64_t i = s - static_cast<int64_t>(v) * in.n;
-    const CamDev& cam = fd.cam[v];
-    const double px = in.pos[3 * i + 0], py = in.pos[3 * i + 1], pz = in.pos[3 * i + 2];
-    // camera coordinates t = R p + trans (camera.py:29-32)
-    const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
-    const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
-    const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
-    out.dval[s] = static_cast<uint32_t>(s);
-    out.dkey[s] = 0xffffffffu;
-    if (!(tz > kNear)) {  // near-plane cull, render.py:149
-      out.n_tiles[s] = 0;
-      continue;
-    }
-    const double* cv = in.sr_cov + static_cast<int64_t>(in.g2sr[i]) * 8;
-    if (cv[6] != 0.0) {  // zero quaternion: reference raises ValueError
-      out.n_tiles[s] = 0;
-      out.hdr->stats.zero_quaternion = 1;
-      continue;
-    }
-    const double mx = cam.fx * tx / tz + cam.cx;
-    const double my = cam.fy * ty / tz + cam.cy;
-    // J (render.py:160-164) and M = J R (render.py:165)
-    const double j00 = cam.fx / tz, j02 = -cam.fx * tx / (tz * tz);
-    const double j11 = cam.fy / tz, j12 = -cam.fy * ty / (tz * tz);
-    double m0[3], m1[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      m0[k] = j00 * cam.R[k] + j02 * cam.R[6 + k];
-      m1[k] = j11 * cam.R[3 + k] + j12 * cam.R[6 + k];
-    }
-    const double S[9] = {cv[0], cv[1], cv[2], cv[1], cv[3], cv[4], cv[2], cv[4], cv[5]};
-    double sm0[3], sm1[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      sm0[k] = S[k * 3 + 0] * m0[0] + S[k * 3 + 1] * m0[1] + S[k * 3 + 2] * m0[2];
-      sm1[k] = S[k * 3 + 0] * m1[0] + S[k * 3 + 1] * m1[1] + S[k * 3 + 2] * m1[2];
-    }
-    // Sigma2 = M Sigma3 M^T + 0.3 I (render.py:171-174)
-    const double a = m0[0] * sm0[0] + m0[1] * sm0[1] + m0[2] * sm0[2] + kBlur;
-    const double b = m0[0] * sm1[0] + m0[1] * sm1[1] + m0[2] * sm1[2];
-    const double c = m1[0] * sm1[0] + m1[1] * sm1[1] + m1[2] * sm1[2] + kBlur;
-    const double det = a * c - b * b;
-    const double lam = 0.5 * (a + c) + sqrt(0.25 * (a - c) * (a - c) + b * b);
-    const double rad = kFootprint * sqrt(lam) + 1e-9;
-    // inclusive pixel rect on pixel centres (render.py:110-115)
-    const double x0 = fmax(0.0, ceil(mx - rad - 0.5));
-    const double x1 = fmin(cam.width - 1.0, floor(mx + rad - 0.5));
-    const double y0 = fmax(0.0, ceil(my - rad - 0.5));
-    const double y1 = fmin(cam.height - 1.0, floor(my + rad - 0.5));
-    if (!(x0 <= x1 && y0 <= y1)) {
-      out.n_tiles[s] = 0;
-      continue;
-    }
-    const int tx0 = static_cast<int>(x0) / kTile, tx1 = static_cast<int>(x1) / kTile;
-    const int ty0 = static_cast<int>(y0) / kTile, ty1 = static_cast<int>(y1) / kTile;
-    // view direction and SH colour (render.py:187-198)
-    double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
-    const double len = sqrt((ox * ox + oy * oy) + oz * oz);
-    ox /= len;
-    oy /= len;
-    oz /= len;
-    double B[NB];
-    sh_basis<DEG>(ox, oy, oz, B);
-    const float* row = in.sh_rows + static_cast<int64_t>(in.g2sh[i]) * D;
-    double col[3] = {0.0, 0.0, 0.0};
-    if constexpr (D % 4 == 0) {
-      const float4* r4 = reinterpret_cast<const float4*>(row);
-#pragma unroll
-      for (int q = 0; q < D / 4; ++q) {
-        const float4 f = __ldg(r4 + q);
-        const float fv[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = 4 * q + u;
-          col[e % 3] += B[e / 3] * static_cast<double>(fv[u]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < D; ++e) col[e % 3] += B[e / 3] * static_cast<double>(__ldg(row + e));
-    }
-    SplatRec rec;
-    rec.mx = mx;
-    rec.my = my;
-    rec.ca = c / det;  // conic = adj(Sigma2) / det (render.py:176-181)
-    rec.cb = -b / det;
-    rec.cc = a / det;
-    const double opac = 1.0 / (1.0 + exp(-static_cast<double>(in.logit[i])));
-    rec.opac = static_cast<float>(opac);
-    rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
-    rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
-    rec.b = static_cast<float>(fmax(col[2] + 0.5, 0.0));
-    // Contribution box for the raster's warp-level skip: pixels whose centre
-    // lies outside the bounding box of {d : o exp(-d^T conic d / 2) >= 1/255}
-    // have alpha < 1/255 in the reference's float64 arithmetic (render.py:
-    // 274-280), so they are never kept there and skipping them is exact.  The
-    // box half-widths are sqrt(t Sigma2_xx), sqrt(t Sigma2_yy) with
-    // t = 2 ln(255 o), widened by a relative 1e-7 for rounding; it lies inside
-    // the pixel rect (o < 1, Sigma2_xx <= lambda_max).  o < 1/255: no pixel.
-    {
-      const double t = 2.0 * log(255.0 * opac) * (1.0 + 1e-7) + 1e-12;
-      uint16_t bx0 = 0xffff, bx1 = 0, by0 = 0xffff, by1 = 0;
-      if (t > 0.0) {
-        const double hx = sqrt(t * a) * (1.0 + 1e-7) + 1e-7;
-        const double hy = sqrt(t * c) * (1.0 + 1e-7) + 1e-7;
-        const double cx0 = fmax(x0, ceil(mx - hx - 0.5)), cx1 = fmin(x1, floor(mx + hx - 0.5));
-        const double cy0 = fmax(y0, ceil(my - hy - 0.5)), cy1 = fmin(y1, floor(my + hy - 0.5));
-        if (cx0 <= cx1 && cy0 <= cy1) {
-          bx0 = static_cast<uint16_t>(cx0);
-          bx1 = static_cast<uint16_t>(cx1);
-          by0 = static_cast<uint16_t>(cy0);
-          by1 = static_cast<uint16_t>(cy1);
-        }
-      }
-      rec.px0 = bx0;  // empty box: px0 = py0 = 0xffff
-      rec.px1 = bx1;
-      rec.py0 = by0;
-      rec.py1 = by1;
-    }
-    out.recs[s] = rec;
-    out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
-    out.dkey[s] = __float_as_uint(__double2float_rz(tz));  // tz > 0: monotone bits
-    out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
-    out.rect[s] = static_cast<uint64_t>(tx0) | (static_cast<uint64_t>(tx1) << 16) |
-                  (static_cast<uint64_t>(ty0) << 32) | (static_cast<uint64_t>(ty1) << 48);
+  const int v = static_cast<int>(s / in.n);
+  const int64_t i = s - static_cast<int64_t>(v) * in.n;
+  const CamDev& cam = fd.cam[v];
+  const double px = in.pos[3 * i + 0], py = in.pos[3 * i + 1], pz = in.pos[3 * i + 2];
+  // camera coordinates t = R p + trans (camera.py:29-32)
+  const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
+  const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
+  const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
+  out.dval[s] = static_cast<uint32_t>(s);
+  out.dkey[s] = 0xffffffffu;
+  if (!(tz > kNear)) {  // near-plane cull, render.py:149
+    out.n_tiles[s] = 0;
+    return 0xffffffffu;
   }
+  const double* cv = in.sr_cov + static_cast<int64_t>(in.g2sr[i]) * 8;
+  if (cv[6] != 0.0) {  // zero quaternion: reference raises ValueError
+    out.n_tiles[s] = 0;
+    out.hdr->stats.zero_quaternion = 1;
+    return 0xffffffffu;
+  }
+  const double mx = cam.fx * tx / tz + cam.cx;
+  const double my = cam.fy * ty / tz + cam.cy;
+  // J (render.py:160-164) and M = J R (render.py:165)
+  const double j00 = cam.fx / tz, j02 = -cam.fx * tx / (tz * tz);
+  const double j11 = cam.fy / tz, j12 = -cam.fy * ty / (tz * tz);
+  double m0[3], m1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    m0[k] = j00 * cam.R[k] + j02 * cam.R[6 + k];
+    m1[k] = j11 * cam.R[3 + k] + j12 * cam.R[6 + k];
+  }
+  const double S[9] = {cv[0], cv[1], cv[2], cv[1], cv[3], cv[4], cv[2], cv[4], cv[5]};
+  double sm0[3], sm1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    sm0[k] = S[k * 3 + 0] * m0[0] + S[k * 3 + 1] * m0[1] + S[k * 3 + 2] * m0[2];
+    sm1[k] = S[k * 3 + 0] * m1[0] + S[k * 3 + 1] * m1[1] + S[k * 3 + 2] * m1[2];
+  }
+  // Sigma2 = M Sigma3 M^T + 0.3 I (render.py:171-174)
+  const double a = m0[0] * sm0[0] + m0[1] * sm0[1] + m0[2] * sm0[2] + kBlur;
+  const double b = m0[0] * sm1[0] + m0[1] * sm1[1] + m0[2] * sm1[2];
+  const double c = m1[0] * sm1[0] + m1[1] * sm1[1] + m1[2] * sm1[2] + kBlur;
+  const double det = a * c - b * b;
+  const double lam = 0.5 * (a + c) + sqrt(0.25 * (a - c) * (a - c) + b * b);
+  const double rad = kFootprint * sqrt(lam) + 1e-9;
+  // inclusive pixel rect on pixel centres (render.py:110-115)
+  const double x0 = fmax(0.0, ceil(mx - rad - 0.5));
+  const double x1 = fmin(cam.width - 1.0, floor(mx + rad - 0.5));
+  const double y0 = fmax(0.0, ceil(my - rad - 0.5));
+  const double y1 = fmin(cam.height - 1.0, floor(my + rad - 0.5));
+  if (!(x0 <= x1 && y0 <= y1)) {
+    out.n_tiles[s] = 0;
+    return 0xffffffffu;
+  }
+  const int tx0 = static_cast<int>(x0) / kTile, tx1 = static_cast<int>(x1) / kTile;
+  const int ty0 = static_cast<int>(y0) / kTile, ty1 = static_cast<int>(y1) / kTile;
+  // view direction and SH colour (render.py:187-198)
+  double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
+  const double len = sqrt((ox * ox + oy * oy) + oz * oz);
+  ox /= len;
+  oy /= len;
+  oz /= len;
+  double B[NB];
+  sh_basis<DEG>(ox, oy, oz, B);
+  const float* row = in.sh_rows + static_cast<int64_t>(in.g2sh[i]) * D;
+  double col[3] = {0.0, 0.0, 0.0};
+  if constexpr (D % 4 == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) {
+      const float4 f = __ldg(r4 + q);
+      const float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = 4 * q + u;
+        col[e % 3] += B[e / 3] * static_cast<double>(fv[u]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < D; ++e) col[e % 3] += B[e / 3] * static_cast<double>(__ldg(row + e));
+  }
+  SplatRec rec;
+  rec.mx = mx;
+  rec.my = my;
+  rec.ca = c / det;  // conic = adj(Sigma2) / det (render.py:176-181)
+  rec.cb = -b / det;
+  rec.cc = a / det;
+  const double opac = 1.0 / (1.0 + exp(-static_cast<double>(in.logit[i])));
+  rec.opac = static_cast<float>(opac);
+  rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
+  rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
+  rec.b = static_cast<float>(fmax(col[2] + 0.5, 0.0));
+  // Contribution box for the raster's warp-level skip: pixels whose centre
+  // lies outside the bounding box of {d : o exp(-d^T conic d / 2) >= 1/255}
+  // have alpha < 1/255 in the reference's float64 arithmetic (render.py:
+  // 274-280), so they are never kept there and skipping them is exact.  The
+  // box half-widths are sqrt(t Sigma2_xx), sqrt(t Sigma2_yy) with
+  // t = 2 ln(255 o), widened by a relative 1e-7 for rounding; it lies inside
+  // the pixel rect (o < 1, Sigma2_xx <= lambda_max).  o < 1/255: no pixel.
+  {
+    const double t = 2.0 * log(255.0 * opac) * (1.0 + 1e-7) + 1e-12;
+    uint16_t bx0 = 0xffff, bx1 = 0, by0 = 0xffff, by1 = 0;
+    if (t > 0.0) {
+      const double hx = sqrt(t * a) * (1.0 + 1e-7) + 1e-7;
+      const double hy = sqrt(t * c) * (1.0 + 1e-7) + 1e-7;
+      const double cx0 = fmax(x0, ceil(mx - hx - 0.5)), cx1 = fmin(x1, floor(mx + hx - 0.5));
+      const double cy0 = fmax(y0, ceil(my - hy - 0.5)), cy1 = fmin(y1, floor(my + hy - 0.5));
+      if (cx0 <= cx1 && cy0 <= cy1) {
+        bx0 = static_cast<uint16_t>(cx0);
+        bx1 = static_cast<uint16_t>(cx1);
+        by0 = static_cast<uint16_t>(cy0);
+        by1 = static_cast<uint16_t>(cy1);
+      }
+    }
+    rec.px0 = bx0;  // empty box: px0 = py0 = 0xffff
+    rec.px1 = bx1;
+    rec.py0 = by0;
+    rec.py1 = by1;
+  }
+  out.recs[s] = rec;
+  out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
+  const uint32_t key = __float_as_uint(__double2float_rz(tz));  // tz > 0: monotone bits
+  out.dkey[s] = key;
+  out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
+  out.rect[s] = static_cast<uint64_t>(tx0) | (static_cast<uint64_t>(tx1) << 16) |
+                (static_cast<uint64_t>(ty0) << 32) | (static_cast<uint64_t>(ty1) << 48);
+  return key;
+}
+
+// Grid-stride over all splats of the frame; also builds the depth sort's
+// 4-pass digit histogram (warp-aggregated shared counters, one global
+// atomic per non-zero bin per CTA) so the sort skips its histogram pass.
+template <int DEG>
+__global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
+  __shared__ uint32_t s_h[4 * 256];
+  for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_h[k] = 0;
+  __syncthreads();
+  const int64_t vn = in.n * fd.n_views;
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x); b < vn;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = b + threadIdx.x;
+    const bool ok = s < vn;
+    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0u;
+    const unsigned valid = __ballot_sync(kFull, ok);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const unsigned d = (key >> (8 * p)) & 255u;
+      const unsigned peers = warp_peers8(d) & valid;
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x)
+    if (s_h[k]) atomicAdd(&out.hist[k], s_h[k]);
 }
 
 // ---------------------------------------------------------------------------
@@ -279,21 +308,36 @@ __global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n
 // emit_long_pairs_kernel, one CTA per splat, so no warp serialises on them.
 // Within one splat, tiles are emitted row-major over its tile rect.
 template <typename KT>
-__device__ __forceinline__ void emit_one(uint64_t p, int k, uint64_t rc, int ntx, int tbase,
-                                         uint32_t s, KT* keys, uint32_t* vals) {
+__device__ __forceinline__ uint32_t emit_one(uint64_t p, int k, uint64_t rc, int ntx, int tbase,
+                                             uint32_t s, KT* keys, uint32_t* vals) {
   const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
   const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
   const int span = tx1 - tx0 + 1;
-  keys[p] = static_cast<KT>(tbase + (ty0 + k / span) * ntx + tx0 + k % span);
+  const uint32_t t = static_cast<uint32_t>(tbase + (ty0 + k / span) * ntx + tx0 + k % span);
+  keys[p] = static_cast<KT>(t);
   vals[p] = s;
+  return t;
+}
+
+// Adds the tile keys of the warp's live lanes to the shared digit histogram.
+template <typename KT>
+__device__ __forceinline__ void hist_keys(uint32_t* s_h, int passes, uint32_t key, bool live,
+                                          int lane) {
+  const unsigned valid = __ballot_sync(kFull, live);
+  if (!valid) return;
+  for (int p = 0; p < passes; ++p) {
+    const unsigned d = (key >> (8 * p)) & 255u;
+    const unsigned peers = warp_peers8(d) & valid;
+    if (live && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
+  }
 }
 
 template <typename KT>
-__global__ void __launch_bounds__(256) emit_pairs_kernel(
+__device__ __forceinline__ void emit_warps(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
-    FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ long_list,
-    KT* __restrict__ keys, uint32_t* __restrict__ vals) {
+    FrameHeader* __restrict__ hdr, const FrameDesc& fd, int64_t n, uint32_t* __restrict__ long_list,
+    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int passes) {
   if (hdr->stats.overflow) return;
   const int lane = threadIdx.x & 31;
   const int64_t ns = static_cast<int64_t>(hdr->n_onscreen);  // ranks with tiles come first
@@ -331,13 +375,31 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
       const int nt = __shfl_sync(kFull, ntx, own);
       const int tb = __shfl_sync(kFull, tbase, own);
       const uint32_t so = __shfl_sync(kFull, s, own);
+      uint32_t key = 0;
       if (q < total) {
         const int k = static_cast<int>(q - lo2);
-        emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
+        key = emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
       }
+      hist_keys<KT>(s_h, passes, key, q < total, lane);
     }
   }
 }
+
+template <typename KT>
+__global__ void __launch_bounds__(256) emit_pairs_kernel(
+    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
+    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
+    FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ long_list,
+    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int passes) {
+  __shared__ uint32_t s_h[4 * 256];  // tile sort digit histogram (this CTA's pairs)
+  for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
+  __syncthreads();
+  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, passes);
+  __syncthreads();
+  for (int k = threadIdx.x; k < passes * 256; k += blockDim.x)
+    if (s_h[k]) atomicAdd(&hist[k], s_h[k]);
+}
+
 
 // One CTA per long splat (near-plane giants): its pair range is contiguous.
 template <typename KT>
@@ -345,18 +407,30 @@ __global__ void __launch_bounds__(256) emit_long_pairs_kernel(
     const uint32_t* __restrict__ long_list, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
     const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, KT* __restrict__ keys,
-    uint32_t* __restrict__ vals) {
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int passes) {
+  __shared__ uint32_t s_h[4 * 256];
   if (hdr->stats.overflow) return;
   const int64_t nl = static_cast<int64_t>(hdr->scratch[2]);
+  if (blockIdx.x >= nl) return;
+  for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   for (int64_t e = blockIdx.x; e < nl; e += gridDim.x) {
     const uint32_t s = long_list[e];
     const uint64_t o = off[s];
     const int cnt = static_cast<int>(n_tiles[s]);
     const uint64_t rc = rect[s];
     const int v = static_cast<int>(s / static_cast<uint32_t>(n));
-    for (int k = threadIdx.x; k < cnt; k += blockDim.x)
-      emit_one<KT>(o + k, k, rc, fd.cam[v].ntx, fd.cam[v].tile_base, s, keys, vals);
+    for (int k0 = 0; k0 < cnt; k0 += blockDim.x) {
+      const int k = k0 + threadIdx.x;
+      uint32_t key = 0;
+      if (k < cnt) key = emit_one<KT>(o + k, k, rc, fd.cam[v].ntx, fd.cam[v].tile_base, s, keys, vals);
+      hist_keys<KT>(s_h, passes, key, k < cnt, lane);
+    }
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < passes * 256; k += blockDim.x)
+    if (s_h[k]) atomicAdd(&hist[k], s_h[k]);
 }
 
 template <typename KT>
@@ -386,17 +460,22 @@ static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
   KT* kres;
   uint32_t* vres;
   const int eg = grid_for(L.vn, 256, 16);
+  // the emission kernels also build the tile sort's digit histogram
+  const int passes = (L.tile_key_bits + 7) / 8;
+  CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
   CGS_PROFILED("emit_pairs_kernel", st,
                emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.pair_off, L.n_tiles, L.rect, L.hdr,
                                                           fd, L.n, L.long_list,
-                                                          static_cast<KT*>(L.pkeys), L.pvals));
+                                                          static_cast<KT*>(L.pkeys), L.pvals,
+                                                          ws.hist, passes));
   CGS_CHECK_LAUNCH("emit_pairs_kernel");
   emit_long_pairs_kernel<KT><<<148 * 4, 256, 0, st>>>(L.long_list, L.pair_off, L.n_tiles, L.rect,
                                                        L.hdr, fd, L.n, static_cast<KT*>(L.pkeys),
-                                                       L.pvals);
+                                                       L.pvals, ws.hist, passes);
   CGS_CHECK_LAUNCH("emit_long_pairs_kernel");
   int rc = launch_radix_sort<KT>(static_cast<KT*>(L.pkeys), L.pvals, &L.hdr->n_pairs, 0,
-                                 L.pair_cap, L.tile_key_bits, ws, &kres, &vres, st);
+                                 L.pair_cap, L.tile_key_bits, ws, &kres, &vres, st,
+                                 /*hist_ready=*/true);
   if (rc) return rc;
   CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * (fd.total_tiles > 0 ? fd.total_tiles : 1), st));
   tile_ranges_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(kres, L.hdr, L.ranges);
@@ -416,7 +495,8 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   }
   if (vn > 0) {
     ProjIn in{sc->n, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, sr_cov};
-    ProjOut out{L.recs, L.depth_key, L.dkey, L.dval, L.n_tiles, L.rect, L.hdr};
+    CGS_CUDA(cudaMemsetAsync(L.dsort.hist, 0, 4 * 256 * sizeof(uint32_t), st));
+    ProjOut out{L.recs, L.depth_key, L.dkey, L.dval, L.dsort.hist, L.n_tiles, L.rect, L.hdr};
     switch (sc->sh_degree) {
       case 0: launch_project<0>(in, fd, out, vn, st); break;
       case 1: launch_project<1>(in, fd, out, vn, st); break;
@@ -431,7 +511,7 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   if (vn > 0) {
     uint32_t* kres;
     int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, nullptr, vn, vn, 32, L.dsort, &kres, &perm,
-                                         st);
+                                         st, /*hist_ready=*/true);
     if (rc) return rc;
     CGS_PROFILED("depth_tie_fix_kernel", st,
                  depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(kres, perm,

@@ -428,16 +428,18 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
 template <typename K>
 int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, int64_t n_host,
                       int64_t n_cap, int key_bits, const SortWs<K>& ws, K** out_keys,
-                      uint32_t** out_vals, cudaStream_t st) {
+                      uint32_t** out_vals, cudaStream_t st, bool hist_ready = false) {
   int passes = (key_bits + 7) / 8;
   if (passes < 1) passes = 1;
   if (passes > ws.passes_cap) return CGS_EINVAL;
-  CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
+  if (!hist_ready) CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
   CGS_CUDA(cudaMemsetAsync(ws.status, 0,
                            static_cast<size_t>(passes) * ws.max_parts * 256 * sizeof(uint32_t), st));
   CGS_CUDA(cudaMemsetAsync(ws.counter, 0, 64 * sizeof(unsigned), st));
-  CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist));
-  CGS_CHECK_LAUNCH("sort_hist_kernel");
+  if (!hist_ready) {  // else the producer of the keys already filled ws.hist
+    CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist));
+    CGS_CHECK_LAUNCH("sort_hist_kernel");
+  }
   static bool attr_set = false;
   const size_t smem = sizeof(SortSmem<K>);
   if (!attr_set) {

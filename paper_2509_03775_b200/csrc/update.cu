@@ -322,6 +322,65 @@ int densify_append(float* pos, float* logit, int32_t* g2sh, int32_t* g2sr, int64
   return CGS_OK;
 }
 
+// Opacity-weighted selection of densify sources on the device (throughput
+// mode).  numpy's choice(n, k, p=o/sum(o)) draws exactly random(k) from the
+// Generator and returns searchsorted(cumsum(p)/cumsum(p)[-1], u, 'right')
+// (verified against numpy 2.3); the host still draws the same uniforms, the
+// device runs the cumulative sum as a fixed-point (2^-40) inclusive scan of
+// sigmoid(logit) and a binary search per draw.  Selections can differ from
+// numpy's only for a uniform within ~1e-12 relative of a cumulative boundary.
+constexpr double kOpacFix = 1099511627776.0;  // 2^40
+
+struct OpacScan {
+  const float* logit;
+  uint64_t* incl;
+  __device__ uint64_t load(int64_t i) const {
+    const double o = 1.0 / (1.0 + exp(-static_cast<double>(logit[i])));
+    return static_cast<uint64_t>(o * kOpacFix);
+  }
+  __device__ void store(int64_t i, uint64_t ex, uint64_t v) const { incl[i] = ex + v; }
+};
+
+__global__ void densify_select_kernel(const uint64_t* __restrict__ incl, int64_t n,
+                                      const unsigned long long* __restrict__ total,
+                                      const double* __restrict__ u, int64_t k,
+                                      int64_t* __restrict__ src) {
+  const double tot = static_cast<double>(*total);
+  for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < k;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t target = static_cast<uint64_t>(u[j] * tot);
+    int64_t lo = 0, hi = n;  // first i with incl[i] > target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (incl[mid] > target) hi = mid;
+      else lo = mid + 1;
+    }
+    src[j] = lo < n ? lo : n - 1;
+  }
+}
+
+size_t densify_select_ws_bytes(int64_t n) {
+  return align_up((n > 0 ? n : 1) * sizeof(uint64_t)) + scan_ws_bytes(n) + 512;
+}
+
+int densify_select(const float* logit, int64_t n, const double* u, int64_t k, int64_t* src,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (k <= 0 || n <= 0) return CGS_OK;
+  Carver c(ws, ws_bytes);
+  uint64_t* incl = c.take<uint64_t>(n);
+  ScanWs sw = carve_scan(c, n);
+  unsigned long long* tot = c.take<unsigned long long>(1);
+  if (!c.fits()) {
+    set_error("densify_select: workspace too small");
+    return CGS_EWORKSPACE;
+  }
+  int rc = launch_scan(OpacScan{logit, incl}, nullptr, n, n, sw, tot, st);
+  if (rc) return rc;
+  densify_select_kernel<<<grid_for(k, 256, 8), 256, 0, st>>>(incl, n, tot, u, k, src);
+  CGS_CHECK_LAUNCH("densify_select_kernel");
+  return CGS_OK;
+}
+
 __global__ void histogram_kernel(const int32_t* idx, int64_t n, int32_t* counts, int64_t cap) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {

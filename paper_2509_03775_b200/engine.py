@@ -215,7 +215,8 @@ class Trainer:
         if c.densify_every > 0 and st.iteration % c.densify_every == 0:
             import time
             t0 = time.perf_counter()
-            densify(st, c.densify_growth, c.gaussian_cap, self.rng, jitter_sigma=c.densify_jitter)
+            densify(st, c.densify_growth, c.gaussian_cap, self.rng, jitter_sigma=c.densify_jitter,
+                    device_select=c.device_noise)
             self.densify_ms.append(1000.0 * (time.perf_counter() - t0))
 
     def mcmc(self):

@@ -72,13 +72,31 @@ class Codebook:
                                 device=dev)
         self._buf[:cap] = r
         self._cap = cap
-        self.refcount = np.zeros(cap, dtype=np.int64)
+        self._rc = np.zeros(cap, dtype=np.int64)
+        self._pending = []  # deferred refcount updates (device densify), see refcount
         self.parent = np.full(cap, -1, dtype=np.int32)
         self._free: list = []
         self._dev_rc = None
         self._dev_rc_host = None
         self._live_cache = None
         self.mutations = 0
+
+    # -- host refcount mirror ----------------------------------------------
+    @property
+    def refcount(self) -> np.ndarray:
+        """Host refcounts (model.py:41-48).  A device-side densify leaves its
+        increments pending until the next host read (applied here, in order),
+        so training steps never wait for the device."""
+        if self._pending:
+            fns, self._pending = self._pending, []
+            for fn in fns:
+                fn(self._rc)
+        return self._rc
+
+    @refcount.setter
+    def refcount(self, value):
+        self._pending = []
+        self._rc = value
 
     # -- shape ------------------------------------------------------------
     @property
@@ -195,11 +213,15 @@ class Codebook:
         return self._dev_rc
 
     def device_live(self) -> torch.Tensor:
-        """int32 device list of live row indices, ascending."""
-        key = self.refcount.tobytes()
+        """int32 device list of live row indices, ascending.  Reads the refcounts
+        without applying pending densify increments: those only raise counts of
+        rows that are already live, so the live set is the same (and the
+        training loop does not wait for the device)."""
+        key = self._rc.tobytes()
         if self._live_cache is None or self._live_cache[0] != key:
             from . import _native as nat
-            self._live_cache = (key, nat.upload(self.live_indices(), self._buf.device, np.int32))
+            self._live_cache = (key, nat.upload(np.flatnonzero(self._rc > 0), self._buf.device,
+                                                np.int32))
         return self._live_cache[1]
 
 
@@ -373,7 +395,15 @@ class ModelState:
             if ent is not None and ent[0] == key:
                 continue
             _, idx = _book_of(self, w)
-            host = torch.empty((idx.shape[0],), dtype=torch.int32, pin_memory=idx.is_cuda)
+            # one pinned buffer per index array, sized for the Gaussian capacity
+            # and reused (a new pinned allocation per densify costs milliseconds)
+            pool = self.__dict__.setdefault("_hidx_buf", {})
+            buf = pool.get(w)
+            if buf is None or buf.numel() < idx.shape[0]:
+                cap = max(idx.shape[0], self.gaussians.capacity)
+                buf = torch.empty((cap,), dtype=torch.int32, pin_memory=idx.is_cuda)
+                pool[w] = buf
+            host = buf[: idx.shape[0]]  # copies into buf are ordered on the stream
             host.copy_(idx, non_blocking=True)
             ev = None
             if idx.is_cuda:
@@ -393,9 +423,10 @@ class ModelState:
         """Cheap identity of the state contents (replaces render.py:227-237's SHA-256)."""
         g = self.gaussians
         ts = (g.positions, g.opacity_logits, g.g2sh, g.g2sr, self.sh.rows, self.sr.rows)
+        # rendering does not read refcounts; their host-side changes all bump
+        # a mutation counter
         return (self.mutations, self.sh.mutations, self.sr.mutations,
-                tuple((t.data_ptr(), t.shape[0], t._version) for t in ts),
-                hash(self.sh.refcount.tobytes()), hash(self.sr.refcount.tobytes()))
+                tuple((t.data_ptr(), t.shape[0], t._version) for t in ts))
 
     # -- construction -----------------------------------------------------
     @classmethod
@@ -485,11 +516,17 @@ def remap_gaussian(state: ModelState, i: int, which: str, new_row: int) -> None:
 
 
 def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Generator,
-            jitter_sigma: float = 0.02) -> int:
+            jitter_sigma: float = 0.02, device_select: bool = False) -> int:
     """Opacity-proportional cloning with shared rows (model.py:235-267).
 
-    Host draws exactly the reference's `choice` and `normal` sequence; the
-    append runs on the device (cgs_densify_append).
+    Parity mode (default): the host draws exactly the reference's `choice`
+    and `normal` sequence from the opacities (one device read); the append
+    runs on the device (cgs_densify_append).  ``device_select`` (throughput
+    mode, the trainer with device noise): the host draws the same uniforms
+    and normals without reading the device, the selection runs on the device
+    (cgs_densify_select) and the refcount increments are applied from the
+    refreshed assignment mirror when the host next reads refcounts -- no
+    synchronisation in the training loop.
     """
     from . import _native as nat
     if growth_rate <= 0:
@@ -501,6 +538,8 @@ def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Gene
     k = min(int(growth_rate * n), cap - n)
     if k <= 0:
         return 0
+    if device_select:
+        return _densify_device(state, n, k, rng, jitter_sigma)
     hsh, hsr = state.host_index("sh"), state.host_index("sr")
     opac = g.opacities()
     probs = opac / opac.sum()
@@ -519,6 +558,33 @@ def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Gene
     state.sr.mutations += 1
     state.touch(assignments=True)
     state.prefetch_host_index()
+    return k
+
+
+def _densify_device(state: ModelState, n: int, k: int, rng, jitter_sigma: float) -> int:
+    from . import _native as nat
+    g = state.gaussians
+    dev = state.device
+    u = rng.random(k)  # == the uniforms numpy's choice(n, k, p=...) draws
+    jitter = rng.normal(0.0, jitter_sigma, size=(k, 3))
+    g.resize(n + k)
+    u_d = nat.upload(u, dev, np.float64)
+    jit_d = nat.upload(jitter, dev, np.float64)
+    src_d = torch.empty((k,), dtype=torch.int64, device=dev)
+    nb = nat.library().cgs_densify_select_workspace_bytes(n)
+    ws = torch.empty((nb,), dtype=torch.uint8, device=dev)
+    st = nat.stream_handle(dev)
+    nat.call("cgs_densify_select", nat.ptr(g._logit), n, nat.ptr(u_d), k, nat.ptr(src_d),
+             nat.ptr(ws), nb, st)
+    nat.call("cgs_densify_append", nat.ptr(g._pos), nat.ptr(g._logit), nat.ptr(g._g2sh),
+             nat.ptr(g._g2sr), n, nat.ptr(src_d), nat.ptr(jit_d), k, st)
+    state.sh.mutations += 1
+    state.sr.mutations += 1
+    state.touch(assignments=True)
+    state.prefetch_host_index()  # includes the clones' rows [n, n + k)
+    for which, book in (("sh", state.sh), ("sr", state.sr)):
+        book._pending.append(
+            lambda rc, w=which: np.add.at(rc, state.host_index(w)[n:n + k], 1))
     return k
 
 

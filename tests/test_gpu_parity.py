@@ -495,3 +495,23 @@ def test_config1_full_size_matches_oracle(cg):
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
         ref = refs[0][k] + refs[1][k]
         assert np.allclose(gr[k], ref, rtol=RTOL, atol=ATOL), (k, np.abs(gr[k] - ref).max())
+
+
+def test_device_densify_matches_host_densify(cg):
+    """Throughput-mode densify (device opacity-weighted selection from the same
+    host uniforms, deferred refcounts) reproduces the parity-mode densify
+    (numpy choice with p, model.py:256) on identical inputs."""
+    from gpu_helpers import state_from
+    d = golden("mcmc")
+    a = state_from(d, "defaults_s0_")
+    b = state_from(d, "defaults_s0_")
+    ra, rb = np.random.default_rng(99), np.random.default_rng(99)
+    for _ in range(3):  # repeated: the second and third read deferred refcounts
+        ka = cg.densify(a, 0.05, 10 ** 6, ra)
+        kb = cg.densify(b, 0.05, 10 ** 6, rb, device_select=True)
+        assert ka == kb
+    ha, hb = a.to_host(), b.to_host()
+    for k in ("positions", "opacity_logits", "g2sh", "g2sr", "sh_refcount", "sr_refcount"):
+        assert np.array_equal(ha[k], hb[k]), k
+    cg.validate_state(b)
+    assert np.array_equal(ra.random(4), rb.random(4))
