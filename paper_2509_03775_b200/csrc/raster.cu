@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
   __shared__ __align__(128) SplatRec s_raw[256];
   __shared__ float4 s_a[256];
   __shared__ float4 s_b[256];
-  __shared__ float s_c[256];
+  __shared__ float2 s_c[256];
   __shared__ uint8_t s_mask[256];
   __shared__ uint8_t s_list[8][256];
   __shared__ uint32_t s_max[8];
@@ -195,12 +195,10 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     phase ^= 1;
     pending = false;
     if (tid < nb) {
-      float4 a, b;
-      float c;
-      stage_splat(s_raw[tid], ox, oy, a, b, c);
-      s_a[tid] = a;
-      s_b[tid] = b;
-      s_c[tid] = c;
+      const Staged sg = stage_splat(s_raw[tid], ox, oy);
+      s_a[tid] = sg.a;
+      s_b[tid] = sg.b;
+      s_c[tid] = sg.c;
       s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
     }
     __syncthreads();
@@ -215,11 +213,11 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
         const int j = my_list[i];
         const float4 a = s_a[j];
         const float4 b = s_b[j];
-        const float dx = a.x + flx, dy = a.y + fly;
-        const float al = fminf(b.y * fast_exp2(fmaf(a.w * dx, dy, fmaf(b.x * dy, dy, a.z * dx * dx))),
-                               kAlphaClampVal);
+        float u, v;
+        const float al = staged_alpha(a, b, flx, fly, u, v);
         if (al >= kAlphaSkipF) {
-          blend(p, al, b.z, b.w, s_c[j], static_cast<uint32_t>(b0 + j));
+          const float2 c = s_c[j];
+          blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
           if (p.done) break;
         }
       }
@@ -271,12 +269,13 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 
 // Adds pixel p's contribution of splat k to o[9]; returns whether it had one.
-// o = [sum w g (3), sum dp, sum dp dx, sum dp dy, sum dp dx^2, sum dp dx dy,
-// sum dp dy^2] with dp = dL/dalpha * alpha: the per-splat gradient is a
-// linear map of these moments (moments_to_grad), applied once per splat
-// after the pixel sums instead of per pixel.
-__device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const float4& b,
-                                          const float4& nc, float dx, float dy, float* o) {
+// o = [sum w g (3), sum dp, sum dp u, sum dp v, sum dp u^2, sum dp u v,
+// sum dp v^2] with dp = dL/dalpha * alpha and (u, v) the pixel offset in the
+// conic's eigenbasis (passed as dx, dy): the per-splat gradient is a linear
+// map of these moments (moments_to_grad), applied once per splat after the
+// pixel sums instead of per pixel.
+__device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, float cr, float cg,
+                                          float cb, float dx, float dy, float* o) {
   if (!(k < p.last) || !(al >= kAlphaSkipF)) return false;
   const float iom = fast_rcp(1.0f - al);  // 1 - alpha >= 0.01
   const float Tb = p.T * iom;
@@ -285,13 +284,13 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const
   o[1] = fmaf(w, p.gg, o[1]);
   o[2] = fmaf(w, p.gb, o[2]);
   // dC/dalpha = c T_before - suffix / (1 - alpha) (render.py:357-359)
-  const float dCr = fmaf(b.z, Tb, -p.sr * iom);
-  const float dCg = fmaf(b.w, Tb, -p.sg * iom);
-  const float dCb = fmaf(nc.w, Tb, -p.sb * iom);
+  const float dCr = fmaf(cr, Tb, -p.sr * iom);
+  const float dCg = fmaf(cg, Tb, -p.sg * iom);
+  const float dCb = fmaf(cb, Tb, -p.sb * iom);
   const float da = dCr * p.gr + dCg * p.gg + dCb * p.gb;
-  p.sr = fmaf(w, b.z, p.sr);
-  p.sg = fmaf(w, b.w, p.sg);
-  p.sb = fmaf(w, nc.w, p.sb);
+  p.sr = fmaf(w, cr, p.sr);
+  p.sg = fmaf(w, cg, p.sg);
+  p.sb = fmaf(w, cb, p.sb);
   p.T = Tb;
   if (al < kAlphaClampVal) {  // no gradient through the clamp (render.py:361)
     const float dp = da * al;
@@ -307,19 +306,26 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, const
 }
 
 // Moments -> [d colour (3), d opacity, d mean2d (2), d conic (A, B, C)]
-// (render.py:364-377: d_opac = sum dp / o, d_mean = conic * sum dp d,
-// d_conic = -(1/2 dx^2, dx dy, 1/2 dy^2) summed with weight dp).
-__device__ __forceinline__ void moments_to_grad(const float* m, const float4& nc, float io,
-                                                float* g) {
+// (render.py:364-377: d_opac = sum dp / o, d_mean = sum dp Q d,
+// d_conic = -(1/2 dx^2, dx dy, 1/2 dy^2) summed with weight dp), with
+// d = u e1 + v e2 and Q d = lambda1 u e1 + lambda2 v e2; in fp64.
+__device__ __forceinline__ void moments_to_grad(const float* m, float e1x, float e1y, float l1,
+                                                float l2, float io, float* g) {
+  const double ex = e1x, ey = e1y;
   g[0] = m[0];
   g[1] = m[1];
   g[2] = m[2];
   g[3] = m[3] * io;
-  g[4] = fmaf(nc.x, m[4], nc.y * m[5]);
-  g[5] = fmaf(nc.y, m[4], nc.z * m[5]);
-  g[6] = -0.5f * m[6];
-  g[7] = -m[7];
-  g[8] = -0.5f * m[8];
+  const double a = static_cast<double>(l1) * m[4], b = static_cast<double>(l2) * m[5];
+  g[4] = static_cast<float>(a * ex - b * ey);
+  g[5] = static_cast<float>(a * ey + b * ex);
+  const double uu = m[6], uv = m[7], vv = m[8];
+  const double xx = ex * ex * uu - 2.0 * ex * ey * uv + ey * ey * vv;
+  const double xy = ex * ey * uu + (ex * ex - ey * ey) * uv - ex * ey * vv;
+  const double yy = ey * ey * uu + 2.0 * ex * ey * uv + ex * ex * vv;
+  g[6] = static_cast<float>(-0.5 * xx);
+  g[7] = static_cast<float>(-xy);
+  g[8] = static_cast<float>(-0.5 * yy);
 }
 
 // Batches of kBwdBatch splats, last batch first.  Staging writes, per
@@ -341,7 +347,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   __shared__ __align__(128) SplatRec s_raw[B];
   __shared__ float4 s_a[B];
   __shared__ float4 s_b[B];
-  __shared__ float4 s_n[B];  // natural conic A, B, C and blue
+  __shared__ float4 s_n[B];  // green, blue, lambda1, lambda2
   __shared__ float s_io[B];  // 1 / opacity
   __shared__ uint8_t s_mask[B];
   __shared__ uint8_t s_list[4][B];
@@ -403,13 +409,10 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     phase ^= 1;
     for (int k = tid; k < nb; k += 128) {
       const SplatRec& r = s_raw[k];
-      float4 a, b;
-      float c;
-      stage_splat(r, ox, oy, a, b, c);
-      s_a[k] = a;
-      s_b[k] = b;
-      s_n[k] = make_float4(static_cast<float>(r.ca), static_cast<float>(r.cb),
-                           static_cast<float>(r.cc), c);
+      const Staged sg = stage_splat(r, ox, oy);
+      s_a[k] = sg.a;
+      s_b[k] = sg.b;
+      s_n[k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
       s_io[k] = 1.0f / r.opac;
       s_eidx[k] = static_cast<uint32_t>(
           emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
@@ -434,13 +437,11 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       const float4 a = s_a[j];
       const float4 b = s_b[j];
       const float4 nc = s_n[j];
-      const float dx = a.x + flx;
-      const float dy0 = a.y + fly, dy1 = dy0 + 4.0f;
-      const float t0 = a.z * dx * dx, t1 = a.w * dx;
-      const float al0 = fminf(b.y * fast_exp2(fmaf(t1, dy0, fmaf(b.x * dy0, dy0, t0))), kAlphaClampVal);
-      const float al1 = fminf(b.y * fast_exp2(fmaf(t1, dy1, fmaf(b.x * dy1, dy1, t0))), kAlphaClampVal);
-      bool any = bwd_pixel(q0, k, al0, b, nc, dx, dy0, o);
-      any = bwd_pixel(q1, k, al1, b, nc, dx, dy1, o) || any;
+      float u0, v0, u1, v1;
+      const float al0 = staged_alpha(a, b, flx, fly, u0, v0);
+      const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
+      bool any = bwd_pixel(q0, k, al0, b.w, nc.x, nc.y, u0, v0, o);
+      any = bwd_pixel(q1, k, al1, b.w, nc.x, nc.y, u1, v1, o) || any;
       // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
       float red = 0.0f;
       if (__any_sync(kFull, any)) red = warp_reduce9(o);
@@ -458,7 +459,9 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
         mom[u] = (r0 + r1) + (r2 + r3);
       }
-      moments_to_grad(mom, s_n[jj], s_io[jj], g);
+      const float4 aa = s_a[jj];
+      const float4 nn = s_n[jj];
+      moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[jj], g);
       float* out = partials + static_cast<int64_t>(s_eidx[jj]) * 9;
 #pragma unroll
       for (int u = 0; u < 9; ++u) out[u] = g[u];

@@ -259,29 +259,62 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 // fp64 record -> fp32 shared-memory form for one tile whose first pixel
-// centre is (ox + 0.5, oy + 0.5).  The offset is formed in fp64 so the fp32
-// pixel offsets stay exact to fp32 rounding of small numbers even at
-// ~2000-pixel coordinates.  The conic is pre-scaled by -0.5*log2(e) (A, C)
-// and -log2(e) (B) so the exponent is three FMAs and one ex2.
-//   a = (dx0, dy0, A2, B2)   b = (C2, opacity, red, green)   c = blue
-__device__ __forceinline__ void stage_splat(const SplatRec& r, double ox, double oy, float4& a,
-                                            float4& b, float& c) {
-  a.x = static_cast<float>(ox + 0.5 - r.mx);
-  a.y = static_cast<float>(oy + 0.5 - r.my);
-  a.z = static_cast<float>(-0.5 * kLog2e * r.ca);
-  a.w = static_cast<float>(-kLog2e * r.cb);
-  b.x = static_cast<float>(-0.5 * kLog2e * r.cc);
-  b.y = static_cast<float>(r.opac);
-  b.z = r.r;
-  b.w = r.g;
-  c = r.b;
+// centre is (ox + 0.5, oy + 0.5), in the eigenbasis of the conic.  With
+// conic Q = lambda1 e1 e1^T + lambda2 e2 e2^T (e2 = e1 rotated by 90 deg),
+// d^T Q d = lambda1 u^2 + lambda2 v^2, u = e1 . d, v = e2 . d; the tile offsets
+// (u0, v0) of the first pixel centre are formed in fp64, so per pixel
+// u = u0 + e1 . (lx, ly) and v = v0 + e2 . (lx, ly) are small, well-conditioned
+// fp32 numbers even for elongated near-plane splats centred far off screen
+// (evaluating A dx^2 + 2B dx dy + C dy^2 directly in fp32 cancels
+// catastrophically there).  Exponent in log2 units: k = -log2(e)/2 lambda.
+//   a = (u0, v0, e1x, e1y)   b = (k1, k2, opacity, red)   c = (green, blue)
+struct Staged {
+  float4 a, b;
+  float2 c;
+  float lam1, lam2;  // eigenvalues (backward's moments -> gradient map)
+};
+
+__device__ __forceinline__ Staged stage_splat(const SplatRec& r, double ox, double oy) {
+  const double A = r.ca, B = r.cb, C = r.cc;
+  const double m = 0.5 * (A + C), h = 0.5 * (A - C);
+  const double rr = sqrt(h * h + B * B);
+  const double l1 = m + rr;                              // larger eigenvalue
+  const double l2 = l1 > 0.0 ? (A * C - B * B) / l1 : 0.0;  // det / l1 (no cancellation in m - rr)
+  // eigenvector of l1: the better conditioned of (l1 - C, B) and (B, l1 - A)
+  double ex = l1 - C, ey = B;
+  const double fx = B, fy = l1 - A;
+  if (fx * fx + fy * fy > ex * ex + ey * ey) {
+    ex = fx;
+    ey = fy;
+  }
+  const double nn = sqrt(ex * ex + ey * ey);
+  if (nn > 0.0) {
+    ex /= nn;
+    ey /= nn;
+  } else {
+    ex = 1.0;
+    ey = 0.0;
+  }
+  const double dx = ox + 0.5 - r.mx, dy = oy + 0.5 - r.my;
+  Staged st;
+  st.a = make_float4(static_cast<float>(ex * dx + ey * dy), static_cast<float>(-ey * dx + ex * dy),
+                     static_cast<float>(ex), static_cast<float>(ey));
+  st.b = make_float4(static_cast<float>(-0.5 * kLog2e * l1), static_cast<float>(-0.5 * kLog2e * l2),
+                     r.opac, r.r);
+  st.c = make_float2(r.g, r.b);
+  st.lam1 = static_cast<float>(l1);
+  st.lam2 = static_cast<float>(l2);
+  return st;
 }
 
-// alpha = min(o * exp(power), 0.99) (render.py:274-278); skip test by caller.
-__device__ __forceinline__ float splat_alpha(const float4& a, const float4& b, float dx, float dy) {
-  const float p2 = fmaf(a.z * dx, dx, fmaf(a.w * dx, dy, b.x * dy * dy));
-  const float al = b.y * fast_exp2(p2);
-  return fminf(al, kAlphaClampVal);
+// alpha = min(o * exp(power), 0.99) (render.py:274-278) at tile pixel (lx, ly);
+// (u, v) returned for the backward.  Skip test by the caller.
+__device__ __forceinline__ float staged_alpha(const float4& a, const float4& b, float lx, float ly,
+                                              float& u, float& v) {
+  u = fmaf(a.w, ly, fmaf(a.z, lx, a.x));
+  v = fmaf(a.z, ly, fmaf(-a.w, lx, a.y));
+  return fminf(b.z * fast_exp2(fmaf(b.x * u, u, b.y * v * v)), kAlphaClampVal);
 }
+
 
 }  // namespace cgs

@@ -515,3 +515,56 @@ def test_device_densify_matches_host_densify(cg):
         assert np.array_equal(ha[k], hb[k]), k
     cg.validate_state(b)
     assert np.array_equal(ra.random(4), rb.random(4))
+
+
+def test_config3_strip_matches_oracle(cg):
+    """BASELINE config 3 scene at full size (4M Gaussians, SH-3 K=65536, near-
+    plane giants), rendered through a 1960x32 strip of pose 0 (the strip is a
+    camera of its own: principal point shifted) so the numpy oracle finishes in
+    about a minute: tile lists, contribution counts bit-exact; images and T
+    within rtol 1e-4 / atol 1e-6.
+
+    Gradients: within the same tolerance for every parameter that no
+    near-plane splat (camera z < 2 x the 0.01 cull distance) feeds.  For those
+    splats the chain rule through J ~ 1/z, 1/z^2, 1/z^3 amplifies the fp32
+    per-pixel partials' ~1e-7 relative error by ~1e5 (their gradient is a
+    near-cancelling sum over ~60k pixels), so the fp32 raster reproduces them
+    only to a few percent; that band is checked separately at 10% group-
+    relative error and documented in DESIGN.md section 3."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import _strip_cam
+    from oracle import cgs_oracle as O
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config3(0)
+    ocam = _strip_cam(O.cam_from_any(a.cameras[0]), 528, 560)
+    cam = cg.Camera(rotation=ocam.R, translation=ocam.t, fx=ocam.fx, fy=ocam.fy, cx=ocam.cx,
+                    cy=ocam.cy, width=ocam.width, height=ocam.height)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    art = cg.rasterize_forward(st, cam)
+    ost = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    fw = O.raster_forward(ost, ocam)
+    offs, ids = art.frame.tile_lists()
+    assert np.array_equal(offs, fw["tile_offsets"]) and np.array_equal(ids, fw["tile_ids"])
+    assert np.array_equal(art.contrib_counts.cpu().numpy(), fw["counts"])
+    img = art.image.cpu().numpy()
+    assert np.allclose(img, fw["image"], rtol=RTOL, atol=ATOL)
+    assert np.allclose(art.final_transmittance.cpu().numpy(), fw["final_T"], rtol=RTOL, atol=ATOL)
+    dL = np.random.default_rng(0).normal(0, 1e-4, img.shape)
+    g = cg.rasterize_backward(st, cam, art, dL).numpy()
+    og = O.raster_backward(ost, ocam, dL)
+    tz = (a.positions.astype(np.float64) @ ocam.R.T + ocam.t)[:, 2]
+    near = (tz > 0.01) & (tz < 0.02)
+    assert near.sum() > 0
+    far = {"positions": ~near, "opacity_logits": ~near}
+    for k, idx in (("sh_rows", a.g2sh), ("sr_rows", a.g2sr)):
+        tainted = np.zeros(g[k].shape[0], bool)
+        tainted[np.unique(idx[near])] = True
+        far[k] = ~tainted
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        m = far[k]
+        assert np.allclose(g[k][m], og[k][m], rtol=RTOL, atol=ATOL), (k, np.abs(g[k][m] - og[k][m]).max())
+        rel = np.abs(g[k][~m] - og[k][~m]).max() / max(np.abs(og[k]).max(), 1e-30)
+        assert rel <= 0.1, (k, rel)
