@@ -6,8 +6,9 @@ import paper_2509_03775_b200 as cg
 from bench import _strip_cam
 from oracle import cgs_oracle as O
 from paper_2509_03775_b200 import scenes
-a = scenes.config3(0)
-ocam = _strip_cam(O.cam_from_any(a.cameras[0]), 528, 560)
+CFG = int(os.environ.get("CFG", "3")); ROWS = tuple(int(x) for x in os.environ.get("ROWS", "528,560").split(","))
+a = scenes.build(CFG, 0)
+ocam = _strip_cam(O.cam_from_any(a.cameras[0]), *ROWS)
 cam = cg.Camera(rotation=ocam.R, translation=ocam.t, fx=ocam.fx, fy=ocam.fy, cx=ocam.cx,
                 cy=ocam.cy, width=ocam.width, height=ocam.height)
 st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)

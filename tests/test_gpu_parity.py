@@ -517,28 +517,30 @@ def test_device_densify_matches_host_densify(cg):
     assert np.array_equal(ra.random(4), rb.random(4))
 
 
-def test_config3_strip_matches_oracle(cg):
-    """BASELINE config 3 scene at full size (4M Gaussians, SH-3 K=65536, near-
+@pytest.mark.parametrize("config,rows", [(2, (344, 376)), (3, (528, 560))])
+def test_full_scene_strip_matches_oracle(cg, config, rows):
+    """BASELINE config 2 / 3 scenes at full size; config 3: (4M Gaussians, SH-3 K=65536, near-
     plane giants), rendered through a 1960x32 strip of pose 0 (the strip is a
     camera of its own: principal point shifted) so the numpy oracle finishes in
     about a minute: tile lists, contribution counts bit-exact; images and T
     within rtol 1e-4 / atol 1e-6.
 
     Gradients: within the same tolerance for every parameter that no
-    near-plane splat (camera z < 2 x the 0.01 cull distance) feeds.  For those
-    splats the chain rule through J ~ 1/z, 1/z^2, 1/z^3 amplifies the fp32
-    per-pixel partials' ~1e-7 relative error by ~1e5 (their gradient is a
-    near-cancelling sum over ~60k pixels), so the fp32 raster reproduces them
-    only to a few percent; that band is checked separately at 10% group-
-    relative error and documented in DESIGN.md section 3."""
+    view-covering splat feeds (a splat whose pixel rect spans every tile, or
+    camera z < 2 x the 0.01 cull distance).  Their gradients are
+    near-cancelling sums over every pixel of the view, amplified through
+    J ~ 1/z, 1/z^2, 1/z^3, so the fp32 per-pixel partials (~1e-7 relative)
+    reproduce them only to a few percent; they are checked separately at 10%
+    group-relative error and documented in DESIGN.md section 3 (< 5e-4 of the
+    Gaussians here)."""
     import sys
     import os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from bench import _strip_cam
     from oracle import cgs_oracle as O
     from paper_2509_03775_b200 import scenes
-    a = scenes.config3(0)
-    ocam = _strip_cam(O.cam_from_any(a.cameras[0]), 528, 560)
+    a = scenes.build(config, 0)
+    ocam = _strip_cam(O.cam_from_any(a.cameras[0]), *rows)
     cam = cg.Camera(rotation=ocam.R, translation=ocam.t, fx=ocam.fx, fy=ocam.fy, cx=ocam.cx,
                     cy=ocam.cy, width=ocam.width, height=ocam.height)
     st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
@@ -555,9 +557,12 @@ def test_config3_strip_matches_oracle(cg):
     dL = np.random.default_rng(0).normal(0, 1e-4, img.shape)
     g = cg.rasterize_backward(st, cam, art, dL).numpy()
     og = O.raster_backward(ost, ocam, dL)
+    # splats covering the whole view, or just beyond the near plane: their
+    # gradients are near-cancelling sums over every pixel (see docstring)
+    ntiles = art.frame.splats(0)["n_tiles"]
     tz = (a.positions.astype(np.float64) @ ocam.R.T + ocam.t)[:, 2]
-    near = (tz > 0.01) & (tz < 0.02)
-    assert near.sum() > 0
+    near = ((tz > 0.01) & (tz < 0.02)) | (ntiles == len(offs) - 1)
+    assert near.sum() < 5e-4 * len(near)
     far = {"positions": ~near, "opacity_logits": ~near}
     for k, idx in (("sh_rows", a.g2sh), ("sr_rows", a.g2sr)):
         tainted = np.zeros(g[k].shape[0], bool)
@@ -566,5 +571,6 @@ def test_config3_strip_matches_oracle(cg):
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
         m = far[k]
         assert np.allclose(g[k][m], og[k][m], rtol=RTOL, atol=ATOL), (k, np.abs(g[k][m] - og[k][m]).max())
-        rel = np.abs(g[k][~m] - og[k][~m]).max() / max(np.abs(og[k]).max(), 1e-30)
-        assert rel <= 0.1, (k, rel)
+        if (~m).any():
+            rel = np.abs(g[k][~m] - og[k][~m]).max() / max(np.abs(og[k]).max(), 1e-30)
+            assert rel <= 0.1, (k, rel)
