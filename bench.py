@@ -194,7 +194,8 @@ def _oracle_iteration(a, gts, cams, lam, pool, strips):
 def _oracle_gts(g, cams):
     from oracle import cgs_oracle as O
     gst = O.OState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows, g.sr_rows)
-    return [O.raster_forward(gst, O.cam_from_any(c))["image"] for c in cams]
+    return [np.round(np.clip(O.raster_forward(gst, O.cam_from_any(c))["image"], 0.0, 1.0) * 255.0)
+            / 255.0 for c in cams]  # 8-bit targets, as in the GPU arm
 
 
 def cpu_iteration_timer(config, seed):
@@ -394,7 +395,9 @@ def main():
                                     g.sr_rows, device=dev)
     gt_frame = cg.render_frame(gst, cams)
     H, W = cams[0].height, cams[0].width
-    gts = gt_frame.image.view(len(cams), H, W, 3).clone()
+    # targets are 8-bit RGB, like the reference's PNG inputs (modelio.py:138-153):
+    # the GT renders quantised to k/255; the e2e path uploads the uint8 bytes
+    gts = (gt_frame.image.view(len(cams), H, W, 3).clamp(0.0, 1.0) * 255.0).round() * (1.0 / 255.0)
     del gt_frame, gst
     lam = 0.0 if args.config == 0 else 0.2
     # Reference defaults except the position Langevin noise: the default
@@ -513,7 +516,8 @@ def main():
     # step's target images, D2H of the recon loss) inside the timed region
     e2e = None
     if not args.no_e2e:
-        host_gt = gts.cpu().pin_memory()
+        host_gt = (gts * 255.0).round().to(torch.uint8).cpu().pin_memory()
+        dev_gt = torch.empty(host_gt.shape, dtype=torch.uint8, device=dev)
         host_loss = torch.empty((3 * len(cams),), dtype=torch.float64).pin_memory()
         e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -523,7 +527,8 @@ def main():
             if not args.no_flush:
                 flush.zero_()
             e_s[k].record()
-            tr.gts.copy_(host_gt, non_blocking=True)
+            dev_gt.copy_(host_gt, non_blocking=True)
+            torch.mul(dev_gt, 1.0 / 255.0, out=tr.gts)  # uint8 -> [0, 1] on the device
             tr.step()
             host_loss.copy_(tr.last_loss, non_blocking=True)
             e_e[k].record()
@@ -536,7 +541,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": (args.steps * world) / (e_ms / 1000.0), "unit": "it/s",
-               "h2d_bytes_per_step": int(host_gt.numel() * 4),
+               "h2d_bytes_per_step": int(host_gt.numel()),
                "d2h_bytes_per_step": int(host_loss.numel() * 8)}
 
     cpu = None
@@ -557,6 +562,7 @@ def main():
                           "image": f"{W}x{H}", "gaussians": st.num_gaussians,
                           "l2": "flushed (256 MB write) between timed iterations"
                           if not args.no_flush else "not flushed",
+                          "targets": "8-bit RGB (the reference's PNG inputs), uint8 upload in e2e",
                           "mcmc_every": args.mcmc_every,
                           "sgld_noise": f"device Philox, noise_pos={args.noise_pos} (reference default 1.0 "
                                         "diffuses the scene out of view; see DESIGN.md)",
