@@ -574,3 +574,24 @@ def test_full_scene_strip_matches_oracle(cg, config, rows):
         if (~m).any():
             rel = np.abs(g[k][~m] - og[k][~m]).max() / max(np.abs(og[k]).max(), 1e-30)
             assert rel <= 0.1, (k, rel)
+
+
+def test_split_eligible_abi_matches_host_rule(cg):
+    """cgs_split_eligible (device compaction of sampler.py:344's eligibility, kept
+    in the ABI for callers without a host assignment mirror) agrees with the
+    host rule the sampler uses."""
+    from gpu_helpers import state_from
+    from paper_2509_03775_b200 import _native as nat
+    d = golden("mcmc")
+    st = state_from(d, "always_s6_")
+    for which, book, idx in (("sh", st.sh, st.gaussians.g2sh), ("sr", st.sr, st.gaussians.g2sr)):
+        n = st.num_gaussians
+        out = torch.empty((n,), dtype=torch.int32, device=st.device)
+        cnt = torch.zeros((1,), dtype=torch.int64, device=st.device)
+        ws = torch.empty((nat.library().cgs_scan_workspace_bytes(n) + 1024,), dtype=torch.uint8,
+                         device=st.device)
+        nat.call("cgs_split_eligible", nat.ptr(idx), n, nat.ptr(book.device_refcount()),
+                 nat.ptr(out), nat.ptr(cnt), nat.ptr(ws), ws.numel(), nat.stream_handle(st.device))
+        k = int(cnt.item())
+        ref = np.flatnonzero(book.refcount[st.host_index(which)] >= 2)
+        assert np.array_equal(out[:k].cpu().numpy(), ref), which
