@@ -114,6 +114,10 @@ CGS_API uint64_t cgs_launch_count(void);
 CGS_API int cgs_profile_kernel(const char* name);
 /* Sum of the recorded launches' durations (synchronizes those events). */
 CGS_API int cgs_profile_read(double* total_ms, int64_t* launches);
+/* Diagnostics: with a device buffer of >= 8 * total_tiles uint64 set, the
+ * raster kernels record {start ns, end ns, SM id, tile} per CTA (forward at
+ * [4 b], backward at [4 (total_tiles + b)]); NULL disables. */
+CGS_API int cgs_trace_tiles(void* dev_buf);
 
 /* ---- render: rasterize_forward / rasterize_backward ------------------- */
 /* Workspace for one batched frame of n_views cameras (host cams).

@@ -77,6 +77,7 @@ SIGNATURES = {
     "cgs_launch_count": (ctypes.c_uint64, []),
     "cgs_profile_kernel": (I32, [ctypes.c_char_p]),
     "cgs_profile_read": (I32, [ctypes.POINTER(F64), ctypes.POINTER(I64)]),
+    "cgs_trace_tiles": (I32, [ctypes.c_void_p]),
     "cgs_frame_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64]),
     "cgs_render_forward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
     "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),

@@ -21,7 +21,9 @@ static std::mutex g_prof_mu;
 static std::string g_prof_name;
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_events;
 static std::vector<cudaEvent_t> g_prof_pool;
+static unsigned long long* g_tile_trace = nullptr;
 
+unsigned long long* tile_trace_buffer() { return g_tile_trace; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static cudaEvent_t prof_event() {
@@ -155,6 +157,11 @@ int cgs_profile_kernel(const char* name) {
   }
   g_prof_events.clear();
   g_prof_name = name ? name : "";
+  return CGS_OK;
+}
+
+int cgs_trace_tiles(void* dev_buf) {
+  g_tile_trace = static_cast<unsigned long long*>(dev_buf);
   return CGS_OK;
 }
 

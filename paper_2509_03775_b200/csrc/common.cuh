@@ -90,6 +90,20 @@ int cuda_status(cudaError_t e, const char* where);
 // kernel named by cgs_profile_kernel is bracketed by CUDA events recorded on
 // its own launch stream (cgs_profile_read).
 void note_launch();
+// Diagnostics: when set (cgs_trace_tiles), the raster kernels write one
+// {start ns, end ns, SM id, tile} record per CTA: forward at [4 b], backward
+// at [4 (total_tiles + b)].
+unsigned long long* tile_trace_buffer();
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 struct ProfScope {
   bool on;
   cudaStream_t st;

@@ -12,6 +12,19 @@ namespace cgs {
 // emission, instead of by the warp that owns their depth rank.
 constexpr uint32_t kLongSplat = 256;
 
+// The backward splits a tile's processed prefix into chunks of kChunk splats
+// (independent CTAs); the forward leaves each pixel's transmittance and
+// colour suffix at every chunk boundary it passes (ckpt).  kChunk is a
+// multiple of the forward's 256-splat batch.
+constexpr int kChunk = 512;
+
+// Checkpoint slot of boundary j >= 1 (splat index j * kChunk) of a tile whose
+// list starts at pair position `start`: distinct over all (tile, j) with
+// j * kChunk < list length, and < total_tiles + pair_cap / kChunk + 1.
+__host__ __device__ __forceinline__ int64_t ckpt_slot(uint32_t start, int tile, int j) {
+  return static_cast<int64_t>(start / kChunk) + tile + (j - 1);
+}
+
 struct FrameLayout {
   FrameHeader* hdr;
   SplatRec* recs;          // V*N
@@ -33,6 +46,10 @@ struct FrameLayout {
   uint32_t* px_last;       // total_pixels
   uint32_t* tile_nproc;    // total_tiles
   uint32_t* tile_order;    // total_tiles: raster CTA -> tile, longest work first
+  float4* ckpt;            // n_ckpt x 256: per-pixel (T, colour suffix) at chunk boundaries
+  uint2* units;            // n_ckpt: backward work units (tile, chunk), longest first
+  uint32_t* unit_ctl;      // [0] unit count, [1] fetch counter
+  int64_t n_ckpt;
   ScanWs scan;
   double* sr_cov;          // sr_cap * 8 (Sigma3 + zero-quaternion flag)
   size_t bytes;
@@ -111,6 +128,10 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.last_rank = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.tile_order = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.n_ckpt = fd.total_tiles + pc / kChunk + 2;
+  L.ckpt = c.take<float4>(L.n_ckpt * 256);
+  L.units = c.take<uint2>(L.n_ckpt);
+  L.unit_ctl = c.take<uint32_t>(2);
   L.scan = carve_scan(c, vn1 > fd.total_tiles ? vn1 : fd.total_tiles);
   L.sr_cov = c.take<double>((sr_cap > 0 ? sr_cap : 1) * 8);
   L.bytes = c.off + 256;

@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
     uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
-    uint32_t* __restrict__ last_rank) {
+    uint32_t* __restrict__ last_rank, float4* __restrict__ ckpt,
+    unsigned long long* __restrict__ trace) {
+  const unsigned long long t_start = trace ? global_ns() : 0ull;
   __shared__ __align__(128) SplatRec s_raw[256];
   __shared__ float4 s_a[256];
   __shared__ float4 s_b[256];
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
   const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
   uint8_t* my_list = s_list[warp];
   PixState p{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in};
+  int n_ckpt = 0;
 
   if (tid == 0) mbar_init(&s_bar, 1);
   __syncthreads();
@@ -223,8 +226,26 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
       }
     }
     if (__syncthreads_count(p.done) == 256) break;
+    if (b0 + 256 < n && ((b0 + 256) % kChunk) == 0) {  // chunk boundary for the backward
+      // T after the chunk and the chunk's own colour sum; colour restarts at 0
+      ckpt[ckpt_slot(rg.x, tile, (b0 + 256) / kChunk) * kTilePixels + ly * kTile + lx] =
+          make_float4(p.T, p.r, p.g, p.b);
+      p.r = p.g = p.b = 0.0f;
+      ++n_ckpt;
+    }
   }
   if (pending) mbar_wait(&s_bar, phase);
+  // Chunk sums -> suffix at each boundary (sum of the later chunks, so it
+  // carries rounding relative to itself, like a back-to-front running sum)
+  // and the pixel colour = sum of all chunks.  Only this thread's own writes.
+  for (int j = n_ckpt; j >= 1; --j) {
+    float4& c = ckpt[ckpt_slot(rg.x, tile, j) * kTilePixels + ly * kTile + lx];
+    const float4 q = c;
+    c = make_float4(q.x, p.r, p.g, p.b);
+    p.r += q.y;
+    p.g += q.z;
+    p.b += q.w;
+  }
   if (in && !p.done) p.last = static_cast<uint32_t>(n);
   if (in) {
     const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
@@ -246,6 +267,13 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     for (int w = 0; w < 8; ++w) np = max(np, s_max[w]);
     tile_nproc[tile] = np;
     last_rank[tile] = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;
+    if (trace) {
+      unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x);
+      t[0] = t_start;
+      t[1] = global_ns();
+      t[2] = smid();
+      t[3] = static_cast<unsigned long long>(tile);
+    }
   }
 }
 
@@ -335,15 +363,78 @@ __device__ __forceinline__ void moments_to_grad(const float* m, float e1x, float
 // slice; the combine sums the present warps in fixed order.
 constexpr int kBwdBatch = 128;
 
+// Backward work units: chunk c of tile t covers splats [c kChunk, min((c+1)
+// kChunk, nproc_t)).  Sorted by length, longest first (counting sort in one
+// CTA, as tile_order_kernel); ctl[0] = unit count, ctl[1] = fetch counter.
+__global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ nproc,
+                                                          int total_tiles,
+                                                          uint2* __restrict__ units,
+                                                          uint32_t* __restrict__ ctl) {
+  __shared__ uint32_t cnt[256];
+  __shared__ uint32_t s_total;
+  const int tid = threadIdx.x;
+  auto bucket = [](uint32_t w) -> uint32_t {  // w in [1, kChunk]
+    return 255u - min(255u, ((w - 1u) * 256u) / kChunk);
+  };
+  if (tid < 256) cnt[tid] = 0;
+  __syncthreads();
+  for (int t = tid; t < total_tiles; t += blockDim.x) {
+    const uint32_t np = nproc[t];
+    for (uint32_t k0 = 0; k0 < np; k0 += kChunk) atomicAdd(&cnt[bucket(min(np - k0, uint32_t(kChunk)))], 1u);
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of 256 counts, 8 per lane
+    uint32_t c[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      c[k] = cnt[tid * 8 + k];
+      sum += c[k];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, inc, o);
+      if (tid >= o) inc += y;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      cnt[tid * 8 + k] = run;
+      run += c[k];
+    }
+    if (tid == 31) s_total = inc;
+  }
+  __syncthreads();
+  for (int t = tid; t < total_tiles; t += blockDim.x) {
+    const uint32_t np = nproc[t];
+    for (uint32_t k0 = 0; k0 < np; k0 += kChunk)
+      units[atomicAdd(&cnt[bucket(min(np - k0, uint32_t(kChunk)))], 1u)] =
+          make_uint2(static_cast<uint32_t>(t), k0 / kChunk);
+  }
+  if (tid == 0) {
+    ctl[0] = s_total;
+    ctl[1] = 0u;
+  }
+}
+
+// Persistent CTAs fetch work units (unit_order_kernel) from a global
+// counter.  A unit starts from the pixel state the forward left at its chunk
+// end (ckpt: T and the colour suffix of the later splats; the tile's last
+// chunk starts from final_T and an empty suffix), so the chunks of one tile
+// run on different SMs at once and no tile's list length bounds the kernel.
 __global__ void __launch_bounds__(128) raster_bwd_kernel(
-    FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
+    FrameDesc fd, const uint2* __restrict__ units, uint32_t* __restrict__ unit_ctl,
+    const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ fh,
     const uint32_t* __restrict__ px_last, const uint32_t* __restrict__ tile_nproc,
     const float* __restrict__ final_T, const float* __restrict__ dL,
+    const float4* __restrict__ ckpt,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect, int64_t n,
-    float* __restrict__ partials, unsigned long long* __restrict__ n_processed) {
+    float* __restrict__ partials, unsigned long long* __restrict__ n_processed,
+    unsigned long long* __restrict__ trace) {
   constexpr int B = kBwdBatch;
+  const unsigned long long t_start = trace ? global_ns() : 0ull;
   __shared__ __align__(128) SplatRec s_raw[B];
   __shared__ float4 s_a[B];
   __shared__ float4 s_b[B];
@@ -354,119 +445,143 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   __shared__ uint32_t s_eidx[B];  // emission index of each staged pair
   __shared__ float s_red[4][B][9];
   __shared__ uint32_t s_wlast[4];
+  __shared__ uint32_t s_unit;
   __shared__ __align__(8) uint64_t s_bar;
   if (fh->stats.overflow) return;
-  const int tile = static_cast<int>(order[blockIdx.x]);
-  const int nproc = static_cast<int>(tile_nproc[tile]);
-  if (nproc == 0) return;
-  if (threadIdx.x == 0) atomicAdd(n_processed, static_cast<unsigned long long>(nproc));  // P_x
-  int v = 0;
-  while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
-  const CamDev& cam = fd.cam[v];
-  const int lt = tile - cam.tile_base;
-  const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qx = (warp & 1) * 8, qy = (warp >> 1) * 8;
   const int lx = qx + (lane & 7), ly = qy + (lane >> 3);
-  const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
-  const uint2 rg = ranges[tile];
-  const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
   const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
-  uint8_t* my_list = s_list[warp];
-
-  PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
-  PixBwd q1 = q0;
-  if (px < cam.width && py0 < cam.height) {
-    const int64_t pix = cam.pix_base + static_cast<int64_t>(py0) * cam.width + px;
-    q0.T = final_T[pix];
-    q0.last = px_last[pix];
-    q0.gr = dL[3 * pix + 0];
-    q0.gg = dL[3 * pix + 1];
-    q0.gb = dL[3 * pix + 2];
-  }
-  if (px < cam.width && py1 < cam.height) {
-    const int64_t pix = cam.pix_base + static_cast<int64_t>(py1) * cam.width + px;
-    q1.T = final_T[pix];
-    q1.last = px_last[pix];
-    q1.gr = dL[3 * pix + 0];
-    q1.gg = dL[3 * pix + 1];
-    q1.gb = dL[3 * pix + 2];
-  }
   const int slot = reduce9_slot(lane);
-  uint32_t wlast = max(q0.last, q1.last);  // warp-uniform upper bound of k
-#pragma unroll
-  for (int k = 16; k > 0; k >>= 1) wlast = max(wlast, __shfl_xor_sync(kFull, wlast, k));
-  if (lane == 0) s_wlast[warp] = wlast;
-
+  uint8_t* my_list = s_list[warp];
+  const uint32_t n_units = unit_ctl[0];
   if (tid == 0) mbar_init(&s_bar, 1);
-  __syncthreads();
   uint32_t phase = 0;
-  int b0 = ((nproc - 1) / B) * B;
-  issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(B, nproc - b0), tid, 128);
-  for (; b0 >= 0; b0 -= B) {
-    const int nb = min(B, nproc - b0);
-    mbar_wait(&s_bar, phase);
-    phase ^= 1;
-    for (int k = tid; k < nb; k += 128) {
-      const SplatRec& r = s_raw[k];
-      const Staged sg = stage_splat(r, ox, oy);
-      s_a[k] = sg.a;
-      s_b[k] = sg.b;
-      s_n[k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
-      s_io[k] = 1.0f / r.opac;
-      s_eidx[k] = static_cast<uint32_t>(
-          emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
-      uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-        if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);
-      s_mask[k] = static_cast<uint8_t>(m);
-    }
+  for (;;) {
+    if (tid == 0) s_unit = atomicAdd(&unit_ctl[1], 1u);
     __syncthreads();
-    if (b0 > 0) {
-      fence_proxy_async_smem();
-      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
-    }
-    const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
-    for (int i = hits - 1; i >= 0; --i) {
-      const int j = my_list[i];
-      const uint32_t k = static_cast<uint32_t>(b0 + j);
-      float o[9];
-#pragma unroll
-      for (int u = 0; u < 9; ++u) o[u] = 0.0f;
-      const float4 a = s_a[j];
-      const float4 b = s_b[j];
-      const float4 nc = s_n[j];
-      float u0, v0, u1, v1;
-      const float al0 = staged_alpha(a, b, flx, fly, u0, v0);
-      const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
-      bool any = bwd_pixel(q0, k, al0, b.w, nc.x, nc.y, u0, v0, o);
-      any = bwd_pixel(q1, k, al1, b.w, nc.x, nc.y, u1, v1, o) || any;
-      // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
-      float red = 0.0f;
-      if (__any_sync(kFull, any)) red = warp_reduce9(o);
-      if (slot >= 0) s_red[warp][j][slot] = red;
-    }
-    __syncthreads();
-    for (int jj = tid; jj < nb; jj += 128) {  // one splat per thread, warps in fixed order
-      const uint32_t m = s_mask[jj];
-      float mom[9], g[9];
-#pragma unroll
-      for (int u = 0; u < 9; ++u) {
-        const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
-        const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
-        const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
-        const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
-        mom[u] = (r0 + r1) + (r2 + r3);
+    const uint32_t ui = s_unit;
+    if (ui >= n_units) break;
+    const uint2 un = units[ui];
+    const int tile = static_cast<int>(un.x);
+    const int nproc = static_cast<int>(tile_nproc[tile]);
+    const int k0 = static_cast<int>(un.y) * kChunk;
+    const int k_end = min(k0 + kChunk, nproc);
+    if (tid == 0) atomicAdd(n_processed, static_cast<unsigned long long>(k_end - k0));  // P_x
+    int v = 0;
+    while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
+    const CamDev& cam = fd.cam[v];
+    const int lt = tile - cam.tile_base;
+    const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
+    const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
+    const uint2 rg = ranges[tile];
+    const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
+    const bool last_chunk = k_end == nproc;
+    const float4* ck = last_chunk ? nullptr
+                                  : ckpt + ckpt_slot(rg.x, tile, k_end / kChunk) * kTilePixels;
+
+    PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
+    PixBwd q1 = q0;
+    auto load_px = [&](PixBwd& q, int py, int lyy) {
+      if (px < cam.width && py < cam.height) {
+        const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
+        q.last = px_last[pix];
+        q.gr = dL[3 * pix + 0];
+        q.gg = dL[3 * pix + 1];
+        q.gb = dL[3 * pix + 2];
+        if (last_chunk) {
+          q.T = final_T[pix];
+        } else {
+          const float4 c = ck[lyy * kTile + lx];
+          q.T = c.x;
+          q.sr = c.y;
+          q.sg = c.z;
+          q.sb = c.w;
+        }
       }
-      const float4 aa = s_a[jj];
-      const float4 nn = s_n[jj];
-      moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[jj], g);
-      float* out = partials + static_cast<int64_t>(s_eidx[jj]) * 9;
+    };
+    load_px(q0, py0, ly);
+    load_px(q1, py1, ly + 4);
+    uint32_t wlast = max(q0.last, q1.last);  // warp-uniform upper bound of k
 #pragma unroll
-      for (int u = 0; u < 9; ++u) out[u] = g[u];
-    }
+    for (int k = 16; k > 0; k >>= 1) wlast = max(wlast, __shfl_xor_sync(kFull, wlast, k));
+    if (lane == 0) s_wlast[warp] = wlast;
     __syncthreads();
+    int b0 = k0 + ((k_end - 1 - k0) / B) * B;
+    fence_proxy_async_smem();  // s_raw was read by the previous unit's staging
+    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(B, k_end - b0), tid, 128);
+    for (; b0 >= k0; b0 -= B) {
+      const int nb = min(B, k_end - b0);
+      mbar_wait(&s_bar, phase);
+      phase ^= 1;
+      for (int k = tid; k < nb; k += 128) {
+        const SplatRec& r = s_raw[k];
+        const Staged sg = stage_splat(r, ox, oy);
+        s_a[k] = sg.a;
+        s_b[k] = sg.b;
+        s_n[k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
+        s_io[k] = 1.0f / r.opac;
+        s_eidx[k] = static_cast<uint32_t>(
+            emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
+        uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);
+        s_mask[k] = static_cast<uint8_t>(m);
+      }
+      __syncthreads();
+      if (b0 > k0) {
+        fence_proxy_async_smem();
+        issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
+      }
+      const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
+      for (int i = hits - 1; i >= 0; --i) {
+        const int j = my_list[i];
+        const uint32_t k = static_cast<uint32_t>(b0 + j);
+        float o[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) o[u] = 0.0f;
+        const float4 a = s_a[j];
+        const float4 b = s_b[j];
+        const float4 nc = s_n[j];
+        float u0, v0, u1, v1;
+        const float al0 = staged_alpha(a, b, flx, fly, u0, v0);
+        const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
+        bool any = bwd_pixel(q0, k, al0, b.w, nc.x, nc.y, u0, v0, o);
+        any = bwd_pixel(q1, k, al1, b.w, nc.x, nc.y, u1, v1, o) || any;
+        // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
+        float red = 0.0f;
+        if (__any_sync(kFull, any)) red = warp_reduce9(o);
+        if (slot >= 0) s_red[warp][j][slot] = red;
+      }
+      __syncthreads();
+      for (int jj = tid; jj < nb; jj += 128) {  // one splat per thread, warps in fixed order
+        const uint32_t m = s_mask[jj];
+        float mom[9], g[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) {
+          const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
+          const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
+          const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
+          const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
+          mom[u] = (r0 + r1) + (r2 + r3);
+        }
+        const float4 aa = s_a[jj];
+        const float4 nn = s_n[jj];
+        moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[jj], g);
+        float* out = partials + static_cast<int64_t>(s_eidx[jj]) * 9;
+#pragma unroll
+        for (int u = 0; u < 9; ++u) out[u] = g[u];
+      }
+      __syncthreads();
+    }
+  }
+  if (trace && tid == 0) {
+    unsigned long long* t = trace + 4 * (static_cast<int64_t>(fd.total_tiles) + blockIdx.x);
+    t[0] = t_start;
+    t[1] = global_ns();
+    t[2] = smid();
+    t[3] = static_cast<unsigned long long>(blockIdx.x);
   }
 }
 
@@ -486,7 +601,8 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                                                                  L.recs, L.hdr,
                                                                  image, final_T, counts, L.px_last,
                                                                  L.tile_nproc, L.rank_of,
-                                                                 L.last_rank));
+                                                                 L.last_rank, L.ckpt,
+                                                                 tile_trace_buffer()));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
   return CGS_OK;
 }
@@ -494,17 +610,25 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
                       cudaStream_t st) {
-  int rc = launch_tile_order(fd, L, L.tile_nproc, st);
-  if (rc) return rc;
+  unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl);
+  CGS_CHECK_LAUNCH("unit_order_kernel");
+  static int resident = 0;  // persistent grid: every resident CTA slot
+  if (resident == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    CGS_CUDA(cudaGetDevice(&dev));
+    CGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_bwd_kernel, 128, 0));
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int grid = static_cast<int>(L.n_ckpt < resident ? L.n_ckpt : resident);
   CGS_PROFILED("raster_bwd_kernel", st,
-               raster_bwd_kernel<<<fd.total_tiles, 128, 0, st>>>(fd, L.tile_order, L.ranges,
-                                                                 sorted_pair_vals(L),
-                                                                 L.recs, L.hdr, L.px_last,
-                                                                 L.tile_nproc, final_T, dL,
-                                                                 L.pair_off, L.rect, L.n,
-                                                                 partials, n_processed));
+               raster_bwd_kernel<<<grid, 128, 0, st>>>(fd, L.units, L.unit_ctl, L.ranges,
+                                                       sorted_pair_vals(L), L.recs, L.hdr,
+                                                       L.px_last, L.tile_nproc, final_T, dL,
+                                                       L.ckpt, L.pair_off, L.rect, L.n,
+                                                       partials, n_processed,
+                                                       tile_trace_buffer()));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   return CGS_OK;
 }
-
 }  // namespace cgs
