@@ -32,7 +32,7 @@ for _ in range(5):
 torch.cuda.synchronize()
 T = tr.frame.desc_total_tiles if hasattr(tr.frame, "desc_total_tiles") else sum(
     ((c.width + 15) // 16) * ((c.height + 15) // 16) for c in cams)
-buf = torch.zeros(8 * T, dtype=torch.int64, device=dev)
+buf = torch.zeros(8 * T + 33, dtype=torch.int64, device=dev)
 lib = nat.library()
 for rep in range(3):
     buf.zero_()
@@ -40,7 +40,14 @@ for rep in range(3):
     tr.step()
     torch.cuda.synchronize()
     lib.cgs_trace_tiles(None)
-    rec = buf.view(2, T, 4).cpu().numpy().astype(np.int64)
+    allb = buf.cpu().numpy().astype(np.int64)
+    rec = allb[:8 * T].reshape(2, T, 4)
+    hist = allb[8 * T:]
+    tot = hist.sum()
+    print(f"[{rep}] bwd warp hits {tot}: no contribution {hist[0] / tot:.1%}, "
+          f"1-4 lanes {hist[1:5].sum() / tot:.1%}, 5-16 {hist[5:17].sum() / tot:.1%}, "
+          f"17-31 {hist[17:32].sum() / tot:.1%}, 32 {hist[32] / tot:.1%}")
+    print("   per-lane-count fractions 0..32:", " ".join(f"{x / tot:.3f}" for x in hist))
     for name, r in (("fwd", rec[0]), ("bwd", rec[1])):
         r = r[r[:, 1] > 0]
         t0 = r[:, 0].min()

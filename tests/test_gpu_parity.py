@@ -386,6 +386,54 @@ def test_near_plane_giants_match_oracle(cg):
         assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
 
 
+def _deep_stack_scene(seed=7, n=2400, size=48):
+    """Thousands of faint, wide Gaussians stacked in depth over 9 tiles: the
+    processed prefixes span several backward chunks (kChunk = 512 splats),
+    pixels terminate inside and across chunks, some never do."""
+    from paper_2509_03775_b200 import camera, scenes
+    a = scenes.config0(seed)
+    rng = np.random.default_rng(seed)
+    cam = camera.ring_cameras(1, (0.0, 0.0, 0.0), 3.0, 0.0, float(size), size, size)[0]
+    pos = np.empty((n, 3), np.float32)
+    pos[:, :2] = rng.uniform(-0.3, 0.3, size=(n, 2))
+    pos[:, 2] = rng.uniform(-1.0, 1.0, size=n)
+    pos = pos @ cam.rotation.astype(np.float32)  # x, y across the view, z along it
+    idx = rng.integers(0, a.sr_rows.shape[0], n).astype(np.int32)
+    sr = a.sr_rows.copy()
+    sr[:, 0:3] = rng.uniform(-0.8, -0.4, size=(sr.shape[0], 3))
+    logit = rng.normal(-4.5, 0.5, n).astype(np.float32)
+    return pos, logit, idx, idx, a.sh_rows, sr, cam
+
+
+def test_deep_stack_chunked_backward_matches_oracle(cg):
+    """Backward work units split a tile's processed prefix into 512-splat
+    chunks started from the forward's per-pixel checkpoints (T and colour
+    suffix): image, T, counts and gradients match the oracle."""
+    from gpu_helpers import group_rel
+    from oracle import cgs_oracle as O
+    pos, logit, g2sh, g2sr, sh, sr, cam = _deep_stack_scene()
+    st = cg.ModelState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    art = cg.rasterize_forward(st, cam)
+    ost = O.OState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    ocam = O.cam_from_any(cam)
+    fw = O.raster_forward(ost, ocam)
+    offs, ids = art.frame.tile_lists()
+    assert np.array_equal(offs, fw["tile_offsets"]) and np.array_equal(ids, fw["tile_ids"])
+    cnt = art.contrib_counts.cpu().numpy()
+    assert cnt.max() > 1024 and np.diff(offs).min() > 1600  # >= 3 chunks per tile
+    knife = cnt != fw["counts"]
+    assert knife.sum() <= 4 and np.all(np.abs(cnt[knife] - fw["counts"][knife]) == 1)
+    img = art.image.cpu().numpy()
+    assert np.allclose(img[~knife], fw["image"][~knife], rtol=RTOL, atol=ATOL)
+    dL = np.random.default_rng(2).normal(0, 1e-3, img.shape)
+    dL[knife] = 0.0
+    g = cg.rasterize_backward(st, cam, art, dL).numpy()
+    og = O.raster_backward(ost, ocam, dL)
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        assert group_rel(g[k], og[k]) <= 1e-4, (k, group_rel(g[k], og[k]))
+        assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
+
+
 def test_sgld_device_noise_statistics(cg):
     """Throughput mode (device Philox noise): with zero gradients the update is
     exactly k * eta per coordinate, eta ~ N(0, 1) i.i.d.; fresh draws per
