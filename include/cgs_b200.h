@@ -114,9 +114,11 @@ CGS_API uint64_t cgs_launch_count(void);
 CGS_API int cgs_profile_kernel(const char* name);
 /* Sum of the recorded launches' durations (synchronizes those events). */
 CGS_API int cgs_profile_read(double* total_ms, int64_t* launches);
-/* Diagnostics: with a device buffer of >= 8 * total_tiles uint64 set, the
- * raster kernels record {start ns, end ns, SM id, tile} per CTA (forward at
- * [4 b], backward at [4 (total_tiles + b)]); NULL disables. */
+/* Diagnostics: with a zeroed device buffer of >= 8 * total_tiles + 33
+ * uint64 set, the raster kernels record {start ns, end ns, SM id, tile} per
+ * CTA (forward at [4 b], backward persistent CTA b at [4 (total_tiles + b)])
+ * and the backward adds a histogram of contributing lanes per warp hit at
+ * [8 total_tiles + 0..32]; NULL disables. */
 CGS_API int cgs_trace_tiles(void* dev_buf);
 
 /* ---- render: rasterize_forward / rasterize_backward ------------------- */

@@ -148,7 +148,7 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
   return m;
 }
 
-__global__ void __launch_bounds__(256) raster_fwd_kernel(
+__global__ void __launch_bounds__(256, 6) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
 // end (ckpt: T and the colour suffix of the later splats; the tile's last
 // chunk starts from final_T and an empty suffix), so the chunks of one tile
 // run on different SMs at once and no tile's list length bounds the kernel.
+template <bool TRACE>
 __global__ void __launch_bounds__(128) raster_bwd_kernel(
     FrameDesc fd, const uint2* __restrict__ units, uint32_t* __restrict__ unit_ctl,
     const uint2* __restrict__ ranges,
@@ -549,6 +550,9 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
         bool any = bwd_pixel(q0, k, al0, b.w, nc.x, nc.y, u0, v0, o);
         any = bwd_pixel(q1, k, al1, b.w, nc.x, nc.y, u1, v1, o) || any;
+        if (TRACE && lane == 0)  // diagnostics: lanes with a contribution per warp hit
+          atomicAdd(trace + 8 * static_cast<int64_t>(fd.total_tiles) + __popc(__ballot_sync(kFull, any)), 1ull);
+        else if (TRACE) __ballot_sync(kFull, any);
         // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
         float red = 0.0f;
         if (__any_sync(kFull, any)) red = warp_reduce9(o);
@@ -576,7 +580,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       __syncthreads();
     }
   }
-  if (trace && tid == 0) {
+  if (TRACE && tid == 0) {
     unsigned long long* t = trace + 4 * (static_cast<int64_t>(fd.total_tiles) + blockIdx.x);
     t[0] = t_start;
     t[1] = global_ns();
@@ -617,17 +621,17 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
     int dev = 0, sms = 0, per_sm = 0;
     CGS_CUDA(cudaGetDevice(&dev));
     CGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_bwd_kernel, 128, 0));
+    CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_bwd_kernel<false>, 128, 0));
     resident = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int grid = static_cast<int>(L.n_ckpt < resident ? L.n_ckpt : resident);
+  unsigned long long* trace = tile_trace_buffer();
+  auto kern = trace ? raster_bwd_kernel<true> : raster_bwd_kernel<false>;
   CGS_PROFILED("raster_bwd_kernel", st,
-               raster_bwd_kernel<<<grid, 128, 0, st>>>(fd, L.units, L.unit_ctl, L.ranges,
-                                                       sorted_pair_vals(L), L.recs, L.hdr,
-                                                       L.px_last, L.tile_nproc, final_T, dL,
-                                                       L.ckpt, L.pair_off, L.rect, L.n,
-                                                       partials, n_processed,
-                                                       tile_trace_buffer()));
+               kern<<<grid, 128, 0, st>>>(fd, L.units, L.unit_ctl, L.ranges, sorted_pair_vals(L),
+                                          L.recs, L.hdr, L.px_last, L.tile_nproc, final_T, dL,
+                                          L.ckpt, L.pair_off, L.rect, L.n, partials, n_processed,
+                                          trace));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   return CGS_OK;
 }
