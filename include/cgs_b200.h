@@ -40,6 +40,7 @@ extern "C" {
 #define CGS_ECUDA 2      /* CUDA runtime error                                */
 #define CGS_EWORKSPACE 3 /* workspace too small                               */
 #define CGS_ENONFINITE 4 /* non-finite gradients (reference: SamplerError)    */
+#define CGS_EINTERNAL 5  /* internal invariant violated (a bug, not an input) */
 
 #if defined(__GNUC__)
 #define CGS_API __attribute__((visibility("default")))
@@ -181,6 +182,59 @@ CGS_API int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* ca
                         void* workspace, size_t workspace_bytes,
                         float* grad_positions, float* grad_logits,
                         float* grad_sh_rows, float* grad_sr_rows, cgs_stream_t stream);
+
+/* ---- staged entry points (SURVEY.md 8(b) proposed exports) ----------- */
+/* cgs_render_forward = cgs_project -> cgs_sort_depth -> cgs_duplicate_tiles
+ * -> cgs_sort_pairs -> cgs_raster_fwd on the same frame workspace and
+ * arguments, in that order on one stream (bit-identical results); likewise
+ * cgs_render_backward = cgs_raster_bwd -> cgs_gaussian_reduce_pullback ->
+ * cgs_codebook_reduce on the same backward workspace.  Stages read only what
+ * the earlier stages left in the workspaces.
+ *   project        render.py:145-203  fp64 projection, SH colour, pixel rect,
+ *                  contribution box, depth keys (+ depth-key histograms)
+ *   sort_depth     render.py:203      stable depth order (lexsort (idx, tz)),
+ *                  per-splat pair offsets, pair count / overflow stats
+ *   duplicate      render.py:240-254  (tile, splat) pairs in depth order
+ *   sort_pairs     render.py:240-254  stable tile sort, tile ranges
+ *   raster_fwd     render.py:287-315  blend, T, counts (+ chunk checkpoints)
+ *   raster_bwd     render.py:318-379  per processed pair 9-float partials
+ *   gaussian_reduce_pullback render.py:382-455 per splat sums + fp64 chain
+ *                  rule; grad_positions / grad_logits fully written (x scale)
+ *   codebook_reduce render.py:456-458 per code row segmented sums (CSRs
+ *                  optional, NULL = build in the workspace); grads x scale */
+CGS_API int cgs_project(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                        void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                        cgs_stream_t stream);
+CGS_API int cgs_sort_depth(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                           void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                           cgs_stream_t stream);
+CGS_API int cgs_duplicate_tiles(const cgs_scene_t* scene, const cgs_camera_t* cams,
+                                int32_t n_views, void* workspace, size_t workspace_bytes,
+                                int64_t pair_capacity, cgs_stream_t stream);
+CGS_API int cgs_sort_pairs(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                           void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                           cgs_stream_t stream);
+CGS_API int cgs_raster_fwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                           void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                           float* image, float* final_T, int32_t* contrib_counts,
+                           cgs_stream_t stream);
+CGS_API int cgs_raster_bwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                           const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
+                           const float* final_T, const float* dL_dimage, void* workspace,
+                           size_t workspace_bytes, cgs_stream_t stream);
+CGS_API int cgs_gaussian_reduce_pullback(const cgs_scene_t* scene, const cgs_camera_t* cams,
+                                         int32_t n_views, const void* frame_ws,
+                                         size_t frame_ws_bytes, int64_t pair_capacity,
+                                         float scale, void* workspace, size_t workspace_bytes,
+                                         float* grad_positions, float* grad_logits,
+                                         cgs_stream_t stream);
+CGS_API int cgs_codebook_reduce(const cgs_scene_t* scene, const cgs_camera_t* cams,
+                                int32_t n_views, const void* frame_ws, size_t frame_ws_bytes,
+                                int64_t pair_capacity, float scale,
+                                const int32_t* sh_csr_offsets, const int32_t* sh_csr_members,
+                                const int32_t* sr_csr_offsets, const int32_t* sr_csr_members,
+                                void* workspace, size_t workspace_bytes, float* grad_sh_rows,
+                                float* grad_sr_rows, cgs_stream_t stream);
 
 /* code -> members CSR of an index array (g2sh or g2sr): offsets (capacity+1)
  * and members (n, ascending Gaussian index within each row).  Rebuild only

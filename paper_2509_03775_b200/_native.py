@@ -81,6 +81,14 @@ SIGNATURES = {
     "cgs_frame_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64]),
     "cgs_render_forward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
     "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),
+    "cgs_project": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
+    "cgs_sort_depth": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
+    "cgs_duplicate_tiles": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
+    "cgs_sort_pairs": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
+    "cgs_raster_fwd": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
+    "cgs_raster_bwd": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, SZ, P]),
+    "cgs_gaussian_reduce_pullback": (I32, [SCNP, CAMP, I32, P, SZ, I64, F32, P, SZ, P, P, P]),
+    "cgs_codebook_reduce": (I32, [SCNP, CAMP, I32, P, SZ, I64, F32, P, P, P, P, P, SZ, P, P, P]),
     "cgs_frame_tile_lists": (I32, [CAMP, I32, I64, I64, I64, P, SZ, P, P, P]),
     "cgs_frame_splats": (I32, [CAMP, I32, I64, I64, I64, P, SZ, I32, P, P, P, P, P, P]),
     "cgs_backward_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64, I64]),

@@ -64,7 +64,19 @@ int cuda_status(cudaError_t e, const char* where) {
 // defined in the kernel translation units
 int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, float* image,
                   float* final_T, int32_t* counts, double* sr_cov, cudaStream_t st);
+int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L,
+                        double* sr_cov, cudaStream_t st);
+int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
+int frame_stage_duplicate(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
+int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
+int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, float* image, float* final_T,
+                       int32_t* counts, cudaStream_t st);
 struct BwdLayout;
+int bwd_stage_entry(int stage, const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
+                    void* ws, size_t ws_bytes, const float* dL, const float* final_T, float scale,
+                    float* gpos, float* glogit, float* gsh, float* gsr,
+                    const int32_t* const csr_off[2], const int32_t* const csr_mem[2],
+                    cudaStream_t st);
 size_t bwd_ws_bytes(int64_t n, int n_views, int total_tiles, int64_t pair_cap, int64_t sh_cap,
                     int64_t sr_cap);
 int frame_backward_entry(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
@@ -207,6 +219,75 @@ int cgs_render_forward(const cgs_scene_t* scene, const cgs_camera_t* cams, int32
   }
   return frame_forward(scene, fd, L, image, final_T, contrib_counts, L.sr_cov,
                        static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// validated scene, frame descriptor and layout for the staged entry points
+static int staged_frame(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                        const void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                        FrameDesc* fd, FrameLayout* L) {
+  int rc = check_scene(scene);
+  if (rc) return rc;
+  rc = check_cams(cams, n_views);
+  if (rc) return rc;
+  *fd = make_frame_desc(cams, n_views);
+  *L = plan_frame(const_cast<void*>(workspace), workspace_bytes, scene->n, *fd, pair_capacity,
+                  scene->sr_capacity);
+  if (L->bytes > workspace_bytes || !workspace) {
+    set_error("frame workspace too small: need " + std::to_string(L->bytes));
+    return CGS_EWORKSPACE;
+  }
+  if (scene->n * n_views >= (1LL << 32) - 1) {
+    set_error("views * Gaussians must be < 2^32");
+    return CGS_EINVAL;
+  }
+  return CGS_OK;
+}
+
+extern "C" {
+
+#define CGS_STAGE_PROLOGUE                                                                   \
+  FrameDesc fd;                                                                              \
+  FrameLayout L;                                                                             \
+  int rc = staged_frame(scene, cams, n_views, workspace, workspace_bytes, pair_capacity, &fd, \
+                        &L);                                                                 \
+  if (rc) return rc;                                                                         \
+  cudaStream_t st = static_cast<cudaStream_t>(stream)
+
+int cgs_project(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                cgs_stream_t stream) {
+  CGS_STAGE_PROLOGUE;
+  return frame_stage_project(scene, fd, L, L.sr_cov, st);
+}
+
+int cgs_sort_depth(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                   void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                   cgs_stream_t stream) {
+  CGS_STAGE_PROLOGUE;
+  return frame_stage_sort_depth(fd, L, st);
+}
+
+int cgs_duplicate_tiles(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                        void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                        cgs_stream_t stream) {
+  CGS_STAGE_PROLOGUE;
+  return frame_stage_duplicate(fd, L, st);
+}
+
+int cgs_sort_pairs(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                   void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                   cgs_stream_t stream) {
+  CGS_STAGE_PROLOGUE;
+  return frame_stage_sort_pairs(fd, L, st);
+}
+
+int cgs_raster_fwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                   void* workspace, size_t workspace_bytes, int64_t pair_capacity, float* image,
+                   float* final_T, int32_t* contrib_counts, cgs_stream_t stream) {
+  CGS_STAGE_PROLOGUE;
+  return frame_stage_raster(fd, L, image, final_T, contrib_counts, st);
 }
 
 int cgs_frame_stats(const void* workspace, cgs_frame_stats_t* out, cgs_stream_t stream) {
@@ -373,6 +454,52 @@ int cgs_render_backward(const cgs_scene_t* scene, const cgs_camera_t* cams, int3
   return frame_backward_entry(scene, fd, L, workspace, workspace_bytes, dL_dimage, final_T, scale,
                               grad_positions, grad_logits, grad_sh_rows, grad_sr_rows, off, mem,
                               static_cast<cudaStream_t>(stream));
+}
+
+static int bwd_stage(int stage, const cgs_scene_t* scene, const cgs_camera_t* cams,
+                     int32_t n_views, const void* frame_ws, size_t frame_ws_bytes,
+                     int64_t pair_capacity, void* workspace, size_t workspace_bytes,
+                     const float* final_T, const float* dL, float scale, float* gpos,
+                     float* glogit, float* gsh, float* gsr, const int32_t* const off[2],
+                     const int32_t* const mem[2], cgs_stream_t stream) {
+  FrameDesc fd;
+  FrameLayout L;
+  int rc = staged_frame(scene, cams, n_views, frame_ws, frame_ws_bytes, pair_capacity, &fd, &L);
+  if (rc) return rc;
+  return bwd_stage_entry(stage, scene, fd, L, workspace, workspace_bytes, dL, final_T, scale, gpos,
+                         glogit, gsh, gsr, off, mem, static_cast<cudaStream_t>(stream));
+}
+
+int cgs_raster_bwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                   const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
+                   const float* final_T, const float* dL_dimage, void* workspace,
+                   size_t workspace_bytes, cgs_stream_t stream) {
+  return bwd_stage(0, scene, cams, n_views, frame_ws, frame_ws_bytes, pair_capacity, workspace,
+                   workspace_bytes, final_T, dL_dimage, 1.0f, nullptr, nullptr, nullptr, nullptr,
+                   nullptr, nullptr, stream);
+}
+
+int cgs_gaussian_reduce_pullback(const cgs_scene_t* scene, const cgs_camera_t* cams,
+                                 int32_t n_views, const void* frame_ws, size_t frame_ws_bytes,
+                                 int64_t pair_capacity, float scale, void* workspace,
+                                 size_t workspace_bytes, float* grad_positions,
+                                 float* grad_logits, cgs_stream_t stream) {
+  return bwd_stage(1, scene, cams, n_views, frame_ws, frame_ws_bytes, pair_capacity, workspace,
+                   workspace_bytes, nullptr, nullptr, scale, grad_positions, grad_logits, nullptr,
+                   nullptr, nullptr, nullptr, stream);
+}
+
+int cgs_codebook_reduce(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n_views,
+                        const void* frame_ws, size_t frame_ws_bytes, int64_t pair_capacity,
+                        float scale, const int32_t* sh_csr_offsets,
+                        const int32_t* sh_csr_members, const int32_t* sr_csr_offsets,
+                        const int32_t* sr_csr_members, void* workspace, size_t workspace_bytes,
+                        float* grad_sh_rows, float* grad_sr_rows, cgs_stream_t stream) {
+  const int32_t* const off[2] = {sh_csr_offsets, sr_csr_offsets};
+  const int32_t* const mem[2] = {sh_csr_members, sr_csr_members};
+  return bwd_stage(2, scene, cams, n_views, frame_ws, frame_ws_bytes, pair_capacity, workspace,
+                   workspace_bytes, nullptr, nullptr, scale, nullptr, nullptr, grad_sh_rows,
+                   grad_sr_rows, off, mem, stream);
 }
 
 size_t cgs_loss_workspace_bytes(int32_t n_views, int32_t height, int32_t width) {

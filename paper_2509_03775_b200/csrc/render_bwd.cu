@@ -604,32 +604,21 @@ static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap
                    off, mem, cap, n, nv, B, scale, gsh));
 }
 
-int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L, BwdLayout& B,
-                   const float* dL, const float* final_T, float scale, float* gpos, float* glogit,
-                   float* gsh, float* gsr, const int32_t* const csr_off_in[2],
-                   const int32_t* const csr_mem_in[2], cudaStream_t st) {
-  const int D = 3 * (sc->sh_degree + 1) * (sc->sh_degree + 1);
+// The frame backward in three stages (exported as cgs_raster_bwd,
+// cgs_gaussian_reduce_pullback, cgs_codebook_reduce; each reads what the
+// earlier stages left in the backward workspace).
+int bwd_stage_raster(const FrameDesc& fd, const FrameLayout& L, BwdLayout& B, const float* dL,
+                     const float* final_T, cudaStream_t st) {
   CGS_CUDA(cudaMemsetAsync(B.hdr, 0, sizeof(BwdHeader), st));
   if (L.vn > 0) CGS_CUDA(cudaMemsetAsync(B.touched, 0, L.vn, st));
-  const int32_t* off[2];
-  const int32_t* mem[2];
-  const int32_t* idx[2] = {sc->g2sh, sc->g2sr};
-  const int64_t caps[2] = {sc->sh_capacity, sc->sr_capacity};
-  for (int b = 0; b < 2; ++b) {
-    if (csr_off_in && csr_off_in[b] && csr_mem_in && csr_mem_in[b]) {
-      off[b] = csr_off_in[b];
-      mem[b] = csr_mem_in[b];
-    } else {
-      int rc = build_code_csr(idx[b], sc->n, caps[b], B.csr_off[b], B.csr_mem[b], B.csr_ws,
-                              B.csr_ws_bytes, st);
-      if (rc) return rc;
-      off[b] = B.csr_off[b];
-      mem[b] = B.csr_mem[b];
-    }
-  }
+  if (fd.total_tiles > 0 && L.vn > 0)
+    return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed, st);
+  return CGS_OK;
+}
+
+int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
+                       BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st) {
   if (fd.total_tiles > 0 && L.vn > 0) {
-    int rc = launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed, st);
-    if (rc) return rc;
     PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
@@ -646,6 +635,29 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
                                                                              scale, gpos, glogit));
     CGS_CHECK_LAUNCH("gauss_write_kernel");
   }
+  return CGS_OK;
+}
+
+int bwd_stage_codebook(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
+                       BwdLayout& B, float scale, float* gsh, float* gsr,
+                       const int32_t* const csr_off_in[2], const int32_t* const csr_mem_in[2],
+                       cudaStream_t st) {
+  const int32_t* off[2];
+  const int32_t* mem[2];
+  const int32_t* idx[2] = {sc->g2sh, sc->g2sr};
+  const int64_t caps[2] = {sc->sh_capacity, sc->sr_capacity};
+  for (int b = 0; b < 2; ++b) {
+    if (csr_off_in && csr_off_in[b] && csr_mem_in && csr_mem_in[b]) {
+      off[b] = csr_off_in[b];
+      mem[b] = csr_mem_in[b];
+    } else {
+      int rc = build_code_csr(idx[b], sc->n, caps[b], B.csr_off[b], B.csr_mem[b], B.csr_ws,
+                              B.csr_ws_bytes, st);
+      if (rc) return rc;
+      off[b] = B.csr_off[b];
+      mem[b] = B.csr_mem[b];
+    }
+  }
   if (sc->sh_capacity > 0) {
     switch (sc->sh_degree) {
       case 0: launch_sh_reduce<0>(off[0], mem[0], sc->sh_capacity, sc->n, fd.n_views, B, scale, gsh, st); break;
@@ -655,7 +667,6 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
     }
     CGS_CHECK_LAUNCH("sh_code_reduce_kernel");
   }
-  (void)D;
   if (sc->sr_capacity > 0) {
     CGS_PROFILED("sr_code_reduce_kernel", st,
                  sr_code_reduce_kernel<<<grid_for(sc->sr_capacity * 32, 256, 16), 256, 0, st>>>(
@@ -667,9 +678,47 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
   return CGS_OK;
 }
 
+int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L, BwdLayout& B,
+                   const float* dL, const float* final_T, float scale, float* gpos, float* glogit,
+                   float* gsh, float* gsr, const int32_t* const csr_off_in[2],
+                   const int32_t* const csr_mem_in[2], cudaStream_t st) {
+  int rc = bwd_stage_raster(fd, L, B, dL, final_T, st);
+  if (!rc) rc = bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st);
+  if (!rc) rc = bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off_in, csr_mem_in, st);
+  return rc;
+}
+
 size_t bwd_ws_bytes(int64_t n, int n_views, int total_tiles, int64_t pair_cap, int64_t sh_cap,
                     int64_t sr_cap) {
   return plan_bwd(nullptr, 0, n, n_views, total_tiles, pair_cap, sh_cap, sr_cap).bytes;
+}
+
+int plan_bwd_checked(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L, void* ws,
+                     size_t ws_bytes, BwdLayout* out) {
+  *out = plan_bwd(ws, ws_bytes, sc->n, fd.n_views, fd.total_tiles, L.pair_cap, sc->sh_capacity,
+                  sc->sr_capacity);
+  if (out->bytes > ws_bytes || !ws) {
+    set_error("backward workspace too small: need " + std::to_string(out->bytes));
+    return CGS_EWORKSPACE;
+  }
+  return CGS_OK;
+}
+
+// One backward stage (0 raster, 1 per-Gaussian reduce + pull-back,
+// 2 codebook reduce) on caller workspaces (the staged C ABI).
+int bwd_stage_entry(int stage, const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
+                    void* ws, size_t ws_bytes, const float* dL, const float* final_T, float scale,
+                    float* gpos, float* glogit, float* gsh, float* gsr,
+                    const int32_t* const csr_off[2], const int32_t* const csr_mem[2],
+                    cudaStream_t st) {
+  BwdLayout B;
+  int rc = plan_bwd_checked(sc, fd, L, ws, ws_bytes, &B);
+  if (rc) return rc;
+  switch (stage) {
+    case 0: return bwd_stage_raster(fd, L, B, dL, final_T, st);
+    case 1: return bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st);
+    default: return bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off, csr_mem, st);
+  }
 }
 
 int frame_backward_entry(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,

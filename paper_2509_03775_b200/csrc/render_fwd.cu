@@ -455,10 +455,8 @@ static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut&
 }
 
 template <typename KT>
-static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
-                           const uint32_t* perm, cudaStream_t st) {
-  KT* kres;
-  uint32_t* vres;
+static int emit_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
+                            const uint32_t* perm, cudaStream_t st) {
   const int eg = grid_for(L.vn, 256, 16);
   // the emission kernels also build the tile sort's digit histogram
   const int passes = (L.tile_key_bits + 7) / 8;
@@ -473,18 +471,32 @@ static int emit_sort_range(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
                                                        L.hdr, fd, L.n, static_cast<KT*>(L.pkeys),
                                                        L.pvals, ws.hist, passes);
   CGS_CHECK_LAUNCH("emit_long_pairs_kernel");
+  return CGS_OK;
+}
+
+template <typename KT>
+static int sort_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws, cudaStream_t st) {
+  KT* kres;
+  uint32_t* vres;
   int rc = launch_radix_sort<KT>(static_cast<KT*>(L.pkeys), L.pvals, &L.hdr->n_pairs, 0,
                                  L.pair_cap, L.tile_key_bits, ws, &kres, &vres, st,
                                  /*hist_ready=*/true);
   if (rc) return rc;
+  if (vres != sorted_pair_vals(L)) {
+    set_error("tile sort: unexpected result buffer");
+    return CGS_EINTERNAL;
+  }
   CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * (fd.total_tiles > 0 ? fd.total_tiles : 1), st));
   tile_ranges_kernel<KT><<<grid_for(L.pair_cap, 256, 8), 256, 0, st>>>(kres, L.hdr, L.ranges);
   CGS_CHECK_LAUNCH("tile_ranges_kernel");
   return CGS_OK;
 }
 
-int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, float* image,
-                  float* final_T, int32_t* counts, double* sr_cov, cudaStream_t st) {
+// The frame forward in five stages (exported one by one as cgs_project,
+// cgs_sort_depth, cgs_duplicate_tiles, cgs_sort_pairs, cgs_raster_fwd; each
+// reads only what the earlier stages left in the frame workspace).
+int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L,
+                        double* sr_cov, cudaStream_t st) {
   const int64_t vn = L.vn;
   CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
   if (sc->sr_capacity > 0) {
@@ -505,14 +517,24 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
     }
     CGS_CHECK_LAUNCH("project_kernel");
   }
-  // depth order of every splat of the frame (all views; the tile sort below
-  // separates the views again)
+  return CGS_OK;
+}
+
+// Depth order of every splat of the frame (all views; the tile sort
+// separates the views again), then per-splat pair offsets in that order.
+// 4 passes over the 32-bit keys: the permutation ends in L.dval.
+int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
+  const int64_t vn = L.vn;
   uint32_t* perm = L.dval;
   if (vn > 0) {
     uint32_t* kres;
     int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, nullptr, vn, vn, 32, L.dsort, &kres, &perm,
                                          st, /*hist_ready=*/true);
     if (rc) return rc;
+    if (perm != L.dval) {
+      set_error("depth sort: unexpected result buffer");
+      return CGS_EINTERNAL;
+    }
     CGS_PROFILED("depth_tie_fix_kernel", st,
                  depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(kres, perm,
                                                                            L.depth_key, vn));
@@ -524,16 +546,38 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views,
                                           vn > 0 ? L.dsort.hist + 3 * 256 : nullptr, vn);
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
-  rc = L.tile_key_bytes == 2 ? emit_sort_range<uint16_t>(L, fd, L.psort16, perm, st)
-                             : emit_sort_range<uint32_t>(L, fd, L.psort32, perm, st);
-  if (rc) return rc;
+  return CGS_OK;
+}
+
+int frame_stage_duplicate(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
+  return L.tile_key_bytes == 2 ? emit_pairs_stage<uint16_t>(L, fd, L.psort16, L.dval, st)
+                               : emit_pairs_stage<uint32_t>(L, fd, L.psort32, L.dval, st);
+}
+
+int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
+  return L.tile_key_bytes == 2 ? sort_pairs_stage<uint16_t>(L, fd, L.psort16, st)
+                               : sort_pairs_stage<uint32_t>(L, fd, L.psort32, st);
+}
+
+int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, float* image, float* final_T,
+                       int32_t* counts, cudaStream_t st) {
   if (fd.total_tiles > 0) {
-    rc = launch_tile_order(fd, L, nullptr, st);
+    int rc = launch_tile_order(fd, L, nullptr, st);
     if (rc) return rc;
     rc = launch_raster_fwd(fd, L, sorted_pair_vals(L), image, final_T, counts, st);
     if (rc) return rc;
   }
   return CGS_OK;
+}
+
+int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, float* image,
+                  float* final_T, int32_t* counts, double* sr_cov, cudaStream_t st) {
+  int rc = frame_stage_project(sc, fd, L, sr_cov, st);
+  if (!rc) rc = frame_stage_sort_depth(fd, L, st);
+  if (!rc) rc = frame_stage_duplicate(fd, L, st);
+  if (!rc) rc = frame_stage_sort_pairs(fd, L, st);
+  if (!rc) rc = frame_stage_raster(fd, L, image, final_T, counts, st);
+  return rc;
 }
 
 }  // namespace cgs

@@ -103,6 +103,22 @@ class Frame:
         self._stats = None
         return self
 
+    FORWARD_STAGES = ("cgs_project", "cgs_sort_depth", "cgs_duplicate_tiles", "cgs_sort_pairs")
+
+    def run_staged(self):
+        """``run`` through the staged ABI, one entry point per stage (same results)."""
+        self.scene = scene_struct(self.state)
+        args = (ctypes.byref(self.scene), self.c_cams, len(self.cams), nat.ptr(self.ws),
+                self.ws.numel(), self.pair_cap)
+        h = nat.stream_handle(self.device)
+        for fn in self.FORWARD_STAGES:
+            nat.call(fn, *args, h)
+        nat.call("cgs_raster_fwd", *args, nat.ptr(self.image), nat.ptr(self.final_T),
+                 nat.ptr(self.counts), h)
+        self.token = self.state.token()
+        self._stats = None
+        return self
+
     def stats(self) -> nat.CFrameStats:
         if self._stats is None:
             st = nat.CFrameStats()
@@ -193,6 +209,30 @@ class Frame:
                  nat.ptr(sr_mem), nat.ptr(ws), ws.numel(), nat.ptr(grads.positions),
                  nat.ptr(grads.opacity_logits), nat.ptr(grads.sh_rows), nat.ptr(grads.sr_rows),
                  nat.stream_handle(dev))
+        return grads
+
+
+    def backward_staged(self, dL: torch.Tensor, scale: float = 1.0) -> "GradientSet":
+        """``backward`` through the staged ABI (raster, per-Gaussian reduce +
+        pull-back, codebook reduce; same results)."""
+        st = self.state
+        dev = self.device
+        grads = GradientSet.empty(st)
+        nb = backward_workspace_bytes(st, self)
+        ws = torch.empty((nb,), dtype=torch.uint8, device=dev)
+        self.scene = scene_struct(st)
+        sh_off, sh_mem = st.code_csr("sh")
+        sr_off, sr_mem = st.code_csr("sr")
+        args = (ctypes.byref(self.scene), self.c_cams, len(self.cams), nat.ptr(self.ws),
+                self.ws.numel(), self.pair_cap)
+        h = nat.stream_handle(dev)
+        nat.call("cgs_raster_bwd", *args, nat.ptr(self.final_T), nat.ptr(dL), nat.ptr(ws),
+                 ws.numel(), h)
+        nat.call("cgs_gaussian_reduce_pullback", *args, float(scale), nat.ptr(ws), ws.numel(),
+                 nat.ptr(grads.positions), nat.ptr(grads.opacity_logits), h)
+        nat.call("cgs_codebook_reduce", *args, float(scale), nat.ptr(sh_off), nat.ptr(sh_mem),
+                 nat.ptr(sr_off), nat.ptr(sr_mem), nat.ptr(ws), ws.numel(),
+                 nat.ptr(grads.sh_rows), nat.ptr(grads.sr_rows), h)
         return grads
 
 

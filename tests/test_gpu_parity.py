@@ -405,6 +405,29 @@ def _deep_stack_scene(seed=7, n=2400, size=48):
     return pos, logit, idx, idx, a.sh_rows, sr, cam
 
 
+def test_staged_abi_equals_fused(cg):
+    """The staged entry points (cgs_project ... cgs_raster_fwd, cgs_raster_bwd
+    ... cgs_codebook_reduce) reproduce cgs_render_forward / _backward bit for
+    bit on a config-1 frame (2 views, 256x256)."""
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config1(0)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    cams = a.cameras[:2]
+    fused = cg.Frame(st, cams).run_checked()
+    staged = cg.Frame(st, cams, pair_capacity=fused.pair_cap).run_staged()
+    for x in ("image", "final_T", "counts"):
+        assert torch.equal(getattr(fused, x), getattr(staged, x)), x
+    o1, i1 = fused.tile_lists()
+    o2, i2 = staged.tile_lists()
+    assert np.array_equal(o1, o2) and np.array_equal(i1, i2)
+    dL = torch.randn_like(fused.image) * 1e-3
+    g1 = fused.backward(dL, scale=0.5)
+    g2 = staged.backward_staged(dL, scale=0.5)
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        assert torch.equal(getattr(g1, k), getattr(g2, k)), k
+
+
 def test_deep_stack_chunked_backward_matches_oracle(cg):
     """Backward work units split a tile's processed prefix into 512-splat
     chunks started from the forward's per-pixel checkpoints (T and colour
