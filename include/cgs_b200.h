@@ -309,6 +309,21 @@ CGS_API int cgs_densify_select(const float* opacity_logits, int64_t n, const dou
                                int64_t k, int64_t* src, void* ws, size_t ws_bytes,
                                cgs_stream_t stream);
 
+/* ---- nearest code rows (code reassignment extension) ------------------ */
+/* No reference counterpart: the reference never recomputes assignments by
+ * distance.  For every live row i (indices
+ * `live`, n_live of them) of rows (capacity x dim, dim <= 64):
+ *   nn_index[i] = argmin over live j != i of sum_k fl(fl(r_ik - r_jk)^2)
+ *   (fp64, sequential in k, ties -> smaller j), nn_dist2[i] = that sum;
+ * -1 / 0 for rows that are not live (or when n_live < 2).  Candidates come
+ * from a tcgen05 tf32 distance GEMM; an fp64 check with a rounding bound
+ * (and an fp64 brute force for any row it cannot certify) makes the result
+ * exact. */
+CGS_API size_t cgs_code_nn_workspace_bytes(int64_t n_live, int32_t dim);
+CGS_API int cgs_code_nn(const float* rows, int32_t dim, int64_t capacity, const int32_t* live,
+                        int64_t n_live, int32_t* nn_index, double* nn_dist2, void* workspace,
+                        size_t workspace_bytes, cgs_stream_t stream);
+
 /* counts[r] = #{i : idx[i] == r} (validate_state, model.py:297). */
 CGS_API int cgs_refcount_histogram(const int32_t* idx, int64_t n, int32_t* counts, int64_t capacity,
                            cgs_stream_t stream);

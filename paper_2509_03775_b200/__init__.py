@@ -14,6 +14,7 @@ from .model import (Codebook, GaussianArrays, ModelState, densify, init_one_to_o
                     model_bytes, remap_gaussian, sh_dim, validate_state)
 from .render import (Frame, GradientSet, ProjectedSplat, RenderArtifacts, build_covariance,
                      project_gaussian, rasterize_backward, rasterize_forward, render_frame)
+from .reassign import mutual_pairs, nearest_codes, reassign_codes
 from .sampler import (MergeProposal, SamplerConfig, SamplerError, SplitProposal,
                       TransitionRecord, accept_merge, accept_split, acceptance_probability,
                       apply_merge, apply_split, choose_transition, propose_merge, propose_split,

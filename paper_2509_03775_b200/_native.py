@@ -81,6 +81,8 @@ SIGNATURES = {
     "cgs_frame_workspace_bytes": (SZ, [I64, CAMP, I32, I64, I64]),
     "cgs_render_forward": (I32, [SCNP, CAMP, I32, P, SZ, I64, P, P, P, P]),
     "cgs_frame_stats": (I32, [P, ctypes.POINTER(CFrameStats), P]),
+    "cgs_code_nn_workspace_bytes": (SZ, [I64, I32]),
+    "cgs_code_nn": (I32, [P, I32, I64, P, I64, P, P, P, SZ, P]),
     "cgs_project": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
     "cgs_sort_depth": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),
     "cgs_duplicate_tiles": (I32, [SCNP, CAMP, I32, P, SZ, I64, P]),

@@ -60,6 +60,8 @@ class Trainer:
         self.mcmc_events = 0
         self.mcmc_ms = []
         self.densify_ms = []
+        self.reassign_ms = []
+        self.reassigned = {"sh": 0, "sr": 0}
         self.capture_ms = []
         self.last_loss = None
         self.use_graphs = use_graphs
@@ -218,6 +220,13 @@ class Trainer:
             densify(st, c.densify_growth, c.gaussian_cap, self.rng, jitter_sigma=c.densify_jitter,
                     device_select=c.device_noise)
             self.densify_ms.append(1000.0 * (time.perf_counter() - t0))
+        if c.reassign_every > 0 and st.iteration % c.reassign_every == 0:
+            import time
+            from .reassign import reassign_codes
+            t0 = time.perf_counter()
+            for which in ("sh", "sr"):
+                self.reassigned[which] += reassign_codes(st, which, c.reassign_tau)
+            self.reassign_ms.append(1000.0 * (time.perf_counter() - t0))
 
     def mcmc(self):
         """One forced split and one forced merge transition (reference rules)."""

@@ -66,6 +66,11 @@ class SamplerConfig:
     exact_ratio: bool = False
     seed: int = 0
     device_noise: bool = False
+    # code reassignment extension (reassign.py; not in the reference): every
+    # reassign_every iterations merge mutual nearest code rows within
+    # squared distance reassign_tau.  0 = off (the reference's behaviour).
+    reassign_every: int = 0
+    reassign_tau: float = 0.0
 
     def validate(self) -> None:
         if abs(self.p_update + self.p_split + self.p_merge - 1.0) > 1e-12:
