@@ -312,11 +312,11 @@ CGS_API int cgs_densify_select(const float* opacity_logits, int64_t n, const dou
 /* ---- nearest code rows (code reassignment extension) ------------------ */
 /* No reference counterpart: the reference never recomputes assignments by
  * distance.  For every live row i (indices
- * `live`, n_live of them) of rows (capacity x dim, dim <= 64):
+ * `live`, n_live of them) of rows (capacity x dim, dim <= 48 = SH degree 3):
  *   nn_index[i] = argmin over live j != i of sum_k fl(fl(r_ik - r_jk)^2)
  *   (fp64, sequential in k, ties -> smaller j), nn_dist2[i] = that sum;
  * -1 / 0 for rows that are not live (or when n_live < 2).  Candidates come
- * from a tcgen05 tf32 distance GEMM; an fp64 check with a rounding bound
+ * from a tcgen05 3xTF32 distance GEMM; an fp64 check with a rounding bound
  * (and an fp64 brute force for any row it cannot certify) makes the result
  * exact. */
 CGS_API size_t cgs_code_nn_workspace_bytes(int64_t n_live, int32_t dim);

@@ -25,7 +25,7 @@ static NnLayout plan_nn(void* base, size_t cap_bytes, int64_t n_live, int d) {
   const int dp = nn_dpad(d);
   const int64_t mpad = (n_live + kNnN - 1) / kNnN * kNnN;
   const int64_t m1 = mpad > 0 ? mpad : kNnN;
-  L.packed = c.take<float>(m1 * dp);
+  L.packed = c.take<float>(2 * m1 * dp);  // tf32 heads, then tails
   L.norms = c.take<float>(m1);
   L.cand_d = c.take<float>(m1 * kNnCand);
   L.cand_j = c.take<int32_t>(m1 * kNnCand);
@@ -80,14 +80,14 @@ using namespace cgs;
 extern "C" {
 
 size_t cgs_code_nn_workspace_bytes(int64_t n_live, int32_t dim) {
-  if (n_live < 0 || dim < 1 || dim > 64) return 0;
+  if (n_live < 0 || dim < 1 || dim > 48) return 0;
   return plan_nn(nullptr, 0, n_live, dim).bytes;
 }
 
 int cgs_code_nn(const float* rows, int32_t dim, int64_t capacity, const int32_t* live,
                 int64_t n_live, int32_t* nn_index, double* nn_dist2, void* workspace,
                 size_t workspace_bytes, cgs_stream_t stream) {
-  if (!rows || !live || !nn_index || !nn_dist2 || dim < 1 || dim > 64 || n_live < 0 ||
+  if (!rows || !live || !nn_index || !nn_dist2 || dim < 1 || dim > 48 || n_live < 0 ||
       capacity < n_live || n_live >= (1LL << 31)) {
     set_error("code_nn: invalid arguments");
     return CGS_EINVAL;

@@ -12,12 +12,14 @@
 //     no-swizzle "core matrix" order (8 rows x 16 B per core matrix), row
 //     norms; padding rows get norm +inf.
 //  2. codenn_gemm: S = R R^T on the 5th-gen tensor cores (tcgen05.mma
-//     kind::tf32, M=128 x N=256 per instruction, accumulators in TMEM,
+//     kind::tf32 as 3xTF32 -- head/tail split, three MMAs per K step -- for
+//     ~fp32 accuracy; M=128 x N=128 per instruction, accumulators in TMEM,
 //     double-buffered), operand tiles brought in by the bulk-copy engine
-//     (one cp.async.bulk per 256-row tile: the packed order makes a tile
-//     contiguous).  Warp roles: 4 epilogue warps (TMEM lane quarter w), one
-//     producer, one MMA issuer.  The epilogue turns S into approximate
-//     distances n_i + n_j - 2 s_ij and keeps each row's kCand best.
+//     (one cp.async.bulk per 128-row tile and part: the packed order makes a
+//     tile contiguous).  Warp roles: 8 epilogue warps (TMEM lane quarter
+//     w % 4, column half w / 4), one producer, one MMA issuer.  The epilogue
+//     turns S into approximate distances n_i + n_j - 2 s_ij and keeps each
+//     row's kNnCand best.
 //  3. codenn_refine: exact fp64 distances of the candidates; accepted when
 //     the best exact distance is strictly below (kCand-th approximate
 //     distance - error bound), which no row outside the candidate set can
@@ -31,7 +33,7 @@
 namespace cgs {
 
 constexpr int kNnM = 128;       // rows per CTA (UMMA M)
-constexpr int kNnN = 256;       // columns per B tile (UMMA N)
+constexpr int kNnN = 128;       // columns per B tile (UMMA N)
 constexpr int kNnCand = 8;      // candidates kept per row
 constexpr int kNnStages = 2;    // B-tile smem stages
 constexpr int kNnThreads = 320; // 8 epilogue warps + producer + MMA
@@ -109,8 +111,10 @@ __device__ __forceinline__ void tmem_ld_wait() {
 
 // ---- 1. pack -----------------------------------------------------------------
 // live rows (indices `live`, n_live of them) of rows (cap x d, row stride d)
-// -> packed (mpad x dp, core-matrix order); norms (fp32 of the fp64 sum);
-// rows >= n_live are zero with norm +inf.
+// -> packed: two (mpad x dp) arrays in core-matrix order, the tf32 head
+// hi = rna_tf32(x) and the tail lo = x - hi (exact in fp32), for the 3xTF32
+// product hi hi' + hi lo' + lo hi' (error ~2^-20 |x||x'| instead of tf32's
+// 2^-10); norms (fp32 of the fp64 sum); rows >= n_live are zero with norm +inf.
 __global__ void codenn_pack_kernel(const float* __restrict__ rows, int d,
                                    const int32_t* __restrict__ live, int64_t n_live, int64_t mpad,
                                    int dp, float* __restrict__ packed, float* __restrict__ norms,
@@ -123,7 +127,11 @@ __global__ void codenn_pack_kernel(const float* __restrict__ rows, int d,
     for (int k = 0; k < dp; ++k) {
       const float x = (src && k < d) ? src[k] : 0.0f;
       nn += static_cast<double>(x) * x;
-      *reinterpret_cast<float*>(base + nn_packed_off(r, k, dp)) = x;
+      uint32_t hb;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+      const float hi = __uint_as_float(hb);
+      *reinterpret_cast<float*>(base + nn_packed_off(r, k, dp)) = hi;
+      *reinterpret_cast<float*>(base + mpad * dp * 4 + nn_packed_off(r, k, dp)) = x - hi;
     }
     norms[r] = r < n_live ? static_cast<float>(nn) : __int_as_float(0x7f800000);
     // non-negative floats order as their bit patterns
@@ -132,9 +140,13 @@ __global__ void codenn_pack_kernel(const float* __restrict__ rows, int d,
 }
 
 // ---- 2. tensor-core distance GEMM + per-row candidates ------------------------
+constexpr int kNnNormSlots = 4;  // column-norm ring, decoupled from the B stages
+
 struct NnSmem {
   uint64_t full[kNnStages];
   uint64_t empty[kNnStages];
+  uint64_t nfull[kNnNormSlots];
+  uint64_t nempty[kNnNormSlots];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t afull;
@@ -144,12 +156,13 @@ struct NnSmem {
 constexpr int kNnEpiWarps = 8;  // warp w: TMEM lanes [32 (w % 4), +32), column half w / 4
 constexpr int kNnChunk = 64;    // columns per TMEM read
 
-// Dynamic smem: [NnSmem | pad to 1024 | A tile (128 x dp) | B stages (256 x dp
-// each) | B-stage norms (256 each) | epilogue spill (64 x 256 floats) |
-// candidate merge (128 x 8 x 2 words)]
+// Dynamic smem: [NnSmem | pad to 1024 | A tile (hi, lo: 2 x 128 x dp) | B
+// stages (hi, lo: 2 x 128 x dp each) | B-stage norms (128 each) | epilogue
+// spill (64 x 256 floats) | candidate merge (128 x 8 x 2 words)]: 218 KB at
+// dp = 48, the widest row supported (SH degree 3).
 inline size_t codenn_gemm_smem(int dp) {
-  return 1024 + static_cast<size_t>(kNnM) * dp * 4 +
-         static_cast<size_t>(kNnStages) * (kNnN * dp * 4 + kNnN * 4) +
+  return 1024 + 2 * static_cast<size_t>(kNnM) * dp * 4 +
+         static_cast<size_t>(kNnStages) * 2 * kNnN * dp * 4 + kNnNormSlots * kNnN * 4 +
          static_cast<size_t>(kNnChunk) * 256 * 4 + static_cast<size_t>(kNnM) * kNnCand * 8;
 }
 
@@ -185,9 +198,9 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   NnSmem& S = *reinterpret_cast<NnSmem*>(smem_raw);
   float* sA = reinterpret_cast<float*>(smem_raw + 1024);
-  float* sB = sA + kNnM * dp;
-  float* sN = sB + static_cast<size_t>(kNnStages) * kNnN * dp;  // kNnStages x 256 norms
-  float* sV = sN + kNnStages * kNnN;                              // kNnChunk x 256 spill
+  float* sB = sA + 2 * kNnM * dp;                                   // stages x [hi | lo]
+  float* sN = sB + static_cast<size_t>(kNnStages) * 2 * kNnN * dp;  // kNnNormSlots x kNnN norms
+  float* sV = sN + kNnNormSlots * kNnN;  // kNnChunk x 256 (epilogue threads) spill
   float* sMd = sV + kNnChunk * 256;                               // 128 x kNnCand
   int* sMj = reinterpret_cast<int*>(sMd + kNnM * kNnCand);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -200,7 +213,11 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
   if (tid == 0) {
     for (int s = 0; s < kNnStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1 + kNnEpiWarps);  // MMA commit + every epilogue warp
+      mbar_init(&S.empty[s], 1);  // the MMA commit
+    }
+    for (int s = 0; s < kNnNormSlots; ++s) {
+      mbar_init(&S.nfull[s], 1);
+      mbar_init(&S.nempty[s], kNnEpiWarps);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&S.tfull[s], 1);
@@ -208,8 +225,8 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
     }
     mbar_init(&S.afull, 1);
   }
-  if (warp == kMma) {  // TMEM: 2 accumulator stages x 256 fp32 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+  if (warp == kMma) {  // TMEM: 2 accumulator stages x kNnN fp32 columns (256 allocated)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                      smem_u32(&S.tmem_base))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -222,18 +239,24 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
   if (warp == kProducer) {
     // ===== producer: A tile once, then B tiles (+ their norms) through the stages =====
     if (lane == 0) {
-      mbar_arrive_expect_tx(&S.afull, a_bytes);
+      const char* lo = reinterpret_cast<const char*>(packed) + mpad * dp * 4;
+      mbar_arrive_expect_tx(&S.afull, 2 * a_bytes);
       bulk_g2s(sA, reinterpret_cast<const char*>(packed) + row0 * dp * 4, a_bytes, &S.afull);
+      bulk_g2s(sA + kNnM * dp, lo + row0 * dp * 4, a_bytes, &S.afull);
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % kNnStages;
         const uint32_t ph = (t / kNnStages) & 1u;
         mbar_wait(&S.empty[s], ph ^ 1u);
         if (trace && blockIdx.x == 0 && t < 256) trace[4 * t + 3] = global_ns();
-        mbar_arrive_expect_tx(&S.full[s], b_bytes + kNnN * 4);
-        bulk_g2s(sB + static_cast<size_t>(s) * kNnN * dp,
-                 reinterpret_cast<const char*>(packed) + static_cast<int64_t>(t) * kNnN * dp * 4,
-                 b_bytes, &S.full[s]);
-        bulk_g2s(sN + s * kNnN, norms + static_cast<int64_t>(t) * kNnN, kNnN * 4, &S.full[s]);
+        mbar_arrive_expect_tx(&S.full[s], 2 * b_bytes);
+        float* dst = sB + static_cast<size_t>(s) * 2 * kNnN * dp;
+        const int64_t off = static_cast<int64_t>(t) * kNnN * dp * 4;
+        bulk_g2s(dst, reinterpret_cast<const char*>(packed) + off, b_bytes, &S.full[s]);
+        bulk_g2s(dst + kNnN * dp, lo + off, b_bytes, &S.full[s]);
+        const int ns = t % kNnNormSlots;
+        mbar_wait(&S.nempty[ns], ((t / kNnNormSlots) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&S.nfull[ns], kNnN * 4);
+        bulk_g2s(sN + ns * kNnN, norms + static_cast<int64_t>(t) * kNnN, kNnN * 4, &S.nfull[ns]);
       }
     }
   } else if (warp == kMma) {
@@ -250,12 +273,18 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
         mbar_wait(&S.full[s], ph);
         tmem_fence_after();
         if (trace && blockIdx.x == 0 && t < 256) trace[4 * t] = global_ns();
-        const uint32_t a0 = smem_u32(sA);
-        const uint32_t b0 = smem_u32(sB + static_cast<size_t>(s) * kNnN * dp);
+        const uint32_t a0 = smem_u32(sA), a1 = smem_u32(sA + kNnM * dp);
+        const uint32_t b0 = smem_u32(sB + static_cast<size_t>(s) * 2 * kNnN * dp);
+        const uint32_t b1 = b0 + static_cast<uint32_t>(kNnN * dp * 4);
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * kNnN);
         for (int ks = 0; ks < dp / 8; ++ks) {  // K step of 8 tf32 = two 16-B core matrices
-          const uint64_t ad = umma_desc(a0 + ks * 256u, 128u, sbo);
-          const uint64_t bd = umma_desc(b0 + ks * 256u, 128u, sbo);
-          umma_tf32(tmem + static_cast<uint32_t>(acc * kNnN), ad, bd, idesc, ks > 0 ? 1u : 0u);
+          const uint64_t ah = umma_desc(a0 + ks * 256u, 128u, sbo);
+          const uint64_t al = umma_desc(a1 + ks * 256u, 128u, sbo);
+          const uint64_t bh = umma_desc(b0 + ks * 256u, 128u, sbo);
+          const uint64_t bl = umma_desc(b1 + ks * 256u, 128u, sbo);
+          umma_tf32(d, ah, bh, idesc, ks > 0 ? 1u : 0u);  // 3xTF32: hi hi' + hi lo' + lo hi'
+          umma_tf32(d, ah, bl, idesc, 1u);
+          umma_tf32(d, al, bh, idesc, 1u);
         }
         umma_commit(&S.empty[s]);    // B operand consumed once these MMAs complete
         umma_commit(&S.tfull[acc]);  // accumulator ready
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
     }
   } else {
     // ===== epilogue: warp w reads TMEM lanes [32 (w % 4), +32) (its tile rows),
-    // columns [128 (w / 4), +128) of each tile =====
+    // columns [kNnN / 2 (w / 4), +kNnN / 2) of each tile =====
     const int quarter = warp & 3, half = warp >> 2;
     const int r = quarter * 32 + lane;
     const int64_t gi = row0 + r;
@@ -276,15 +305,16 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
       bj[k] = -1;
     }
     for (int t = 0; t < n_tiles; ++t) {
-      const int acc = t & 1, s = t % kNnStages;
+      const int acc = t & 1, ns = t % kNnNormSlots;
+      mbar_wait(&S.nfull[ns], (t / kNnNormSlots) & 1u);
       mbar_wait(&S.tfull[acc], (t >> 1) & 1u);
       tmem_fence_after();
       if (trace && blockIdx.x == 0 && t < 256 && tid == 0) trace[4 * t + 1] = global_ns();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
-                             static_cast<uint32_t>(acc * kNnN + half * 128);
+                             static_cast<uint32_t>(acc * kNnN + half * (kNnN / 2));
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += kNnChunk) {
-        const int cl = half * 128 + c0;  // column within the tile
+      for (int c0 = 0; c0 < kNnN / 2; c0 += kNnChunk) {
+        const int cl = half * (kNnN / 2) + c0;  // column within the tile
         const int64_t j0 = static_cast<int64_t>(t) * kNnN + cl;
         float v[kNnChunk];
 #pragma unroll
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
 #pragma unroll
           for (int k = 0; k < kNnChunk; ++k) debug_s[gi * mpad + j0 + k] = v[k];
         }
-        const float4* n4 = reinterpret_cast<const float4*>(sN + s * kNnN + cl);  // broadcast
+        const float4* n4 = reinterpret_cast<const float4*>(sN + ns * kNnN + cl);  // broadcast
 #pragma unroll
         for (int q = 0; q < kNnChunk / 4; ++q) {
           const float4 f = n4[q];
@@ -338,7 +368,7 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
       if (trace && blockIdx.x == 0 && t < 256 && tid == 0) trace[4 * t + 2] = global_ns();
       if (lane == 0) {
         mbar_arrive(&S.tempty[acc]);
-        mbar_arrive(&S.empty[s]);  // done with this stage's norms
+        mbar_arrive(&S.nempty[ns]);  // done with this tile's norms
       }
     }
     // merge the two column halves of each row
@@ -364,7 +394,7 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
   __syncthreads();
   if (warp == kMma) {
     tmem_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -383,11 +413,13 @@ __device__ __forceinline__ double nn_dist64(const float* __restrict__ rows, int 
 
 // One thread per live row: exact distances of the candidates; rows whose
 // candidate set is not provably complete are appended to `redo`.
-// Error bound of an approximate distance n_i + n_j - 2 s~_ij: tf32 operands
-// (relative error <= 2^-10 each) and fp32 accumulation over <= 64 terms give
-// |s~ - s| <= 2^-8.9 |a| |b|, the fp32 norms and the final fma add
-// <= 2^-22 (n_i + n_j + 2 |a| |b|); with |b| <= max |row| the bound used,
-// 1e-2 |a| M + 1e-6 (n_i + M^2), is above both for every j.
+// Error bound of an approximate distance n_i + n_j - 2 s~_ij: the 3xTF32
+// product drops lo lo' (<= 2^-22 |ab|) and reads lo truncated to tf32
+// (<= 2^-21 |ab| per term), and accumulates 3 x 64 products in fp32
+// (<= 2^-16 sum |ab|), so |s~ - s| <= 2^-15 |a| |b|; the fp32 norms and the
+// final fma add <= 2^-22 (n_i + n_j + 2 |a| |b|).  With |b| <= M = max |row|
+// the bound used, 2e-4 |a| M + 1e-6 (n_i + M^2), is ~3x above both for
+// every j (tests/test_gpu_codenn.py measures the product error).
 __global__ void codenn_refine_kernel(const float* __restrict__ rows, int d,
                                      const int32_t* __restrict__ live, int64_t n_live,
                                      const float* __restrict__ norms,
@@ -416,7 +448,7 @@ __global__ void codenn_refine_kernel(const float* __restrict__ rows, int d,
     // with an outside row would need the index rule)
     const double m2 = static_cast<double>(__uint_as_float(*max_norm_bits));
     const double ni = static_cast<double>(norms[i]);
-    const double bound = 1e-2 * sqrt(ni) * sqrt(m2) + 1e-6 * (ni + m2) + 1e-30;
+    const double bound = 2e-4 * sqrt(ni) * sqrt(m2) + 1e-6 * (ni + m2) + 1e-30;
     const float last = cand_d[i * kNnCand + kNnCand - 1];
     const bool full_set = n_live - 1 <= kNnCand;  // every other row is a candidate
     if (bidx >= 0 && (full_set || static_cast<double>(last) - bound > best)) {
