@@ -47,12 +47,11 @@ def nearest_codes(state: ModelState, which: str):
 
 def mutual_pairs(nn_index: np.ndarray, nn_dist2: np.ndarray, tau: float) -> list:
     """(parent i, child j) for every mutual nearest pair i < j with d <= tau."""
-    out = []
-    for i in np.nonzero(nn_index >= 0)[0]:
-        j = int(nn_index[i])
-        if j > i and nn_index[j] == i and nn_dist2[i] <= tau:
-            out.append((int(i), j))
-    return out
+    nn = np.asarray(nn_index)
+    i = np.arange(nn.shape[0])
+    j = np.where(nn >= 0, nn, 0)
+    keep = (nn > i) & (nn[j] == i) & (np.asarray(nn_dist2) <= tau)
+    return [(int(a), int(b)) for a, b in zip(i[keep], nn[keep])]
 
 
 def reassign_codes(state: ModelState, which: str, tau: float) -> int:
