@@ -67,3 +67,30 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     assert rc == _native.CGS_EINVAL
     with pytest.raises(ValueError):
         _native.check(rc)
+
+
+def test_staged_and_code_nn_validation_without_gpu(lib):
+    """The staged entry points and cgs_code_nn validate before any CUDA call."""
+    from paper_2509_03775_b200 import _native
+    from paper_2509_03775_b200.camera import ring_cameras
+    L = _native.library()
+    cams = _native.cams_array(ring_cameras(1, (0, 0, 0), 3.0, 0.0, 64, 64, 64))
+    bad = _native.CScene()
+    bad.sh_degree = 7
+    for fn in ("cgs_project", "cgs_sort_depth", "cgs_duplicate_tiles", "cgs_sort_pairs"):
+        assert getattr(L, fn)(ctypes.byref(bad), cams, 1, None, 0, 1000, None) == _native.CGS_EINVAL
+    assert L.cgs_raster_fwd(ctypes.byref(bad), cams, 1, None, 0, 1000, None, None, None,
+                            None) == _native.CGS_EINVAL
+    assert L.cgs_raster_bwd(ctypes.byref(bad), cams, 1, None, 0, 1000, None, None, None, 0,
+                            None) == _native.CGS_EINVAL
+    assert L.cgs_gaussian_reduce_pullback(ctypes.byref(bad), cams, 1, None, 0, 1000, 1.0, None,
+                                          0, None, None, None) == _native.CGS_EINVAL
+    assert L.cgs_codebook_reduce(ctypes.byref(bad), cams, 1, None, 0, 1000, 1.0, None, None,
+                                 None, None, None, 0, None, None, None) == _native.CGS_EINVAL
+    assert L.cgs_project(ctypes.byref(bad), cams, 17, None, 0, 1000, None) == _native.CGS_EINVAL
+    # code_nn: widths 1..48 (SH degree 3), non-null arrays
+    assert L.cgs_code_nn_workspace_bytes(1000, 48) > 0
+    assert L.cgs_code_nn_workspace_bytes(1000, 49) == 0
+    assert L.cgs_code_nn_workspace_bytes(1000, 0) == 0
+    assert L.cgs_code_nn(None, 48, 10, None, 5, None, None, None, 0, None) == _native.CGS_EINVAL
+    assert "code_nn" in _native.last_error()
