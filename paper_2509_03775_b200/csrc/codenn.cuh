@@ -34,7 +34,7 @@ namespace cgs {
 
 constexpr int kNnM = 128;       // rows per CTA (UMMA M)
 constexpr int kNnN = 128;       // columns per B tile (UMMA N)
-constexpr int kNnCand = 8;      // candidates kept per row
+constexpr int kNnCand = 4;      // candidates kept per row
 constexpr int kNnStages = 2;    // B-tile smem stages
 constexpr int kNnThreads = 320; // 8 epilogue warps + producer + MMA
 
@@ -158,12 +158,12 @@ constexpr int kNnChunk = 64;    // columns per TMEM read
 
 // Dynamic smem: [NnSmem | pad to 1024 | A tile (hi, lo: 2 x 128 x dp) | B
 // stages (hi, lo: 2 x 128 x dp each) | B-stage norms (128 each) | epilogue
-// spill (64 x 256 floats) | candidate merge (128 x 8 x 2 words)]: 218 KB at
+// compaction slots (2 x 32 x 256 words) | candidate merge (128 x 4 x 2 words)]: 213 KB at
 // dp = 48, the widest row supported (SH degree 3).
 inline size_t codenn_gemm_smem(int dp) {
   return 1024 + 2 * static_cast<size_t>(kNnM) * dp * 4 +
          static_cast<size_t>(kNnStages) * 2 * kNnN * dp * 4 + kNnNormSlots * kNnN * 4 +
-         static_cast<size_t>(kNnChunk) * 256 * 4 + static_cast<size_t>(kNnM) * kNnCand * 8;
+         2 * static_cast<size_t>(32) * 256 * 4 + static_cast<size_t>(kNnM) * kNnCand * 8;
 }
 
 __device__ __forceinline__ void nn_insert(float d, int j, float (&bd)[kNnCand], int (&bj)[kNnCand]) {
@@ -200,8 +200,9 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
   float* sA = reinterpret_cast<float*>(smem_raw + 1024);
   float* sB = sA + 2 * kNnM * dp;                                   // stages x [hi | lo]
   float* sN = sB + static_cast<size_t>(kNnStages) * 2 * kNnN * dp;  // kNnNormSlots x kNnN norms
-  float* sV = sN + kNnNormSlots * kNnN;  // kNnChunk x 256 (epilogue threads) spill
-  float* sMd = sV + kNnChunk * 256;                               // 128 x kNnCand
+  float* sV = sN + kNnNormSlots * kNnN;  // 32 x 256 (epilogue threads) compaction slots
+  int* sVi = reinterpret_cast<int*>(sV + 32 * 256);       // 32 x 256 column ids
+  float* sMd = reinterpret_cast<float*>(sVi + 32 * 256);  // 128 x kNnCand
   int* sMj = reinterpret_cast<int*>(sMd + kNnM * kNnCand);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kNnM;
@@ -325,13 +326,15 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
           for (int k = 0; k < kNnChunk; ++k) debug_s[gi * mpad + j0 + k] = v[k];
         }
         const float4* n4 = reinterpret_cast<const float4*>(sN + ns * kNnN + cl);  // broadcast
+        // row-relative distance n_j - 2 s_ij (n_i is the same for the whole row;
+        // it is added to the candidates at the end)
 #pragma unroll
         for (int q = 0; q < kNnChunk / 4; ++q) {
           const float4 f = n4[q];
-          v[4 * q] = fmaf(-2.0f, v[4 * q], ni + f.x);  // approximate squared distance
-          v[4 * q + 1] = fmaf(-2.0f, v[4 * q + 1], ni + f.y);
-          v[4 * q + 2] = fmaf(-2.0f, v[4 * q + 2], ni + f.z);
-          v[4 * q + 3] = fmaf(-2.0f, v[4 * q + 3], ni + f.w);
+          v[4 * q] = fmaf(-2.0f, v[4 * q], f.x);
+          v[4 * q + 1] = fmaf(-2.0f, v[4 * q + 1], f.y);
+          v[4 * q + 2] = fmaf(-2.0f, v[4 * q + 2], f.z);
+          v[4 * q + 3] = fmaf(-2.0f, v[4 * q + 3], f.w);
         }
         if (gi >= j0 && gi < j0 + kNnChunk) {  // the diagonal: never its own neighbour
 #pragma unroll
@@ -347,19 +350,22 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
 #pragma unroll
           for (int k = 0; k < w; ++k) m[k] = fminf(m[2 * k], m[2 * k + 1]);
         if (m[0] < bd[kNnCand - 1]) {
-          // qualifying columns through shared memory (dynamic index without
-          // local memory; [k][thread] layout, conflict-free)
-          const float thr = bd[kNnCand - 1];
-          unsigned long long mask = 0;
+          // compact the qualifying columns into this thread's shared-memory
+          // slots ([slot][thread], conflict-free), then insert them in order
 #pragma unroll
-          for (int k = 0; k < kNnChunk; ++k) {
-            sV[k * 256 + tid] = v[k];
-            mask |= static_cast<unsigned long long>(v[k] < thr ? 1u : 0u) << k;
-          }
-          while (mask) {
-            const int k = __ffsll(static_cast<long long>(mask)) - 1;
-            mask &= mask - 1;
-            nn_insert(sV[k * 256 + tid], static_cast<int>(j0 + k), bd, bj);
+          for (int h = 0; h < kNnChunk / 32; ++h) {  // 32 slots per thread
+            const float thr = bd[kNnCand - 1];
+            int cnt = 0;
+#pragma unroll
+            for (int k = 32 * h; k < 32 * h + 32; ++k) {
+              if (v[k] < thr) {
+                sV[cnt * 256 + tid] = v[k];
+                sVi[cnt * 256 + tid] = k;
+                ++cnt;
+              }
+            }
+            for (int q = 0; q < cnt; ++q)
+              nn_insert(sV[q * 256 + tid], static_cast<int>(j0 + sVi[q * 256 + tid]), bd, bj);
           }
         }
       }
@@ -384,8 +390,8 @@ __global__ void __launch_bounds__(kNnThreads, 1) codenn_gemm_kernel(
 #pragma unroll
       for (int k = 0; k < kNnCand; ++k) nn_insert(sMd[r * kNnCand + k], sMj[r * kNnCand + k], bd, bj);
 #pragma unroll
-      for (int k = 0; k < kNnCand; ++k) {
-        cand_d[gi * kNnCand + k] = bd[k];
+      for (int k = 0; k < kNnCand; ++k) {  // + n_i: monotone, so the order is kept
+        cand_d[gi * kNnCand + k] = bd[k] + ni;
         cand_j[gi * kNnCand + k] = bj[k];
       }
     }
