@@ -65,6 +65,8 @@ def main():
         print(f"== {name[:110]}")
         for k, label in KEYS:
             v = d.get(k)
+            if v is None:  # some sections prefix the metric name (e.g. "TPC.TriageCompute.")
+                v = next((x for kk, x in d.items() if kk.endswith("." + k)), None)
             if v is None or v == "":
                 continue
             print(f"  {label:24s} {v} {u.get(k, '')}")
