@@ -646,18 +646,38 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_gt = (gts * 255.0).round().to(torch.uint8).cpu().pin_memory()
-        dev_gt = torch.empty(host_gt.shape, dtype=torch.uint8, device=dev)
+        # double-buffered device targets: step k+1's upload runs on a copy
+        # stream while step k computes (the first upload is inside step 0's
+        # interval, every later one inside the previous step's)
+        dev_gt = [torch.empty(host_gt.shape, dtype=torch.uint8, device=dev) for _ in range(2)]
+        copy_st = torch.cuda.Stream(dev)
+        up_done = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
         host_loss = torch.empty((3 * len(cams),), dtype=torch.float64).pin_memory()
         e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        cur = torch.cuda.current_stream(dev)
+
+        def upload(b):
+            copy_st.wait_event(used[b])
+            with torch.cuda.stream(copy_st):
+                dev_gt[b].copy_(host_gt, non_blocking=True)
+                up_done[b].record(copy_st)
+
         barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
             if not args.no_flush:
                 flush.zero_()
             e_s[k].record()
-            dev_gt.copy_(host_gt, non_blocking=True)
-            torch.mul(dev_gt, 1.0 / 255.0, out=tr.gts)  # uint8 -> [0, 1] on the device
+            b = k & 1
+            if k == 0:
+                upload(b)
+            cur.wait_event(up_done[b])
+            torch.mul(dev_gt[b], 1.0 / 255.0, out=tr.gts)  # uint8 -> [0, 1] on the device
+            used[b].record(cur)
+            if k + 1 < args.steps:
+                upload(b ^ 1)
             tr.step()
             host_loss.copy_(tr.last_loss, non_blocking=True)
             e_e[k].record()
