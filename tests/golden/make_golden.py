@@ -441,8 +441,40 @@ def make_exact():
           "attempts", [int(out[f"s{i + 1}_rec"][0]) for i in range(len(schedule))])
 
 
+def make_train():
+    """train() (sampler.py:402-420) end to end on config 0: the reference's own
+    loop with a mixed transition schedule (updates, splits, merges drawn by
+    choose_transition), densify every 5 iterations and PSNR evaluation every
+    4; records every TransitionRecord and the final state."""
+    out = {}
+    a, g = scenes.config0(0), scenes.config0(1)
+    cam = to_rcam(a.cameras[0])
+    gt = rrender.rasterize_forward(ref_state(g), cam).image
+    cfg = rsampler.SamplerConfig.for_synthetic_fixture(seed=7)
+    cfg.p_update, cfg.p_split, cfg.p_merge = 0.6, 0.2, 0.2
+    cfg.lambda_sh = cfg.lambda_sr = 0.0   # with eps_s == eps_m: every move accepted
+    cfg.eps_merge_sh, cfg.eps_merge_sr = cfg.eps_split_sh, cfg.eps_split_sr
+    cfg.densify_every, cfg.gaussian_cap = 5, 4400
+    st = ref_state(a)
+    state_arrays(st, "s0_", out)
+    out["gt"] = gt
+    for k, v in _cfg_arrays(cfg).items():
+        out[f"cfg_{k}"] = np.asarray(v)
+    recs = rsampler.train(st, [(cam, gt)], cfg, 16, rng=np.random.default_rng(11), eval_every=4,
+                          check_invariants=True)
+    out["kinds"] = np.array([r.kind for r in recs])
+    out["codebooks"] = np.array([r.codebook for r in recs])
+    out["ints"] = np.array([[r.iteration, r.attempts, r.accepts, r.live_sh, r.live_sr]
+                            for r in recs], dtype=np.int64)
+    out["floats"] = np.array([[r.recon, r.psnr] for r in recs], dtype=np.float64)
+    state_arrays(st, "s1_", out)
+    np.savez_compressed(os.path.join(OUT, "train.npz"), **out)
+    print("train written", list(out["kinds"]))
+
+
 MAKERS = {"loss_sh": make_loss_sh, "sgld": make_sgld, "mcmc": make_mcmc, "render": make_render,
-          "gradcheck": make_gradcheck, "modelio": make_modelio, "exact": make_exact}
+          "gradcheck": make_gradcheck, "modelio": make_modelio, "exact": make_exact,
+          "train": make_train}
 
 if __name__ == "__main__":
     print("numpy", np.__version__)

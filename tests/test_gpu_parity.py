@@ -228,6 +228,42 @@ def test_mcmc_chain_bit_exact(cg, chain):
     assert np.array_equal(rng.random(4), d[f"{chain}_rng_after"])
 
 
+def test_train_loop_matches_reference(cg):
+    """train() (sampler.py:402-420) for 16 iterations on config 0 against the
+    reference's own run (tests/golden/train.npz): a mixed schedule of updates,
+    splits and merges drawn by choose_transition, densify every 5 and PSNR
+    every 4.  Discrete outcomes (transition kinds, codebooks, attempts,
+    accepts, live counts, final assignments / refcounts / lineage / free
+    lists) are bit-exact; recon and PSNR, and the final float state after
+    ten fp32-gradient SGLD updates, within tolerance."""
+    from gpu_helpers import state_from
+    d = golden("train")
+    st = state_from(d, "s0_")
+    kw = {k[len("cfg_"):]: (v.item() if v.shape == () else v) for k, v in d.items()
+          if k.startswith("cfg_")}
+    cfg = cg.SamplerConfig(**kw)
+    cam = cg.ring_cameras(1, (0, 0, 0), 3.0, 0.0, 64, 64, 64)[0]
+    recs = cg.train(st, [(cam, d["gt"])], cfg, 16, rng=np.random.default_rng(11), eval_every=4,
+                    check_invariants=True)
+    assert [r.kind for r in recs] == [str(k) for k in d["kinds"]]
+    assert [r.codebook for r in recs] == [str(k) for k in d["codebooks"]]
+    assert np.array_equal(np.array([[r.iteration, r.attempts, r.accepts, r.live_sh, r.live_sr]
+                                    for r in recs]), d["ints"])
+    got = np.array([[r.recon, r.psnr] for r in recs], dtype=np.float64)
+    want = d["floats"]
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert np.allclose(got[:, 0][ok[:, 0]], want[:, 0][ok[:, 0]], rtol=1e-4, atol=1e-7)
+    assert np.allclose(got[:, 1][ok[:, 1]], want[:, 1][ok[:, 1]], rtol=0, atol=2e-3)  # dB
+    h = st.to_host()
+    for k in ("g2sh", "g2sr", "sh_refcount", "sr_refcount", "sh_parent", "sr_parent", "sh_free",
+              "sr_free"):
+        assert np.array_equal(h[k], d["s1_" + k]), k
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        assert np.allclose(h[k], d["s1_" + k], rtol=1e-4, atol=1e-5), (
+            k, np.abs(h[k] - d["s1_" + k]).max())
+
+
 def test_densify_bit_exact(cg):
     from gpu_helpers import assert_state_equal, state_from
     d = golden("mcmc")
