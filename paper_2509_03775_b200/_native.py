@@ -13,7 +13,8 @@ import os
 
 from .camera import CCamera
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcgs_b200.so")
+LIB_PATH = os.environ.get("CGS_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libcgs_b200.so")  # override: tuning variants
 
 CGS_OK, CGS_EINVAL, CGS_ECUDA, CGS_EWORKSPACE, CGS_ENONFINITE = 0, 1, 2, 3, 4
 MAX_VIEWS = 16

@@ -148,7 +148,10 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
   return m;
 }
 
-__global__ void __launch_bounds__(256, 6) raster_fwd_kernel(
+#ifndef CGS_FWD_MINB
+#define CGS_FWD_MINB 6
+#endif
+__global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
@@ -361,7 +364,12 @@ __device__ __forceinline__ void moments_to_grad(const float* m, float e1x, float
 // quadrant and k < the warp's last index); each warp walks its ordered hit
 // list backwards and stores its 9 reduced values per hit in its own s_red
 // slice; the combine sums the present warps in fixed order.
-constexpr int kBwdBatch = 128;
+#ifndef CGS_BWD_BATCH
+#define CGS_BWD_BATCH 64
+#endif
+constexpr int kBwdBatch = CGS_BWD_BATCH;
+static_assert(kBwdBatch % 32 == 0 && kChunk % kBwdBatch == 0 && kBwdBatch <= 256,
+              "batch: whole ballots, whole batches per chunk, u8 hit-list entries");
 
 // Backward work units: chunk c of tile t covers splats [c kChunk, min((c+1)
 // kChunk, nproc_t)).  Sorted by length, longest first (counting sort in one

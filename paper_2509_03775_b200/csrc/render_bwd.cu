@@ -245,7 +245,10 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
 // splats processed in every tile) are walked by the whole warp.  The sum
 // order is fixed, so the result is deterministic.
 template <int DEG>
-__global__ void __launch_bounds__(256) splat_reduce_kernel(PairWalk pw, const FrameHeader* __restrict__ fh,
+#ifndef CGS_SR_MINB
+#define CGS_SR_MINB 1
+#endif
+__global__ void __launch_bounds__(256, CGS_SR_MINB) splat_reduce_kernel(PairWalk pw, const FrameHeader* __restrict__ fh,
                                                            FrameDesc fd, int64_t n, int64_t vn,
                                                            GaussIn g, BwdLayout B) {
   if (fh->stats.overflow) return;
