@@ -16,7 +16,10 @@ constexpr uint32_t kLongSplat = 256;
 // (independent CTAs); the forward leaves each pixel's transmittance and
 // colour suffix at every chunk boundary it passes (ckpt).  kChunk is a
 // multiple of the forward's 256-splat batch.
-constexpr int kChunk = 512;
+#ifndef CGS_CHUNK
+#define CGS_CHUNK 256
+#endif
+constexpr int kChunk = CGS_CHUNK;
 
 // Checkpoint slot of boundary j >= 1 (splat index j * kChunk) of a tile whose
 // list starts at pair position `start`: distinct over all (tile, j) with

@@ -424,7 +424,7 @@ def test_near_plane_giants_match_oracle(cg):
 
 def _deep_stack_scene(seed=7, n=2400, size=48):
     """Thousands of faint, wide Gaussians stacked in depth over 9 tiles: the
-    processed prefixes span several backward chunks (kChunk = 512 splats),
+    processed prefixes span several backward chunks (kChunk = 256 splats),
     pixels terminate inside and across chunks, some never do."""
     from paper_2509_03775_b200 import camera, scenes
     a = scenes.config0(seed)
@@ -465,7 +465,7 @@ def test_staged_abi_equals_fused(cg):
 
 
 def test_deep_stack_chunked_backward_matches_oracle(cg):
-    """Backward work units split a tile's processed prefix into 512-splat
+    """Backward work units split a tile's processed prefix into 256-splat
     chunks started from the forward's per-pixel checkpoints (T and colour
     suffix): image, T, counts and gradients match the oracle."""
     from gpu_helpers import group_rel
