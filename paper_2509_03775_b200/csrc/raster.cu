@@ -44,7 +44,9 @@ __device__ __forceinline__ bool quad_hit(uint32_t rc, int qx, int qy) {
 __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges,
                                                           const uint32_t* __restrict__ nproc,
                                                           int total_tiles,
-                                                          uint32_t* __restrict__ order) {
+                                                          uint32_t* __restrict__ order,
+                                                          uint32_t* __restrict__ zero_a,
+                                                          uint32_t* __restrict__ zero_b) {
   __shared__ uint32_t cnt[256];
   const int tid = threadIdx.x;
   auto bucket = [&](int t) -> uint32_t {
@@ -77,6 +79,8 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
   }
   __syncthreads();
   for (int t = tid; t < total_tiles; t += blockDim.x) order[atomicAdd(&cnt[bucket(t)], 1u)] = t;
+  if (zero_a)  // the forward's per-tile maxima start from 0 (split tiles combine with atomicMax)
+    for (int t = tid; t < total_tiles; t += blockDim.x) zero_a[t] = zero_b[t] = 0u;
 }
 
 struct PixState {
@@ -148,10 +152,24 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
   return m;
 }
 
-#ifndef CGS_FWD_MINB
-#define CGS_FWD_MINB 6
+// HALVES = 2 splits every tile over two CTAs of 128 threads (rows 0-7 and
+// 8-15, batches of 128 splats): a tile's blend is sequential in its list, so
+// one CTA per tile makes the longest list the kernel's floor; two CTAs halve
+// it for the price of staging each record twice.  Per-tile results (processed
+// count, last rank) are combined with atomicMax (zeroed by tile_order_kernel).
+#ifndef CGS_FWD_HALVES
+#define CGS_FWD_HALVES 1
 #endif
-__global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
+#ifndef CGS_FWD_MINB
+#define CGS_FWD_MINB (CGS_FWD_HALVES == 2 ? 12 : 6)
+#endif
+constexpr int kFwdHalves = CGS_FWD_HALVES;
+constexpr int kFwdThreads = 256 / kFwdHalves;  // one pixel per thread
+constexpr int kFwdBatch = 256 / kFwdHalves;
+constexpr int kFwdWarps = kFwdThreads / 32;
+static_assert(kChunk % kFwdBatch == 0, "checkpoints sit on batch boundaries");
+
+__global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     const FrameHeader* __restrict__ hdr, float* __restrict__ image,
@@ -159,24 +177,27 @@ __global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
     uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
     uint32_t* __restrict__ last_rank, float4* __restrict__ ckpt,
     unsigned long long* __restrict__ trace) {
+  constexpr int B = kFwdBatch, NT = kFwdThreads;
   const unsigned long long t_start = trace ? global_ns() : 0ull;
-  __shared__ __align__(128) SplatRec s_raw[256];
-  __shared__ float4 s_a[256];
-  __shared__ float4 s_b[256];
-  __shared__ float2 s_c[256];
-  __shared__ uint8_t s_mask[256];
-  __shared__ uint8_t s_list[8][256];
-  __shared__ uint32_t s_max[8];
+  __shared__ __align__(128) SplatRec s_raw[B];
+  __shared__ float4 s_a[B];
+  __shared__ float4 s_b[B];
+  __shared__ float2 s_c[B];
+  __shared__ uint8_t s_mask[B];
+  __shared__ uint8_t s_list[kFwdWarps][B];
+  __shared__ uint32_t s_max[kFwdWarps];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
-  const int tile = static_cast<int>(order[blockIdx.x]);
+  const int half = kFwdHalves == 2 ? static_cast<int>(blockIdx.x & 1u) : 0;
+  const int tile = static_cast<int>(order[blockIdx.x / kFwdHalves]);
   int v = 0;
   while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
   const CamDev& cam = fd.cam[v];
   const int lt = tile - cam.tile_base;
   const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+  const int wb = warp + half * kFwdWarps;  // 8x4 block index within the tile
+  const int lx = (wb & 1) * 8 + (lane & 7), ly = (wb >> 1) * 4 + (lane >> 3);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool in = px < cam.width && py < cam.height;
   const uint2 rg = ranges[tile];
@@ -192,11 +213,11 @@ __global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
   uint32_t phase = 0;
   bool pending = false;
   if (n > 0) {
-    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(256, n), tid, 256);
+    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(B, n), tid, NT);
     pending = true;
   }
-  for (int b0 = 0; b0 < n; b0 += 256) {
-    const int nb = min(256, n - b0);
+  for (int b0 = 0; b0 < n; b0 += B) {
+    const int nb = min(B, n - b0);
     mbar_wait(&s_bar, phase);
     phase ^= 1;
     pending = false;
@@ -205,15 +226,16 @@ __global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
       s_a[tid] = sg.a;
       s_b[tid] = sg.b;
       s_c[tid] = sg.c;
-      s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
+      const uint32_t m8 = block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile));
+      s_mask[tid] = static_cast<uint8_t>(m8 >> (half * kFwdWarps));
     }
     __syncthreads();
-    if (b0 + 256 < n) {
+    if (b0 + B < n) {
       fence_proxy_async_smem();
-      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + 256, min(256, n - b0 - 256), tid, 256);
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + B, min(B, n - b0 - B), tid, NT);
       pending = true;
     }
-    const int hits = warp_hit_list<256>(s_mask, nb, warp, lane, my_list);
+    const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
     if (!p.done) {
       for (int i = 0; i < hits; ++i) {
         const int j = my_list[i];
@@ -228,10 +250,10 @@ __global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
         }
       }
     }
-    if (__syncthreads_count(p.done) == 256) break;
-    if (b0 + 256 < n && ((b0 + 256) % kChunk) == 0) {  // chunk boundary for the backward
+    if (__syncthreads_count(p.done) == NT) break;
+    if (b0 + B < n && ((b0 + B) % kChunk) == 0) {  // chunk boundary for the backward
       // T after the chunk and the chunk's own colour sum; colour restarts at 0
-      ckpt[ckpt_slot(rg.x, tile, (b0 + 256) / kChunk) * kTilePixels + ly * kTile + lx] =
+      ckpt[ckpt_slot(rg.x, tile, (b0 + B) / kChunk) * kTilePixels + ly * kTile + lx] =
           make_float4(p.T, p.r, p.g, p.b);
       p.r = p.g = p.b = 0.0f;
       ++n_ckpt;
@@ -267,11 +289,17 @@ __global__ void __launch_bounds__(256, CGS_FWD_MINB) raster_fwd_kernel(
   if (tid == 0) {
     uint32_t np = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) np = max(np, s_max[w]);
-    tile_nproc[tile] = np;
-    last_rank[tile] = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;
+    for (int w = 0; w < kFwdWarps; ++w) np = max(np, s_max[w]);
+    const uint32_t lr = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;  // ranks grow along the list
+    if (kFwdHalves == 1) {
+      tile_nproc[tile] = np;
+      last_rank[tile] = lr;
+    } else {
+      atomicMax(&tile_nproc[tile], np);
+      atomicMax(&last_rank[tile], lr);
+    }
     if (trace) {
-      unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x);
+      unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x / kFwdHalves);
       t[0] = t_start;
       t[1] = global_ns();
       t[2] = smid();
@@ -498,7 +526,9 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         q.gr = dL[3 * pix + 0];
         q.gg = dL[3 * pix + 1];
         q.gb = dL[3 * pix + 2];
-        if (last_chunk) {
+        if (last_chunk || q.last <= static_cast<uint32_t>(k_end)) {
+          // done before this chunk ends: final state, nothing behind it (a
+          // split forward tile may not have written this boundary)
           q.T = final_T[pix];
         } else {
           const float4 c = ck[lyy * kTile + lx];
@@ -600,7 +630,9 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
 // ---------------------------------------------------------------------------
 int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
                       cudaStream_t st) {
-  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nproc, fd.total_tiles, L.tile_order);
+  tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nproc, fd.total_tiles, L.tile_order,
+                                        nproc ? nullptr : L.tile_nproc,
+                                        nproc ? nullptr : L.last_rank);
   CGS_CHECK_LAUNCH("tile_order_kernel");
   return CGS_OK;
 }
@@ -609,7 +641,8 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       float* image, float* final_T, int32_t* counts, cudaStream_t st) {
   // L.tile_order was computed from the list lengths before the depth sort
   CGS_PROFILED("raster_fwd_kernel", st,
-               raster_fwd_kernel<<<fd.total_tiles, 256, 0, st>>>(fd, L.tile_order, L.ranges, vals,
+               raster_fwd_kernel<<<fd.total_tiles * kFwdHalves, kFwdThreads, 0, st>>>(
+                   fd, L.tile_order, L.ranges, vals,
                                                                  L.recs, L.hdr,
                                                                  image, final_T, counts, L.px_last,
                                                                  L.tile_nproc, L.rank_of,
