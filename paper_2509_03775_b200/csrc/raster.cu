@@ -1,25 +1,26 @@
 // Tile rasterizer kernels, forward and backward (reference render.py:265-377).
 //
-// One CTA per 16x16 tile.  The forward runs 256 threads, one pixel each,
-// warp w on the 8x4 block ((w & 1) * 8, (w >> 1) * 4); the backward runs 128
-// threads, warp w on the 8x8 quadrant ((w & 1) * 8, (w >> 1) * 8), each lane
-// on pixels (x, y) and (x, y + 4) (two pixels per lane amortise its per-splat
-// warp reduction).  A splat whose contribution box (projection: the bounding
-// box of its alpha >= 1/255 ellipse, inside the pixel rect of
-// render.py:110-115) misses a warp's pixel block is skipped by that warp
-// without evaluating it: outside the box the reference's float64 alpha is
-// < 1/255, so the skip changes no result.
-//
-// CTAs take tiles longest-work-first (tile_order_kernel): the block
-// scheduler hands out CTAs in blockIdx order as slots free up, so this is
-// greedy longest-processing-time scheduling of the uneven tile lists and the
-// last wave is made of short tiles.  Tiles are independent, so the order
+// Forward: one CTA per 16x16 tile, 256 threads, one pixel each, warp w on
+// the 8x4 block ((w & 1) * 8, (w >> 1) * 4).  Backward: persistent CTAs of
+// 128 threads over (tile, 256-splat chunk) work units; warp w on the 8x8
+// quadrant ((w & 1) * 8, (w >> 1) * 8), each lane on pixels (x, y) and
+// (x, y + 4) (two pixels per lane amortise its per-splat warp reduction); a
+// unit starts from the per-pixel state the forward left at its chunk end.
+// A splat whose contribution box (projection: the bounding box of its
+// alpha >= 1/255 ellipse, inside the pixel rect of render.py:110-115) misses
+// a warp's pixel block is skipped by that warp without evaluating it:
+// outside the box the reference's float64 alpha is < 1/255, so the skip
 // changes no result.
 //
+// Work is taken longest-first (tile_order_kernel for the forward's tiles,
+// unit_order_kernel for the backward's units): greedy longest-processing-time
+// scheduling of the uneven lists, so the last wave is made of short ones.
+// Tiles and units are independent, so the order changes no result.
+//
 // Splat records are gathered by the bulk-copy engine (cp.async.bulk, one
-// 64-byte record per copy, completion on an mbarrier) one batch of 256 ahead
-// of the blending, and converted once per batch to tile-relative fp32 form
-// in shared memory.
+// 64-byte record per copy, completion on an mbarrier) one batch ahead of the
+// blending, and converted once per batch to tile-relative fp32 form in shared
+// memory.
 #include "frame.cuh"
 #include "raster_common.cuh"
 
