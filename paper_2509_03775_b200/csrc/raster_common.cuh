@@ -104,49 +104,48 @@ __device__ __forceinline__ double sh_basis_one(int b, double x, double y, double
 
 // d basis_b / d dir accumulated against weights: g += sum_b w[b] * dB_b/d(x,y,z)
 // (reference sh.py:56-100).
-template <int DEG>
-__device__ __forceinline__ void sh_basis_grad_dot(double x, double y, double z, const double* w,
-                                                  double* g) {
-  g[0] = g[1] = g[2] = 0.0;
+template <int DEG, typename T = double>
+__device__ __forceinline__ void sh_basis_grad_dot(T x, T y, T z, const T* w, T* g) {
+  g[0] = g[1] = g[2] = T(0);
   if constexpr (DEG >= 1) {
-    g[1] += -kC1 * w[1];
-    g[2] += kC1 * w[2];
-    g[0] += -kC1 * w[3];
+    g[1] += -T(kC1) * w[1];
+    g[2] += T(kC1) * w[2];
+    g[0] += -T(kC1) * w[3];
   }
   if constexpr (DEG >= 2) {
-    g[0] += kC2_0 * y * w[4];
-    g[1] += kC2_0 * x * w[4];
-    g[1] += kC2_1 * z * w[5];
-    g[2] += kC2_1 * y * w[5];
-    g[0] += -2.0 * kC2_2 * x * w[6];
-    g[1] += -2.0 * kC2_2 * y * w[6];
-    g[2] += 4.0 * kC2_2 * z * w[6];
-    g[0] += kC2_3 * z * w[7];
-    g[2] += kC2_3 * x * w[7];
-    g[0] += 2.0 * kC2_4 * x * w[8];
-    g[1] += -2.0 * kC2_4 * y * w[8];
+    g[0] += T(kC2_0) * y * w[4];
+    g[1] += T(kC2_0) * x * w[4];
+    g[1] += T(kC2_1) * z * w[5];
+    g[2] += T(kC2_1) * y * w[5];
+    g[0] += -T(2.0) * T(kC2_2) * x * w[6];
+    g[1] += -T(2.0) * T(kC2_2) * y * w[6];
+    g[2] += T(4.0) * T(kC2_2) * z * w[6];
+    g[0] += T(kC2_3) * z * w[7];
+    g[2] += T(kC2_3) * x * w[7];
+    g[0] += T(2.0) * T(kC2_4) * x * w[8];
+    g[1] += -T(2.0) * T(kC2_4) * y * w[8];
   }
   if constexpr (DEG >= 3) {
-    const double xx = x * x, yy = y * y, zz = z * z;
-    g[0] += kC3_0 * 6.0 * x * y * w[9];
-    g[1] += kC3_0 * (3.0 * xx - 3.0 * yy) * w[9];
-    g[0] += kC3_1 * y * z * w[10];
-    g[1] += kC3_1 * x * z * w[10];
-    g[2] += kC3_1 * x * y * w[10];
-    g[0] += -2.0 * kC3_2 * x * y * w[11];
-    g[1] += kC3_2 * (4.0 * zz - xx - 3.0 * yy) * w[11];
-    g[2] += 8.0 * kC3_2 * y * z * w[11];
-    g[0] += -6.0 * kC3_3 * x * z * w[12];
-    g[1] += -6.0 * kC3_3 * y * z * w[12];
-    g[2] += kC3_3 * (6.0 * zz - 3.0 * xx - 3.0 * yy) * w[12];
-    g[0] += kC3_4 * (4.0 * zz - 3.0 * xx - yy) * w[13];
-    g[1] += -2.0 * kC3_4 * x * y * w[13];
-    g[2] += 8.0 * kC3_4 * x * z * w[13];
-    g[0] += 2.0 * kC3_5 * x * z * w[14];
-    g[1] += -2.0 * kC3_5 * y * z * w[14];
-    g[2] += kC3_5 * (xx - yy) * w[14];
-    g[0] += kC3_6 * (3.0 * xx - 3.0 * yy) * w[15];
-    g[1] += -6.0 * kC3_6 * x * y * w[15];
+    const T xx = x * x, yy = y * y, zz = z * z;
+    g[0] += T(kC3_0) * T(6.0) * x * y * w[9];
+    g[1] += T(kC3_0) * (T(3.0) * xx - T(3.0) * yy) * w[9];
+    g[0] += T(kC3_1) * y * z * w[10];
+    g[1] += T(kC3_1) * x * z * w[10];
+    g[2] += T(kC3_1) * x * y * w[10];
+    g[0] += -T(2.0) * T(kC3_2) * x * y * w[11];
+    g[1] += T(kC3_2) * (T(4.0) * zz - xx - T(3.0) * yy) * w[11];
+    g[2] += T(8.0) * T(kC3_2) * y * z * w[11];
+    g[0] += -T(6.0) * T(kC3_3) * x * z * w[12];
+    g[1] += -T(6.0) * T(kC3_3) * y * z * w[12];
+    g[2] += T(kC3_3) * (T(6.0) * zz - T(3.0) * xx - T(3.0) * yy) * w[12];
+    g[0] += T(kC3_4) * (T(4.0) * zz - T(3.0) * xx - yy) * w[13];
+    g[1] += -T(2.0) * T(kC3_4) * x * y * w[13];
+    g[2] += T(8.0) * T(kC3_4) * x * z * w[13];
+    g[0] += T(2.0) * T(kC3_5) * x * z * w[14];
+    g[1] += -T(2.0) * T(kC3_5) * y * z * w[14];
+    g[2] += T(kC3_5) * (xx - yy) * w[14];
+    g[0] += T(kC3_6) * (T(3.0) * xx - T(3.0) * yy) * w[15];
+    g[1] += -T(6.0) * T(kC3_6) * x * y * w[15];
   }
 }
 

@@ -93,6 +93,9 @@ struct GaussIn {
 // Chain rule from screen space to model space for one (view, Gaussian)
 // splat (render.py:382-446).  acc = [d_color(3), d_opac, d_mean2d(2),
 // d_conic(A, B, C)].  Writes the per-splat pull-back record s.
+#ifndef CGS_PULLBACK_SH_F32
+#define CGS_PULLBACK_SH_F32 1
+#endif
 template <int DEG>
 __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const CamDev& cam,
                                 const GaussIn& g, const BwdLayout& B) {
@@ -114,6 +117,26 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   double dpc[3] = {0.0, 0.0, 0.0};
   if constexpr (DEG >= 1) {
     const float* row = g.sh_rows + static_cast<int64_t>(g.g2sh[gi]) * D;
+#if CGS_PULLBACK_SH_F32
+    // view-direction term in fp32 (it enters d_pos additively and the result
+    // is stored in fp32): half the registers of the fp64 form
+    const float d0 = static_cast<float>(draw[0]), d1 = static_cast<float>(draw[1]),
+                d2 = static_cast<float>(draw[2]);
+    float wb[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+      wb[b] = fmaf(d2, __ldg(row + 3 * b + 2), fmaf(d1, __ldg(row + 3 * b + 1),
+                                                     d0 * __ldg(row + 3 * b + 0)));
+    const float fx = static_cast<float>(ox), fy = static_cast<float>(oy),
+                fz = static_cast<float>(oz);
+    float dv[3];
+    sh_basis_grad_dot<DEG, float>(fx, fy, fz, wb, dv);
+    const float vd = fx * dv[0] + fy * dv[1] + fz * dv[2];
+    const float il = static_cast<float>(1.0 / len);
+    dpc[0] = (dv[0] - fx * vd) * il;
+    dpc[1] = (dv[1] - fy * vd) * il;
+    dpc[2] = (dv[2] - fz * vd) * il;
+#else
     double wb[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -126,6 +149,7 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
     dpc[0] = (dv[0] - ox * vd) / len;
     dpc[1] = (dv[1] - oy * vd) / len;
     dpc[2] = (dv[2] - oz * vd) / len;
+#endif
   }
   const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
   const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
@@ -341,7 +365,10 @@ __global__ void __launch_bounds__(256) splat_reduce_long_kernel(PairWalk pw,
 // Chain rule per touched splat (kept apart from the gather walk so the
 // latency-bound walk runs at full occupancy).
 template <int DEG>
-__global__ void __launch_bounds__(128, 4) pull_back_kernel(const FrameHeader* __restrict__ fh,
+#ifndef CGS_PB_MINB
+#define CGS_PB_MINB 4
+#endif
+__global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const FrameHeader* __restrict__ fh,
                                                         FrameDesc fd, int64_t n, int64_t vn,
                                                         GaussIn g, BwdLayout B) {
   if (fh->stats.overflow) return;
