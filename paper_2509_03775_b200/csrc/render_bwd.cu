@@ -365,6 +365,9 @@ __global__ void __launch_bounds__(256) splat_reduce_long_kernel(PairWalk pw,
 // Chain rule per touched splat (kept apart from the gather walk so the
 // latency-bound walk runs at full occupancy).
 template <int DEG>
+#ifndef CGS_PULLBACK_VIEW_INNER
+#define CGS_PULLBACK_VIEW_INNER 1
+#endif
 #ifndef CGS_PB_MINB
 #define CGS_PB_MINB 4
 #endif
@@ -372,8 +375,15 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
                                                         FrameDesc fd, int64_t n, int64_t vn,
                                                         GaussIn g, BwdLayout B) {
   if (fh->stats.overflow) return;
-  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < vn;
-       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < vn;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+#if CGS_PULLBACK_VIEW_INNER
+    // consecutive threads take the views of one Gaussian (its gathers coalesce)
+    const int64_t gi = t / fd.n_views;
+    const int64_t s = (t - gi * fd.n_views) * n + gi;
+#else
+    const int64_t s = t;
+#endif
     if (!B.touched[s]) continue;
     const float4 a0 = B.acc0[s], a1 = B.acc1[s];
     const double acc[9] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, B.acc2[s]};

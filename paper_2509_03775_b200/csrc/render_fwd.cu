@@ -216,6 +216,9 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
 // 4-pass digit histogram (warp-aggregated shared counters, one global
 // atomic per non-zero bin per CTA) so the sort skips its histogram pass.
 template <int DEG>
+#ifndef CGS_PROJECT_VIEW_INNER
+#define CGS_PROJECT_VIEW_INNER 1
+#endif
 __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
   __shared__ uint32_t s_h[4 * 256];
   for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_h[k] = 0;
@@ -224,8 +227,16 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
   const int lane = threadIdx.x & 31;
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x); b < vn;
        b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = b + threadIdx.x;
-    const bool ok = s < vn;
+    const int64_t t = b + threadIdx.x;
+    const bool ok = t < vn;
+#if CGS_PROJECT_VIEW_INNER
+    // consecutive threads take the views of one Gaussian: its gathers
+    // (position, logit, indices, SR / SH rows) coalesce across the views
+    const int64_t gi = t / fd.n_views;
+    const int64_t s = (t - gi * fd.n_views) * in.n + gi;
+#else
+    const int64_t s = t;
+#endif
     const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0u;
     const unsigned valid = __ballot_sync(kFull, ok);
 #pragma unroll
