@@ -414,65 +414,56 @@ __global__ void __launch_bounds__(256) gauss_write_kernel(BwdLayout B, int64_t n
 }
 
 // SH row gradient = sum over members of basis(view) (x) d_raw (render.py:421,
-// 456).  One 128-thread CTA per codebook row: warp w owns the column group
-// [w*CPW, (w+1)*CPW) (warp-uniform, so the basis index of every column is a
-// compile-time constant after the switch on w) and its lanes take the row's
-// (member, view) splats round-robin; the 32 lane sums are combined by a fixed
-// xor tree.  Members ascend by Gaussian index, views ascend; every addition
-// has a fixed order, so the result is deterministic.  Writes every row.
-template <int DEG, int W>
-__device__ __forceinline__ void sh_row_columns(const int32_t* __restrict__ mem, int m0, int m1,
-                                               int64_t n, int n_views, const BwdLayout& B,
-                                               float scale, float* __restrict__ out) {
-  constexpr int NB = (DEG + 1) * (DEG + 1);
-  constexpr int D = 3 * NB;
-  constexpr int CPW = (D + 3) / 4;
-  const int lane = threadIdx.x & 31;
-  const int items = (m1 - m0) * n_views;
-  double a[CPW];
-#pragma unroll
-  for (int c = 0; c < CPW; ++c) a[c] = 0.0;
-  for (int t = lane; t < items; t += 32) {
-    const int mi = t / n_views, v = t - mi * n_views;
-    const int64_t sp = static_cast<int64_t>(v) * n + mem[m0 + mi];
-    if (!B.touched[sp]) continue;
-    const float4 vd = B.s_view[sp];
-    const float4 dr = B.s_draw[sp];
-    float Bv[NB];
-    sh_basis_f<DEG>(vd.x, vd.y, vd.z, Bv);
-    const float d3[3] = {dr.x, dr.y, dr.z};
-#pragma unroll
-    for (int c = 0; c < CPW; ++c) {
-      constexpr int base = W * CPW;
-      if (base + c < D) a[c] += static_cast<double>(Bv[(base + c) / 3] * d3[(base + c) % 3]);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < CPW; ++c) a[c] = warp_sum(a[c]);
-  if (lane < CPW && W * CPW + lane < D) {
-    double v = a[0];
-#pragma unroll
-    for (int c = 1; c < CPW; ++c)
-      if (lane == c) v = a[c];
-    out[W * CPW + lane] = static_cast<float>(v * scale);
-  }
-}
-
+// 456).  One warp per SH row: lane t takes (member, view) items t, t + 32, ... and
+// accumulates all D coefficient products in registers; the 32 lane partials
+// then go through shared memory and each lane sums whole columns over the
+// lanes in fixed order (deterministic; fp32 partials of a few items each).
 template <int DEG>
 __global__ void __launch_bounds__(128) sh_code_reduce_kernel(
     const int32_t* __restrict__ off, const int32_t* __restrict__ mem, int64_t cap, int64_t n,
     int n_views, BwdLayout B, float scale, float* __restrict__ gsh) {
-  constexpr int D = 3 * (DEG + 1) * (DEG + 1);
-  const int w = threadIdx.x >> 5;
-  for (int64_t r = blockIdx.x; r < cap; r += gridDim.x) {
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  constexpr int D = 3 * NB;
+  __shared__ float s_part[4][32][D + 1];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < cap;
+       r += warps) {
     const int m0 = off[r], m1 = off[r + 1];
-    float* out = gsh + r * D;
-    switch (w) {
-      case 0: sh_row_columns<DEG, 0>(mem, m0, m1, n, n_views, B, scale, out); break;
-      case 1: sh_row_columns<DEG, 1>(mem, m0, m1, n, n_views, B, scale, out); break;
-      case 2: sh_row_columns<DEG, 2>(mem, m0, m1, n, n_views, B, scale, out); break;
-      default: sh_row_columns<DEG, 3>(mem, m0, m1, n, n_views, B, scale, out); break;
+    const int items = (m1 - m0) * n_views;
+    float acc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = 0.0f;
+    for (int t = lane; t < items; t += 32) {
+      const int mi = t / n_views, v = t - mi * n_views;
+      const int64_t sp = static_cast<int64_t>(v) * n + mem[m0 + mi];
+      if (!B.touched[sp]) continue;
+      const float4 vd = B.s_view[sp];
+      const float4 dr = B.s_draw[sp];
+      float Bv[NB];
+      sh_basis_f<DEG>(vd.x, vd.y, vd.z, Bv);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        acc[3 * b + 0] = fmaf(Bv[b], dr.x, acc[3 * b + 0]);
+        acc[3 * b + 1] = fmaf(Bv[b], dr.y, acc[3 * b + 1]);
+        acc[3 * b + 2] = fmaf(Bv[b], dr.z, acc[3 * b + 2]);
+      }
     }
+    float* out = gsh + r * D;
+    if (items == 0) {  // no member: the row's gradient is zero
+      for (int c = lane; c < D; c += 32) out[c] = 0.0f;
+      continue;
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) s_part[wl][lane][c] = acc[c];
+    __syncwarp();
+    for (int c = lane; c < D; c += 32) {
+      float sum = 0.0f;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) sum += s_part[wl][l][c];
+      out[c] = sum * scale;
+    }
+    __syncwarp();
   }
 }
 
@@ -640,7 +631,7 @@ template <int DEG>
 static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap, int64_t n,
                              int nv, const BwdLayout& B, float scale, float* gsh, cudaStream_t st) {
   CGS_PROFILED("sh_code_reduce_kernel", st,
-               sh_code_reduce_kernel<DEG><<<grid_for(cap, 1, 16), 128, 0, st>>>(
+               sh_code_reduce_kernel<DEG><<<grid_for(cap * 32, 128, 16), 128, 0, st>>>(
                    off, mem, cap, n, nv, B, scale, gsh));
 }
 
