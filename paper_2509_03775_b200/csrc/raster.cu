@@ -469,7 +469,8 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const float* __restrict__ final_T, const float* __restrict__ dL,
     const float4* __restrict__ ckpt,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect, int64_t n,
-    float* __restrict__ partials, unsigned long long* __restrict__ n_processed,
+    float* __restrict__ partials, int64_t partial9_offset,
+    unsigned long long* __restrict__ n_processed,
     unsigned long long* __restrict__ trace) {
   constexpr int B = kBwdBatch;
   const unsigned long long t_start = trace ? global_ns() : 0ull;
@@ -612,9 +613,13 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         const float4 aa = s_a[jj];
         const float4 nn = s_n[jj];
         moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[jj], g);
-        float* out = partials + static_cast<int64_t>(s_eidx[jj]) * 9;
-#pragma unroll
-        for (int u = 0; u < 9; ++u) out[u] = g[u];
+        // values 0-7 as two aligned float4 (pair-major, 32 B), value 8 in a
+        // separate array after them (partials layout: pair_cap x 8, then pair_cap)
+        const int64_t e = s_eidx[jj];
+        float4* o4 = reinterpret_cast<float4*>(partials) + 2 * e;
+        o4[0] = make_float4(g[0], g[1], g[2], g[3]);
+        o4[1] = make_float4(g[4], g[5], g[6], g[7]);
+        partials[partial9_offset + e] = g[8];
       }
       __syncthreads();
     }
@@ -672,7 +677,8 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
   CGS_PROFILED("raster_bwd_kernel", st,
                kern<<<grid, 128, 0, st>>>(fd, L.units, L.unit_ctl, L.ranges, sorted_pair_vals(L),
                                           L.recs, L.hdr, L.px_last, L.tile_nproc, final_T, dL,
-                                          L.ckpt, L.pair_off, L.rect, L.n, partials, n_processed,
+                                          L.ckpt, L.pair_off, L.rect, L.n, partials,
+                                          8 * (L.pair_cap > 0 ? L.pair_cap : 1), n_processed,
                                           trace));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
   return CGS_OK;

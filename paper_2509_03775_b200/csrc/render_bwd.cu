@@ -56,7 +56,7 @@ inline BwdLayout plan_bwd(void* base, size_t cap, int64_t n, int n_views, int to
   const int64_t pc = pair_cap > 0 ? pair_cap : 1;
   const int64_t vn = n * n_views > 0 ? n * n_views : 1;
   B.hdr = c.take<BwdHeader>(1);
-  B.partials = c.take<float>(pc * 9);
+  B.partials = c.take<float>(pc * 9);  // [pc x 8 | pc]: values 0-7 as float4 pairs, value 8
   B.touched = c.take<uint8_t>(vn);
   B.s_posl = c.take<float4>(vn);
   B.s_view = c.take<float4>(vn);
@@ -236,7 +236,8 @@ struct PairWalk {
   const uint64_t* rect;
   const uint32_t* rank_of;
   const uint32_t* last_rank;
-  const float* partials;  // by emission index
+  const float* partials;  // by emission index: [pair_cap x 8 | pair_cap]
+  int64_t p9;             // offset of value 8 (8 * pair_cap)
 };
 
 // Adds the partials of splat s's processed pairs k = k0, k0+kstep, ... (in
@@ -257,9 +258,12 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
     const int t = tb + (ty0 + static_cast<int>(k) / span) * ntx + tx0 + static_cast<int>(k) % span;
     if (r < w.last_rank[t]) {  // inside the tile's processed prefix
       any = true;
-      const float* pp = w.partials + static_cast<int64_t>(o + k) * 9;
-#pragma unroll
-      for (int u = 0; u < 9; ++u) acc[u] += static_cast<double>(pp[u]);
+      const int64_t e = static_cast<int64_t>(o + k);
+      const float4* p4 = reinterpret_cast<const float4*>(w.partials) + 2 * e;
+      const float4 x = p4[0], y = p4[1];
+      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+      acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+      acc[8] += w.partials[w.p9 + e];
     }
   }
   return any;
@@ -650,7 +654,8 @@ int bwd_stage_raster(const FrameDesc& fd, const FrameLayout& L, BwdLayout& B, co
 int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                        BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st) {
   if (fd.total_tiles > 0 && L.vn > 0) {
-    PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials};
+    PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials,
+                8 * (L.pair_cap > 0 ? L.pair_cap : 1)};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
       case 0: launch_splat_reduce<0>(pw, L, fd, gi, B, st); break;
