@@ -94,7 +94,7 @@ int main() {
   cudaFuncSetAttribute(onesweep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   cudaMemsetAsync(w.hist, 0, 4 * 256 * 4, st);
-  sort_hist_kernel<uint32_t><<<grid_for(n, 256, 4), 256, 0, st>>>(dk, nullptr, n, 4, w.hist);
+  sort_hist_kernel<uint32_t><<<grid_for(n, 256, 4), 256, 0, st>>>(dk, nullptr, n, 32, w.hist);
   cudaMemsetAsync(w.status, 0, 4 * w.max_parts * 256 * 4, st);
   cudaMemsetAsync(w.counter, 0, 64 * 4, st);
   const unsigned grid = static_cast<unsigned>(ceil_div(n, kSortTile));
@@ -104,7 +104,7 @@ int main() {
   cudaStreamSynchronize(st);
   cudaEventRecord(ev[0], st);
   for (int p = 0; p < 4; ++p) {
-    onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(ki, vi, ko, vo, nullptr, n, 8 * p,
+    onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(ki, vi, ko, vo, nullptr, n, 8 * p, 8,
                                                        w.hist + p * 256,
                                                        w.status + static_cast<size_t>(p) * w.max_parts * 256,
                                                        w.counter + p);
@@ -152,7 +152,7 @@ int main() {
            cudaMemsetAsync(w.counter, 0, 64 * 4, st);
            uint32_t *a = dk, *b = dv, *c2 = w.keys_alt, *d2 = w.vals_alt;
            for (int p = 0; p < 4; ++p) {
-             onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(a, b, c2, d2, nullptr, n, 8 * p,
+             onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(a, b, c2, d2, nullptr, n, 8 * p, 8,
                  w.hist + p * 256, w.status + static_cast<size_t>(p) * w.max_parts * 256,
                  w.counter + p);
              std::swap(a, c2);
@@ -173,7 +173,7 @@ int main() {
       cudaMemsetAsync(w.status, 0, 4 * w.max_parts * 256 * 4, st);
       cudaMemsetAsync(w.counter, 0, 64 * 4, st);
       marker_kernel<<<1, 1, 0, st>>>(mk, 0);
-      onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(dk, dv, w.keys_alt, w.vals_alt, nullptr, n, 0,
+      onesweep_kernel<uint32_t><<<grid, 256, smem, st>>>(dk, dv, w.keys_alt, w.vals_alt, nullptr, n, 0, 8,
                                                          w.hist, w.status, w.counter);
       marker_kernel<<<1, 1, 0, st>>>(mk, 1);
       cudaStreamEndCapture(st, &g);

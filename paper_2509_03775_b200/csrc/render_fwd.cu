@@ -332,13 +332,13 @@ __device__ __forceinline__ uint32_t emit_one(uint64_t p, int k, uint64_t rc, int
 
 // Adds the tile keys of the warp's live lanes to the shared digit histogram.
 template <typename KT>
-__device__ __forceinline__ void hist_keys(uint32_t* s_h, int passes, uint32_t key, bool live,
-                                          int lane) {
+__device__ __forceinline__ void hist_keys(uint32_t* s_h, int passes, int key_bits, uint32_t key,
+                                          bool live, int lane) {
   const unsigned valid = __ballot_sync(kFull, live);
   if (!valid) return;
   for (int p = 0; p < passes; ++p) {
     const unsigned d = (key >> (8 * p)) & 255u;
-    const unsigned peers = warp_peers8(d) & valid;
+    const unsigned peers = warp_peers_bits(d, key_bits - 8 * p) & valid;
     if (live && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
   }
 }
@@ -348,7 +348,8 @@ __device__ __forceinline__ void emit_warps(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
     FrameHeader* __restrict__ hdr, const FrameDesc& fd, int64_t n, uint32_t* __restrict__ long_list,
-    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int passes) {
+    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int key_bits) {
+  const int passes = (key_bits + 7) / 8;
   if (hdr->stats.overflow) return;
   const int lane = threadIdx.x & 31;
   const int64_t ns = static_cast<int64_t>(hdr->n_onscreen);  // ranks with tiles come first
@@ -391,7 +392,7 @@ __device__ __forceinline__ void emit_warps(
         const int k = static_cast<int>(q - lo2);
         key = emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
       }
-      hist_keys<KT>(s_h, passes, key, q < total, lane);
+      hist_keys<KT>(s_h, passes, key_bits, key, q < total, lane);
     }
   }
 }
@@ -401,11 +402,12 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
     FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ long_list,
-    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int passes) {
+    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int key_bits) {
+  const int passes = (key_bits + 7) / 8;
   __shared__ uint32_t s_h[4 * 256];  // tile sort digit histogram (this CTA's pairs)
   for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
   __syncthreads();
-  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, passes);
+  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, key_bits);
   __syncthreads();
   for (int k = threadIdx.x; k < passes * 256; k += blockDim.x)
     if (s_h[k]) atomicAdd(&hist[k], s_h[k]);
@@ -418,7 +420,8 @@ __global__ void __launch_bounds__(256) emit_long_pairs_kernel(
     const uint32_t* __restrict__ long_list, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
     const FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, KT* __restrict__ keys,
-    uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int passes) {
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int key_bits) {
+  const int passes = (key_bits + 7) / 8;
   __shared__ uint32_t s_h[4 * 256];
   if (hdr->stats.overflow) return;
   const int64_t nl = static_cast<int64_t>(hdr->scratch[2]);
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(256) emit_long_pairs_kernel(
       const int k = k0 + threadIdx.x;
       uint32_t key = 0;
       if (k < cnt) key = emit_one<KT>(o + k, k, rc, fd.cam[v].ntx, fd.cam[v].tile_base, s, keys, vals);
-      hist_keys<KT>(s_h, passes, key, k < cnt, lane);
+      hist_keys<KT>(s_h, passes, key_bits, key, k < cnt, lane);
     }
   }
   __syncthreads();
@@ -476,11 +479,11 @@ static int emit_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
                emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.pair_off, L.n_tiles, L.rect, L.hdr,
                                                           fd, L.n, L.long_list,
                                                           static_cast<KT*>(L.pkeys), L.pvals,
-                                                          ws.hist, passes));
+                                                          ws.hist, L.tile_key_bits));
   CGS_CHECK_LAUNCH("emit_pairs_kernel");
   emit_long_pairs_kernel<KT><<<148 * 4, 256, 0, st>>>(L.long_list, L.pair_off, L.n_tiles, L.rect,
                                                        L.hdr, fd, L.n, static_cast<KT*>(L.pkeys),
-                                                       L.pvals, ws.hist, passes);
+                                                       L.pvals, ws.hist, L.tile_key_bits);
   CGS_CHECK_LAUNCH("emit_long_pairs_kernel");
   return CGS_OK;
 }

@@ -47,6 +47,21 @@ __device__ __forceinline__ unsigned warp_peers8(unsigned d) {
   return peers;
 }
 
+// Same for a digit of `bits` <= 8 significant bits (warp-uniform): the
+// ballots of bits every key has zero are skipped (keys narrower than the
+// last 8-bit pass, e.g. 11-bit tile keys).
+__device__ __forceinline__ unsigned warp_peers_bits(unsigned d, int bits) {
+  unsigned peers = kFull;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (b >= bits) break;
+    const bool bit = (d >> b) & 1u;
+    const unsigned bal = __ballot_sync(kFull, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
   const int lane = threadIdx.x & 31;
@@ -230,8 +245,9 @@ inline SortWs<K> carve_sort(Carver& c, int64_t n_cap) {
 template <typename K>
 __global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ keys,
                                                         const unsigned long long* n_dev,
-                                                        int64_t n_host, int passes,
+                                                        int64_t n_host, int key_bits,
                                                         uint32_t* __restrict__ hist) {
+  const int passes = (key_bits + 7) / 8;
   __shared__ uint32_t s_h[8 * 256];
   for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) s_h[i] = 0;
   __syncthreads();
@@ -245,7 +261,8 @@ __global__ void __launch_bounds__(256) sort_hist_kernel(const K* __restrict__ ke
     const uint64_t k = ok ? static_cast<uint64_t>(keys[i]) : 0ULL;
     const unsigned valid = __ballot_sync(kFull, ok);
     for (int p = 0; p < passes; ++p) {
-      const unsigned d = static_cast<unsigned>((k >> (8 * p)) & 255u);
+      const int db = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
+      const unsigned d = static_cast<unsigned>((k >> (8 * p)) & ((1u << db) - 1u));
       const unsigned peers = warp_peers8(d) & valid;
       if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
     }
@@ -283,11 +300,12 @@ template <typename K>
 __global__ void __launch_bounds__(256) onesweep_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-    const unsigned long long* n_dev, int64_t n_host, int shift,
+    const unsigned long long* n_dev, int64_t n_host, int shift, int digit_bits,
     const uint32_t* __restrict__ hist, uint32_t* status, unsigned* counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<K>& S = *reinterpret_cast<SortSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned dmask = (1u << digit_bits) - 1u;  // only the low key_bits are sorted on
   if (tid == 0) S.part = atomicAdd(counter, 1u);
   for (int i = tid; i < kSortWarps * 256; i += 256) S.wcnt[i] = 0;
   __syncthreads();
@@ -321,8 +339,8 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
   uint32_t* wc = S.wcnt + warp * 256;
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & 255u);
-    const unsigned peers = warp_peers8(d);
+    const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
+    const unsigned peers = warp_peers_bits(d, digit_bits);
     const unsigned before = wc[d];
     rank[j] = before + __popc(peers & lanemask_lt());
     __syncwarp();
@@ -404,7 +422,7 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
   SORT_TRACE(part, 3);
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & 255u);
+    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
     const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
     S.keys[pos] = key[j];
     S.vals[pos] = val[j];
@@ -413,7 +431,7 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
   const int nvalid = static_cast<int>(n - base < kSortTile ? n - base : kSortTile);
   for (int i = tid; i < nvalid; i += 256) {
     const K k = S.keys[i];
-    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & 255u);
+    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & dmask);
     const int64_t o = static_cast<int64_t>(S.goff[dd]) + i;
     keys_out[o] = k;
     vals_out[o] = S.vals[i];
@@ -437,7 +455,7 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
                            static_cast<size_t>(passes) * ws.max_parts * 256 * sizeof(uint32_t), st));
   CGS_CUDA(cudaMemsetAsync(ws.counter, 0, 64 * sizeof(unsigned), st));
   if (!hist_ready) {  // else the producer of the keys already filled ws.hist
-    CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, passes, ws.hist));
+    CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, key_bits, ws.hist));
     CGS_CHECK_LAUNCH("sort_hist_kernel");
   }
   static bool attr_set = false;
@@ -453,7 +471,8 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
   uint32_t* vout = ws.vals_alt;
   const unsigned grid = static_cast<unsigned>(ceil_div(n_cap > 0 ? n_cap : 1, kSortTile));
   for (int p = 0; p < passes; ++p) {
-    CGS_PROFILED("onesweep_kernel", st, onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p,
+    const int dbits = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
+    CGS_PROFILED("onesweep_kernel", st, onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p, dbits,
                                                 ws.hist + p * 256,
                                                 ws.status + static_cast<size_t>(p) * ws.max_parts * 256,
                                                 ws.counter + p));
