@@ -63,7 +63,10 @@ struct GradSmem {
 };
 
 // grid: (ceil(W/32), ceil(H/32), view*3 + channel); block 256.
-__global__ void __launch_bounds__(256) ssim_stats_kernel(const float* __restrict__ img,
+#ifndef CGS_SSIM_MINB
+#define CGS_SSIM_MINB 3
+#endif
+__global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const float* __restrict__ img,
                                                          const float* __restrict__ gt, int H, int W,
                                                          int do_ssim, LossLayout L) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
