@@ -636,7 +636,7 @@ def main():
                 "traffic": traffic, "traffic_source": traffic_src,
                 "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
                 "alg_bytes_per_launch": alg, "P_x": P_x, "pixels": px,
-                "note": "the raster kernels are instruction-issue bound (ncu: ~73% issue slots "
+                "note": "the raster kernels are instruction-issue bound (ncu: ~74% issue slots "
                         "busy, FMA+ALU pipes, see profiles/r1_ncu_raster_bwd_config1.txt), not "
                         "HBM bound; achieved uses processed-prefix algorithmic bytes only "
                         "(SURVEY.md §8(d)), traffic is the ncu DRAM bytes of one launch"}
