@@ -475,14 +475,15 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   constexpr int B = kBwdBatch;
   const unsigned long long t_start = trace ? global_ns() : 0ull;
   __shared__ __align__(128) SplatRec s_raw[B];
-  __shared__ float4 s_a[B];
-  __shared__ float4 s_b[B];
-  __shared__ float4 s_n[B];  // green, blue, lambda1, lambda2
-  __shared__ float s_io[B];  // 1 / opacity
-  __shared__ uint8_t s_mask[B];
+  static_assert(2 * B == 128, "staging and combine each take half of the CTA");
+  __shared__ float4 s_a[2][B];
+  __shared__ float4 s_b[2][B];
+  __shared__ float4 s_n[2][B];  // green, blue, lambda1, lambda2
+  __shared__ float s_io[2][B];  // 1 / opacity
+  __shared__ uint8_t s_mask[2][B];
   __shared__ uint8_t s_list[4][B];
-  __shared__ uint32_t s_eidx[B];  // emission index of each staged pair
-  __shared__ float s_red[4][B][9];
+  __shared__ uint32_t s_eidx[2][B];  // emission index of each staged pair
+  __shared__ float s_red[2][4][B][9];
   __shared__ uint32_t s_wlast[4];
   __shared__ uint32_t s_unit;
   __shared__ __align__(8) uint64_t s_bar;
@@ -494,6 +495,29 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   const int slot = reduce9_slot(lane);
   uint8_t* my_list = s_list[warp];
   const uint32_t n_units = unit_ctl[0];
+  // splat jj of buffer cb: sum the present warps in fixed order, chain to the
+  // 9 gradients, store at the pair's emission index (values 0-7 as two
+  // aligned float4, value 8 in the separate array after them)
+  auto combine_splat = [&](int cb, int jj) {
+    const uint32_t m = s_mask[cb][jj];
+    float mom[9], g[9];
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const float r0 = (m & 1u) ? s_red[cb][0][jj][u] : 0.0f;
+      const float r1 = (m & 2u) ? s_red[cb][1][jj][u] : 0.0f;
+      const float r2 = (m & 4u) ? s_red[cb][2][jj][u] : 0.0f;
+      const float r3 = (m & 8u) ? s_red[cb][3][jj][u] : 0.0f;
+      mom[u] = (r0 + r1) + (r2 + r3);
+    }
+    const float4 aa = s_a[cb][jj];
+    const float4 nn = s_n[cb][jj];
+    moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[cb][jj], g);
+    const int64_t e = s_eidx[cb][jj];
+    float4* o4 = reinterpret_cast<float4*>(partials) + 2 * e;
+    o4[0] = make_float4(g[0], g[1], g[2], g[3]);
+    o4[1] = make_float4(g[4], g[5], g[6], g[7]);
+    partials[partial9_offset + e] = g[8];
+  };
   if (tid == 0) mbar_init(&s_bar, 1);
   uint32_t phase = 0;
   for (;;) {
@@ -551,40 +575,49 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     int b0 = k0 + ((k_end - 1 - k0) / B) * B;
     fence_proxy_async_smem();  // s_raw was read by the previous unit's staging
     issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(B, k_end - b0), tid, 128);
+    // Two-buffer pipeline: threads [0, B) stage batch i while threads
+    // [B, 2B) combine batch i-1 (its staged values and warp sums live in the
+    // other buffer), so a batch costs two barriers instead of three.
+    int buf = 0, cnb = 0;
     for (; b0 >= k0; b0 -= B) {
       const int nb = min(B, k_end - b0);
       mbar_wait(&s_bar, phase);
       phase ^= 1;
-      for (int k = tid; k < nb; k += 128) {
-        const SplatRec& r = s_raw[k];
-        const Staged sg = stage_splat(r, ox, oy);
-        s_a[k] = sg.a;
-        s_b[k] = sg.b;
-        s_n[k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
-        s_io[k] = 1.0f / r.opac;
-        s_eidx[k] = static_cast<uint32_t>(
-            emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
-        uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
+      if (tid < B) {
+        const int k = tid;
+        if (k < nb) {
+          const SplatRec& r = s_raw[k];
+          const Staged sg = stage_splat(r, ox, oy);
+          s_a[buf][k] = sg.a;
+          s_b[buf][k] = sg.b;
+          s_n[buf][k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
+          s_io[buf][k] = 1.0f / r.opac;
+          s_eidx[buf][k] = static_cast<uint32_t>(
+              emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
+          uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
 #pragma unroll
-        for (int w = 0; w < 4; ++w)
-          if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);
-        s_mask[k] = static_cast<uint8_t>(m);
+          for (int w = 0; w < 4; ++w)
+            if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);
+          s_mask[buf][k] = static_cast<uint8_t>(m);
+        }
+      } else if (tid - B < cnb) {
+        combine_splat(buf ^ 1, tid - B);
       }
       __syncthreads();
       if (b0 > k0) {
         fence_proxy_async_smem();
         issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
       }
-      const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
+      const int hits = warp_hit_list<B>(s_mask[buf], nb, warp, lane, my_list);
       for (int i = hits - 1; i >= 0; --i) {
         const int j = my_list[i];
         const uint32_t k = static_cast<uint32_t>(b0 + j);
         float o[9];
 #pragma unroll
         for (int u = 0; u < 9; ++u) o[u] = 0.0f;
-        const float4 a = s_a[j];
-        const float4 b = s_b[j];
-        const float4 nc = s_n[j];
+        const float4 a = s_a[buf][j];
+        const float4 b = s_b[buf][j];
+        const float4 nc = s_n[buf][j];
         float u0, v0, u1, v1;
         const float al0 = staged_alpha(a, b, flx, fly, u0, v0);
         const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
@@ -596,33 +629,13 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         // lanes 0,2,4,8,10,16,18,20,24 end up holding the warp sums of values 0..8
         float red = 0.0f;
         if (__any_sync(kFull, any)) red = warp_reduce9(o);
-        if (slot >= 0) s_red[warp][j][slot] = red;
+        if (slot >= 0) s_red[buf][warp][j][slot] = red;
       }
       __syncthreads();
-      for (int jj = tid; jj < nb; jj += 128) {  // one splat per thread, warps in fixed order
-        const uint32_t m = s_mask[jj];
-        float mom[9], g[9];
-#pragma unroll
-        for (int u = 0; u < 9; ++u) {
-          const float r0 = (m & 1u) ? s_red[0][jj][u] : 0.0f;
-          const float r1 = (m & 2u) ? s_red[1][jj][u] : 0.0f;
-          const float r2 = (m & 4u) ? s_red[2][jj][u] : 0.0f;
-          const float r3 = (m & 8u) ? s_red[3][jj][u] : 0.0f;
-          mom[u] = (r0 + r1) + (r2 + r3);
-        }
-        const float4 aa = s_a[jj];
-        const float4 nn = s_n[jj];
-        moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[jj], g);
-        // values 0-7 as two aligned float4 (pair-major, 32 B), value 8 in a
-        // separate array after them (partials layout: pair_cap x 8, then pair_cap)
-        const int64_t e = s_eidx[jj];
-        float4* o4 = reinterpret_cast<float4*>(partials) + 2 * e;
-        o4[0] = make_float4(g[0], g[1], g[2], g[3]);
-        o4[1] = make_float4(g[4], g[5], g[6], g[7]);
-        partials[partial9_offset + e] = g[8];
-      }
-      __syncthreads();
+      cnb = nb;
+      buf ^= 1;
     }
+    if (tid >= B && tid - B < cnb) combine_splat(buf ^ 1, tid - B);  // the unit's last batch
   }
   if (TRACE && tid == 0) {
     unsigned long long* t = trace + 4 * (static_cast<int64_t>(fd.total_tiles) + blockIdx.x);
