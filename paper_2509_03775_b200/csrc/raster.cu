@@ -158,6 +158,9 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
 // one CTA per tile makes the longest list the kernel's floor; two CTAs halve
 // it for the price of staging each record twice.  Per-tile results (processed
 // count, last rank) are combined with atomicMax (zeroed by tile_order_kernel).
+#ifndef CGS_FWD_PAIRS
+#define CGS_FWD_PAIRS 1
+#endif
 #ifndef CGS_FWD_HALVES
 #define CGS_FWD_HALVES 1
 #endif
@@ -238,6 +241,40 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     }
     const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
     if (!p.done) {
+#if CGS_FWD_PAIRS
+      // two hits per iteration: both alphas are independent of the blend
+      // state, so they issue together; the blends stay in list order
+      int i = 0;
+      for (; i + 1 < hits; i += 2) {
+        const int j0 = my_list[i], j1 = my_list[i + 1];
+        const float4 a0 = s_a[j0], b0v = s_b[j0];
+        const float4 a1 = s_a[j1], b1v = s_b[j1];
+        float u, v;
+        const float al0 = staged_alpha(a0, b0v, flx, fly, u, v);
+        const float al1 = staged_alpha(a1, b1v, flx, fly, u, v);
+        if (al0 >= kAlphaSkipF) {
+          const float2 c = s_c[j0];
+          blend(p, al0, b0v.w, c.x, c.y, static_cast<uint32_t>(b0 + j0));
+          if (p.done) break;
+        }
+        if (al1 >= kAlphaSkipF) {
+          const float2 c = s_c[j1];
+          blend(p, al1, b1v.w, c.x, c.y, static_cast<uint32_t>(b0 + j1));
+          if (p.done) break;
+        }
+      }
+      if (!p.done && i < hits) {
+        const int j = my_list[i];
+        const float4 a = s_a[j];
+        const float4 b = s_b[j];
+        float u, v;
+        const float al = staged_alpha(a, b, flx, fly, u, v);
+        if (al >= kAlphaSkipF) {
+          const float2 c = s_c[j];
+          blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
+        }
+      }
+#else
       for (int i = 0; i < hits; ++i) {
         const int j = my_list[i];
         const float4 a = s_a[j];
@@ -250,6 +287,7 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
           if (p.done) break;
         }
       }
+#endif
     }
     if (__syncthreads_count(p.done) == NT) break;
     if (b0 + B < n && ((b0 + B) % kChunk) == 0) {  // chunk boundary for the backward
