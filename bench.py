@@ -621,7 +621,7 @@ def main():
     achieved = alg / avg_s / 1e9 if avg_s > 0 else 0.0
     # DRAM bytes per launch of the same kernel from the committed ncu --set full
     # capture (profiles/ncu_traffic.json, written by scripts/ncu_summary.py)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, issue_pct = None, None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
@@ -629,6 +629,7 @@ def main():
             if t:
                 traffic = float(t["bytes_per_launch"])
                 traffic_src = f"profiles/ncu_traffic.json ({t.get('source')}, ncu --set full)"
+                issue_pct = t.get("issue_active_pct")
         except Exception:
             pass
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
@@ -636,6 +637,7 @@ def main():
                 "traffic": traffic, "traffic_source": traffic_src,
                 "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
                 "alg_bytes_per_launch": alg, "P_x": P_x, "pixels": px,
+                "issue_active_frac": issue_pct / 100.0 if issue_pct else None,
                 "note": "the raster kernels are instruction-issue bound (ncu: ~74% issue slots "
                         "busy, FMA+ALU pipes, see profiles/r1_ncu_raster_bwd_config1.txt), not "
                         "HBM bound; achieved uses processed-prefix algorithmic bytes only "

@@ -86,8 +86,10 @@ def main():
         if rd is not None and wr is not None:
             print(f"  DRAM traffic/launch     {(rd + wr) / 1e6:.2f} MB"
                   + (f"  ({(rd + wr) / dur / 1e9:.1f} GB/s over the launch)" if dur else ""))
+            issue = num(d, u, "smsp__issue_active.avg.pct_of_peak_sustained_active")
             traffic[short] = {"bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                              "duration_s": dur, "source": os.path.basename(a.rep)}
+                              "duration_s": dur, "issue_active_pct": issue,
+                              "source": os.path.basename(a.rep)}
     if a.traffic_json:
         json.dump(traffic, open(a.traffic_json, "w"), indent=1, sort_keys=True)
 
