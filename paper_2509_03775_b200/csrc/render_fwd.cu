@@ -343,12 +343,49 @@ __device__ __forceinline__ void hist_keys(uint32_t* s_h, int passes, int key_bit
   }
 }
 
+// Tile-sort digit histogram of one splat's tiles, per row of its rect
+// instead of per pair: a row is a contiguous range [a, b] of tile ids, so the
+// low digit (t & 255) gets a wrapped range increment (difference array d0 +
+// a count base0 added to every digit) and each higher digit (t >> 8p) is
+// constant over whole 256^p-aligned segments (one add per segment).
+__device__ __forceinline__ void hist_rect(uint32_t* s_h, int* d0, int* base0, int passes,
+                                          uint64_t rc, int ntx, int tbase) {
+  const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
+  const int ty0 = static_cast<int>((rc >> 32) & 0xffff), ty1 = static_cast<int>((rc >> 48) & 0xffff);
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    const uint32_t a = static_cast<uint32_t>(tbase + ty * ntx + tx0);
+    const uint32_t b = a + static_cast<uint32_t>(tx1 - tx0);
+    const uint32_t len = b - a + 1u;
+    if (len >> 8) atomicAdd(base0, static_cast<int>(len >> 8));
+    const uint32_t rem = len & 255u;
+    if (rem) {
+      const uint32_t st = a & 255u, en = st + rem;  // digits [st, en) mod 256
+      atomicAdd(&d0[st], 1);
+      if (en <= 256u) {
+        atomicAdd(&d0[en], -1);
+      } else {
+        atomicAdd(&d0[256], -1);
+        atomicAdd(&d0[0], 1);
+        atomicAdd(&d0[en - 256u], -1);
+      }
+    }
+    for (int p = 1; p < passes; ++p) {
+      const int sh = 8 * p;
+      for (uint32_t seg = a >> sh; seg <= (b >> sh); ++seg) {
+        const uint32_t lo = max(a, seg << sh), hi = min(b, ((seg + 1u) << sh) - 1u);
+        atomicAdd(&s_h[p * 256 + (seg & 255u)], hi - lo + 1u);
+      }
+    }
+  }
+}
+
 template <typename KT>
 __device__ __forceinline__ void emit_warps(
     const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
     const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
     FrameHeader* __restrict__ hdr, const FrameDesc& fd, int64_t n, uint32_t* __restrict__ long_list,
-    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int key_bits) {
+    KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int* d0, int* base0,
+    int key_bits) {
   const int passes = (key_bits + 7) / 8;
   if (hdr->stats.overflow) return;
   const int lane = threadIdx.x & 31;
@@ -372,6 +409,7 @@ __device__ __forceinline__ void emit_warps(
     const int v = ok ? static_cast<int>(s / static_cast<uint32_t>(n)) : 0;
     const int ntx = fd.cam[v].ntx;
     const int tbase = fd.cam[v].tile_base;
+    if (c) hist_rect(s_h, d0, base0, passes, rc, ntx, tbase);
     for (uint32_t q0 = 0; q0 < total; q0 += 32) {
       const uint32_t q = q0 + lane;
       const uint32_t end = loc + c;
@@ -387,12 +425,10 @@ __device__ __forceinline__ void emit_warps(
       const int nt = __shfl_sync(kFull, ntx, own);
       const int tb = __shfl_sync(kFull, tbase, own);
       const uint32_t so = __shfl_sync(kFull, s, own);
-      uint32_t key = 0;
       if (q < total) {
         const int k = static_cast<int>(q - lo2);
-        key = emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
+        emit_one<KT>(oo + k, k, rco, nt, tb, so, keys, vals);
       }
-      hist_keys<KT>(s_h, passes, key_bits, key, q < total, lane);
     }
   }
 }
@@ -405,9 +441,36 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
     KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int key_bits) {
   const int passes = (key_bits + 7) / 8;
   __shared__ uint32_t s_h[4 * 256];  // tile sort digit histogram (this CTA's pairs)
+  __shared__ int s_d0[257];          // low digit as a difference array
+  __shared__ int s_base0;
   for (int k = threadIdx.x; k < passes * 256; k += blockDim.x) s_h[k] = 0;
+  for (int k = threadIdx.x; k < 257; k += blockDim.x) s_d0[k] = 0;
+  if (threadIdx.x == 0) s_base0 = 0;
   __syncthreads();
-  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, key_bits);
+  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, s_d0,
+                 &s_base0, key_bits);
+  __syncthreads();
+  if (threadIdx.x < 32) {  // low digit: prefix sum of the difference array (8 per lane)
+    const int lane = threadIdx.x;
+    int v8[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      v8[k] = s_d0[lane * 8 + k];
+      sum += v8[k];
+    }
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int run = inc - sum + s_base0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      run += v8[k];
+      s_h[lane * 8 + k] += static_cast<uint32_t>(run);
+    }
+  }
   __syncthreads();
   for (int k = threadIdx.x; k < passes * 256; k += blockDim.x)
     if (s_h[k]) atomicAdd(&hist[k], s_h[k]);
