@@ -216,6 +216,9 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
 // 4-pass digit histogram (warp-aggregated shared counters, one global
 // atomic per non-zero bin per CTA) so the sort skips its histogram pass.
 template <int DEG>
+#ifndef CGS_PROJECT_HIST_DIRECT
+#define CGS_PROJECT_HIST_DIRECT 1
+#endif
 #ifndef CGS_PROJECT_VIEW_INNER
 #define CGS_PROJECT_VIEW_INNER 1
 #endif
@@ -239,12 +242,26 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
 #endif
     const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0u;
     const unsigned valid = __ballot_sync(kFull, ok);
+#if CGS_PROJECT_HIST_DIRECT
+    // low three bytes of a depth key are spread over the digits: one shared
+    // atomic per lane is cheaper than eight ballots; the top byte (sign and
+    // high exponent bits) takes few values, so it is warp-aggregated
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+      if (ok) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
+    {
+      const unsigned d = key >> 24;
+      const unsigned peers = warp_peers8(d) & valid;
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[3 * 256 + d], __popc(peers));
+    }
+#else
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       const unsigned d = (key >> (8 * p)) & 255u;
       const unsigned peers = warp_peers8(d) & valid;
       if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
     }
+#endif
   }
   __syncthreads();
   for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x)
