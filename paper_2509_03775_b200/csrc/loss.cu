@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
 
 // dL/dimage: adjoint filtering of the three seed maps (metrics.py:40-45, the
 // window is symmetric) fused with the L1 sign term; 32x32 pixels per CTA.
-__global__ void __launch_bounds__(256) ssim_grad_kernel(const float* __restrict__ img,
+#ifndef CGS_SSIMG_MINB
+#define CGS_SSIMG_MINB 4
+#endif
+__global__ void __launch_bounds__(256, CGS_SSIMG_MINB) ssim_grad_kernel(const float* __restrict__ img,
                                                         const float* __restrict__ gt, int H, int W,
                                                         double lam, double inv_size,
                                                         double inv_count, float grad_scale,

@@ -89,7 +89,10 @@ __device__ __forceinline__ T warp_sum(T v) {
 // order.  Status words: value in bits 0..61, flag in 62..63.
 // ===========================================================================
 constexpr int kScanWarps = 8;
-constexpr int kScanRounds = 8;
+#ifndef CGS_SCAN_ROUNDS
+#define CGS_SCAN_ROUNDS 8
+#endif
+constexpr int kScanRounds = CGS_SCAN_ROUNDS;
 constexpr int kScanTile = kScanWarps * kScanRounds * 32;  // 2048
 constexpr unsigned long long kScanAgg = 1ULL << 62;
 constexpr unsigned long long kScanPre = 2ULL << 62;
