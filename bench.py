@@ -562,6 +562,12 @@ def main():
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     views_done = 0
+    # Python's cyclic GC is paused inside the timed loops (collected just
+    # before), as timeit does: a generation-2 pass is a host stall unrelated
+    # to the workload.  The trainer itself allocates no Python cycles.
+    import gc
+    gc.collect()
+    gc.disable()
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -577,6 +583,7 @@ def main():
         views_done += len(cams)
     torch.cuda.synchronize()
     barrier()
+    gc.enable()
     clk = clocks.stop()
     # ABI launch calls + kernels executed by graph replays - calls recorded
     # (not executed) while capturing
@@ -666,6 +673,8 @@ def main():
                 dev_gt[b].copy_(host_gt, non_blocking=True)
                 up_done[b].record(copy_st)
 
+        gc.collect()
+        gc.disable()
         barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
@@ -685,6 +694,7 @@ def main():
             e_e[k].record()
         torch.cuda.synchronize()
         barrier()
+        gc.enable()
         tr.check()
         e_ms = sum(s.elapsed_time(e) for s, e in zip(e_s, e_e))
         if world > 1:
@@ -714,6 +724,7 @@ def main():
                           "l2": "flushed (256 MB write) between timed iterations"
                           if not args.no_flush else "not flushed",
                           "targets": "8-bit RGB (the reference's PNG inputs), uint8 upload in e2e",
+                          "python_gc": "cyclic GC collected before and paused inside the timed loops",
                           "mcmc_every": args.mcmc_every,
                           "sgld_noise": f"device Philox, noise_pos={args.noise_pos} (reference default 1.0 "
                                         "diffuses the scene out of view; see DESIGN.md)",
