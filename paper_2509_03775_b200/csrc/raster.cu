@@ -445,50 +445,69 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
                                                           int total_tiles,
                                                           uint2* __restrict__ units,
                                                           uint32_t* __restrict__ ctl) {
+  // Full chunks (length kChunk, the longest) first, in tile order, placed by
+  // a block scan of per-tile counts (no shared-atomic contention on one
+  // bucket); then the partial last chunks by length, longest first, through
+  // 256 length buckets.
   __shared__ uint32_t cnt[256];
-  __shared__ uint32_t s_total;
-  const int tid = threadIdx.x;
-  auto bucket = [](uint32_t w) -> uint32_t {  // w in [1, kChunk]
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_full;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto bucket = [](uint32_t w) -> uint32_t {  // w in [1, kChunk)
     return 255u - min(255u, ((w - 1u) * 256u) / kChunk);
   };
   if (tid < 256) cnt[tid] = 0;
+  if (tid == 0) s_full = 0;
   __syncthreads();
+  uint32_t full = 0;
   for (int t = tid; t < total_tiles; t += blockDim.x) {
     const uint32_t np = nproc[t];
-    for (uint32_t k0 = 0; k0 < np; k0 += kChunk) atomicAdd(&cnt[bucket(min(np - k0, uint32_t(kChunk)))], 1u);
+    full += np / kChunk;
+    if (np % kChunk) atomicAdd(&cnt[bucket(np % kChunk)], 1u);
   }
+  full = warp_incl_scan(full);
+  if (lane == 31 && full) atomicAdd(&s_full, full);
   __syncthreads();
-  if (tid < 32) {  // exclusive scan of 256 counts, 8 per lane
+  if (tid < 32) {  // exclusive scan of the 256 partial buckets, after the full chunks
     uint32_t c[8], sum = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       c[k] = cnt[tid * 8 + k];
       sum += c[k];
     }
-    uint32_t inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, inc, o);
-      if (tid >= o) inc += y;
-    }
-    uint32_t run = inc - sum;
+    uint32_t inc = warp_incl_scan(sum);
+    uint32_t run = inc - sum + s_full;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       cnt[tid * 8 + k] = run;
       run += c[k];
     }
-    if (tid == 31) s_total = inc;
+    if (tid == 31) {
+      ctl[0] = run;  // all units
+      ctl[1] = 0u;
+    }
   }
   __syncthreads();
-  for (int t = tid; t < total_tiles; t += blockDim.x) {
-    const uint32_t np = nproc[t];
-    for (uint32_t k0 = 0; k0 < np; k0 += kChunk)
-      units[atomicAdd(&cnt[bucket(min(np - k0, uint32_t(kChunk)))], 1u)] =
-          make_uint2(static_cast<uint32_t>(t), k0 / kChunk);
-  }
-  if (tid == 0) {
-    ctl[0] = s_total;
-    ctl[1] = 0u;
+  uint32_t base = 0;
+  for (int t0 = 0; t0 < total_tiles; t0 += blockDim.x) {
+    const int t = t0 + tid;
+    const uint32_t np = t < total_tiles ? nproc[t] : 0u;
+    const uint32_t nf = np / kChunk;
+    const uint32_t inc = warp_incl_scan(nf);
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      const uint32_t x = s_warp[w];
+      if (w < warp) wpre += x;
+      tot += x;
+    }
+    const uint32_t off = base + wpre + inc - nf;
+    for (uint32_t c = 0; c < nf; ++c) units[off + c] = make_uint2(static_cast<uint32_t>(t), c);
+    if (np % kChunk)
+      units[atomicAdd(&cnt[bucket(np % kChunk)], 1u)] = make_uint2(static_cast<uint32_t>(t), nf);
+    base += tot;
+    __syncthreads();
   }
 }
 
