@@ -229,7 +229,11 @@ def run_reference(args):
     if rank != 0:
         return 0
     run, cores, sample, pool = cpu_iteration_timer(args.config, args.seed)
-    first = run()  # warm-up (at most one; a CPU has nothing to warm beyond caches)
+    first = run()  # warm-up: the requested W (>= 1), bounded to ~30 s of CPU work
+    n_warm = 1
+    while n_warm < args.warmup and first * (n_warm + 1) <= 30.0:
+        run()
+        n_warm += 1
     budget = 150.0
     k_eff = max(2, min(args.steps, int(budget / max(first, 1e-3))))
     times = [run() for _ in range(k_eff)]
@@ -237,7 +241,7 @@ def run_reference(args):
     total = sum(times)
     value = k_eff / total
     out = {"impl": "reference", "metric": "train iters/s", "value": value, "unit": "it/s",
-           "n_gpus": args.gpus, "steps": k_eff, "warmup": 1, "ms_per_step": 1000 * total / k_eff,
+           "n_gpus": args.gpus, "steps": k_eff, "warmup": n_warm, "ms_per_step": 1000 * total / k_eff,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded scene, SURVEY.md §8(d))",
            "config": {"workload": workload_name(args.config), "seed": args.seed},
