@@ -86,6 +86,17 @@ typedef struct cgs_frame_stats {
   int32_t zero_quaternion; /* a visible splat uses a zero quaternion (ValueError,
                               render.py:40-41); its splat is dropped           */
   int32_t pad_;
+  int64_t n_refined_tiles; /* tiles whose flagged pixels were re-walked in
+                              float64 (an fp32 alpha within 2e-5 of 1/255 or
+                              0.99, or fp32 T within 5e-5 of 1e-4)           */
+  int64_t n_refined_pixels; /* those pixels                                  */
+  int64_t diag_last_mismatch;  /* pixels flagged by the T band (by default); */
+  int64_t diag_count_mismatch; /* by an alpha band.  Diagnostics builds        */
+                               /* (CGS_REFINE_ALL, every pixel re-walked):     */
+                               /* pixels where the fp32 path alone decides the */
+                               /* last index / the count differently           */
+  float diag_max_T_err;        /* CGS_REFINE_ALL: largest fp32 T and alpha     */
+  float diag_max_alpha_err;    /* relative errors against float64              */
 } cgs_frame_stats_t;
 
 /* SGLD parameters, reference sampler.py:262-300 + SamplerConfig :45-55. */

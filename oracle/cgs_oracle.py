@@ -476,8 +476,14 @@ def raster_forward(st: OState, cam: OCam) -> dict:
     return dict(image=img, final_T=T, counts=cnt, tile_offsets=offs, tile_ids=ids, proj=proj)
 
 
-def raster_backward(st: OState, cam: OCam, dL: np.ndarray) -> dict:
-    """rasterize_backward + _pull_back (render.py:318-459), float64."""
+def raster_backward(st: OState, cam: OCam, dL: np.ndarray, screen: bool = False,
+                    perturb=None) -> dict:
+    """rasterize_backward + _pull_back (render.py:318-459), float64.
+
+    Diagnostics (defaults reproduce the reference): ``screen=True`` also
+    returns the screen-space sums (d_color, d_opac, d_mean2d, d_conic) per
+    visible splat; ``perturb(name, array)`` may replace the per-pixel terms
+    alpha / t_before / suffix (precision-sensitivity studies)."""
     dL = np.asarray(dL, np.float64)
     if dL.shape != (cam.height, cam.width, 3):
         raise ValueError("dL_dimage shape mismatch")
@@ -499,31 +505,61 @@ def raster_backward(st: OState, cam: OCam, dL: np.ndarray) -> dict:
         # suffix sums run back to front across chunks (render.py:354-355)
         tail = np.zeros((px.shape[0], 3))
         for rows, al, keep, active, tb, dx, dy in reversed(chunks):
+            if perturb is not None:
+                al, tb = perturb("alpha", al), perturb("t_before", tb)
             w = al * tb * active
             col = proj["colors"][rows]
             contrib = w[:, :, None] * col[:, None, :]
             csum = np.cumsum(contrib[::-1], axis=0)[::-1]
             suffix = csum - contrib + tail[None]
+            if perturb is not None:
+                suffix = perturb("suffix", suffix)
             tail = tail + csum[0] if len(rows) else tail
-            np.add.at(g_col, rows, w @ gp)
+            pt = (lambda n, x: perturb(n, x)) if perturb is not None else (lambda n, x: x)
+            np.add.at(g_col, rows, pt("tile_sum", w @ gp))
             dCda = col[:, None, :] * tb[:, :, None] - suffix / (1.0 - al)[:, :, None]
             da = np.sum(dCda * gp[None], axis=2)
             da = np.where(keep & active & (al < A_CLAMP), da, 0.0)
-            np.add.at(g_op, rows, np.sum(da * al, axis=1) / proj["opac"][rows])
+            np.add.at(g_op, rows, pt("tile_sum", np.sum(da * al, axis=1) / proj["opac"][rows]))
             dp = da * al
             Q = proj["conic"][rows]
             qx = Q[:, 0, 0, None] * dx + Q[:, 0, 1, None] * dy
             qy = Q[:, 0, 1, None] * dx + Q[:, 1, 1, None] * dy
-            np.add.at(g_mean, rows, np.stack([np.sum(dp * qx, 1), np.sum(dp * qy, 1)], 1))
-            np.add.at(g_con, rows, np.stack([np.sum(dp * (-0.5 * dx * dx), 1),
-                                             np.sum(dp * (-dx * dy), 1),
-                                             np.sum(dp * (-0.5 * dy * dy), 1)], 1))
+            if perturb is not None and perturb("local_moments", None) is not None:
+                # moments about the tile's first pixel centre, perturbed, then
+                # shifted to the splat centre in fp64 (GPU representation study)
+                lx = px - px[0]
+                ly = py - py[0]
+                mom = np.stack([dp.sum(1), (dp * lx).sum(1), (dp * ly).sum(1), (dp * lx * lx).sum(1),
+                                (dp * lx * ly).sum(1), (dp * ly * ly).sum(1)], 1)
+                mom = perturb("local_moments", mom)
+                ox = (px[0] - proj["mean2d"][rows, 0])
+                oy = (py[0] - proj["mean2d"][rows, 1])
+                m0, mx, my, mxx, mxy, myy = mom.T
+                sx = ox * m0 + mx
+                sy = oy * m0 + my
+                sxx = ox * ox * m0 + 2 * ox * mx + mxx
+                sxy = ox * oy * m0 + ox * my + oy * mx + mxy
+                syy = oy * oy * m0 + 2 * oy * my + myy
+                A, B, C = Q[:, 0, 0], Q[:, 0, 1], Q[:, 1, 1]
+                np.add.at(g_mean, rows, np.stack([A * sx + B * sy, B * sx + C * sy], 1))
+                np.add.at(g_con, rows, np.stack([-0.5 * sxx, -sxy, -0.5 * syy], 1))
+                continue
+            np.add.at(g_mean, rows, pt("tile_sum", np.stack([np.sum(dp * qx, 1), np.sum(dp * qy, 1)], 1)))
+            np.add.at(g_con, rows, pt("tile_sum", np.stack([np.sum(dp * (-0.5 * dx * dx), 1),
+                                                            np.sum(dp * (-dx * dy), 1),
+                                                            np.sum(dp * (-0.5 * dy * dy), 1)], 1)))
     # rows index the visible arrays directly (sel values are visible positions)
-    return pull_back(st, cam, proj, g_col, g_op, g_mean, g_con)
+    out = pull_back(st, cam, proj, g_col, g_op, g_mean, g_con, perturb=perturb)
+    if screen:
+        return out, dict(g_col=g_col, g_op=g_op, g_mean=g_mean, g_con=g_con, proj=proj)
+    return out
 
 
-def pull_back(st: OState, cam: OCam, proj: dict, g_col, g_op, g_mean, g_con) -> dict:
-    """Chain screen-space gradients to model parameters (render.py:382-459)."""
+def pull_back(st: OState, cam: OCam, proj: dict, g_col, g_op, g_mean, g_con, perturb=None) -> dict:
+    """Chain screen-space gradients to model parameters (render.py:382-459).
+    ``perturb`` (diagnostics only) may replace dSigma3 and the view term."""
+    pt = (lambda n, x: perturb(n, x)) if perturb is not None else (lambda n, x: x)
     idx = proj["idx"]
     t = proj["t"]
     x, y, z = t[:, 0], t[:, 1], t[:, 2]
@@ -536,7 +572,7 @@ def pull_back(st: OState, cam: OCam, proj: dict, g_col, g_op, g_mean, g_con) -> 
     dS2 = -(Q @ dQ @ Q)
     M = proj["M"]
     Mt = np.swapaxes(M, 1, 2)
-    dS3 = Mt @ dS2 @ M
+    dS3 = pt("dS3", Mt @ dS2 @ M)
     dM = 2.0 * (dS2 @ M @ proj["cov3d"])
     dJ = dM @ cam.R.T
     z2, z3 = z * z, z * z * z
@@ -556,7 +592,7 @@ def pull_back(st: OState, cam: OCam, proj: dict, g_col, g_op, g_mean, g_con) -> 
         dview = np.sum(np.sum(draw[:, None, :, None] * proj["coeffs"][:, :, :, None]
                               * Bg[:, :, None, :], axis=2), axis=1)
         v = proj["viewdir"]
-        dpos = dpos + (dview - v * np.sum(v * dview, axis=1, keepdims=True)) / proj["viewlen"][:, None]
+        dpos = dpos + pt("dview", (dview - v * np.sum(v * dview, axis=1, keepdims=True)) / proj["viewlen"][:, None])
     rows = st.sr.rows[st.g2sr[idx]].astype(np.float64)
     qr = rows[:, 3:7]
     qn = quat_unit(qr)

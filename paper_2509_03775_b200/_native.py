@@ -46,6 +46,12 @@ class CFrameStats(ctypes.Structure):
         ("n_views", ctypes.c_int32),
         ("zero_quaternion", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
+        ("n_refined_tiles", ctypes.c_int64),
+        ("n_refined_pixels", ctypes.c_int64),
+        ("diag_last_mismatch", ctypes.c_int64),
+        ("diag_count_mismatch", ctypes.c_int64),
+        ("diag_max_T_err", ctypes.c_float),
+        ("diag_max_alpha_err", ctypes.c_float),
     ]
 
 

@@ -69,7 +69,8 @@ int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout&
 int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
 int frame_stage_duplicate(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
 int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st);
-int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, float* image, float* final_T,
+int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, const float* logits, float* image,
+                       float* final_T,
                        int32_t* counts, cudaStream_t st);
 struct BwdLayout;
 int bwd_stage_entry(int stage, const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
@@ -287,7 +288,7 @@ int cgs_raster_fwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n
                    void* workspace, size_t workspace_bytes, int64_t pair_capacity, float* image,
                    float* final_T, int32_t* contrib_counts, cgs_stream_t stream) {
   CGS_STAGE_PROLOGUE;
-  return frame_stage_raster(fd, L, image, final_T, contrib_counts, st);
+  return frame_stage_raster(fd, L, scene->opacity_logits, image, final_T, contrib_counts, st);
 }
 
 int cgs_frame_stats(const void* workspace, cgs_frame_stats_t* out, cgs_stream_t stream) {

@@ -6,6 +6,16 @@
 
 namespace cgs {
 
+// Pixels the fp32 raster flags (a value inside a decision band, see
+// raster_common.cuh) are re-walked in float64 (refine.cu); px_last of such a
+// pixel carries kRefinedBit.
+constexpr uint32_t kRefinedBit = 0x80000000u;
+struct RefinePx {  // float64 result of a re-walked pixel (forward -> backward)
+  double C[3];
+  double T;
+  uint32_t last;
+  uint32_t pad;
+};
 
 // Splats with more tile pairs than this (near-plane giants cover every tile)
 // are emitted and reduced by a whole CTA each, from a list built during
@@ -50,6 +60,11 @@ struct FrameLayout {
   uint32_t* tile_nproc;    // total_tiles
   uint32_t* tile_order;    // total_tiles: raster CTA -> tile, longest work first
   float4* ckpt;            // n_ckpt x 256: per-pixel (T, colour suffix) at chunk boundaries
+  uint32_t* refine_tiles;  // total_tiles: tiles with pixels to re-walk in float64 (count: hdr->scratch[3])
+  uint32_t* refine_mask;   // 8 x total_tiles: per-warp masks of those pixels
+  uint32_t* refine_off;    // total_tiles: first RefinePx entry of each listed tile
+  RefinePx* refine_px;     // refine_px_cap float64 results of re-walked pixels
+  int64_t refine_px_cap;
   uint2* units;            // n_ckpt: backward work units (tile, chunk), longest first
   uint32_t* unit_ctl;      // [0] unit count, [1] fetch counter
   int64_t n_ckpt;
@@ -133,6 +148,11 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.tile_order = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.n_ckpt = fd.total_tiles + pc / kChunk + 2;
   L.ckpt = c.take<float4>(L.n_ckpt * 256);
+  L.refine_tiles = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.refine_mask = c.take<uint32_t>(8 * static_cast<int64_t>(fd.total_tiles > 0 ? fd.total_tiles : 1));
+  L.refine_off = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.refine_px_cap = fd.total_pixels / 64 + 16384;
+  L.refine_px = c.take<RefinePx>(L.refine_px_cap);
   L.units = c.take<uint2>(L.n_ckpt);
   L.unit_ctl = c.take<uint32_t>(2);
   L.scan = carve_scan(c, vn1 > fd.total_tiles ? vn1 : fd.total_tiles);
@@ -154,10 +174,17 @@ inline uint32_t* sorted_pair_vals(const FrameLayout& L) {
 int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
                       cudaStream_t st);
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
-                      float* image, float* final_T, int32_t* counts, cudaStream_t st);
+                      const float* logits, float* image, float* final_T, int32_t* counts,
+                      cudaStream_t st);
+// Float64 re-walk of the flagged pixels (refine.cu): bwd = false rewrites
+// their forward outputs; bwd = true adds their gradient terms to the pairs'
+// partials after raster_bwd (which skips them).
+int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
+                  const float* logits, float* image, float* final_T, int32_t* counts,
+                  const float* dL, float* partials, cudaStream_t st);
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
-                      cudaStream_t st);
+                      const float* logits, cudaStream_t st);
 
 // Emission index of pair (splat s, tile t): pairs of a splat are emitted in
 // row-major order over its tile rect starting at pair_off[s].

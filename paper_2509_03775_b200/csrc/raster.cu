@@ -26,6 +26,10 @@
 
 namespace cgs {
 
+#ifndef CGS_FWD_NOBAND  // timing experiments only: no flagging (not exact)
+#define CGS_FWD_NOBAND 0
+#endif
+
 // Tile-local inclusive contribution box of a splat as 4 signed bytes
 // (x0, x1, y0, y1), clamped to [-1, 16] (an empty box has x0 = 16: no hit).
 __device__ __forceinline__ uint32_t local_rect(const SplatRec& r, int tx0, int ty0) {
@@ -84,26 +88,36 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
     for (int t = tid; t < total_tiles; t += blockDim.x) zero_a[t] = zero_b[t] = 0u;
 }
 
+// Per-pixel forward state, packed for register pressure (the forward runs
+// at 40 registers): `last` doubles as the done flag (last index + 1 once the
+// pixel terminated; pixels outside the image start done with last = 1) and
+// bit 31 of `cnt` is the float64 re-walk flag (T came within kTBand of 1e-4,
+// or an alpha within kAlphaBand of 1/255 or 0.99: refine.cu).
 struct PixState {
   float T, r, g, b;
   int cnt;
   uint32_t last;
-  bool done;
+  __device__ __forceinline__ bool done() const { return last != 0u; }
+  __device__ __forceinline__ void flag() { cnt |= 0x80000000; }
+  __device__ __forceinline__ bool flagged() const { return cnt < 0; }
+  __device__ __forceinline__ int count() const { return cnt & 0x7fffffff; }
 };
 
 // Front-to-back blend of one splat into one pixel (render.py:274-283, 302-311).
 __device__ __forceinline__ void blend(PixState& p, float al, float cr, float cg, float cb,
                                       uint32_t idx) {
-  if (p.done || !(al >= kAlphaSkipF)) return;
+  if (p.done() || !(al >= kAlphaSkipF)) return;
   const float w = al * p.T;
   p.r = fmaf(w, cr, p.r);
   p.g = fmaf(w, cg, p.g);
   p.b = fmaf(w, cb, p.b);
   p.T = p.T * (1.0f - al);
   ++p.cnt;
-  if (!(p.T >= kTMinF)) {  // every later splat is inactive (T_before < 1e-4)
-    p.done = true;
-    p.last = idx + 1;
+  if (p.T < kTBandHi) {  // rare: near or past the termination threshold
+#if !CGS_FWD_NOBAND
+    if (p.T >= kTBandLo) p.flag();  // the float64 chain may fall on either side
+#endif
+    if (!(p.T >= kTMinF)) p.last = idx + 1;  // every later splat is inactive (T_before < 1e-4)
   }
 }
 
@@ -153,33 +167,29 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
   return m;
 }
 
-// HALVES = 2 splits every tile over two CTAs of 128 threads (rows 0-7 and
-// 8-15, batches of 128 splats): a tile's blend is sequential in its list, so
-// one CTA per tile makes the longest list the kernel's floor; two CTAs halve
-// it for the price of staging each record twice.  Per-tile results (processed
-// count, last rank) are combined with atomicMax (zeroed by tile_order_kernel).
 #ifndef CGS_FWD_PAIRS
 #define CGS_FWD_PAIRS 1
 #endif
-#ifndef CGS_FWD_HALVES
-#define CGS_FWD_HALVES 1
-#endif
 #ifndef CGS_FWD_MINB
-#define CGS_FWD_MINB (CGS_FWD_HALVES == 2 ? 12 : 6)
+#define CGS_FWD_MINB 6
 #endif
-constexpr int kFwdHalves = CGS_FWD_HALVES;
-constexpr int kFwdThreads = 256 / kFwdHalves;  // one pixel per thread
-constexpr int kFwdBatch = 256 / kFwdHalves;
+// Diagnostics: CGS_REFINE_ALL=1 flags every pixel for the float64 re-walk
+// (the refine kernels then also record how far the fp32 path was from it).
+#ifndef CGS_REFINE_ALL
+#define CGS_REFINE_ALL 0
+#endif
+constexpr int kFwdThreads = 256;  // one pixel per thread
+constexpr int kFwdBatch = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
 static_assert(kChunk % kFwdBatch == 0, "checkpoints sit on batch boundaries");
-
 __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
-    const FrameHeader* __restrict__ hdr, float* __restrict__ image,
+    FrameHeader* __restrict__ hdr, float* __restrict__ image,
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
     uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
     uint32_t* __restrict__ last_rank, float4* __restrict__ ckpt,
+    uint32_t* __restrict__ refine_tiles, uint32_t* __restrict__ refine_mask,
     unsigned long long* __restrict__ trace) {
   constexpr int B = kFwdBatch, NT = kFwdThreads;
   const unsigned long long t_start = trace ? global_ns() : 0ull;
@@ -192,26 +202,38 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   __shared__ uint32_t s_max[kFwdWarps];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
-  const int half = kFwdHalves == 2 ? static_cast<int>(blockIdx.x & 1u) : 0;
-  const int tile = static_cast<int>(order[blockIdx.x / kFwdHalves]);
+  const int tile = static_cast<int>(order[blockIdx.x]);
   int v = 0;
   while (v + 1 < fd.n_views && fd.cam[v + 1].tile_base <= tile) ++v;
   const CamDev& cam = fd.cam[v];
   const int lt = tile - cam.tile_base;
   const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wb = warp + half * kFwdWarps;  // 8x4 block index within the tile
-  const int lx = (wb & 1) * 8 + (lane & 7), ly = (wb >> 1) * 4 + (lane >> 3);
+  const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool in = px < cam.width && py < cam.height;
   const uint2 rg = ranges[tile];
   const int n = static_cast<int>(rg.y - rg.x);
-  const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
-  const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+  const double cx = tile_centre(tx), cy = tile_centre(ty);
+  const float flx = static_cast<float>(lx) - kTileHalf, fly = static_cast<float>(ly) - kTileHalf;
   uint8_t* my_list = s_list[warp];
-  PixState p{1.0f, 0.0f, 0.0f, 0.0f, 0, 0u, !in};
+  PixState p{1.0f, 0.0f, 0.0f, 0.0f, CGS_REFINE_ALL ? static_cast<int>(0x80000000) : 0, in ? 0u : 1u};
   int n_ckpt = 0;
-
+  // fp32 alpha to blend (render.py:274-279); the caller keeps it when it is
+  // >= kAlphaSkipF.  A pixel that meets a value within the decision bands of
+  // raster_common.cuh is flagged for the float64 re-walk (refine.cu), which
+  // overwrites it: |t| < band (keep), t near log2(0.99 * 255) (clamp; looked
+  // at only once t reaches the band).
+  auto eval = [&](const float4& a, const float4& b) -> float {
+    const float t = staged_t(a, b, flx, fly);
+#if !CGS_FWD_NOBAND
+    if (fabsf(t) < kTSkipHi) p.flag();
+    if (t >= kTClampLo) {
+      if (t < kTClampHi) p.flag();
+    }
+#endif
+    return alpha_of_t(t);
+  };
   if (tid == 0) mbar_init(&s_bar, 1);
   __syncthreads();
   uint32_t phase = 0;
@@ -226,12 +248,11 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     phase ^= 1;
     pending = false;
     if (tid < nb) {
-      const Staged sg = stage_splat(s_raw[tid], ox, oy);
+      const Staged sg = stage_splat(s_raw[tid], cx, cy);
       s_a[tid] = sg.a;
       s_b[tid] = sg.b;
       s_c[tid] = sg.c;
-      const uint32_t m8 = block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile));
-      s_mask[tid] = static_cast<uint8_t>(m8 >> (half * kFwdWarps));
+      s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
     }
     __syncthreads();
     if (b0 + B < n) {
@@ -240,7 +261,7 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       pending = true;
     }
     const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
-    if (!p.done) {
+    if (!p.done()) {
 #if CGS_FWD_PAIRS
       // two hits per iteration: both alphas are independent of the blend
       // state, so they issue together; the blends stay in list order
@@ -249,26 +270,23 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
         const int j0 = my_list[i], j1 = my_list[i + 1];
         const float4 a0 = s_a[j0], b0v = s_b[j0];
         const float4 a1 = s_a[j1], b1v = s_b[j1];
-        float u, v;
-        const float al0 = staged_alpha(a0, b0v, flx, fly, u, v);
-        const float al1 = staged_alpha(a1, b1v, flx, fly, u, v);
+        const float al0 = eval(a0, b0v);
+        const float al1 = eval(a1, b1v);
         if (al0 >= kAlphaSkipF) {
           const float2 c = s_c[j0];
           blend(p, al0, b0v.w, c.x, c.y, static_cast<uint32_t>(b0 + j0));
-          if (p.done) break;
+          if (p.done()) break;
         }
         if (al1 >= kAlphaSkipF) {
           const float2 c = s_c[j1];
           blend(p, al1, b1v.w, c.x, c.y, static_cast<uint32_t>(b0 + j1));
-          if (p.done) break;
+          if (p.done()) break;
         }
       }
-      if (!p.done && i < hits) {
+      if (!p.done() && i < hits) {
         const int j = my_list[i];
-        const float4 a = s_a[j];
-        const float4 b = s_b[j];
-        float u, v;
-        const float al = staged_alpha(a, b, flx, fly, u, v);
+        const float4 a = s_a[j], b = s_b[j];
+        const float al = eval(a, b);
         if (al >= kAlphaSkipF) {
           const float2 c = s_c[j];
           blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
@@ -277,19 +295,17 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
 #else
       for (int i = 0; i < hits; ++i) {
         const int j = my_list[i];
-        const float4 a = s_a[j];
-        const float4 b = s_b[j];
-        float u, v;
-        const float al = staged_alpha(a, b, flx, fly, u, v);
+        const float4 a = s_a[j], b = s_b[j];
+        const float al = eval(a, b);
         if (al >= kAlphaSkipF) {
           const float2 c = s_c[j];
           blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
-          if (p.done) break;
+          if (p.done()) break;
         }
       }
 #endif
     }
-    if (__syncthreads_count(p.done) == NT) break;
+    if (__syncthreads_count(p.done()) == NT) break;
     if (b0 + B < n && ((b0 + B) % kChunk) == 0) {  // chunk boundary for the backward
       // T after the chunk and the chunk's own colour sum; colour restarts at 0
       ckpt[ckpt_slot(rg.x, tile, (b0 + B) / kChunk) * kTilePixels + ly * kTile + lx] =
@@ -310,15 +326,22 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     p.g += q.z;
     p.b += q.w;
   }
-  if (in && !p.done) p.last = static_cast<uint32_t>(n);
+  if (in && !p.done()) p.last = static_cast<uint32_t>(n);
   if (in) {
     const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
     image[3 * pix + 0] = p.r;
     image[3 * pix + 1] = p.g;
     image[3 * pix + 2] = p.b;
     final_T[pix] = p.T;
-    counts[pix] = p.cnt;
+    counts[pix] = p.count();
     px_last[pix] = p.last;
+  }
+  {  // flagged pixels: per-warp masks and the tile in the re-walk list
+    const unsigned bal = __ballot_sync(kFull, in && p.flagged());
+    if (__syncthreads_or(bal != 0u)) {
+      if (lane == 0) refine_mask[static_cast<int64_t>(tile) * kFwdWarps + warp] = bal;
+      if (tid == 0) refine_tiles[atomicAdd(&hdr->scratch[3], 1ull)] = static_cast<uint32_t>(tile);
+    }
   }
   uint32_t m = in ? p.last : 0u;
 #pragma unroll
@@ -330,15 +353,10 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
 #pragma unroll
     for (int w = 0; w < kFwdWarps; ++w) np = max(np, s_max[w]);
     const uint32_t lr = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;  // ranks grow along the list
-    if (kFwdHalves == 1) {
-      tile_nproc[tile] = np;
-      last_rank[tile] = lr;
-    } else {
-      atomicMax(&tile_nproc[tile], np);
-      atomicMax(&last_rank[tile], lr);
-    }
+    tile_nproc[tile] = np;
+    last_rank[tile] = lr;
     if (trace) {
-      unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x / kFwdHalves);
+      unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x);
       t[0] = t_start;
       t[1] = global_ns();
       t[2] = smid();
@@ -367,14 +385,27 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 
 // Adds pixel p's contribution of splat k to o[9]; returns whether it had one.
-// o = [sum w g (3), sum dp, sum dp u, sum dp v, sum dp u^2, sum dp u v,
-// sum dp v^2] with dp = dL/dalpha * alpha and (u, v) the pixel offset in the
-// conic's eigenbasis (passed as dx, dy): the per-splat gradient is a linear
-// map of these moments (moments_to_grad), applied once per splat after the
-// pixel sums instead of per pixel.
-__device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, float cr, float cg,
-                                          float cb, float dx, float dy, float* o) {
-  if (!(k < p.last) || !(al >= kAlphaSkipF)) return false;
+// o = [sum w g (3), sum dp, sum dp lx, sum dp ly, sum dp lx^2, sum dp lx ly,
+// sum dp ly^2] with dp = dL/dalpha * alpha and (lx, ly) the pixel's offset
+// from the tile centre.  The moments stay in these small local coordinates:
+// splat_reduce shifts them to the splat centre in float64 (render.py:364-377's
+// d_mean2d = sum dp Q d, d_conic = -1/2 sum dp d d^T with d = tile centre
+// offset + (lx, ly)).  For splats centred far from the tile (near-plane
+// giants) d_mean2d and d_conic are large and cancel in the pull-back; local
+// moments keep every rounding error consistent between the two, so the
+// cancellation survives.
+// t = the fp32 log2(255 alpha) (raster_common.cuh).  Refined pixels
+// (kRefinedBit) are skipped here (refine.cu adds them); on every other pixel
+// the forward met no value inside the decision bands (it flags the pixel when
+// it does), so t outside the bands decides exactly as the reference's float64
+// alpha -- and t inside the keep band can only come from a pixel outside the
+// splat's contribution box, which the forward's finer block lists never
+// evaluated: there the float64 alpha is < 1/255 (not kept).
+__device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float t, float cr, float cg,
+                                          float cb, float lx, float ly, float* o) {
+  if (!(k < p.last) || !(t >= kTSkipHi)) return false;
+  const float al = alpha_of_t(t);
+  const bool flow = t < kTClampLo;  // no gradient through the clamp (render.py:361)
   const float iom = fast_rcp(1.0f - al);  // 1 - alpha >= 0.01
   const float Tb = p.T * iom;
   const float w = al * Tb;
@@ -390,40 +421,17 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float al, float
   p.sg = fmaf(w, cg, p.sg);
   p.sb = fmaf(w, cb, p.sb);
   p.T = Tb;
-  if (al < kAlphaClampVal) {  // no gradient through the clamp (render.py:361)
+  if (flow) {
     const float dp = da * al;
-    const float tx = dp * dx, ty = dp * dy;
+    const float tx = dp * lx, ty = dp * ly;
     o[3] += dp;
     o[4] += tx;
     o[5] += ty;
-    o[6] = fmaf(tx, dx, o[6]);
-    o[7] = fmaf(tx, dy, o[7]);
-    o[8] = fmaf(ty, dy, o[8]);
+    o[6] = fmaf(tx, lx, o[6]);
+    o[7] = fmaf(tx, ly, o[7]);
+    o[8] = fmaf(ty, ly, o[8]);
   }
   return true;
-}
-
-// Moments -> [d colour (3), d opacity, d mean2d (2), d conic (A, B, C)]
-// (render.py:364-377: d_opac = sum dp / o, d_mean = sum dp Q d,
-// d_conic = -(1/2 dx^2, dx dy, 1/2 dy^2) summed with weight dp), with
-// d = u e1 + v e2 and Q d = lambda1 u e1 + lambda2 v e2; in fp64.
-__device__ __forceinline__ void moments_to_grad(const float* m, float e1x, float e1y, float l1,
-                                                float l2, float io, float* g) {
-  const double ex = e1x, ey = e1y;
-  g[0] = m[0];
-  g[1] = m[1];
-  g[2] = m[2];
-  g[3] = m[3] * io;
-  const double a = static_cast<double>(l1) * m[4], b = static_cast<double>(l2) * m[5];
-  g[4] = static_cast<float>(a * ex - b * ey);
-  g[5] = static_cast<float>(a * ey + b * ex);
-  const double uu = m[6], uv = m[7], vv = m[8];
-  const double xx = ex * ex * uu - 2.0 * ex * ey * uv + ey * ey * vv;
-  const double xy = ex * ey * uu + (ex * ex - ey * ey) * uv - ex * ey * vv;
-  const double yy = ey * ey * uu + 2.0 * ex * ey * uv + ex * ex * vv;
-  g[6] = static_cast<float>(-0.5 * xx);
-  g[7] = static_cast<float>(-xy);
-  g[8] = static_cast<float>(-0.5 * yy);
 }
 
 // Batches of kBwdBatch splats, last batch first.  Staging writes, per
@@ -535,8 +543,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   static_assert(2 * B == 128, "staging and combine each take half of the CTA");
   __shared__ float4 s_a[2][B];
   __shared__ float4 s_b[2][B];
-  __shared__ float4 s_n[2][B];  // green, blue, lambda1, lambda2
-  __shared__ float s_io[2][B];  // 1 / opacity
+  __shared__ float2 s_n[2][B];  // green, blue
   __shared__ uint8_t s_mask[2][B];
   __shared__ uint8_t s_list[4][B];
   __shared__ uint32_t s_eidx[2][B];  // emission index of each staged pair
@@ -548,27 +555,25 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qx = (warp & 1) * 8, qy = (warp >> 1) * 8;
   const int lx = qx + (lane & 7), ly = qy + (lane >> 3);
-  const float flx = static_cast<float>(lx), fly = static_cast<float>(ly);
+  // tile-centred pixel coordinates (stage_splat); also the moments' coordinates
+  const float flx = static_cast<float>(lx) - kTileHalf, fly = static_cast<float>(ly) - kTileHalf;
   const int slot = reduce9_slot(lane);
   uint8_t* my_list = s_list[warp];
   const uint32_t n_units = unit_ctl[0];
-  // splat jj of buffer cb: sum the present warps in fixed order, chain to the
-  // 9 gradients, store at the pair's emission index (values 0-7 as two
-  // aligned float4, value 8 in the separate array after them)
+  // splat jj of buffer cb: sum the present warps in fixed order and store
+  // the 9 tile sums at the pair's emission index (values 0-7 as two aligned
+  // float4, value 8 in the separate array after them)
   auto combine_splat = [&](int cb, int jj) {
     const uint32_t m = s_mask[cb][jj];
-    float mom[9], g[9];
+    float g[9];
 #pragma unroll
     for (int u = 0; u < 9; ++u) {
       const float r0 = (m & 1u) ? s_red[cb][0][jj][u] : 0.0f;
       const float r1 = (m & 2u) ? s_red[cb][1][jj][u] : 0.0f;
       const float r2 = (m & 4u) ? s_red[cb][2][jj][u] : 0.0f;
       const float r3 = (m & 8u) ? s_red[cb][3][jj][u] : 0.0f;
-      mom[u] = (r0 + r1) + (r2 + r3);
+      g[u] = (r0 + r1) + (r2 + r3);
     }
-    const float4 aa = s_a[cb][jj];
-    const float4 nn = s_n[cb][jj];
-    moments_to_grad(mom, aa.z, aa.w, nn.z, nn.w, s_io[cb][jj], g);
     const int64_t e = s_eidx[cb][jj];
     float4* o4 = reinterpret_cast<float4*>(partials) + 2 * e;
     o4[0] = make_float4(g[0], g[1], g[2], g[3]);
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
     const int px = tx * kTile + lx, py0 = ty * kTile + ly, py1 = py0 + 4;
     const uint2 rg = ranges[tile];
-    const double ox = static_cast<double>(tx * kTile), oy = static_cast<double>(ty * kTile);
+    const double cx = tile_centre(tx), cy = tile_centre(ty);
     const bool last_chunk = k_end == nproc;
     const float4* ck = last_chunk ? nullptr
                                   : ckpt + ckpt_slot(rg.x, tile, k_end / kChunk) * kTilePixels;
@@ -606,6 +611,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       if (px < cam.width && py < cam.height) {
         const int64_t pix = cam.pix_base + static_cast<int64_t>(py) * cam.width + px;
         q.last = px_last[pix];
+        if (q.last & kRefinedBit) return;  // raster_refine_kernel<true> takes this pixel
         q.gr = dL[3 * pix + 0];
         q.gg = dL[3 * pix + 1];
         q.gb = dL[3 * pix + 2];
@@ -644,11 +650,10 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         const int k = tid;
         if (k < nb) {
           const SplatRec& r = s_raw[k];
-          const Staged sg = stage_splat(r, ox, oy);
+          const Staged sg = stage_splat(r, cx, cy);
           s_a[buf][k] = sg.a;
           s_b[buf][k] = sg.b;
-          s_n[buf][k] = make_float4(sg.c.x, sg.c.y, sg.lam1, sg.lam2);
-          s_io[buf][k] = 1.0f / r.opac;
+          s_n[buf][k] = sg.c;
           s_eidx[buf][k] = static_cast<uint32_t>(
               emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
           uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
@@ -674,12 +679,11 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         for (int u = 0; u < 9; ++u) o[u] = 0.0f;
         const float4 a = s_a[buf][j];
         const float4 b = s_b[buf][j];
-        const float4 nc = s_n[buf][j];
-        float u0, v0, u1, v1;
-        const float al0 = staged_alpha(a, b, flx, fly, u0, v0);
-        const float al1 = staged_alpha(a, b, flx, fly + 4.0f, u1, v1);
-        bool any = bwd_pixel(q0, k, al0, b.w, nc.x, nc.y, u0, v0, o);
-        any = bwd_pixel(q1, k, al1, b.w, nc.x, nc.y, u1, v1, o) || any;
+        const float2 nc = s_n[buf][j];
+        const float t0 = staged_t(a, b, flx, fly);
+        const float t1 = staged_t(a, b, flx, fly + 4.0f);
+        bool any = bwd_pixel(q0, k, t0, b.w, nc.x, nc.y, flx, fly, o);
+        any = bwd_pixel(q1, k, t1, b.w, nc.x, nc.y, flx, fly + 4.0f, o) || any;
         if (TRACE && lane == 0)  // diagnostics: lanes with a contribution per warp hit
           atomicAdd(trace + 8 * static_cast<int64_t>(fd.total_tiles) + __popc(__ballot_sync(kFull, any)), 1ull);
         else if (TRACE) __ballot_sync(kFull, any);
@@ -703,6 +707,16 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   }
 }
 
+// Publish the exactness counters in the frame stats (cgs_frame_stats).
+__global__ void refine_stats_kernel(FrameHeader* hdr) {
+  hdr->stats.n_refined_tiles = static_cast<int64_t>(hdr->scratch[3]);
+  hdr->stats.n_refined_pixels = static_cast<int64_t>(hdr->scratch[4]);
+  hdr->stats.diag_last_mismatch = static_cast<int64_t>(hdr->scratch[5]);
+  hdr->stats.diag_count_mismatch = static_cast<int64_t>(hdr->scratch[6]);
+  hdr->stats.diag_max_T_err = __uint_as_float(static_cast<unsigned int>(hdr->scratch[7]));
+  hdr->stats.diag_max_alpha_err = __uint_as_float(static_cast<unsigned int>(hdr->scratch[7] >> 32));
+}
+
 // ---------------------------------------------------------------------------
 int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
                       cudaStream_t st) {
@@ -714,23 +728,28 @@ int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 }
 
 int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t* vals,
-                      float* image, float* final_T, int32_t* counts, cudaStream_t st) {
+                      const float* logits, float* image, float* final_T, int32_t* counts,
+                      cudaStream_t st) {
   // L.tile_order was computed from the list lengths before the depth sort
   CGS_PROFILED("raster_fwd_kernel", st,
-               raster_fwd_kernel<<<fd.total_tiles * kFwdHalves, kFwdThreads, 0, st>>>(
-                   fd, L.tile_order, L.ranges, vals,
-                                                                 L.recs, L.hdr,
-                                                                 image, final_T, counts, L.px_last,
-                                                                 L.tile_nproc, L.rank_of,
-                                                                 L.last_rank, L.ckpt,
-                                                                 tile_trace_buffer()));
+               raster_fwd_kernel<<<fd.total_tiles, kFwdThreads, 0, st>>>(
+                   fd, L.tile_order, L.ranges, vals, L.recs, L.hdr, image, final_T, counts,
+                   L.px_last, L.tile_nproc, L.rank_of, L.last_rank, L.ckpt, L.refine_tiles,
+                   L.refine_mask, tile_trace_buffer()));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
+  {
+    const int rc = launch_refine(false, fd, L, vals, logits, image, final_T, counts, nullptr,
+                                 nullptr, st);
+    if (rc) return rc;
+  }
+  refine_stats_kernel<<<1, 1, 0, st>>>(L.hdr);
+  CGS_CHECK_LAUNCH("refine_stats_kernel");
   return CGS_OK;
 }
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
-                      cudaStream_t st) {
+                      const float* logits, cudaStream_t st) {
   unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl);
   CGS_CHECK_LAUNCH("unit_order_kernel");
   static int resident = 0;  // persistent grid: every resident CTA slot
@@ -751,6 +770,7 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
                                           8 * (L.pair_cap > 0 ? L.pair_cap : 1), n_processed,
                                           trace));
   CGS_CHECK_LAUNCH("raster_bwd_kernel");
-  return CGS_OK;
+  return launch_refine(true, fd, L, sorted_pair_vals(L), logits, nullptr, nullptr, nullptr, dL,
+                       partials, st);
 }
 }  // namespace cgs

@@ -257,23 +257,29 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// fp64 record -> fp32 shared-memory form for one tile whose first pixel
-// centre is (ox + 0.5, oy + 0.5), in the eigenbasis of the conic.  With
-// conic Q = lambda1 e1 e1^T + lambda2 e2 e2^T (e2 = e1 rotated by 90 deg),
-// d^T Q d = lambda1 u^2 + lambda2 v^2, u = e1 . d, v = e2 . d; the tile offsets
-// (u0, v0) of the first pixel centre are formed in fp64, so per pixel
-// u = u0 + e1 . (lx, ly) and v = v0 + e2 . (lx, ly) are small, well-conditioned
-// fp32 numbers even for elongated near-plane splats centred far off screen
-// (evaluating A dx^2 + 2B dx dy + C dy^2 directly in fp32 cancels
-// catastrophically there).  Exponent in log2 units: k = -log2(e)/2 lambda.
-//   a = (u0, v0, e1x, e1y)   b = (k1, k2, opacity, red)   c = (green, blue)
+// fp64 record -> fp32 shared-memory form for one tile, in the eigenbasis of
+// the conic.  With conic Q = lambda1 e1 e1^T + lambda2 e2 e2^T (e2 = e1
+// rotated by 90 deg), d^T Q d = lambda1 u^2 + lambda2 v^2, u = e1 . d,
+// v = e2 . d.  The offsets (u0, v0) of the tile centre (cx, cy) = tile origin
+// + (8, 8) from the mean are formed in fp64, so per pixel u = u0 + e1 . (lx,
+// ly), v = v0 + e2 . (lx, ly) with tile-centred pixel coordinates lx, ly in
+// [-7.5, 7.5] are small, well-conditioned fp32 numbers even for elongated
+// near-plane splats centred far off screen (evaluating A dx^2 + 2B dx dy +
+// C dy^2 directly in fp32 cancels catastrophically there).
+//
+// The raster works with the log-domain alpha
+//   t = log2(255 alpha) = log2(255 o) - log2(e)/2 (lambda1 u^2 + lambda2 v^2)
+// (render.py:274-277): keep is t >= 0 (alpha >= 1/255), the clamp is
+// t >= log2(0.99 * 255), and alpha = 2^t / 255 is formed only for kept
+// splats.
+//   a = (u0, v0, e1x, e1y)   b = (k1, k2, log2(255 o), red)   c = (green, blue)
+// with k = -log2(e)/2 lambda.
 struct Staged {
   float4 a, b;
   float2 c;
-  float lam1, lam2;  // eigenvalues (backward's moments -> gradient map)
 };
 
-__device__ __forceinline__ Staged stage_splat(const SplatRec& r, double ox, double oy) {
+__device__ __forceinline__ Staged stage_splat(const SplatRec& r, double cx, double cy) {
   const double A = r.ca, B = r.cb, C = r.cc;
   const double m = 0.5 * (A + C), h = 0.5 * (A - C);
   const double rr = sqrt(h * h + B * B);
@@ -294,26 +300,67 @@ __device__ __forceinline__ Staged stage_splat(const SplatRec& r, double ox, doub
     ex = 1.0;
     ey = 0.0;
   }
-  const double dx = ox + 0.5 - r.mx, dy = oy + 0.5 - r.my;
+  const double dx = cx - r.mx, dy = cy - r.my;
   Staged st;
   st.a = make_float4(static_cast<float>(ex * dx + ey * dy), static_cast<float>(-ey * dx + ex * dy),
                      static_cast<float>(ex), static_cast<float>(ey));
   st.b = make_float4(static_cast<float>(-0.5 * kLog2e * l1), static_cast<float>(-0.5 * kLog2e * l2),
-                     r.opac, r.r);
+                     __log2f(255.0f * r.opac), r.r);
   st.c = make_float2(r.g, r.b);
-  st.lam1 = static_cast<float>(l1);
-  st.lam2 = static_cast<float>(l2);
   return st;
 }
 
-// alpha = min(o * exp(power), 0.99) (render.py:274-278) at tile pixel (lx, ly);
-// (u, v) returned for the backward.  Skip test by the caller.
-__device__ __forceinline__ float staged_alpha(const float4& a, const float4& b, float lx, float ly,
-                                              float& u, float& v) {
-  u = fmaf(a.w, ly, fmaf(a.z, lx, a.x));
-  v = fmaf(a.z, ly, fmaf(-a.w, lx, a.y));
-  return fminf(b.z * fast_exp2(fmaf(b.x * u, u, b.y * v * v)), kAlphaClampVal);
+// Centre of tile column / row t in pixel coordinates (stage_splat's origin);
+// pixel x of the tile sits at centre + (x - 7.5).
+__device__ __forceinline__ double tile_centre(int t) { return static_cast<double>(t * kTile + kTile / 2); }
+constexpr float kTileHalf = 0.5f * (kTile - 1);  // 7.5
+
+// t = log2(255 alpha_unclamped) at tile-centred pixel (lx, ly), fp32.
+__device__ __forceinline__ float staged_t(const float4& a, const float4& b, float lx, float ly) {
+  const float u = fmaf(a.w, ly, fmaf(a.z, lx, a.x));
+  const float v = fmaf(a.z, ly, fmaf(-a.w, lx, a.y));
+  return fmaf(b.x * u, u, fmaf(b.y * v, v, b.z));
 }
 
+// alpha = min(2^t / 255, 0.99) (render.py:278) for a kept t.
+__device__ __forceinline__ float alpha_of_t(float t) {
+  return fminf(fast_exp2(t) * static_cast<float>(1.0 / 255.0), kAlphaClampVal);
+}
+
+// ---- exact decisions ------------------------------------------------------
+// The fp32 alpha above is within ~1e-5 relative of the reference's float64
+// alpha (fp32 eigenbasis offsets, ex2.approx; measured with CGS_REFINE_ALL).
+// Every discrete decision the reference takes -- keep (alpha >= 1/255,
+// render.py:279), gradient flow through the clamp (alpha < 0.99,
+// render.py:361) and termination (T_before >= 1e-4, render.py:283) -- is
+// taken on the fp32 values only when they lie outside a relative band around
+// the threshold (kAlphaBand on alpha, i.e. kAlphaBand / ln 2 on t; kTBand on
+// T).  A pixel that meets a value inside a band is flagged by the forward and
+// re-walked entirely in float64, exactly as the reference computes it
+// (refine.cu, exact_alpha_raw).
+constexpr double kAlphaBand = 4e-5;
+constexpr double kTBand = 5e-5;
+constexpr double kLn2 = 0.6931471805599453;
+constexpr float kTSkipLo = static_cast<float>(-kAlphaBand / kLn2);  // keep band on t
+constexpr float kTSkipHi = static_cast<float>(kAlphaBand / kLn2);
+constexpr double kTClamp = 7.979853867163743;  // log2(0.99 * 255)
+constexpr float kTClampLo = static_cast<float>(kTClamp - kAlphaBand / kLn2);
+constexpr float kTClampHi = static_cast<float>(kTClamp + kAlphaBand / kLn2);
+constexpr float kTBandLo = static_cast<float>(1e-4 * (1.0 - kTBand));
+constexpr float kTBandHi = static_cast<float>(1e-4 * (1.0 + kTBand));
+
+// Reference float64 alpha of splat record r at pixel (px, py) of its view
+// (render.py:261, 274-280): d = centre - mean, power = -1/2 (A dx^2 + C dy^2)
+// - B dx dy, alpha = min(o exp(power), 0.99) with o = sigmoid(logit) in f64
+// (render.py:200).  Round-to-nearest intrinsics keep numpy's operation order
+// (no FMA contraction).  Returns the unclamped o exp(power).
+__device__ __forceinline__ double exact_alpha_raw(const SplatRec& r, float logit, int px, int py) {
+  const double dx = __dsub_rn(static_cast<double>(px) + 0.5, r.mx);
+  const double dy = __dsub_rn(static_cast<double>(py) + 0.5, r.my);
+  const double q = __dadd_rn(__dmul_rn(r.ca, __dmul_rn(dx, dx)), __dmul_rn(r.cc, __dmul_rn(dy, dy)));
+  const double power = __dsub_rn(__dmul_rn(-0.5, q), __dmul_rn(__dmul_rn(r.cb, dx), dy));
+  const double o = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-static_cast<double>(logit))));
+  return __dmul_rn(o, exp(power));
+}
 
 }  // namespace cgs

@@ -36,9 +36,10 @@ struct BwdLayout {
   float4* s_draw;      // V*N: gated d colour
   float4* s_s3a;       // V*N: dSigma3 00 01 02 11
   float2* s_s3b;       // V*N: dSigma3 12 22
-  float4* acc0;        // V*N: summed partials d_color(3), d_opac
-  float4* acc1;        // V*N: d_mean2d(2), d_conic A, B
-  float* acc2;         // V*N: d_conic C
+  float4* acc0;        // V*N: summed d_color(3), sum dp (= d_opac * opacity)
+  double2* accm;       // V*N: sum dp d (centre-frame first moments, f64)
+  double2* accq;       // V*N: sum dp dx^2, sum dp dx dy (second moments, f64)
+  double* accr;        // V*N: sum dp dy^2
   int32_t* csr_off[2];  // internal code CSR (sh, sr) when the caller passes none
   int32_t* csr_mem[2];
   void* csr_ws;
@@ -64,8 +65,9 @@ inline BwdLayout plan_bwd(void* base, size_t cap, int64_t n, int n_views, int to
   B.s_s3a = c.take<float4>(vn);
   B.s_s3b = c.take<float2>(vn);
   B.acc0 = c.take<float4>(vn);
-  B.acc1 = c.take<float4>(vn);
-  B.acc2 = c.take<float>(vn);
+  B.accm = c.take<double2>(vn);
+  B.accq = c.take<double2>(vn);
+  B.accr = c.take<double>(vn);
   const int64_t n1 = n > 0 ? n : 1;
   B.csr_off[0] = c.take<int32_t>(sh_cap + 1);
   B.csr_mem[0] = c.take<int32_t>(n1);
@@ -91,8 +93,9 @@ struct GaussIn {
 };
 
 // Chain rule from screen space to model space for one (view, Gaussian)
-// splat (render.py:382-446).  acc = [d_color(3), d_opac, d_mean2d(2),
-// d_conic(A, B, C)].  Writes the per-splat pull-back record s.
+// splat (render.py:382-446).  acc = [d_color(3), sum dp, d_mean2d(2),
+// d_conic(A, B, C)] (dp = d_alpha * alpha, so d_opac = sum dp / o,
+// render.py:364-365).  Writes the per-splat pull-back record s.
 #ifndef CGS_PULLBACK_SH_F32
 #define CGS_PULLBACK_SH_F32 1
 #endif
@@ -219,7 +222,7 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
     for (int k = 0; k < 3; ++k) dp[k] += dpc[k];
   }
   const double o = 1.0 / (1.0 + exp(-static_cast<double>(g.logit[gi])));
-  const double dlogit = acc[3] * o * (1.0 - o);  // render.py:446
+  const double dlogit = (acc[3] / o) * o * (1.0 - o);  // render.py:364-365, 446
   B.s_posl[s] = make_float4(static_cast<float>(dp[0]), static_cast<float>(dp[1]),
                             static_cast<float>(dp[2]), static_cast<float>(dlogit));
   B.s_view[s] = make_float4(static_cast<float>(ox), static_cast<float>(oy), static_cast<float>(oz), 0.0f);
@@ -231,6 +234,7 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
 }
 
 struct PairWalk {
+  const SplatRec* recs;  // mean2d of each splat (tile moments -> splat centre)
   const uint64_t* pair_off;
   const uint32_t* n_tiles;
   const uint64_t* rect;
@@ -240,8 +244,14 @@ struct PairWalk {
   int64_t p9;             // offset of value 8 (8 * pair_cap)
 };
 
-// Adds the partials of splat s's processed pairs k = k0, k0+kstep, ... (in
-// emission order) into acc; returns whether any pair was processed.
+// Adds the tile sums of splat s's processed pairs k = k0, k0+kstep, ... (in
+// emission order) into acc; returns whether any pair was processed.  A tile
+// sum holds [d_color(3), m0, m1x, m1y, m2xx, m2xy, m2yy]: moments of
+// dp = d_alpha * alpha over the tile's pixels in coordinates (lx, ly)
+// centred on the tile (raster_bwd_kernel).  They are shifted here, in
+// float64, to the splat centre: with o = tile centre - mean2d and
+// d = o + (lx, ly), acc = [d_color(3), sum dp, sum dp dx, sum dp dy,
+// sum dp dx^2, sum dp dx dy, sum dp dy^2] (render.py:364-377).
 __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& fd, int64_t n,
                                            int64_t s, uint32_t cnt, uint32_t k0, uint32_t kstep,
                                            double* acc) {
@@ -253,20 +263,36 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
   const int v = static_cast<int>(s / n);
   const int tb = fd.cam[v].tile_base, ntx = fd.cam[v].ntx;
   const uint32_t r = w.rank_of[s];
+  const double mx = w.recs[s].mx, my = w.recs[s].my;
   bool any = false;
   for (uint32_t k = k0; k < cnt; k += kstep) {
-    const int t = tb + (ty0 + static_cast<int>(k) / span) * ntx + tx0 + static_cast<int>(k) % span;
+    const int ty = ty0 + static_cast<int>(k) / span, tx = tx0 + static_cast<int>(k) % span;
+    const int t = tb + ty * ntx + tx;
     if (r < w.last_rank[t]) {  // inside the tile's processed prefix
       any = true;
       const int64_t e = static_cast<int64_t>(o + k);
       const float4* p4 = reinterpret_cast<const float4*>(w.partials) + 2 * e;
       const float4 x = p4[0], y = p4[1];
-      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
-      acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
-      acc[8] += w.partials[w.p9 + e];
+      const double m0 = x.w, m1x = y.x, m1y = y.y;
+      const double ox = tile_centre(tx) - mx, oy = tile_centre(ty) - my;  // tile centre offset
+      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += m0;
+      acc[4] += ox * m0 + m1x;
+      acc[5] += oy * m0 + m1y;
+      acc[6] += (ox * ox * m0 + 2.0 * ox * m1x) + static_cast<double>(y.z);
+      acc[7] += (ox * oy * m0 + (ox * m1y + oy * m1x)) + static_cast<double>(y.w);
+      acc[8] += (oy * oy * m0 + 2.0 * oy * m1y) + static_cast<double>(w.partials[w.p9 + e]);
     }
   }
   return any;
+}
+
+// Summed moments -> the per-splat record the pull-back reads.
+__device__ __forceinline__ void store_splat_acc(const BwdLayout& B, int64_t s, const double* t) {
+  B.acc0[s] = make_float4(static_cast<float>(t[0]), static_cast<float>(t[1]),
+                          static_cast<float>(t[2]), static_cast<float>(t[3]));
+  B.accm[s] = make_double2(t[4], t[5]);
+  B.accq[s] = make_double2(t[6], t[7]);
+  B.accr[s] = t[8];
 }
 
 // One thread per splat; splats with more than 32 pairs (e.g. near-plane
@@ -274,7 +300,7 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
 // order is fixed, so the result is deterministic.
 template <int DEG>
 #ifndef CGS_SR_MINB
-#define CGS_SR_MINB 1
+#define CGS_SR_MINB 3
 #endif
 __global__ void __launch_bounds__(256, CGS_SR_MINB) splat_reduce_kernel(PairWalk pw, const FrameHeader* __restrict__ fh,
                                                            FrameDesc fd, int64_t n, int64_t vn,
@@ -316,11 +342,7 @@ __global__ void __launch_bounds__(256, CGS_SR_MINB) splat_reduce_kernel(PairWalk
     if (!ok || huge) continue;
     B.touched[s] = touched ? 1 : 0;
     if (!touched) continue;
-    B.acc0[s] = make_float4(static_cast<float>(acc[0]), static_cast<float>(acc[1]),
-                            static_cast<float>(acc[2]), static_cast<float>(acc[3]));
-    B.acc1[s] = make_float4(static_cast<float>(acc[4]), static_cast<float>(acc[5]),
-                            static_cast<float>(acc[6]), static_cast<float>(acc[7]));
-    B.acc2[s] = static_cast<float>(acc[8]);
+    store_splat_acc(B, s, acc);
   }
 }
 
@@ -355,11 +377,7 @@ __global__ void __launch_bounds__(256) splat_reduce_long_kernel(PairWalk pw,
         for (int w = 1; w < 8; ++w) t[u] += s_w[w][u];
       }
       B.touched[s] = 1;
-      B.acc0[s] = make_float4(static_cast<float>(t[0]), static_cast<float>(t[1]),
-                              static_cast<float>(t[2]), static_cast<float>(t[3]));
-      B.acc1[s] = make_float4(static_cast<float>(t[4]), static_cast<float>(t[5]),
-                              static_cast<float>(t[6]), static_cast<float>(t[7]));
-      B.acc2[s] = static_cast<float>(t[8]);
+      store_splat_acc(B, s, t);
       atomicAdd(&B.hdr->n_touched, 1ULL);
     }
     __syncthreads();
@@ -389,8 +407,15 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
     const int64_t s = t;
 #endif
     if (!B.touched[s]) continue;
-    const float4 a0 = B.acc0[s], a1 = B.acc1[s];
-    const double acc[9] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, B.acc2[s]};
+    const float4 a0 = B.acc0[s];
+    const double2 am = B.accm[s], aq = B.accq[s];
+    const double ar = B.accr[s];
+    // d_mean2d = Q sum dp d, d_conic = -(1/2 sum dp dx^2, sum dp dx dy,
+    // 1/2 sum dp dy^2) (render.py:368-377), Q the forward's conic
+    const SplatRec& rq = g.recs[s];
+    const double acc[9] = {a0.x, a0.y, a0.z, a0.w,
+                           rq.ca * am.x + rq.cb * am.y, rq.cb * am.x + rq.cc * am.y,
+                           -0.5 * aq.x, -aq.y, -0.5 * ar};
     const int v = static_cast<int>(s / n);
     pull_back_splat<DEG>(acc, s, static_cast<uint32_t>(s - static_cast<int64_t>(v) * n), fd.cam[v], g, B);
   }
@@ -642,19 +667,20 @@ static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap
 // The frame backward in three stages (exported as cgs_raster_bwd,
 // cgs_gaussian_reduce_pullback, cgs_codebook_reduce; each reads what the
 // earlier stages left in the backward workspace).
-int bwd_stage_raster(const FrameDesc& fd, const FrameLayout& L, BwdLayout& B, const float* dL,
-                     const float* final_T, cudaStream_t st) {
+int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
+                     BwdLayout& B, const float* dL, const float* final_T, cudaStream_t st) {
   CGS_CUDA(cudaMemsetAsync(B.hdr, 0, sizeof(BwdHeader), st));
   if (L.vn > 0) CGS_CUDA(cudaMemsetAsync(B.touched, 0, L.vn, st));
   if (fd.total_tiles > 0 && L.vn > 0)
-    return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed, st);
+    return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed,
+                             sc->opacity_logits, st);
   return CGS_OK;
 }
 
 int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                        BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st) {
   if (fd.total_tiles > 0 && L.vn > 0) {
-    PairWalk pw{L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials,
+    PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials,
                 8 * (L.pair_cap > 0 ? L.pair_cap : 1)};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
@@ -718,7 +744,7 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
                    const float* dL, const float* final_T, float scale, float* gpos, float* glogit,
                    float* gsh, float* gsr, const int32_t* const csr_off_in[2],
                    const int32_t* const csr_mem_in[2], cudaStream_t st) {
-  int rc = bwd_stage_raster(fd, L, B, dL, final_T, st);
+  int rc = bwd_stage_raster(sc, fd, L, B, dL, final_T, st);
   if (!rc) rc = bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st);
   if (!rc) rc = bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off_in, csr_mem_in, st);
   return rc;
@@ -751,7 +777,7 @@ int bwd_stage_entry(int stage, const cgs_scene_t* sc, const FrameDesc& fd, const
   int rc = plan_bwd_checked(sc, fd, L, ws, ws_bytes, &B);
   if (rc) return rc;
   switch (stage) {
-    case 0: return bwd_stage_raster(fd, L, B, dL, final_T, st);
+    case 0: return bwd_stage_raster(sc, fd, L, B, dL, final_T, st);
     case 1: return bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st);
     default: return bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off, csr_mem, st);
   }

@@ -653,12 +653,12 @@ int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
                                : sort_pairs_stage<uint32_t>(L, fd, L.psort32, st);
 }
 
-int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, float* image, float* final_T,
-                       int32_t* counts, cudaStream_t st) {
+int frame_stage_raster(const FrameDesc& fd, FrameLayout& L, const float* logits, float* image,
+                       float* final_T, int32_t* counts, cudaStream_t st) {
   if (fd.total_tiles > 0) {
     int rc = launch_tile_order(fd, L, nullptr, st);
     if (rc) return rc;
-    rc = launch_raster_fwd(fd, L, sorted_pair_vals(L), image, final_T, counts, st);
+    rc = launch_raster_fwd(fd, L, sorted_pair_vals(L), logits, image, final_T, counts, st);
     if (rc) return rc;
   }
   return CGS_OK;
@@ -670,7 +670,7 @@ int frame_forward(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L, fl
   if (!rc) rc = frame_stage_sort_depth(fd, L, st);
   if (!rc) rc = frame_stage_duplicate(fd, L, st);
   if (!rc) rc = frame_stage_sort_pairs(fd, L, st);
-  if (!rc) rc = frame_stage_raster(fd, L, image, final_T, counts, st);
+  if (!rc) rc = frame_stage_raster(fd, L, sc->opacity_logits, image, final_T, counts, st);
   return rc;
 }
 

@@ -480,12 +480,11 @@ def test_deep_stack_chunked_backward_matches_oracle(cg):
     assert np.array_equal(offs, fw["tile_offsets"]) and np.array_equal(ids, fw["tile_ids"])
     cnt = art.contrib_counts.cpu().numpy()
     assert cnt.max() > 1024 and np.diff(offs).min() > 1600  # >= 3 chunks per tile
-    knife = cnt != fw["counts"]
-    assert knife.sum() <= 4 and np.all(np.abs(cnt[knife] - fw["counts"][knife]) == 1)
+    assert np.array_equal(cnt, fw["counts"])
     img = art.image.cpu().numpy()
-    assert np.allclose(img[~knife], fw["image"][~knife], rtol=RTOL, atol=ATOL)
+    assert np.allclose(img, fw["image"], rtol=RTOL, atol=ATOL)
+    assert np.allclose(art.final_transmittance.cpu().numpy(), fw["final_T"], rtol=RTOL, atol=ATOL)
     dL = np.random.default_rng(2).normal(0, 1e-3, img.shape)
-    dL[knife] = 0.0
     g = cg.rasterize_backward(st, cam, art, dL).numpy()
     og = O.raster_backward(ost, ocam, dL)
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
@@ -557,23 +556,23 @@ def test_exact_ratio_chain_matches_reference(cg):
     assert np.array_equal(rng.random(4), d["rng_after"])
 
 
-def test_config1_full_size_matches_oracle(cg):
-    """BASELINE config 1 at full size (100k Gaussians, SH-3, 256x256, two views
-    rendered as one batched frame) against the oracle (~6 s of numpy per view).
+@pytest.mark.parametrize("views", [(0, 1), (2, 3)])
+def test_config1_full_size_matches_oracle(cg, views):
+    """BASELINE config 1 at full size (100k Gaussians, SH-3, 256x256), all four
+    views (two batched frames of two) against the oracle (~6 s of numpy per
+    view): contribution counts bit-exact, images / transmittance within rtol
+    1e-4, atol 1e-6, every gradient entry within the same tolerance.
 
-    The raster computes alpha and T in fp32; the reference in fp64.  At this
-    size a handful of pixels per view sit on a knife edge -- T_before within
-    ~1e-6 relative of the 1e-4 termination threshold (or alpha of 1/255) --
-    where the two precisions take different discrete decisions (SURVEY.md
-    section 7, hard part 1).  Those pixels are identified by their
-    contribution count differing by exactly one; everything else must match:
-    counts bit-exact, images / transmittance within rtol 1e-4, atol 1e-6, and
-    gradients within the same tolerance elementwise with the knife-edge pixels
-    removed from dL/dimage."""
+    The raster computes alpha and T in fp32 and the reference in fp64; the
+    discrete decisions are nevertheless the reference's: alphas within 2e-5
+    of 1/255 or 0.99 are recomputed in float64, and pixels whose fp32
+    transmittance comes within 2e-3 of the 1e-4 termination threshold are
+    re-walked in float64 (frame stats n_exact_alpha / n_refined; views 1-2
+    hold pixels that an fp32-only raster decides differently)."""
     from oracle import cgs_oracle as O
     from paper_2509_03775_b200 import scenes
     a, g = scenes.config1(0), scenes.config1(1)
-    cams = a.cameras[1:3]  # views with knife-edge pixels
+    cams = [a.cameras[v] for v in views]
     st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
                                    a.sr_rows)
     gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows,
@@ -586,17 +585,16 @@ def test_config1_full_size_matches_oracle(cg):
         ocam = O.cam_from_any(cam)
         fw = O.raster_forward(ost, ocam)
         cnt = fr.view_counts(v).cpu().numpy()
-        knife = cnt != fw["counts"]
-        assert knife.sum() <= 16 and np.all(np.abs(cnt[knife] - fw["counts"][knife]) == 1)
-        ok = ~knife
+        assert np.array_equal(cnt, fw["counts"]), int((cnt != fw["counts"]).sum())
         img = fr.view_image(v).cpu().numpy()
         T = fr.view_T(v).cpu().numpy()
-        assert np.allclose(img[ok], fw["image"][ok], rtol=RTOL, atol=ATOL)
-        assert np.allclose(T[ok], fw["final_T"][ok], rtol=RTOL, atol=ATOL)
+        assert np.allclose(img, fw["image"], rtol=RTOL, atol=ATOL)
+        assert np.allclose(T, fw["final_T"], rtol=RTOL, atol=ATOL)
         dL = O.recon_loss_grad(fw["image"], gfr.view_image(v).cpu().numpy().astype(np.float64), 0.2)
-        dL[knife] = 0.0
         dls.append(dL)
         refs.append(O.raster_backward(ost, ocam, dL))
+    st_ = fr.stats()
+    assert st_.n_refined_tiles > 0  # the float64 re-walk ran (and decided like the oracle above)
     dl = torch.as_tensor(np.concatenate([x.reshape(-1) for x in dls]).astype(np.float32)).cuda()
     gr = fr.backward(dl).numpy()
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
@@ -624,22 +622,22 @@ def test_device_densify_matches_host_densify(cg):
     assert np.array_equal(ra.random(4), rb.random(4))
 
 
-@pytest.mark.parametrize("config,rows", [(2, (344, 376)), (3, (528, 560))])
-def test_full_scene_strip_matches_oracle(cg, config, rows):
-    """BASELINE config 2 / 3 scenes at full size; config 3: (4M Gaussians, SH-3 K=65536, near-
-    plane giants), rendered through a 1960x32 strip of pose 0 (the strip is a
-    camera of its own: principal point shifted) so the numpy oracle finishes in
-    about a minute: tile lists, contribution counts bit-exact; images and T
-    within rtol 1e-4 / atol 1e-6.
+@pytest.mark.parametrize("config,pose,rows", [(2, 0, (344, 376)), (3, 0, (528, 560)),
+                                              (2, 5, (688, 720)), (3, 3, (96, 128))])
+def test_full_scene_strip_matches_oracle(cg, config, pose, rows):
+    """BASELINE config 2 / 3 scenes at full size (config 3: 4M Gaussians, SH-3
+    K=65536, near-plane giants), rendered through a 32-row strip of a pose (the
+    strip is a camera of its own: principal point shifted) so the numpy oracle
+    finishes in about a minute: tile lists and contribution counts bit-exact;
+    images, T and every gradient entry within rtol 1e-4 / atol 1e-6.
 
-    Gradients: within the same tolerance for every parameter that no
-    view-covering splat feeds (a splat whose pixel rect spans every tile, or
-    camera z < 2 x the 0.01 cull distance).  Their gradients are
-    near-cancelling sums over every pixel of the view, amplified through
-    J ~ 1/z, 1/z^2, 1/z^3, so the fp32 per-pixel partials (~1e-7 relative)
-    reproduce them only to a few percent; they are checked separately at 10%
-    group-relative error and documented in DESIGN.md section 3 (< 5e-4 of the
-    Gaussians here)."""
+    The strips hold view-covering and near-plane splats (camera z within a
+    few times the 0.01 cull distance).  Their d_mean2d and d_conic are large
+    sums over every pixel that cancel in the pull-back through J ~ 1/z^3;
+    the backward keeps its per-tile moments in tile-local coordinates and
+    shifts and sums them in float64, so the cancellation is exact enough for
+    the tolerance (the earlier fp32 centre-frame partials missed it by up to
+    10%, scripts/diag_sensitivity.py)."""
     import sys
     import os
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -647,7 +645,7 @@ def test_full_scene_strip_matches_oracle(cg, config, rows):
     from oracle import cgs_oracle as O
     from paper_2509_03775_b200 import scenes
     a = scenes.build(config, 0)
-    ocam = _strip_cam(O.cam_from_any(a.cameras[0]), *rows)
+    ocam = _strip_cam(O.cam_from_any(a.cameras[pose]), *rows)
     cam = cg.Camera(rotation=ocam.R, translation=ocam.t, fx=ocam.fx, fy=ocam.fy, cx=ocam.cx,
                     cy=ocam.cy, width=ocam.width, height=ocam.height)
     st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
@@ -664,23 +662,17 @@ def test_full_scene_strip_matches_oracle(cg, config, rows):
     dL = np.random.default_rng(0).normal(0, 1e-4, img.shape)
     g = cg.rasterize_backward(st, cam, art, dL).numpy()
     og = O.raster_backward(ost, ocam, dL)
-    # splats covering the whole view, or just beyond the near plane: their
-    # gradients are near-cancelling sums over every pixel (see docstring)
     ntiles = art.frame.splats(0)["n_tiles"]
     tz = (a.positions.astype(np.float64) @ ocam.R.T + ocam.t)[:, 2]
-    near = ((tz > 0.01) & (tz < 0.02)) | (ntiles == len(offs) - 1)
-    assert near.sum() < 5e-4 * len(near)
-    far = {"positions": ~near, "opacity_logits": ~near}
-    for k, idx in (("sh_rows", a.g2sh), ("sr_rows", a.g2sr)):
-        tainted = np.zeros(g[k].shape[0], bool)
-        tainted[np.unique(idx[near])] = True
-        far[k] = ~tainted
+    giants = ((tz > 0.01) & (tz < 0.02)) | (ntiles == len(offs) - 1)
+    assert giants.any()  # the strip exercises the cancelling case
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
-        m = far[k]
-        assert np.allclose(g[k][m], og[k][m], rtol=RTOL, atol=ATOL), (k, np.abs(g[k][m] - og[k][m]).max())
-        if (~m).any():
-            rel = np.abs(g[k][~m] - og[k][~m]).max() / max(np.abs(og[k]).max(), 1e-30)
-            assert rel <= 0.1, (k, rel)
+        assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
+        assert group_rel_np(g[k], og[k]) <= 1e-4, k
+
+
+def group_rel_np(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
 
 
 def test_split_eligible_abi_matches_host_rule(cg):
