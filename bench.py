@@ -506,9 +506,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # CGS_DIST_BACKEND=gloo (tests, one-GPU boxes): every rank may share a GPU
+    # (device = local rank mod the visible devices); the default is NCCL, one
+    # rank per GPU
+    backend = os.environ.get("CGS_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2509_03775_b200 as cg
     from paper_2509_03775_b200 import _native as nat
@@ -545,7 +553,8 @@ def main():
     allreduce = cdist.make_allreduce() if world > 1 else None
     rng = np.random.default_rng(args.seed)
     tr = Trainer(st, cams, gts, cfg, rng, mcmc_every=args.mcmc_every, world=world,
-                 allreduce=allreduce, use_graphs=not args.no_graphs)
+                 allreduce=allreduce, use_graphs=not args.no_graphs,
+                 total_views=len(cams) * world)
 
     flush = torch.empty((64 * 1024 * 1024,), dtype=torch.float32, device=dev)  # 256 MB > L2
 
@@ -732,7 +741,7 @@ def main():
                           "mcmc_every": args.mcmc_every,
                           "sgld_noise": f"device Philox, noise_pos={args.noise_pos} (reference default 1.0 "
                                         "diffuses the scene out of view; see DESIGN.md)",
-                          "parallelism": f"dp{world} (views sharded, NCCL allreduce)"},
+                          "parallelism": f"dp{world} (views sharded, {backend} allreduce)"},
                "mpix_per_s": mpix, "gpu_launches": launches,
                "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms),
                            "max": max(step_ms)}, "roofline": roofline,

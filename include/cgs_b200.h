@@ -11,8 +11,11 @@
  *   - all array arguments are DEVICE pointers unless marked "host";
  *   - every call is asynchronous on `stream` (a cudaStream_t) unless marked
  *     "synchronizes";
- *   - all buffers, including workspaces, are caller-allocated; the library
- *     holds no global state besides a thread-local last-error string;
+ *   - all buffers, including workspaces, are caller-allocated; besides a
+ *     thread-local last-error string and the diagnostics switches below, the
+ *     library keeps only per-device caches of launch configuration (kernel
+ *     shared-memory attributes, occupancy-sized grids), indexed by the
+ *     current device ordinal, so one process may drive several GPUs;
  *   - functions return 0 on success and a nonzero CGS_E* code otherwise,
  *     never throwing across the ABI; cgs_last_error() describes the failure.
  *
@@ -111,6 +114,11 @@ typedef struct cgs_sgld_params {
   uint64_t* offset_dev;  /* optional device counter: incremented by the update
                             and used as the Philox offset instead of `offset`
                             (CUDA-graph replays then draw fresh noise)       */
+  const int32_t* skip_if; /* optional device flag (e.g. the frame's
+                            stats.overflow): when nonzero the update writes
+                            nothing and sets flags[0] |= 2                   */
+  int32_t* sticky;       /* optional device accumulator: sticky |= flags[0]
+                            (so a run can be checked once, at its end)       */
 } cgs_sgld_params_t;
 
 /* ---- library --------------------------------------------------------- */
@@ -269,7 +277,8 @@ CGS_API int cgs_recon_loss(const float* image, const float* gt, int32_t n_views,
 
 /* ---- SGLD update (sampler.py:262-300) --------------------------------- */
 /* Checks every gradient for finiteness first; if any is non-finite nothing
- * is written and flags[0] = 1 (host raises SamplerError).  Live rows are
+ * is written and flags[0] |= 1 (host raises SamplerError); params.skip_if
+ * set likewise writes nothing (flags[0] |= 2).  Live rows are
  * given as index lists; the finiteness check covers all sh_capacity /
  * sr_capacity gradient rows (GradientSet.all_finite, render.py:222-224).
  * Parity noise arrays (noise_source 1) hold the reference's standard

@@ -65,6 +65,8 @@ class CSgldParams(ctypes.Structure):
         ("seed", ctypes.c_uint64), ("offset", ctypes.c_uint64),
         ("noise_source", ctypes.c_int32), ("pad_", ctypes.c_int32),
         ("offset_dev", ctypes.c_void_p),
+        ("skip_if", ctypes.c_void_p),
+        ("sticky", ctypes.c_void_p),
     ]
 
 

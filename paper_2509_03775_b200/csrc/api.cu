@@ -26,6 +26,17 @@ static unsigned long long* g_tile_trace = nullptr;
 unsigned long long* tile_trace_buffer() { return g_tile_trace; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int current_device(int* dev) {
+  int d = 0;
+  CGS_CUDA(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) {
+    set_error("device ordinal out of range");
+    return CGS_EINTERNAL;
+  }
+  *dev = d;
+  return CGS_OK;
+}
+
 static cudaEvent_t prof_event() {
   if (!g_prof_pool.empty()) {
     cudaEvent_t e = g_prof_pool.back();

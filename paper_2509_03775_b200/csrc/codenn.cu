@@ -1,6 +1,7 @@
 // Host side of the nearest-code search (codenn.cuh): workspace layout,
 // launches and the C ABI entry points cgs_code_nn_workspace_bytes /
 // cgs_code_nn.
+#include <atomic>
 #include "codenn.cuh"
 
 #include <string>
@@ -54,11 +55,13 @@ static int code_nn(const float* rows, int d, int64_t cap, const int32_t* live, i
   // one CTA per SM: the kernel takes all 512 TMEM columns
   size_t smem = codenn_gemm_smem(dp);
   if (smem < 120 * 1024) smem = 120 * 1024;
-  static size_t attr = 0;
-  if (attr < smem) {
+  static std::atomic<size_t> attr[kMaxDevices] = {};  // per device ordinal
+  int dev = 0;
+  if (int rc = current_device(&dev)) return rc;
+  if (attr[dev].load() < smem) {
     CGS_CUDA(cudaFuncSetAttribute(codenn_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    attr = smem;
+    attr[dev].store(smem);
   }
   CGS_PROFILED("codenn_gemm_kernel", st,
                codenn_gemm_kernel<<<static_cast<unsigned>(mpad / kNnM), kNnThreads, smem, st>>>(

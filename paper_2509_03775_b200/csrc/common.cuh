@@ -80,6 +80,12 @@ struct FrameHeader {
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* where);
 
+// Lazily initialised per-device values (function attributes, occupancy-sized
+// grids) are kept in arrays indexed by the current device ordinal: one
+// process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+int current_device(int* dev);
+
 #define CGS_CUDA(call)                                      \
   do {                                                      \
     cudaError_t e_ = (call);                                \

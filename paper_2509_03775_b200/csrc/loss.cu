@@ -8,13 +8,18 @@
 //   ssim_grad   32x32 pixels per CTA: adjoint filtering of the seeds
 //               (metrics.py:40-45) fused with the L1 sign term -> dL/dimage
 // Per-CTA partial sums are reduced in fixed order (deterministic).
+#include <atomic>
 #include <cmath>
 
 #include "common.cuh"
 
 namespace cgs {
 
-__constant__ double c_win[11];
+// 11-tap Gaussian window (sigma 1.5, metrics.py:20-30), passed by value so
+// that it lives in each launch's parameter bank: no per-device state.
+struct SsimWin {
+  double k[11];
+};
 
 struct LossLayout {
   float* seeds;      // V * 3 * 3 * (H-10)*(W-10)  [view][chan][map][pos]
@@ -68,7 +73,7 @@ struct GradSmem {
 #endif
 __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const float* __restrict__ img,
                                                          const float* __restrict__ gt, int H, int W,
-                                                         int do_ssim, LossLayout L) {
+                                                         int do_ssim, LossLayout L, SsimWin win) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   StatsSmem& S = *reinterpret_cast<StatsSmem*>(smem_raw);
   const int vc = blockIdx.z;
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
         double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
 #pragma unroll
         for (int j = 0; j < 11; ++j) {
-          const double a = av[o + j], b = bv[o + j], k = c_win[j];
+          const double a = av[o + j], b = bv[o + j], k = win.k[j];
           m0 += k * a; m1 += k * b; m2 += k * a * a; m3 += k * b * b; m4 += k * a * b;
         }
         S.hm[0][row][c0 + o] = m0; S.hm[1][row][c0 + o] = m1; S.hm[2][row][c0 + o] = m2;
@@ -150,7 +155,7 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
       for (int o = 0; o < 4; ++o) {
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < 11; ++j) acc += c_win[j] * hv[o + j];
+        for (int j = 0; j < 11; ++j) acc += win.k[j] * hv[o + j];
         m[q][o] = acc;
       }
     }
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(256, CGS_SSIMG_MINB) ssim_grad_kernel(const fl
                                                         double lam, double inv_size,
                                                         double inv_count, float grad_scale,
                                                         int do_ssim, LossLayout L,
-                                                        float* __restrict__ dL) {
+                                                        float* __restrict__ dL, SsimWin win) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GradSmem& S = *reinterpret_cast<GradSmem*>(smem_raw);
   const int vc = blockIdx.z;
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(256, CGS_SSIMG_MINB) ssim_grad_kernel(const fl
         for (int o = 0; o < 4; ++o) {
           double acc = 0.0;
 #pragma unroll
-          for (int j = 0; j < 11; ++j) acc += c_win[j] * sv[o + j];
+          for (int j = 0; j < 11; ++j) acc += win.k[j] * sv[o + j];
           S.hv[q][row][c0 + o] = acc;
         }
       }
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(256, CGS_SSIMG_MINB) ssim_grad_kernel(const fl
       for (int o = 0; o < 4; ++o) {
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < 11; ++j) acc += c_win[j] * hv[o + j];
+        for (int j = 0; j < 11; ++j) acc += win.k[j] * hv[o + j];
         r[q][o] = acc;
       }
     }
@@ -326,20 +331,16 @@ __global__ void __launch_bounds__(256) loss_final_kernel(LossLayout L, int64_t n
   }
 }
 
-static bool g_win_ready = false;
-
-static int ensure_window() {
-  if (g_win_ready) return CGS_OK;
-  double k[11], s = 0;
+static SsimWin make_window() {
+  SsimWin w;
+  double s = 0;
   for (int j = 0; j < 11; ++j) {
     const double r = (j - 5.0) / 1.5;
-    k[j] = exp(-0.5 * r * r);
-    s += k[j];
+    w.k[j] = exp(-0.5 * r * r);
+    s += w.k[j];
   }
-  for (int j = 0; j < 11; ++j) k[j] /= s;
-  CGS_CUDA(cudaMemcpyToSymbol(c_win, k, sizeof(k)));
-  g_win_ready = true;
-  return CGS_OK;
+  for (int j = 0; j < 11; ++j) w.k[j] /= s;
+  return w;
 }
 
 size_t loss_ws_bytes(int nv, int h, int w) {
@@ -349,8 +350,7 @@ size_t loss_ws_bytes(int nv, int h, int w) {
 int recon_loss(const float* img, const float* gt, int nv, int H, int W, double lam, float gscale,
                float* dL, double* losses, int want_ssim, void* ws, size_t ws_bytes,
                cudaStream_t st) {
-  int rc = ensure_window();
-  if (rc) return rc;
+  static const SsimWin win = make_window();
   LossLayout L = plan_loss(ws, ws_bytes, nv, H, W);
   if (L.bytes > ws_bytes) {
     set_error("loss workspace too small");
@@ -362,21 +362,23 @@ int recon_loss(const float* img, const float* gt, int nv, int H, int W, double l
   }
   const bool has_ssim = (H >= 11 && W >= 11) && (lam != 0.0 || want_ssim);
   const dim3 grid(blocks_x(W), blocks_y(H), 3 * nv);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<bool> attr[kMaxDevices] = {};  // per device ordinal
+  int dev = 0;
+  if (int rc = current_device(&dev)) return rc;
+  if (!attr[dev].load()) {
     CGS_CUDA(cudaFuncSetAttribute(ssim_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(StatsSmem))));
     CGS_CUDA(cudaFuncSetAttribute(ssim_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(GradSmem))));
-    attr = true;
+    attr[dev].store(true);
   }
-  CGS_PROFILED("ssim_stats_kernel", st, ssim_stats_kernel<<<grid, 256, sizeof(StatsSmem), st>>>(img, gt, H, W, has_ssim ? 1 : 0, L));
+  CGS_PROFILED("ssim_stats_kernel", st, ssim_stats_kernel<<<grid, 256, sizeof(StatsSmem), st>>>(img, gt, H, W, has_ssim ? 1 : 0, L, win));
   CGS_CHECK_LAUNCH("ssim_stats_kernel");
   const double inv_size = 1.0 / (3.0 * H * W);
   const double inv_count = has_ssim ? 1.0 / (3.0 * (H - 10.0) * (W - 10.0)) : 0.0;
   if (dL) {
     CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, sizeof(GradSmem), st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
-                                           (has_ssim && lam != 0.0) ? 1 : 0, L, dL));
+                                           (has_ssim && lam != 0.0) ? 1 : 0, L, dL, win));
     CGS_CHECK_LAUNCH("ssim_grad_kernel");
   }
   const int64_t nb = static_cast<int64_t>(blocks_x(W)) * blocks_y(H) * 3;

@@ -21,6 +21,8 @@
 // 64-byte record per copy, completion on an mbarrier) one batch ahead of the
 // blending, and converted once per batch to tile-relative fp32 form in shared
 // memory.
+#include <atomic>
+
 #include "frame.cuh"
 #include "raster_common.cuh"
 
@@ -752,13 +754,17 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
                       const float* logits, cudaStream_t st) {
   unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl);
   CGS_CHECK_LAUNCH("unit_order_kernel");
-  static int resident = 0;  // persistent grid: every resident CTA slot
+  // persistent grid: every resident CTA slot (per device ordinal)
+  static std::atomic<int> resident_dev[kMaxDevices] = {};
+  int dev = 0;
+  if (int rc = current_device(&dev)) return rc;
+  int resident = resident_dev[dev].load();
   if (resident == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    CGS_CUDA(cudaGetDevice(&dev));
+    int sms = 0, per_sm = 0;
     CGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raster_bwd_kernel<false>, 128, 0));
     resident = sms * (per_sm > 0 ? per_sm : 1);
+    resident_dev[dev].store(resident);
   }
   const int grid = static_cast<int>(L.n_ckpt < resident ? L.n_ckpt : resident);
   unsigned long long* trace = tile_trace_buffer();

@@ -31,6 +31,8 @@
 //            pair's partial by the thread that owns the record; pixels are
 //            walked in a fixed order with barriers in between, so the
 //            backward stays deterministic.
+#include <atomic>
+
 #include "frame.cuh"
 #include "raster_common.cuh"
 
@@ -404,23 +406,19 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                   const float* dL, float* partials, cudaStream_t st) {
   const int64_t p9 = 8 * (L.pair_cap > 0 ? L.pair_cap : 1);
   // one wave of resident CTAs (per device ordinal: a process may drive several GPUs)
-  static int resident[2][64] = {};
+  static std::atomic<int> resident[2][kMaxDevices] = {};
   int dev = 0;
-  CGS_CUDA(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 64) {
-    set_error("device ordinal out of range");
-    return CGS_EINTERNAL;
-  }
-  if (resident[bwd][dev] == 0) {
+  if (int rc = current_device(&dev)) return rc;
+  if (resident[bwd][dev].load() == 0) {
     int sms = 0, per_sm = 0;
     CGS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (bwd)
       CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel<true>, kThreads, 0));
     else
       CGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel<false>, kThreads, 0));
-    resident[bwd][dev] = sms * (per_sm > 0 ? per_sm : 1);
+    resident[bwd][dev].store(sms * (per_sm > 0 ? per_sm : 1));
   }
-  const int grid = resident[bwd][dev];
+  const int grid = resident[bwd][dev].load();
   if (bwd) {
     CGS_PROFILED("refine_bwd_kernel", st,
                  (refine_kernel<true><<<grid, kThreads, 0, st>>>(

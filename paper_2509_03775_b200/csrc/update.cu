@@ -61,6 +61,7 @@ struct SgldDev {
   uint64_t seed, offset;
   int noise_src;
   const uint64_t* offset_dev;
+  int32_t* sticky;
 };
 
 __device__ __forceinline__ float sgld_one(float v, float g, double c, double k, double gscale,
@@ -80,8 +81,12 @@ __global__ void __launch_bounds__(256) finite_check_kernel(const float* __restri
                                                            const float* __restrict__ b, int64_t nb,
                                                            const float* __restrict__ c, int64_t nc,
                                                            const float* __restrict__ d, int64_t nd,
-                                                           int32_t* flags, uint64_t* ctr) {
-  if (ctr && blockIdx.x == 0 && threadIdx.x == 0) *ctr += 1;  // noise offset for this update
+                                                           int32_t* flags, uint64_t* ctr,
+                                                           const int32_t* __restrict__ skip_if) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (ctr) *ctr += 1;  // noise offset for this update
+    if (skip_if && *skip_if) atomicOr(flags, 2);
+  }
   const int64_t tot = na + nb + nc + nd;
   bool bad = false;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < tot;
@@ -93,7 +98,11 @@ __global__ void __launch_bounds__(256) finite_check_kernel(const float* __restri
     else x = d[i - na - nb - nc];
     if (!isfinite(x)) bad = true;
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) flags[0] = 1;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 1);
+}
+
+__global__ void sticky_or_kernel(int32_t* sticky, const int32_t* flags) {
+  if (flags[0]) atomicOr(sticky, flags[0]);
 }
 
 __global__ void __launch_bounds__(256) sgld_kernel(
@@ -104,7 +113,8 @@ __global__ void __launch_bounds__(256) sgld_kernel(
     const float* __restrict__ gsr, SgldDev p, const double* __restrict__ npos,
     const double* __restrict__ nlog, const double* __restrict__ nsh,
     const double* __restrict__ nsr, const int32_t* __restrict__ flags) {
-  if (flags[0]) return;  // non-finite gradients: reject before any mutation
+  if (p.sticky && blockIdx.x == 0 && threadIdx.x == 0 && flags[0]) atomicOr(p.sticky, flags[0]);
+  if (flags[0]) return;  // non-finite gradients or skip: reject before any mutation
   const uint64_t offset = p.offset_dev ? *p.offset_dev : p.offset;
   const int64_t a = p.on_pos ? 3 * n : 0;
   const int64_t b = p.on_op ? n : 0;
@@ -190,7 +200,8 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
   CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
   const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
   CGS_PROFILED("finite_check_kernel", st, finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
-                                                                          nc, gsr, nd, flags, hp->offset_dev));
+                                                                          nc, gsr, nd, flags, hp->offset_dev,
+                                                                          hp->skip_if));
   CGS_CHECK_LAUNCH("finite_check_kernel");
   SgldDev p{};
   // exactly numpy's scalar sub-expressions: 0.5 * eps and mult * sqrt(eps)
@@ -211,6 +222,7 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
   p.offset = hp->offset;
   p.noise_src = hp->noise_source;
   p.offset_dev = hp->offset_dev;
+  p.sticky = hp->sticky;
   if (p.noise_src == 1) {
     if ((p.k_pos != 0.0 && !npos) || (p.k_op != 0.0 && !nlog) || (p.k_sh != 0.0 && !nsh) ||
         (p.k_sr != 0.0 && !nsr)) {
@@ -225,6 +237,9 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
                                                        sr_live, n_sr, gpos, glogit, gsh, gsr, p,
                                                        npos, nlog, nsh, nsr, flags));
     CGS_CHECK_LAUNCH("sgld_kernel");
+  } else if (p.sticky) {
+    sticky_or_kernel<<<1, 1, 0, st>>>(p.sticky, flags);
+    CGS_CHECK_LAUNCH("sticky_or_kernel");
   }
   return CGS_OK;
 }

@@ -7,9 +7,10 @@ followed, on the schedule, by one forced split and one forced merge
 transition (`sampler.py:339-385`) and densify when due (`sampler.py:387-390`).
 
 No host synchronisation inside an update: the frame's pair buffers are sized
-from a warm-up render and any overflow is latched in a sticky device flag
-that is checked when the caller reads results; non-finite gradients make the
-SGLD kernel skip the update and latch a flag as well.  Across GPUs, views are
+from a warm-up render (pairs per Gaussian x the current N x headroom, so they
+grow with densify); an overflowing frame makes the SGLD kernels skip the
+update (no state change), as non-finite gradients do, and both latch a sticky
+device flag that is checked when the caller reads results.  Across GPUs, views are
 sharded by rank and the flat gradient buffer is summed with one NCCL
 allreduce (``torch.distributed``); MCMC decisions use the same host
 Generator seed on every rank, so replicas stay identical with no broadcast.
@@ -30,10 +31,22 @@ from .sampler import (SamplerConfig, SamplerError, TransitionRecord, merge_step,
                       split_step)
 
 
+def _host_noise_groups(config: SamplerConfig) -> bool:
+    """Whether the reference's update draws noise (sampler.py:276-297)."""
+    return any(eps > 0.0 and mult != 0.0 for eps, mult in (
+        (config.step_pos, config.noise_pos), (config.step_opacity, config.noise_opacity),
+        (config.step_sh, config.noise_sh), (config.step_sr, config.noise_sr)))
+
+
 class Trainer:
     def __init__(self, state: ModelState, cams, gts: torch.Tensor, config: SamplerConfig,
                  rng: np.random.Generator, mcmc_every: int = 25, world: int = 1,
-                 pair_headroom: float = 1.5, allreduce=None, use_graphs: bool = False):
+                 pair_headroom: float = 1.5, allreduce=None, use_graphs: bool = False,
+                 total_views: int = None):
+        if use_graphs and not config.device_noise and _host_noise_groups(config):
+            # a captured graph would replay the noise drawn once at capture
+            raise ValueError("use_graphs needs config.device_noise=True when the SGLD update draws "
+                             "noise (host-drawn noise cannot be replayed from a CUDA graph)")
         self.state = state
         self.cams = list(cams)
         self.config = config
@@ -46,6 +59,11 @@ class Trainer:
         if any((c.height, c.width) != (h, w) for c in self.cams):
             raise ValueError("batched views need equal sizes")
         self.V = len(self.cams)
+        # gradients are summed over every view of the step on every rank, then
+        # divided by their total: the mean even when shards are unequal
+        self.total_views = total_views if total_views is not None else self.V * world
+        if self.total_views < self.V:
+            raise ValueError("total_views must count every rank's views")
         self.dev = state.device
         self.gts = gts
         self.loss_ws = LossWorkspace(self.V, h, w, self.dev)
@@ -56,6 +74,7 @@ class Trainer:
         self.bws = None
         self.dL = None
         self.pair_cap = None
+        self._pairs_per_gaussian = None
         self.updates = 0
         self.mcmc_events = 0
         self.mcmc_ms = []
@@ -104,9 +123,12 @@ class Trainer:
         st = self.state
         fr = self.frame
         if fr is None or fr.n != st.num_gaussians or fr.sr_cap != st.sr.capacity:
-            if self.pair_cap is None:
+            if self._pairs_per_gaussian is None:
                 probe = Frame(st, self.cams).run_checked()
-                self.pair_cap = int(probe.stats().n_pairs * self.headroom) + 4096
+                self._pairs_per_gaussian = probe.stats().n_pairs / max(st.num_gaussians, 1)
+            # pairs grow with N (densify): rescale, never shrink
+            cap = int(self._pairs_per_gaussian * st.num_gaussians * self.headroom) + 4096
+            self.pair_cap = max(self.pair_cap or 0, cap)
             self._capacity_buffers()
             self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap, ws=self._frame_ws)
             if self.dL is None or self.dL.shape != self.frame.image.shape:
@@ -129,20 +151,19 @@ class Trainer:
     def _enqueue_forward(self):
         fr = self.frame
         fr.run()
-        ov = fr.ws[40:44].view(torch.int32)  # cgs_frame_stats_t.overflow (byte 40)
-        torch.maximum(self.sticky, ov, out=self.sticky)
         self.loss_ws.run(fr.image, self.gts, self.config.lambda_ssim, self.dL, 1.0)
 
     def _enqueue_backward(self):
-        self.frame.backward(self.dL, scale=1.0 / (self.V * self.world), grads=self.grads,
-                            ws=self.bws)
+        self.frame.backward(self.dL, scale=1.0 / self.total_views, grads=self.grads, ws=self.bws)
         if self.allreduce is not None:
             self.allreduce(self.grads.flat)
 
     def _enqueue_sgld(self):
+        # cgs_frame_stats_t.overflow (byte 40 of the frame workspace): an
+        # overflowing frame skips the update; flags latch into self.sticky
+        ov = self.frame.ws[40:44].view(torch.int32)
         sgld_update(self.state, self.grads, self.config, self.rng, flags=self.flags, check=False,
-                    offset_dev=self.noise_ctr)
-        torch.maximum(self.sticky, self.flags * 2, out=self.sticky)
+                    offset_dev=self.noise_ctr, skip_if=ov, sticky=self.sticky)
 
     def _graph_key(self):
         st = self.state
@@ -248,10 +269,11 @@ class Trainer:
     def check(self):
         """Raise if any update overflowed its pair buffers or saw non-finite gradients."""
         v = int(self.sticky.item())
-        if v & 1:
-            raise RuntimeError("pair capacity overflow during the run (raise pair_headroom)")
         if v & 2:
-            raise SamplerError("non-finite gradients during the run")
+            raise RuntimeError("pair capacity overflow during the run (raise pair_headroom); "
+                               "the overflowing updates were skipped")
+        if v & 1:
+            raise SamplerError("non-finite gradients during the run (those updates were skipped)")
 
     def recon(self) -> float:
         return float(self.last_loss.view(self.V, 3)[:, 2].mean().item())

@@ -79,6 +79,7 @@ class Codebook:
         self._dev_rc = None
         self._dev_rc_host = None
         self._live_cache = None
+        self._live_version = 0  # bumped whenever the free heap (the dead rows) changes
         self.mutations = 0
 
     # -- host refcount mirror ----------------------------------------------
@@ -159,6 +160,7 @@ class Codebook:
         """Allocate a row index (refcount 1) without writing its value."""
         if parent != -1 and not self.is_live(parent):
             raise ValueError(f"parent row {parent} is not live")
+        self._live_version += 1
         if self._free:
             r = heapq.heappop(self._free)
         else:
@@ -187,6 +189,7 @@ class Codebook:
             self.parent[r] = -1
             self.parent[self.parent == r] = -1
             heapq.heappush(self._free, int(r))
+            self._live_version += 1
             return True
         return False
 
@@ -200,6 +203,7 @@ class Codebook:
         """Rebuild the free heap from zero refcounts (after bulk refcount edits)."""
         self._free = [int(r) for r in np.flatnonzero(self.refcount == 0)]
         heapq.heapify(self._free)
+        self._live_version += 1
 
     # -- device mirrors ---------------------------------------------------
     def device_refcount(self) -> torch.Tensor:
@@ -217,7 +221,9 @@ class Codebook:
         without applying pending densify increments: those only raise counts of
         rows that are already live, so the live set is the same (and the
         training loop does not wait for the device)."""
-        key = self._rc.tobytes()
+        # the live rows are exactly the rows not in the free heap (validate_state):
+        # its size, identity and change counter key the cache (O(1), no scan)
+        key = (self._cap, len(self._free), id(self._free), self._live_version)
         if self._live_cache is None or self._live_cache[0] != key:
             from . import _native as nat
             self._live_cache = (key, nat.upload(np.flatnonzero(self._rc > 0), self._buf.device,

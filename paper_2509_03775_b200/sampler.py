@@ -28,7 +28,7 @@ import torch
 from . import _native as nat
 from .metrics import LossWorkspace, total_loss
 from .model import ModelState, _book_of, densify, validate_state
-from .render import Frame, GradientSet, rasterize_forward
+from .render import Frame, GradientSet, backward_workspace_bytes, rasterize_forward
 
 
 class SamplerError(RuntimeError):
@@ -357,23 +357,42 @@ def _host_noise(state: ModelState, config: SamplerConfig, rng, n_sh_live, n_sr_l
 
 def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
                 rng: np.random.Generator, flags: torch.Tensor = None, check: bool = True,
-                offset_dev: torch.Tensor = None) -> None:
+                offset_dev: torch.Tensor = None, skip_if: torch.Tensor = None,
+                sticky: torch.Tensor = None) -> None:
     """SGLD step per group (sampler.py:262-300) on the device.
 
     ``offset_dev`` (int64 device counter) makes device-noise draws advance on
     the device, so a captured CUDA graph of the update draws fresh noise on
-    every replay."""
+    every replay.  ``skip_if`` (device int32, e.g. the frame's overflow flag)
+    makes the update write nothing when set; ``sticky`` (device int32)
+    accumulates the flags (1 non-finite, 2 skipped) for a check at the end."""
+    noise = _draw_noise(state, config, rng)
+    _sgld_launch(state, grads, config, noise, flags if flags is not None else None, offset_dev,
+                 skip_if, sticky, check)
+
+
+def _draw_noise(state: ModelState, config: SamplerConfig, rng) -> list:
+    """Parity mode: the reference's host draws for this update (None in
+    device-noise mode, where the kernel draws Philox normals)."""
+    if config.device_noise:
+        return [None] * 4
+    return _host_noise(state, config, rng, state.sh.device_live().numel(),
+                       state.sr.device_live().numel())
+
+
+def _sgld_launch(state: ModelState, grads: GradientSet, config: SamplerConfig, noise: list,
+                 flags, offset_dev, skip_if, sticky, check: bool) -> None:
     dev = state.device
     g = state.gaussians
     sh_live = state.sh.device_live()
     sr_live = state.sr.device_live()
     if config.device_noise:
-        noise = [None] * 4
         params = _sgld_params(config, 1.0, config.seed, state.iteration, 0)
         params.offset_dev = nat.ptr(offset_dev)
     else:
-        noise = _host_noise(state, config, rng, sh_live.numel(), sr_live.numel())
         params = _sgld_params(config, 1.0, 0, 0, 1)
+    params.skip_if = nat.ptr(skip_if)
+    params.sticky = nat.ptr(sticky)
     if flags is None:
         flags = torch.zeros((1,), dtype=torch.int32, device=dev)
     nat.call("cgs_sgld_update", nat.ptr(g.positions), nat.ptr(g.opacity_logits), g.count,
@@ -386,8 +405,12 @@ def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
     state.touch()
     state.sh.mutations += 1
     state.sr.mutations += 1
-    if check and int(flags[0].item()) != 0:
-        raise SamplerError(f"non-finite gradients at iteration {state.iteration}")
+    if check:
+        f = int(flags[0].item())
+        if f & 1:
+            raise SamplerError(f"non-finite gradients at iteration {state.iteration}")
+        if f & 2:
+            raise RuntimeError("update skipped: the frame overflowed its pair capacity")
 
 
 def _candidate_count(fraction: float, population: int) -> int:
@@ -417,6 +440,7 @@ def clone_state(state: ModelState) -> ModelState:
                                 iteration=state.iteration, rng_seed=state.rng_seed)
     for src, dst in ((state.sh, st.sh), (state.sr, st.sr)):
         dst._free = list(src._free)
+        dst._live_version += 1
     return st
 
 
@@ -511,39 +535,124 @@ def merge_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
     _apply_remap(state, which, remap)
 
 
-class _GtCache:
-    def __init__(self):
+class _StepEngine:
+    """Buffers of the drop-in update path, cached on the state per camera
+    batch shape: frame / backward / gradient workspaces sized for the current
+    Gaussian count and codebook capacities, the loss workspace, a pinned
+    staging buffer for the host target image, and the pair capacity (probed
+    once, then scaled with N).  An update then needs one host synchronisation
+    (reading the recon loss and the flags together)."""
+
+    def __init__(self, state: ModelState, cams):
+        self.dev = state.device
+        self.shape = tuple((c.width, c.height) for c in cams)
+        v, h, w = len(cams), cams[0].height, cams[0].width
+        self.loss = LossWorkspace(v, h, w, self.dev)
+        self.dL = None
+        self.flags = torch.zeros((1,), dtype=torch.int32, device=self.dev)
+        self.host = torch.zeros((2,), dtype=torch.float64).pin_memory()
+        self.gt_stage = None
+        self.gt_dev = None
+        self.pair_cap = None
+        self.pairs_per_gaussian = None
         self.key = None
-        self.val = None
+        self.frames = {}
 
-    def get(self, img, device):
-        if isinstance(img, torch.Tensor) and img.is_cuda:
-            return img.to(torch.float32).contiguous()
-        k = (id(img), getattr(img, "shape", None))
-        if self.key != k:
-            self.key = k
-            self.val = torch.as_tensor(np.ascontiguousarray(img, dtype=np.float32)).to(device)
-        return self.val
+    def prepare(self, state: ModelState, cams):
+        if self.pairs_per_gaussian is None:
+            probe = Frame(state, cams).run_checked()
+            self.pairs_per_gaussian = probe.stats().n_pairs / max(state.num_gaussians, 1)
+        cap = int(self.pairs_per_gaussian * state.num_gaussians * 1.5) + 4096
+        self.pair_cap = max(self.pair_cap or 0, cap)
+        key = (state.num_gaussians, state.sh.capacity, state.sr.capacity, self.pair_cap)
+        if key != self.key:
+            self.key = key
+            self.frames = {}
+            self.frame_ws = None
+            self.bws = None
+            self.grads = GradientSet.empty(state)
+        ck = tuple(c.key() for c in cams)
+        fr = self.frames.get(ck)
+        if fr is None:
+            fr = Frame(state, cams, pair_capacity=self.pair_cap, ws=self.frame_ws)
+            self.frame_ws = fr.ws
+            if len(self.frames) > 64:
+                self.frames = {}
+            self.frames[ck] = fr
+        if self.dL is None or self.dL.shape != fr.image.shape:
+            self.dL = torch.empty_like(fr.image)
+        nb = backward_workspace_bytes(state, fr)
+        if self.bws is None or self.bws.numel() < nb:
+            self.bws = torch.empty((nb,), dtype=torch.uint8, device=self.dev)
+        return fr
+
+    def grow(self, state: ModelState, fr: Frame):
+        """The frame overflowed: size the pairs from its count and start over."""
+        n_pairs = fr.stats().n_pairs
+        self.pair_cap = max(self.pair_cap, int(n_pairs * 1.25) + 1024)
+        self.pairs_per_gaussian = max(self.pairs_per_gaussian, n_pairs / max(state.num_gaussians, 1))
+        self.key = None
+
+    def target(self, gt) -> torch.Tensor:
+        """The step's target image on the device (uploaded every call, through a
+        pinned staging buffer: a caller may edit or replace its arrays)."""
+        if isinstance(gt, torch.Tensor) and gt.is_cuda:
+            return gt.to(torch.float32).contiguous()
+        a = np.asarray(gt)
+        if self.gt_stage is None or tuple(self.gt_stage.shape) != a.shape:
+            self.gt_stage = torch.empty(a.shape, dtype=torch.float32).pin_memory()
+            self.gt_dev = torch.empty(a.shape, dtype=torch.float32, device=self.dev)
+        np.copyto(self.gt_stage.numpy(), a, casting="unsafe")
+        self.gt_dev.copy_(self.gt_stage, non_blocking=True)
+        return self.gt_dev
 
 
-_gt_cache = _GtCache()
+def _engine(state: ModelState, cams) -> _StepEngine:
+    cache = state.__dict__.setdefault("_step_engines", {})
+    key = tuple((c.width, c.height) for c in cams)
+    eng = cache.get(key)
+    if eng is None:
+        eng = cache[key] = _StepEngine(state, cams)
+    return eng
 
 
 def update_step(state: ModelState, cams, gts, config: SamplerConfig, rng, check: bool = True):
     """Batched SGLD update over views (mean of per-view gradients; reduces to the
-    reference's single-view update when len(cams) == 1).  Returns the device
-    recon loss (mean over views)."""
+    reference's single-view update when len(cams) == 1).  Returns the recon
+    loss (mean over views) as a float; one host synchronisation, which also
+    reads the update's flags.  A frame that overflowed its pair capacity
+    skips the update on the device; it is then re-run with the same noise."""
     v = len(cams)
-    fr = Frame(state, cams).run_checked()
     h, w = cams[0].height, cams[0].width
     if any((c.height, c.width) != (h, w) for c in cams):
         raise ValueError("a batched update needs equal image sizes")
-    lw = LossWorkspace(v, h, w, state.device)
-    dL = torch.empty_like(fr.image)
-    losses = lw.run(fr.image, gts, config.lambda_ssim, dL, 1.0)
-    grads = fr.backward(dL, scale=1.0 / v)
-    sgld_update(state, grads, config, rng, check=check)
-    return losses.view(v, 3)[:, 2].mean()
+    eng = _engine(state, cams)
+    gt_d = eng.target(gts)
+    if tuple(gt_d.shape[-3:]) != (h, w, 3):
+        raise ValueError("ground-truth image shape mismatch")
+    state.code_csr("sh")
+    state.code_csr("sr")
+    noise = _draw_noise(state, config, rng)
+    for _ in range(3):
+        fr = eng.prepare(state, cams)
+        fr.run()
+        losses = eng.loss.run(fr.image, gt_d, config.lambda_ssim, eng.dL, 1.0)
+        fr.backward(eng.dL, scale=1.0 / v, grads=eng.grads, ws=eng.bws)
+        ov = fr.ws[40:44].view(torch.int32)  # cgs_frame_stats_t.overflow
+        _sgld_launch(state, eng.grads, config, noise, eng.flags, None, ov, None, False)
+        eng.host[0].copy_(losses.view(v, 3)[:, 2].mean(), non_blocking=True)
+        eng.host[1].copy_(eng.flags[0], non_blocking=True)
+        torch.cuda.current_stream(state.device).synchronize()
+        f = int(eng.host[1].item())
+        if f & 2:  # overflow: nothing was written; grow and redo
+            eng.grow(state, fr)
+            continue
+        if f & 1 and check:
+            raise SamplerError(f"non-finite gradients at iteration {state.iteration}")
+        if fr.stats().zero_quaternion:
+            raise ValueError("zero quaternion")
+        return float(eng.host[0].item())
+    raise RuntimeError("pair capacity overflow persisted")
 
 
 def train_step(state: ModelState, views: list, config: SamplerConfig,
@@ -557,10 +666,7 @@ def train_step(state: ModelState, views: list, config: SamplerConfig,
                            lambdas=(config.lambda_sh, config.lambda_sr))
     if kind == "update":
         cam, gt = views[int(rng.integers(len(views)))]
-        gt_d = _gt_cache.get(gt, state.device)
-        if tuple(gt_d.shape) != (cam.height, cam.width, 3):
-            raise ValueError("ground-truth image shape mismatch")
-        rec.recon = update_step(state, [cam], gt_d, config, rng)
+        rec.recon = update_step(state, [cam], gt, config, rng)
         rec.attempts, rec.accepts = 1, 1
         rec.accept_probs.append(1.0)
     elif kind == "split":
