@@ -84,13 +84,15 @@ def workload_name(config):
 
 
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled every 20 ms through NVML
-    during the timed region (same fields as the recipe's nvidia-smi clocks line)."""
+    """SM clocks and clock-event (throttle) reasons through NVML during the
+    timed region (same fields as the recipe's nvidia-smi clocks line): one
+    sample when the region starts and one when it stops (synchronously, so
+    even a 10 ms region has a record), and every `period` seconds between."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index, period=0.02):
+    def __init__(self, gpu_index, period=0.002):
         import threading
         self.gpu = gpu_index
         self.period = period
@@ -98,32 +100,44 @@ class ClockSampler:
         self.stop_ev = threading.Event()
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.err = None
-
-    def _run(self):
+        self.h = None
+        self.max_sm = None
         try:
             import pynvml as nv
             nv.nvmlInit()
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
             idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
-            h = nv.nvmlDeviceGetHandleByIndex(idx)
-            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self.stop_ev.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                util = nv.nvmlDeviceGetUtilizationRates(h).gpu
-                self.samples.append((sm, rs, util))
-                time.sleep(self.period)
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
         except Exception as e:  # NVML missing: report it instead of inventing clocks
             self.err = repr(e)
 
+    def _sample(self):
+        nv, h = self.nv, self.h
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(h),
+                             nv.nvmlDeviceGetUtilizationRates(h).gpu))
+
+    def _run(self):
+        try:
+            while not self.stop_ev.wait(self.period):
+                self._sample()
+        except Exception as e:
+            self.err = repr(e)
+
     def start(self):
+        if self.h is None:
+            return
+        self._sample()
         self.thread.start()
 
     def stop(self):
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
         self.stop_ev.set()
         self.thread.join(timeout=5)
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        self._sample()
         busy = [s for s in self.samples if s[2] > 0] or self.samples
         reasons = set()
         for _, rs, _ in busy:
@@ -132,7 +146,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(s[0] for s in busy), "sm_max_mhz": self.max_sm,
                 "reasons": sorted(reasons), "samples": len(self.samples),
-                "samples_under_load": len(busy)}
+                "samples_under_load": len(busy), "period_ms": 1000.0 * self.period}
 
 
 # ---------------------------------------------------------------------------
@@ -221,6 +235,37 @@ def cpu_iteration_timer(config, seed):
               "worker processes, mean grad, SGLD) through the numpy oracle port "
               "(oracle/cgs_oracle.py) of the reference")
     return run, cores, sample, pool
+
+
+def cpu_one_core(config, seed):
+    """The reference algorithm (numpy oracle port) on ONE core: forward, L1/SSIM
+    gradient and backward of view 0 in this process with BLAS limited to one
+    thread (SURVEY.md §8(d) asks for a 1-core figure beside the all-cores one).
+    Config 0/1: the whole view, scaled by the step's view count; larger
+    configs: a 32-row strip of it, scaled by its share of the step's pixels.
+    Returns (it/s estimate, seconds measured, description)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import cgs_oracle as O
+    a, g, cams = make_scene(config, seed, 0, 1)
+    cam = O.cam_from_any(cams[0])
+    rows = cam.height if config <= 1 else 32
+    strip = _strip_cam(cam, 0, rows)
+    gst = O.OState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows, g.sr_rows)
+    gt = np.round(np.clip(O.raster_forward(gst, strip)["image"], 0.0, 1.0) * 255.0) / 255.0
+    st = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    lam = 0.0 if config == 0 or rows < 11 else 0.2
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        img = O.raster_forward(st, strip)["image"]
+        dL = O.recon_loss_grad(img, gt, lam)
+        O.raster_backward(st, strip, dL)
+        secs = time.perf_counter() - t0
+    share = (rows * cam.width) / float(sum(c.width * c.height for c in cams))
+    per_iter = secs / share
+    return (1.0 / per_iter, secs,
+            f"view 0 {'rows 0-31 ' if rows != cam.height else ''}fwd + loss grad + bwd through the "
+            f"numpy oracle port in 1 process, BLAS 1 thread: {secs:.1f} s for {share:.3g} of the "
+            f"step's pixels, scaled to one iteration ({per_iter:.1f} s)")
 
 
 def run_reference(args):
@@ -641,7 +686,7 @@ def main():
     achieved = alg / avg_s / 1e9 if avg_s > 0 else 0.0
     # DRAM bytes per launch of the same kernel from the committed ncu --set full
     # capture (profiles/ncu_traffic.json, written by scripts/ncu_summary.py)
-    traffic, traffic_src, issue_pct = None, None, None
+    traffic, traffic_src, issue_pct, compute = None, None, None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
@@ -650,6 +695,16 @@ def main():
                 traffic = float(t["bytes_per_launch"])
                 traffic_src = f"profiles/ncu_traffic.json ({t.get('source')}, ncu --set full)"
                 issue_pct = t.get("issue_active_pct")
+                # the compute side of the same launch: the raster kernels are
+                # bound by instruction issue, not by HBM or FP32 throughput
+                pct = lambda k: (t[k] / 100.0) if t.get(k) is not None else None
+                compute = {"bound": "issue", "issue_active_frac": pct("issue_active_pct"),
+                           "fp32_frac_of_peak": t.get("fp32_frac_of_peak"),
+                           "fp32_peak": "148 SMs x 128 lanes x 2 FLOP per cycle",
+                           "fma_pipe_frac": pct("fma_pipe_pct"), "alu_pipe_frac": pct("alu_pipe_pct"),
+                           "xu_pipe_frac": pct("xu_pipe_pct"),
+                           "lane_efficiency": t.get("lane_efficiency"),
+                           "source": traffic_src}
         except Exception:
             pass
     roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
@@ -658,8 +713,9 @@ def main():
                 "avg_launch_ms": avg_s * 1000.0, "launches": int(prof_n.value),
                 "alg_bytes_per_launch": alg, "P_x": P_x, "pixels": px,
                 "issue_active_frac": issue_pct / 100.0 if issue_pct else None,
-                "note": "the raster kernels are instruction-issue bound (ncu: ~74% issue slots "
-                        "busy, FMA+ALU pipes, see profiles/r1_ncu_raster_bwd_config1.txt), not "
+                "compute": compute,
+                "note": "the raster kernels are instruction-issue bound (ncu: ~75% issue slots "
+                        "busy, ALU + FMA pipes, see profiles/r2_ncu_raster_config1.txt), not "
                         "HBM bound; achieved uses processed-prefix algorithmic bytes only "
                         "(SURVEY.md §8(d)), traffic is the ncu DRAM bytes of one launch"}
 
@@ -667,6 +723,11 @@ def main():
     # step's target images, D2H of the recon loss) inside the timed region
     e2e = None
     if not args.no_e2e:
+        # config 1: BASELINE.json's run definition -- 100 iterations, forced
+        # split + merge every 25, densify when the transition count crosses
+        # 100 -- whatever --steps is; graph re-captures fall inside the window
+        n_e2e = max(args.steps, 100) if args.config == 1 else args.steps
+        ev0, dn0, cp0 = tr.mcmc_events, len(tr.densify_ms), tr.captures
         host_gt = (gts * 255.0).round().to(torch.uint8).cpu().pin_memory()
         # double-buffered device targets: step k+1's upload runs on a copy
         # stream while step k computes (the first upload is inside step 0's
@@ -676,8 +737,8 @@ def main():
         up_done = [torch.cuda.Event() for _ in range(2)]
         used = [torch.cuda.Event() for _ in range(2)]
         host_loss = torch.empty((3 * len(cams),), dtype=torch.float64).pin_memory()
-        e_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        e_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        e_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_e2e)]
+        e_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_e2e)]
         cur = torch.cuda.current_stream(dev)
 
         def upload(b):
@@ -690,7 +751,7 @@ def main():
         gc.disable()
         barrier()
         torch.cuda.synchronize()
-        for k in range(args.steps):
+        for k in range(n_e2e):
             if not args.no_flush:
                 flush.zero_()
             e_s[k].record()
@@ -700,7 +761,7 @@ def main():
             cur.wait_event(up_done[b])
             torch.mul(dev_gt[b], 1.0 / 255.0, out=tr.gts)  # uint8 -> [0, 1] on the device
             used[b].record(cur)
-            if k + 1 < args.steps:
+            if k + 1 < n_e2e:
                 upload(b ^ 1)
             tr.step()
             host_loss.copy_(tr.last_loss, non_blocking=True)
@@ -714,9 +775,15 @@ def main():
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": (args.steps * world) / (e_ms / 1000.0), "unit": "it/s",
+        e2e = {"value": (n_e2e * world) / (e_ms / 1000.0), "unit": "it/s",
                "h2d_bytes_per_step": int(host_gt.numel()),
-               "d2h_bytes_per_step": int(host_loss.numel() * 8)}
+               "d2h_bytes_per_step": int(host_loss.numel() * 8),
+               "iterations": n_e2e, "mcmc_events": tr.mcmc_events - ev0,
+               "densify": len(tr.densify_ms) - dn0, "graph_recaptures": tr.captures - cp0,
+               "note": "engine.Trainer with host (pinned) 8-bit targets uploaded every step and "
+                       "the losses read back; per-step CUDA events"
+                       + ("; BASELINE config-1 run: 100 iterations, MCMC every 25, densify"
+                          if args.config == 1 else "")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -725,6 +792,9 @@ def main():
         pool.close()
         cpu = {"value": 1.0 / secs, "unit": "it/s", "cores": cores, "kind": "port",
                "sample": sample, "seconds": secs}
+        v1, s1, d1 = cpu_one_core(args.config, args.seed)
+        cpu["one_core"] = {"value": v1, "unit": "it/s", "cores": 1, "kind": "port",
+                           "seconds_measured": s1, "sample": d1}
 
     if rank == 0:
         out = {"metric": "train iters/s", "value": iters_value, "unit": "it/s", "n_gpus": world,

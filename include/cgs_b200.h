@@ -294,6 +294,26 @@ CGS_API int cgs_sgld_update(float* positions, float* opacity_logits, int64_t n,
                     const double* noise_sh, const double* noise_sr,
                     int32_t* flags, cgs_stream_t stream);
 
+/* ---- MCMC host helpers (sampler.py:339-364), host memory, no CUDA ------ */
+/* Ascending ids i < n with refcount[idx[i]] >= 2 (sampler.py:344) into out
+ * (capacity n); count in *n_out.  `threads` host threads. */
+CGS_API int cgs_host_split_eligible(const int32_t* idx, int64_t n, const int64_t* refcount,
+                                    int64_t k, int32_t* out, int64_t* n_out, int32_t threads);
+/* The split accept loop over n_cand candidates in order (sampler.py:349-364):
+ * a candidate whose row has refcount < 2 is skipped with no draws
+ * (decision -1); otherwise u = rng.normal(0, eps_split, dim) (numpy's own
+ * random_normal on `bitgen`, the bitgen_t of rng.bit_generator.capsule),
+ * log A = -lam - (-0.5 |u|^2 c_q [+ corr]) with |u|^2 from `ddot` (numpy's
+ * BLAS ddot, as `u @ u`), coin = rng.random(); accepted (decision 1) when
+ * coin < exp(min(0, log A)), and then refcount[row] -= 1.  u (n_cand x dim),
+ * log A and the coins are returned per candidate; *n_attempts counts the
+ * non-skipped ones.  The caller allocates rows (lowest free index) after. */
+CGS_API int cgs_host_split_decide(void* bitgen, void* ddot, int64_t n_cand, const int64_t* rows,
+                                  int64_t* refcount, int64_t k, int32_t dim, double lam,
+                                  double eps_split, double c_q, int32_t use_corr, double corr,
+                                  double* u_out, double* log_a_out, double* uniform_out,
+                                  int8_t* decision_out, int64_t* n_attempts);
+
 /* ---- MCMC / densify device helpers (sampler.py:184-259, model.py:235-267) */
 /* Ascending Gaussian ids i with refcount[idx[i]] >= 2 (sampler.py:344);
  * count written to *count (device int64).  Workspace from

@@ -9,6 +9,8 @@ caller's current torch CUDA stream.
 from __future__ import annotations
 
 import ctypes
+
+import numpy as np
 import os
 
 from .camera import CCamera
@@ -112,6 +114,9 @@ SIGNATURES = {
     "cgs_sgld_update": (I32, [P, P, I64, P, I32, P, I64, P, P, I64, I64, I64, P, P, P, P,
                               ctypes.POINTER(CSgldParams), P, P, P, P, P, P]),
     "cgs_split_eligible": (I32, [P, I64, P, P, P, P, SZ, P]),
+    "cgs_host_split_eligible": (I32, [P, I64, P, I64, P, P, I32]),
+    "cgs_host_split_decide": (I32, [P, P, I64, P, P, I64, I32, F64, F64, F64, I32, F64, P, P, P, P,
+                                    P]),
     "cgs_apply_splits": (I32, [P, I32, P, P, P, P, P, I64, P]),
     "cgs_apply_remap": (I32, [P, I64, P, I64, P]),
     "cgs_densify_append": (I32, [P, P, P, P, I64, P, P, I64, P]),
@@ -199,3 +204,56 @@ def upload(a, device, dtype=None):
     if host.numel() == 0:
         return torch.empty(host.shape, dtype=host.dtype, device=device)
     return host.pin_memory().to(device, non_blocking=True)
+
+
+# ---------------------------------------------------------------------------
+# numpy internals the MCMC host loop (cgs_host_split_decide) runs on
+def bitgen_ptr(rng) -> int:
+    """Address of the bitgen_t behind a numpy Generator (its PyCapsule): the
+    C loop draws from the caller's own stream."""
+    cap = rng.bit_generator.capsule
+    get = ctypes.pythonapi.PyCapsule_GetPointer
+    get.restype = ctypes.c_void_p
+    get.argtypes = [ctypes.py_object, ctypes.c_char_p]
+    return get(cap, b"BitGenerator")
+
+
+_DDOT = []
+
+
+def numpy_ddot_ptr():
+    """numpy's BLAS ddot (what ``u @ u`` runs for float64 vectors), resolved
+    from the OpenBLAS numpy ships and checked against ``u @ u`` bit for bit;
+    None if it cannot be found (callers then keep the Python loop)."""
+    if _DDOT:
+        return _DDOT[0]
+    import glob
+    import os
+    fn = None
+    libdir = os.path.join(os.path.dirname(os.path.dirname(np.__file__)), "numpy.libs")
+    for path in sorted(glob.glob(os.path.join(libdir, "*openblas*.so*"))):
+        try:
+            lib = ctypes.CDLL(path)
+        except OSError:
+            continue
+        for name in ("scipy_cblas_ddot64_", "cblas_ddot64_", "cblas_ddot"):
+            f = getattr(lib, name, None)
+            if f is None:
+                continue
+            f.restype = ctypes.c_double
+            f.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                          ctypes.c_int64]
+            rng = np.random.default_rng(12345)
+            ok = True
+            for d in (1, 3, 7, 12, 48, 100):
+                for _ in range(8):
+                    u = rng.normal(0.0, 0.1, d)
+                    if f(d, u.ctypes.data, 1, u.ctypes.data, 1) != float(u @ u):
+                        ok = False
+            if ok:
+                fn = ctypes.cast(f, ctypes.c_void_p).value
+                break
+        if fn:
+            break
+    _DDOT.append(fn)
+    return fn

@@ -21,8 +21,20 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libcgs_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# host code keeps each floating-point operation separately rounded (the MCMC
+# host loop reproduces numpy's float expressions bit for bit)
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-I", INCLUDE]
+         "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr", "-I", INCLUDE]
+
+
+def _npyrandom() -> str:
+    """numpy's own distributions library (random_normal, as Generator.normal
+    runs it), linked statically for the MCMC host loop (mcmc_host.cu)."""
+    import numpy
+    p = os.path.join(os.path.dirname(numpy.__file__), "random", "lib", "libnpyrandom.a")
+    if not os.path.exists(p):
+        raise RuntimeError(f"numpy's libnpyrandom.a not found at {p}")
+    return p
 
 
 def _nvcc():
@@ -74,7 +86,9 @@ def build(force: bool = False, verbose: bool = False, defines=None, out: str = N
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
     tmp = lib + ".tmp"
-    cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
+    # the static numpy library's symbols stay local to this .so
+    cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-Xlinker", "--exclude-libs,ALL", "-o", tmp,
+           *objs, _npyrandom()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")

@@ -455,7 +455,7 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
     # eligible = Gaussians whose row is shared (sampler.py:344), from the host
     # mirrors of the assignments and refcounts: no device round trip
     hidx = state.host_index(which)
-    elig = np.flatnonzero(book.refcount[hidx] >= 2)
+    elig = _eligible(hidx, book.refcount)
     n_elig = len(elig)
     n_cand = min(_candidate_count(config.split_fraction, n), n_elig)
     if n_cand <= 0:
@@ -465,6 +465,11 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
     rows = hidx[cand]
     lam = config.lambda_for(which)
     es, em = config.eps_for(which)
+    if not config.exact_ratio:
+        moves = _split_loop_native(book, cand, rows, config, rng, rec, lam, es, em)
+        if moves is not None:
+            _apply_split_batch(state, which, moves)
+            return
     moves = []
     # The sequential accept loop is the host's only per-candidate work; the
     # acceptance arithmetic is inlined with exactly the float expressions of
@@ -499,6 +504,64 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
             moves.append((i, row, new_row, u))
             rec.accepts += 1
     _apply_split_batch(state, which, moves)
+
+
+def _eligible(hidx: np.ndarray, refcount: np.ndarray) -> np.ndarray:
+    """np.flatnonzero(refcount[hidx] >= 2) (sampler.py:344), by the library's
+    threaded host scan."""
+    import os
+    n = len(hidx)
+    out = np.empty(max(n, 1), dtype=np.int32)
+    cnt = nat.I64(0)
+    h = np.ascontiguousarray(hidx, dtype=np.int32)
+    rc = np.ascontiguousarray(refcount, dtype=np.int64)
+    nat.call("cgs_host_split_eligible", h.ctypes.data, n, rc.ctypes.data, len(rc), out.ctypes.data,
+             ctypes.byref(cnt), min(16, os.cpu_count() or 1))
+    return out[: cnt.value]
+
+
+def _split_loop_native(book, cand, rows, config: SamplerConfig, rng, rec: TransitionRecord,
+                       lam: float, es: float, em: float):
+    """The split accept loop (sampler.py:349-364) in the library
+    (cgs_host_split_decide) on the caller's Generator stream; returns the
+    accepted moves, or None (nothing consumed) when the native path is
+    unavailable or its exp-based decisions disagree with numpy's exp (then
+    the Generator and refcounts are restored and the Python loop runs)."""
+    ddot = nat.numpy_ddot_ptr()
+    rc = book.refcount
+    if ddot is None or rc.dtype != np.int64 or not rc.flags.c_contiguous:
+        return None
+    n_cand, dim = len(cand), book.dim
+    rows64 = np.ascontiguousarray(rows, dtype=np.int64)
+    saved_state = rng.bit_generator.state
+    saved_rc = rc[rows64].copy()
+    u = np.empty((n_cand, dim), dtype=np.float64)
+    log_a = np.empty(n_cand, dtype=np.float64)
+    coin = np.empty(n_cand, dtype=np.float64)
+    dec = np.empty(n_cand, dtype=np.int8)
+    att = nat.I64(0)
+    c_q = 1.0 / es ** 2 - 1.0 / em ** 2
+    use_corr = 1 if config.normalization_correction else 0
+    corr = dim * math.log(em / es) if use_corr else 0.0
+    nat.call("cgs_host_split_decide", nat.bitgen_ptr(rng), ddot, n_cand, rows64.ctypes.data,
+             rc.ctypes.data, len(rc), dim, float(lam), float(es), float(c_q), use_corr, float(corr),
+             u.ctypes.data, log_a.ctypes.data, coin.ctypes.data, dec.ctypes.data, ctypes.byref(att))
+    tried = dec >= 0
+    probs = np.exp(np.minimum(0.0, log_a[tried]))  # numpy's exp, as acceptance_probability
+    if not np.array_equal(coin[tried] < probs, dec[tried] == 1):
+        rc[rows64] = saved_rc
+        rng.bit_generator.state = saved_state
+        return None
+    rec.accept_probs.extend(probs.tolist())
+    rec.attempts += int(att.value)
+    moves = []
+    for c in np.flatnonzero(dec == 1).tolist():
+        row = int(rows64[c])
+        new_row = book.alloc_index(parent=row)  # lowest free row (the old row's decref is done)
+        book.mutations += 1
+        moves.append((int(cand[c]), row, new_row, u[c]))
+        rec.accepts += 1
+    return moves
 
 
 def merge_step(state: ModelState, views, config: SamplerConfig, rng, rec: TransitionRecord):

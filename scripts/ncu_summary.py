@@ -87,9 +87,35 @@ def main():
             print(f"  DRAM traffic/launch     {(rd + wr) / 1e6:.2f} MB"
                   + (f"  ({(rd + wr) / dur / 1e9:.1f} GB/s over the launch)" if dur else ""))
             issue = num(d, u, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+
+            def metric(k):
+                v = num(d, u, k)
+                if v is None:
+                    kk = next((x for x in d if x.endswith("." + k)), None)
+                    v = num(d, u, kk) if kk else None
+                return v
+            # FP32 work: FADD + FMUL + 2 FFMA thread-instructions per elapsed cycle
+            # (whole GPU) against 148 SMs x 128 lanes x 2 FLOP per cycle
+            per = [metric(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed")
+                   for op in ("fadd", "fmul", "ffma")]
+            fp32 = (per[0] + per[1] + 2.0 * per[2]) if None not in per else None
+            winst = metric("smsp__inst_executed.sum")
+            tinst = metric("sass__thread_inst_executed_true_per_opcode")
             traffic[short] = {"bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                               "duration_s": dur, "issue_active_pct": issue,
+                              "fma_pipe_pct": metric("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                              "alu_pipe_pct": metric("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                              "xu_pipe_pct": metric("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+                              "fp32_flop_per_cycle": fp32,
+                              "fp32_frac_of_peak": fp32 / 37888.0 if fp32 is not None else None,
+                              "lane_efficiency": tinst / (32.0 * winst) if winst and tinst else None,
+                              "warp_instructions": winst,
                               "source": os.path.basename(a.rep)}
+            t = traffic[short]
+            if fp32 is not None:
+                print(f"  FP32 FLOP/cycle         {fp32:.0f} of 37888 ({100 * t['fp32_frac_of_peak']:.1f}% of peak)")
+            if t["lane_efficiency"]:
+                print(f"  lane efficiency         {100 * t['lane_efficiency']:.1f}% (thread instr / 32 x warp instr)")
     if a.traffic_json:
         json.dump(traffic, open(a.traffic_json, "w"), indent=1, sort_keys=True)
 
