@@ -90,19 +90,16 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
     for (int t = tid; t < total_tiles; t += blockDim.x) zero_a[t] = zero_b[t] = 0u;
 }
 
-// Per-pixel forward state, packed for register pressure (the forward runs
-// at 40 registers): `last` doubles as the done flag (last index + 1 once the
-// pixel terminated; pixels outside the image start done with last = 1) and
-// bit 31 of `cnt` is the float64 re-walk flag (T came within kTBand of 1e-4,
-// or an alpha within kAlphaBand of 1/255 or 0.99: refine.cu).
+// Per-pixel forward state.  `last` doubles as the done flag (last index + 1
+// once the pixel terminated; pixels outside the image start done with
+// last = 1); `refine` flags the pixel for the float64 re-walk (T came within
+// kTBand of 1e-4, or an alpha within kAlphaBand of 1/255 or 0.99: refine.cu).
 struct PixState {
   float T, r, g, b;
   int cnt;
   uint32_t last;
+  bool refine;
   __device__ __forceinline__ bool done() const { return last != 0u; }
-  __device__ __forceinline__ void flag() { cnt |= 0x80000000; }
-  __device__ __forceinline__ bool flagged() const { return cnt < 0; }
-  __device__ __forceinline__ int count() const { return cnt & 0x7fffffff; }
 };
 
 // Front-to-back blend of one splat into one pixel (render.py:274-283, 302-311).
@@ -117,7 +114,7 @@ __device__ __forceinline__ void blend(PixState& p, float al, float cr, float cg,
   ++p.cnt;
   if (p.T < kTBandHi) {  // rare: near or past the termination threshold
 #if !CGS_FWD_NOBAND
-    if (p.T >= kTBandLo) p.flag();  // the float64 chain may fall on either side
+    p.refine |= p.T >= kTBandLo;  // the float64 chain may fall on either side
 #endif
     if (!(p.T >= kTMinF)) p.last = idx + 1;  // every later splat is inactive (T_before < 1e-4)
   }
@@ -196,9 +193,8 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   constexpr int B = kFwdBatch, NT = kFwdThreads;
   const unsigned long long t_start = trace ? global_ns() : 0ull;
   __shared__ __align__(128) SplatRec s_raw[B];
-  __shared__ float4 s_a[B];
-  __shared__ float4 s_b[B];
-  __shared__ float2 s_c[B];
+  // staged splats, one 48-byte entry each (a, b, colour): one address per hit
+  __shared__ float4 s_st[B][3];
   __shared__ uint8_t s_mask[B];
   __shared__ uint8_t s_list[kFwdWarps][B];
   __shared__ uint32_t s_max[kFwdWarps];
@@ -219,20 +215,18 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   const double cx = tile_centre(tx), cy = tile_centre(ty);
   const float flx = static_cast<float>(lx) - kTileHalf, fly = static_cast<float>(ly) - kTileHalf;
   uint8_t* my_list = s_list[warp];
-  PixState p{1.0f, 0.0f, 0.0f, 0.0f, CGS_REFINE_ALL ? static_cast<int>(0x80000000) : 0, in ? 0u : 1u};
+  PixState p{1.0f, 0.0f, 0.0f, 0.0f, 0, in ? 0u : 1u, CGS_REFINE_ALL != 0};
   int n_ckpt = 0;
   // fp32 alpha to blend (render.py:274-279); the caller keeps it when it is
-  // >= kAlphaSkipF.  A pixel that meets a value within the decision bands of
+  // >= kAlphaSkipF.  A pixel that meets a t within a decision band of
   // raster_common.cuh is flagged for the float64 re-walk (refine.cu), which
-  // overwrites it: |t| < band (keep), t near log2(0.99 * 255) (clamp; looked
-  // at only once t reaches the band).
+  // overwrites it.  The keep band (|t| < band) and the clamp band
+  // (|t - kTClamp| < band) are symmetric about kTClamp / 2, so one test
+  // catches both: ||t - kTClamp/2| - kTClamp/2| < band.
   auto eval = [&](const float4& a, const float4& b) -> float {
     const float t = staged_t(a, b, flx, fly);
 #if !CGS_FWD_NOBAND
-    if (fabsf(t) < kTSkipHi) p.flag();
-    if (t >= kTClampLo) {
-      if (t < kTClampHi) p.flag();
-    }
+    p.refine |= fabsf(fabsf(t - kTHalfClamp) - kTHalfClamp) < kTSkipHi;
 #endif
     return alpha_of_t(t);
   };
@@ -251,9 +245,9 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     pending = false;
     if (tid < nb) {
       const Staged sg = stage_splat(s_raw[tid], cx, cy);
-      s_a[tid] = sg.a;
-      s_b[tid] = sg.b;
-      s_c[tid] = sg.c;
+      s_st[tid][0] = sg.a;
+      s_st[tid][1] = sg.b;
+      s_st[tid][2] = make_float4(sg.c.x, sg.c.y, 0.0f, 0.0f);
       s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
     }
     __syncthreads();
@@ -270,37 +264,37 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       int i = 0;
       for (; i + 1 < hits; i += 2) {
         const int j0 = my_list[i], j1 = my_list[i + 1];
-        const float4 a0 = s_a[j0], b0v = s_b[j0];
-        const float4 a1 = s_a[j1], b1v = s_b[j1];
+        const float4 a0 = s_st[j0][0], b0v = s_st[j0][1];
+        const float4 a1 = s_st[j1][0], b1v = s_st[j1][1];
         const float al0 = eval(a0, b0v);
         const float al1 = eval(a1, b1v);
         if (al0 >= kAlphaSkipF) {
-          const float2 c = s_c[j0];
+          const float4 c = s_st[j0][2];
           blend(p, al0, b0v.w, c.x, c.y, static_cast<uint32_t>(b0 + j0));
           if (p.done()) break;
         }
         if (al1 >= kAlphaSkipF) {
-          const float2 c = s_c[j1];
+          const float4 c = s_st[j1][2];
           blend(p, al1, b1v.w, c.x, c.y, static_cast<uint32_t>(b0 + j1));
           if (p.done()) break;
         }
       }
       if (!p.done() && i < hits) {
         const int j = my_list[i];
-        const float4 a = s_a[j], b = s_b[j];
+        const float4 a = s_st[j][0], b = s_st[j][1];
         const float al = eval(a, b);
         if (al >= kAlphaSkipF) {
-          const float2 c = s_c[j];
+          const float4 c = s_st[j][2];
           blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
         }
       }
 #else
       for (int i = 0; i < hits; ++i) {
         const int j = my_list[i];
-        const float4 a = s_a[j], b = s_b[j];
+        const float4 a = s_st[j][0], b = s_st[j][1];
         const float al = eval(a, b);
         if (al >= kAlphaSkipF) {
-          const float2 c = s_c[j];
+          const float4 c = s_st[j][2];
           blend(p, al, b.w, c.x, c.y, static_cast<uint32_t>(b0 + j));
           if (p.done()) break;
         }
@@ -335,11 +329,11 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     image[3 * pix + 1] = p.g;
     image[3 * pix + 2] = p.b;
     final_T[pix] = p.T;
-    counts[pix] = p.count();
+    counts[pix] = p.cnt;
     px_last[pix] = p.last;
   }
   {  // flagged pixels: per-warp masks and the tile in the re-walk list
-    const unsigned bal = __ballot_sync(kFull, in && p.flagged());
+    const unsigned bal = __ballot_sync(kFull, in && p.refine);
     if (__syncthreads_or(bal != 0u)) {
       if (lane == 0) refine_mask[static_cast<int64_t>(tile) * kFwdWarps + warp] = bal;
       if (tid == 0) refine_tiles[atomicAdd(&hdr->scratch[3], 1ull)] = static_cast<uint32_t>(tile);

@@ -346,6 +346,7 @@ constexpr float kTSkipHi = static_cast<float>(kAlphaBand / kLn2);
 constexpr double kTClamp = 7.979853867163743;  // log2(0.99 * 255)
 constexpr float kTClampLo = static_cast<float>(kTClamp - kAlphaBand / kLn2);
 constexpr float kTClampHi = static_cast<float>(kTClamp + kAlphaBand / kLn2);
+constexpr float kTHalfClamp = static_cast<float>(0.5 * kTClamp);  // the bands' symmetry point
 constexpr float kTBandLo = static_cast<float>(1e-4 * (1.0 - kTBand));
 constexpr float kTBandHi = static_cast<float>(1e-4 * (1.0 + kTBand));
 
