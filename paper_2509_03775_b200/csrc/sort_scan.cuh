@@ -461,12 +461,14 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
     CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, key_bits, ws.hist));
     CGS_CHECK_LAUNCH("sort_hist_kernel");
   }
-  static bool attr_set = false;
+  static bool attr_set[kMaxDevices] = {};  // per device ordinal
   const size_t smem = sizeof(SortSmem<K>);
-  if (!attr_set) {
+  int dev = 0;
+  if (int rc = current_device(&dev)) return rc;
+  if (!attr_set[dev]) {
     CGS_CUDA(cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   K* kin = keys;
   uint32_t* vin = vals;

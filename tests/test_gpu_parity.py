@@ -694,3 +694,41 @@ def test_split_eligible_abi_matches_host_rule(cg):
         k = int(cnt.item())
         ref = np.flatnonzero(book.refcount[st.host_index(which)] >= 2)
         assert np.array_equal(out[:k].cpu().numpy(), ref), which
+
+
+def test_config4_batched_strips_match_oracle(cg):
+    """BASELINE config 4 (render only, N=6M, K=65536 both) through a batched
+    frame of two views -- a 1920x32 strip of pose 0 (rows 524-556, the
+    horizon) and one of pose 21 (rows 0-32) -- as bench.py --config 4 renders
+    poses in multi-view frames: per view, tile lists and contribution counts
+    bit-exact against the oracle (render.py:240-254, 287-315), image and T
+    within rtol 1e-4 / atol 1e-6."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import _strip_cam
+    from oracle import cgs_oracle as O
+    from paper_2509_03775_b200 import scenes
+    a = scenes.build(4, 0)
+    ocams = [_strip_cam(O.cam_from_any(a.cameras[0]), 524, 556),
+             _strip_cam(O.cam_from_any(a.cameras[21]), 0, 32)]
+    cams = [cg.Camera(rotation=c.R, translation=c.t, fx=c.fx, fy=c.fy, cx=c.cx, cy=c.cy,
+                      width=c.width, height=c.height) for c in ocams]
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    fr = cg.render_frame(st, cams)
+    offs, ids = fr.tile_lists()
+    ost = O.OState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
+    tile0 = 0
+    for v, oc in enumerate(ocams):
+        fw = O.raster_forward(ost, oc)
+        nt = len(fw["tile_offsets"]) - 1
+        vo = offs[tile0: tile0 + nt + 1]
+        vo = vo - vo[0]
+        vids = ids[offs[tile0]: offs[tile0 + nt]]
+        assert np.array_equal(vo, fw["tile_offsets"]), v
+        assert np.array_equal(vids, fw["tile_ids"]), v
+        tile0 += nt
+        assert np.array_equal(fr.view_counts(v).cpu().numpy(), fw["counts"]), v
+        assert np.allclose(fr.view_image(v).cpu().numpy(), fw["image"], rtol=RTOL, atol=ATOL), v
+        assert np.allclose(fr.view_T(v).cpu().numpy(), fw["final_T"], rtol=RTOL, atol=ATOL), v
