@@ -42,7 +42,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kEpt = 4;                     // records per thread per chunk
+#ifndef CGS_REF_EPT
+#define CGS_REF_EPT 4
+#endif
+constexpr int kEpt = CGS_REF_EPT;           // records per thread per chunk
 constexpr int kRefChunk = kThreads * kEpt;  // 1024
 
 struct Carry {  // one flagged pixel, between chunks
