@@ -237,6 +237,35 @@ def cpu_iteration_timer(config, seed):
     return run, cores, sample, pool
 
 
+def api_train_rate(config, seed, noise_pos, iters=60):
+    """The drop-in API as a user of the reference calls it: cg.train (reference
+    sampler.py:402-420) over (Camera, host numpy image) views with reference
+    semantics -- one randomly chosen view per update, split / merge by the
+    reference mixture, host-drawn (parity-mode) SGLD noise, the TransitionRecord
+    read back every step.  Returns (it/s, description)."""
+    import torch
+    import paper_2509_03775_b200 as cg
+    a, g, cams = make_scene(config, seed, 0, 1)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows, gaussian_headroom=0.25)
+    gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows,
+                                    g.sr_rows)
+    views = [(c, cg.rasterize_forward(gst, c).image.cpu().numpy()) for c in cams]
+    del gst
+    cfg = cg.SamplerConfig(lambda_ssim=0.0 if config == 0 else 0.2, noise_pos=noise_pos)
+    rng = np.random.default_rng(seed)
+    cg.train(st, views, cfg, 5, rng)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    recs = cg.train(st, views, cfg, iters, rng)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    kinds = {k: sum(r.kind == k for r in recs) for k in ("update", "split", "merge")}
+    return iters / secs, (f"cg.train({iters} iterations) on config {config}: reference semantics "
+                          f"(one view per update, {kinds}), host numpy targets uploaded per step, "
+                          f"host-drawn SGLD noise (noise_pos={noise_pos}), TransitionRecord per step")
+
+
 def cpu_one_core(config, seed):
     """The reference algorithm (numpy oracle port) on ONE core: forward, L1/SSIM
     gradient and backward of view 0 in this process with BLAS limited to one
@@ -785,6 +814,14 @@ def main():
                        + ("; BASELINE config-1 run: 100 iterations, MCMC every 25, densify"
                           if args.config == 1 else "")}
 
+    api = None
+    if rank == 0 and world == 1 and not args.no_e2e and args.config in (0, 1):
+        api = {}
+        for c in sorted({args.config, 0}, reverse=True):
+            v, d = api_train_rate(c, args.seed, args.noise_pos)
+            api[f"config{c}"] = {"value": v,
+                                 "unit": "train iters/s (reference semantics: 1 view per update)",
+                                 "description": d}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         run, cores, sample, pool = cpu_iteration_timer(args.config, args.seed)
@@ -815,7 +852,7 @@ def main():
                "mpix_per_s": mpix, "gpu_launches": launches,
                "step_ms": {"min": min(step_ms), "p50": statistics.median(step_ms),
                            "max": max(step_ms)}, "roofline": roofline,
-               "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+               "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "drop_in_train": api,
                "frame": {"pairs": int(stats.n_pairs), "processed_pairs": P_x,
                          "touched": int(stats.n_touched), "onscreen": int(stats.n_onscreen)},
                "recon": tr.recon(), "mcmc_events": tr.mcmc_events,

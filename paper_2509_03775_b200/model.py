@@ -521,6 +521,12 @@ def remap_gaussian(state: ModelState, i: int, which: str, new_row: int) -> None:
     state.touch(assignments=True)
 
 
+def _add_counts(rc: np.ndarray, rows: np.ndarray) -> None:
+    """rc[r] += (occurrences of r in rows), in place (== np.add.at(rc, rows, 1),
+    ~10x faster for the 5% of N clones a densify adds)."""
+    rc += np.bincount(rows, minlength=len(rc))[: len(rc)].astype(rc.dtype, copy=False)
+
+
 def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Generator,
             jitter_sigma: float = 0.02, device_select: bool = False) -> int:
     """Opacity-proportional cloning with shared rows (model.py:235-267).
@@ -558,8 +564,8 @@ def densify(state: ModelState, growth_rate: float, cap: int, rng: np.random.Gene
     nat.call("cgs_densify_append", nat.ptr(g._pos), nat.ptr(g._logit), nat.ptr(g._g2sh),
              nat.ptr(g._g2sr), n, nat.ptr(src_d), nat.ptr(jit_d), k, nat.stream_handle(dev))
     new_sh, new_sr = hsh[src], hsr[src]  # clones share their source's rows (model.py:262-266)
-    np.add.at(state.sh.refcount, new_sh, 1)
-    np.add.at(state.sr.refcount, new_sr, 1)
+    _add_counts(state.sh.refcount, new_sh)
+    _add_counts(state.sr.refcount, new_sr)
     state.sh.mutations += 1
     state.sr.mutations += 1
     state.touch(assignments=True)
@@ -590,7 +596,7 @@ def _densify_device(state: ModelState, n: int, k: int, rng, jitter_sigma: float)
     state.prefetch_host_index()  # includes the clones' rows [n, n + k)
     for which, book in (("sh", state.sh), ("sr", state.sr)):
         book._pending.append(
-            lambda rc, w=which: np.add.at(rc, state.host_index(w)[n:n + k], 1))
+            lambda rc, w=which: _add_counts(rc, state.host_index(w)[n:n + k]))
     return k
 
 
