@@ -420,15 +420,82 @@ def _candidate_count(fraction: float, population: int) -> int:
     return max(1, int(round(fraction * population)))
 
 
-def _exact_log_ratio(state, views, config, rng, mutate):
-    """log p(S')/p(S) from one rendered view by trial-applying the move (sampler.py:309-317)."""
+def _exact_log_ratio(state, views, config, rng, trial):
+    """log p(S')/p(S) from one rendered view by trial-applying the move
+    (sampler.py:309-317).  The reference deep-copies the state per candidate;
+    here the move is applied to the device arrays only, rendered and
+    reverted (``trial`` is a context manager: _split_trial / _merge_trial),
+    and the "before" loss is reused while the state and view are unchanged."""
     from .metrics import recon_loss
     cam, gt = views[int(rng.integers(len(views)))]
-    before = recon_loss(rasterize_forward(state, cam).image, gt, config.lambda_ssim)[2]
-    trial = clone_state(state)
-    mutate(trial)
-    after = recon_loss(rasterize_forward(trial, cam).image, gt, config.lambda_ssim)[2]
+    cache = state.__dict__.setdefault("_exact_before", {})
+    key = (state.token(), cam.key(), id(gt), config.lambda_ssim)
+    before = cache.get(key)
+    if before is None:
+        before = recon_loss(rasterize_forward(state, cam).image, gt, config.lambda_ssim)[2]
+        cache.clear()
+        cache[key] = before
+    with trial:
+        after = recon_loss(rasterize_forward(state, cam).image, gt, config.lambda_ssim)[2]
+    # the reverted state renders as before (only its version counters moved)
+    cache.clear()
+    cache[(state.token(), cam.key(), id(gt), config.lambda_ssim)] = before
     return before - after
+
+
+class _split_trial:
+    """Gaussian i on a new row of value f32(f64(row) + u) (apply_split,
+    sampler.py:202-209) for one render: the value goes to the spare row past
+    the codebook's capacity, g2sh/g2sr[i] points at it; all reverted on exit
+    (no host bookkeeping is touched)."""
+
+    def __init__(self, state, which, i, row, u):
+        self.state, self.which, self.i, self.row = state, which, int(i), int(row)
+        self.u = np.asarray(u, np.float64)
+
+    def __enter__(self):
+        from .model import _grow
+        book, idx = _book_of(self.state, self.which)
+        r = book.capacity
+        book._buf = _grow(book._buf, r + 1)
+        uu = torch.as_tensor(self.u, dtype=torch.float64, device=book.device)
+        book._buf[r] = (book._buf[self.row].double() + uu).float()
+        self.old = idx[self.i].clone()
+        idx[self.i] = r
+        book._cap += 1  # the render sees the spare row (rows / capacity)
+        self.state.touch(assignments=True)
+        book.mutations += 1
+        return self
+
+    def __exit__(self, *exc):
+        book, idx = _book_of(self.state, self.which)
+        idx[self.i] = self.old
+        book._cap -= 1
+        self.state.touch(assignments=True)
+        book.mutations += 1
+        return False
+
+
+class _merge_trial:
+    """Every Gaussian on `child` on `parent` instead (apply_merge,
+    sampler.py:240-247) for one render; reverted on exit."""
+
+    def __init__(self, state, which, child, parent):
+        self.state, self.which = state, which
+        self.child, self.parent = int(child), int(parent)
+
+    def __enter__(self):
+        _, idx = _book_of(self.state, self.which)
+        self.members = idx == self.child
+        idx.masked_fill_(self.members, self.parent)
+        self.state.touch(assignments=True)
+        return self
+
+    def __exit__(self, *exc):
+        _, idx = _book_of(self.state, self.which)
+        idx.masked_fill_(self.members, self.child)
+        self.state.touch(assignments=True)
+        return False
 
 
 def clone_state(state: ModelState) -> ModelState:
@@ -489,8 +556,7 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
             # flush pending applies so the trial render sees the current state
             _apply_split_batch(state, which, moves)
             moves = []
-            prop = SplitProposal(which, i, row, u, book.row(row).astype(np.float64) + u)
-            extra = _exact_log_ratio(state, views, config, rng, lambda s: apply_split(s, prop))
+            extra = _exact_log_ratio(state, views, config, rng, _split_trial(state, which, i, row, u))
         log_q = -0.5 * float(u @ u) * c_q
         if corr is not None:
             log_q += corr
@@ -583,7 +649,8 @@ def merge_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
         if config.exact_ratio:
             _apply_remap(state, which, remap)
             remap = {}
-            extra = _exact_log_ratio(state, views, config, rng, lambda s: apply_merge(s, prop))
+            extra = _exact_log_ratio(state, views, config, rng,
+                                     _merge_trial(state, which, prop.child, prop.parent))
         prob = acceptance_probability("merge", prop.u, lam, es, em, config.normalization_correction,
                                       extra)
         rec.accept_probs.append(prob)
