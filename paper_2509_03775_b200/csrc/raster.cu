@@ -28,6 +28,12 @@
 
 namespace cgs {
 
+#ifndef CGS_BWD_EIGEN_CULL
+#define CGS_BWD_EIGEN_CULL 1
+#endif
+#ifndef CGS_FWD_EIGEN_CULL
+#define CGS_FWD_EIGEN_CULL 0
+#endif
 #ifndef CGS_FWD_NOBAND  // timing experiments only: no flagging (not exact)
 #define CGS_FWD_NOBAND 0
 #endif
@@ -248,7 +254,16 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       s_st[tid][0] = sg.a;
       s_st[tid][1] = sg.b;
       s_st[tid][2] = make_float4(sg.c.x, sg.c.y, 0.0f, 0.0f);
-      s_mask[tid] = static_cast<uint8_t>(block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile)));
+      uint32_t m8 = block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile));
+#if CGS_FWD_EIGEN_CULL
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {  // 8x4 blocks the ellipse cannot reach
+        const float x0 = (w & 1) * 8 - kTileHalf, y0 = (w >> 1) * 4 - kTileHalf;
+        if ((m8 >> w) & 1u)
+          if (!staged_may_hit(sg.a, sg.b, x0, x0 + 7.0f, y0, y0 + 3.0f)) m8 &= ~(1u << w);
+      }
+#endif
+      s_mask[tid] = static_cast<uint8_t>(m8);
     }
     __syncthreads();
     if (b0 + B < n) {
@@ -653,6 +668,14 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
           s_eidx[buf][k] = static_cast<uint32_t>(
               emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
           uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
+#if CGS_BWD_EIGEN_CULL
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {  // quadrants the ellipse cannot reach
+            const float x0 = (w & 1) * 8 - kTileHalf, y0 = (w >> 1) * 8 - kTileHalf;
+            if ((m >> w) & 1u)
+              if (!staged_may_hit(sg.a, sg.b, x0, x0 + 7.0f, y0, y0 + 7.0f)) m &= ~(1u << w);
+          }
+#endif
 #pragma unroll
           for (int w = 0; w < 4; ++w)
             if (!(static_cast<uint32_t>(b0 + k) < s_wlast[w])) m &= ~(1u << w);

@@ -350,6 +350,27 @@ constexpr float kTHalfClamp = static_cast<float>(0.5 * kTClamp);  // the bands' 
 constexpr float kTBandLo = static_cast<float>(1e-4 * (1.0 - kTBand));
 constexpr float kTBandHi = static_cast<float>(1e-4 * (1.0 + kTBand));
 
+// Whether any pixel centre of the tile-centred rectangle [x0, x1] x [y0, y1]
+// can have t >= -margin: an upper bound of t over the rectangle from its
+// projections onto the eigen axes (the rectangle lies inside the (u, v) box
+// of those projections, and t decreases with |u| and |v|).  Exact for
+// rectangles aligned with the eigen axes, conservative otherwise; it cuts
+// the blocks that the axis-aligned contribution box keeps for a rotated,
+// elongated ellipse.
+__device__ __forceinline__ bool staged_may_hit(const float4& a, const float4& b, float x0, float x1,
+                                               float y0, float y1) {
+  const float ex = a.z, ey = a.w;
+  const float ulo = a.x + fminf(ex * x0, ex * x1) + fminf(ey * y0, ey * y1);
+  const float uhi = a.x + fmaxf(ex * x0, ex * x1) + fmaxf(ey * y0, ey * y1);
+  const float vlo = a.y + fminf(-ey * x0, -ey * x1) + fminf(ex * y0, ex * y1);
+  const float vhi = a.y + fmaxf(-ey * x0, -ey * x1) + fmaxf(ex * y0, ex * y1);
+  const float du = fmaxf(0.0f, fmaxf(ulo, -uhi));
+  const float dv = fmaxf(0.0f, fmaxf(vlo, -vhi));
+  // t <= log2(255 o) + k1 du^2 + k2 dv^2 (k1, k2 <= 0); margin 1e-3 (log2
+  // units) >> the fp32 error of t, and below the keep band's lower edge
+  return fmaf(b.x * du, du, fmaf(b.y * dv, dv, b.z)) >= kTSkipLo - 1e-3f;
+}
+
 // Reference float64 alpha of splat record r at pixel (px, py) of its view
 // (render.py:261, 274-280): d = centre - mean, power = -1/2 (A dx^2 + C dy^2)
 // - B dx dy, alpha = min(o exp(power), 0.99) with o = sigmoid(logit) in f64
