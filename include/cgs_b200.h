@@ -119,6 +119,10 @@ typedef struct cgs_sgld_params {
                             nothing and sets flags[0] |= 2                   */
   int32_t* sticky;       /* optional device accumulator: sticky |= flags[0]
                             (so a run can be checked once, at its end)       */
+  const int32_t* grads_nonfinite; /* optional device flag that already covers
+                            every gradient entry (cgs_backward_nonfinite_flag
+                            of the backward that wrote them): replaces the
+                            update's own finiteness pass                    */
 } cgs_sgld_params_t;
 
 /* ---- library --------------------------------------------------------- */
@@ -274,6 +278,11 @@ CGS_API int cgs_recon_loss(const float* image, const float* gt, int32_t n_views,
                    int32_t width, double lambda_ssim, int32_t want_ssim, float grad_scale,
                    float* dL_dimage, double* losses, void* workspace, size_t workspace_bytes,
                    cgs_stream_t stream);
+
+/* Device address of the backward workspace's non-finite flag: nonzero when
+ * any gradient entry cgs_render_backward (or the staged backward) wrote was
+ * non-finite.  Pure address arithmetic on the workspace pointer. */
+CGS_API const int32_t* cgs_backward_nonfinite_flag(const void* backward_workspace);
 
 /* ---- SGLD update (sampler.py:262-300) --------------------------------- */
 /* Checks every gradient for finiteness first; if any is non-finite nothing

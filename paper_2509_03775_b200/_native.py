@@ -69,6 +69,7 @@ class CSgldParams(ctypes.Structure):
         ("offset_dev", ctypes.c_void_p),
         ("skip_if", ctypes.c_void_p),
         ("sticky", ctypes.c_void_p),
+        ("grads_nonfinite", ctypes.c_void_p),
     ]
 
 
@@ -115,6 +116,7 @@ SIGNATURES = {
                               ctypes.POINTER(CSgldParams), P, P, P, P, P, P]),
     "cgs_split_eligible": (I32, [P, I64, P, P, P, P, SZ, P]),
     "cgs_host_split_eligible": (I32, [P, I64, P, I64, P, P, I32]),
+    "cgs_backward_nonfinite_flag": (P, [P]),
     "cgs_host_split_decide": (I32, [P, P, I64, P, P, I64, I32, F64, F64, F64, I32, F64, P, P, P, P,
                                     P]),
     "cgs_apply_splits": (I32, [P, I32, P, P, P, P, P, I64, P]),

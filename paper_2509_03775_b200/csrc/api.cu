@@ -302,6 +302,13 @@ int cgs_raster_fwd(const cgs_scene_t* scene, const cgs_camera_t* cams, int32_t n
   return frame_stage_raster(fd, L, scene->opacity_logits, image, final_T, contrib_counts, st);
 }
 
+const int32_t* cgs_backward_nonfinite_flag(const void* backward_workspace) {
+  // BwdHeader.nonfinite (render_bwd.cu) sits at byte 16 of the workspace
+  return backward_workspace
+             ? reinterpret_cast<const int32_t*>(static_cast<const char*>(backward_workspace) + 16)
+             : nullptr;
+}
+
 int cgs_frame_stats(const void* workspace, cgs_frame_stats_t* out, cgs_stream_t stream) {
   if (!workspace || !out) {
     set_error("null argument");

@@ -15,6 +15,7 @@
 //                   d_raw, SR rows = sum dSigma3 then the per-row chain
 //                   (render.py:431-458).  No atomics, no per-step sorts.
 #include <cmath>
+#include <cstddef>
 
 #include "frame.cuh"
 #include "raster_common.cuh"
@@ -24,8 +25,11 @@ namespace cgs {
 struct BwdHeader {
   unsigned long long n_processed;
   unsigned long long n_touched;
-  unsigned long long scratch[6];
+  int nonfinite;  // byte 16: a written gradient entry was non-finite (cgs_backward_nonfinite_flag)
+  int pad;
+  unsigned long long scratch[5];
 };
+static_assert(offsetof(BwdHeader, nonfinite) == 16, "ABI: cgs_backward_nonfinite_flag");
 
 struct BwdLayout {
   BwdHeader* hdr;
@@ -425,6 +429,7 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
 __global__ void __launch_bounds__(256) gauss_write_kernel(BwdLayout B, int64_t n, int n_views,
                                                           float scale, float* __restrict__ gpos,
                                                           float* __restrict__ glogit) {
+  bool bad = false;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
@@ -435,11 +440,17 @@ __global__ void __launch_bounds__(256) gauss_write_kernel(BwdLayout B, int64_t n
         s0 += e.x; s1 += e.y; s2 += e.z; s3 += e.w;
       }
     }
-    gpos[3 * i + 0] = static_cast<float>(s0 * scale);
-    gpos[3 * i + 1] = static_cast<float>(s1 * scale);
-    gpos[3 * i + 2] = static_cast<float>(s2 * scale);
-    glogit[i] = static_cast<float>(s3 * scale);
+    const float g0 = static_cast<float>(s0 * scale), g1 = static_cast<float>(s1 * scale),
+                g2 = static_cast<float>(s2 * scale), g3 = static_cast<float>(s3 * scale);
+    gpos[3 * i + 0] = g0;
+    gpos[3 * i + 1] = g1;
+    gpos[3 * i + 2] = g2;
+    glogit[i] = g3;
+    bad |= !isfinite(g0) || !isfinite(g1) || !isfinite(g2) || !isfinite(g3);
   }
+  // the SGLD update's finiteness check (sampler.py:270-271), done here on
+  // the values as they are written instead of by a second pass
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&B.hdr->nonfinite, 1);
 }
 
 // SH row gradient = sum over members of basis(view) (x) d_raw (render.py:421,
@@ -456,6 +467,7 @@ __global__ void __launch_bounds__(128) sh_code_reduce_kernel(
   __shared__ float s_part[4][32][D + 1];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  bool bad = false;
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < cap;
        r += warps) {
     const int m0 = off[r], m1 = off[r + 1];
@@ -491,9 +503,11 @@ __global__ void __launch_bounds__(128) sh_code_reduce_kernel(
 #pragma unroll 8
       for (int l = 0; l < 32; ++l) sum += s_part[wl][l][c];
       out[c] = sum * scale;
+      bad |= !isfinite(sum * scale);
     }
     __syncwarp();
   }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(&B.hdr->nonfinite, 1);
 }
 
 // SR row gradient: sum dSigma3 over members, then the per-row chain through
@@ -565,8 +579,16 @@ __global__ void __launch_bounds__(256) sr_code_reduce_kernel(
     // through normalisation (render.py:441-444)
     const double qd = w_ * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
     const double qv[4] = {w_, x, y, z};
-    for (int k = 0; k < 3; ++k) out[k] = static_cast<float>(dls[k] * scale);
-    for (int k = 0; k < 4; ++k) out[3 + k] = static_cast<float>((dq[k] - qv[k] * qd) / qn * scale);
+    bool bad = false;
+    for (int k = 0; k < 3; ++k) {
+      out[k] = static_cast<float>(dls[k] * scale);
+      bad |= !isfinite(out[k]);
+    }
+    for (int k = 0; k < 4; ++k) {
+      out[3 + k] = static_cast<float>((dq[k] - qv[k] * qd) / qn * scale);
+      bad |= !isfinite(out[3 + k]);
+    }
+    if (bad) atomicOr(&B.hdr->nonfinite, 1);
   }
 }
 

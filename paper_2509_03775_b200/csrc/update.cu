@@ -101,6 +101,14 @@ __global__ void __launch_bounds__(256) finite_check_kernel(const float* __restri
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 1);
 }
 
+// flags for an update whose gradients were checked by their producers
+// (cgs_sgld_params_t.grads_nonfinite): one thread, no pass over the data
+__global__ void sgld_prologue_kernel(int32_t* flags, uint64_t* ctr, const int32_t* skip_if,
+                                     const int32_t* nonfinite) {
+  if (ctr) *ctr += 1;  // noise offset for this update
+  flags[0] = ((skip_if && *skip_if) ? 2 : 0) | (*nonfinite ? 1 : 0);
+}
+
 __global__ void sticky_or_kernel(int32_t* sticky, const int32_t* flags) {
   if (flags[0]) atomicOr(sticky, flags[0]);
 }
@@ -197,12 +205,17 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
                 int64_t sr_cap, const cgs_sgld_params_t* hp, const double* npos,
                 const double* nlog, const double* nsh, const double* nsr, int32_t* flags,
                 cudaStream_t st) {
-  CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
-  const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
-  CGS_PROFILED("finite_check_kernel", st, finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
-                                                                          nc, gsr, nd, flags, hp->offset_dev,
-                                                                          hp->skip_if));
-  CGS_CHECK_LAUNCH("finite_check_kernel");
+  if (hp->grads_nonfinite) {  // the producers of the gradients checked them
+    sgld_prologue_kernel<<<1, 1, 0, st>>>(flags, hp->offset_dev, hp->skip_if, hp->grads_nonfinite);
+    CGS_CHECK_LAUNCH("sgld_prologue_kernel");
+  } else {
+    CGS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    const int64_t na = 3 * n, nb = n, nc = sh_cap * D, nd = sr_cap * 7;
+    CGS_PROFILED("finite_check_kernel", st, finite_check_kernel<<<grid_for(na + nb + nc + nd, 256, 8), 256, 0, st>>>(gpos, na, glogit, nb, gsh,
+                                                                            nc, gsr, nd, flags, hp->offset_dev,
+                                                                            hp->skip_if));
+    CGS_CHECK_LAUNCH("finite_check_kernel");
+  }
   SgldDev p{};
   // exactly numpy's scalar sub-expressions: 0.5 * eps and mult * sqrt(eps)
   p.c_pos = 0.5 * hp->step_pos;

@@ -162,14 +162,19 @@ class Trainer:
         # cgs_frame_stats_t.overflow (byte 40 of the frame workspace): an
         # overflowing frame skips the update; flags latch into self.sticky
         ov = self.frame.ws[40:44].view(torch.int32)
+        # one rank: the backward's own non-finite flag covers the gradients
+        # (cgs_backward_nonfinite_flag, byte 16); after an allreduce a rank's
+        # flag does not see the other ranks' values, so the update checks
+        nf = self.bws[16:20].view(torch.int32) if self.allreduce is None else None
         sgld_update(self.state, self.grads, self.config, self.rng, flags=self.flags, check=False,
-                    offset_dev=self.noise_ctr, skip_if=ov, sticky=self.sticky)
+                    offset_dev=self.noise_ctr, skip_if=ov, sticky=self.sticky,
+                    grads_nonfinite=nf)
 
     def _graph_key(self):
         st = self.state
         g = st.gaussians
         sl, rl = st.sh.device_live(), st.sr.device_live()
-        return (id(self.frame), id(self.grads), g.positions.data_ptr(), g.count,
+        return (id(self.frame), id(self.grads), self.bws.data_ptr(), g.positions.data_ptr(), g.count,
                 g.g2sh.data_ptr(), g.g2sr.data_ptr(), st.sh.rows.data_ptr(), st.sr.rows.data_ptr(),
                 st.sh.capacity, st.sr.capacity, sl.data_ptr(), sl.numel(), rl.data_ptr(), rl.numel())
 

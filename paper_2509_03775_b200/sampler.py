@@ -358,17 +358,19 @@ def _host_noise(state: ModelState, config: SamplerConfig, rng, n_sh_live, n_sr_l
 def sgld_update(state: ModelState, grads: GradientSet, config: SamplerConfig,
                 rng: np.random.Generator, flags: torch.Tensor = None, check: bool = True,
                 offset_dev: torch.Tensor = None, skip_if: torch.Tensor = None,
-                sticky: torch.Tensor = None) -> None:
+                sticky: torch.Tensor = None, grads_nonfinite: torch.Tensor = None) -> None:
     """SGLD step per group (sampler.py:262-300) on the device.
 
     ``offset_dev`` (int64 device counter) makes device-noise draws advance on
     the device, so a captured CUDA graph of the update draws fresh noise on
     every replay.  ``skip_if`` (device int32, e.g. the frame's overflow flag)
     makes the update write nothing when set; ``sticky`` (device int32)
-    accumulates the flags (1 non-finite, 2 skipped) for a check at the end."""
+    accumulates the flags (1 non-finite, 2 skipped) for a check at the end;
+    ``grads_nonfinite`` (the backward's flag, render.Frame.backward) replaces
+    the update's own finiteness pass over the gradients."""
     noise = _draw_noise(state, config, rng)
     _sgld_launch(state, grads, config, noise, flags if flags is not None else None, offset_dev,
-                 skip_if, sticky, check)
+                 skip_if, sticky, check, grads_nonfinite)
 
 
 def _draw_noise(state: ModelState, config: SamplerConfig, rng) -> list:
@@ -381,7 +383,8 @@ def _draw_noise(state: ModelState, config: SamplerConfig, rng) -> list:
 
 
 def _sgld_launch(state: ModelState, grads: GradientSet, config: SamplerConfig, noise: list,
-                 flags, offset_dev, skip_if, sticky, check: bool) -> None:
+                 flags, offset_dev, skip_if, sticky, check: bool,
+                 grads_nonfinite=None) -> None:
     dev = state.device
     g = state.gaussians
     sh_live = state.sh.device_live()
@@ -393,6 +396,7 @@ def _sgld_launch(state: ModelState, grads: GradientSet, config: SamplerConfig, n
         params = _sgld_params(config, 1.0, 0, 0, 1)
     params.skip_if = nat.ptr(skip_if)
     params.sticky = nat.ptr(sticky)
+    params.grads_nonfinite = nat.ptr(grads_nonfinite)
     if flags is None:
         flags = torch.zeros((1,), dtype=torch.int32, device=dev)
     nat.call("cgs_sgld_update", nat.ptr(g.positions), nat.ptr(g.opacity_logits), g.count,
@@ -769,7 +773,8 @@ def update_step(state: ModelState, cams, gts, config: SamplerConfig, rng, check:
         losses = eng.loss.run(fr.image, gt_d, config.lambda_ssim, eng.dL, 1.0)
         fr.backward(eng.dL, scale=1.0 / v, grads=eng.grads, ws=eng.bws)
         ov = fr.ws[40:44].view(torch.int32)  # cgs_frame_stats_t.overflow
-        _sgld_launch(state, eng.grads, config, noise, eng.flags, None, ov, None, False)
+        _sgld_launch(state, eng.grads, config, noise, eng.flags, None, ov, None, False,
+                     eng.bws[16:20].view(torch.int32))  # the backward's non-finite flag
         eng.host[0].copy_(losses.view(v, 3)[:, 2].mean(), non_blocking=True)
         eng.host[1].copy_(eng.flags[0], non_blocking=True)
         torch.cuda.current_stream(state.device).synchronize()

@@ -160,3 +160,36 @@ def test_two_rank_step_equals_one_rank_batch():
         assert np.allclose(a, b, rtol=1e-6, atol=1e-7), (k, np.abs(a - b).max())
     for k in ("g2sh", "g2sr", "sh_refcount", "sr_refcount"):
         assert np.array_equal(two[k], one[k]), k
+
+
+def test_trainer_rejects_nonfinite_gradients_without_a_pass():
+    """The one-rank trainer takes the gradients' finiteness from the backward's
+    own flag (cgs_backward_nonfinite_flag) instead of a second pass: a NaN in
+    a target still rejects the update (no state change) and check() raises
+    SamplerError (sampler.py:270-271)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2509_03775_b200 as cg
+    from paper_2509_03775_b200 import scenes
+    from paper_2509_03775_b200.engine import Trainer
+    a, g = scenes.config0(0), scenes.config0(1)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    gst = cg.ModelState.from_arrays(g.positions, g.opacity_logits, g.g2sh, g.g2sr, g.sh_rows,
+                                    g.sr_rows)
+    cams = a.cameras
+    H, W = cams[0].height, cams[0].width
+    gts = cg.render_frame(gst, cams).image.view(len(cams), H, W, 3).clone()
+    cfg = cg.SamplerConfig(device_noise=True, noise_pos=0.01)
+    tr = Trainer(st, cams, gts, cfg, np.random.default_rng(0), mcmc_every=0, use_graphs=True)
+    for _ in range(3):
+        tr.step()
+    torch.cuda.synchronize()
+    tr.check()
+    before = st.gaussians.positions.clone()
+    gts[0, H // 2, W // 2, 0] = float("nan")
+    tr.step()
+    torch.cuda.synchronize()
+    assert torch.equal(before, st.gaussians.positions)
+    with pytest.raises(cg.SamplerError):
+        tr.check()
