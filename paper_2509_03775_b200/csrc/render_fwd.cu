@@ -68,8 +68,8 @@ struct ProjIn {
 struct ProjOut {
   SplatRec* recs;
   uint64_t* depth_key;
-  uint32_t* dkey;  // 32-bit depth sort key (~0 for splats without tiles)
-  uint32_t* dval;  // splat id (sort payload)
+  uint32_t* dkey;  // 32-bit depth sort keys of the splats with tiles, compacted
+  uint32_t* dval;  // their splat ids (sort payload)
   uint32_t* hist;  // 4 x 256 digit histogram of dkey (depth sort)
   uint32_t* n_tiles;
   uint64_t* rect;
@@ -90,8 +90,6 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
   const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
   const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
-  out.dval[s] = static_cast<uint32_t>(s);
-  out.dkey[s] = 0xffffffffu;
   if (!(tz > kNear)) {  // near-plane cull, render.py:149
     out.n_tiles[s] = 0;
     return 0xffffffffu;
@@ -205,7 +203,6 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   out.recs[s] = rec;
   out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
   const uint32_t key = __float_as_uint(__double2float_rz(tz));  // tz > 0: monotone bits
-  out.dkey[s] = key;
   out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
   out.rect[s] = static_cast<uint64_t>(tx0) | (static_cast<uint64_t>(tx1) << 16) |
                 (static_cast<uint64_t>(ty0) << 32) | (static_cast<uint64_t>(ty1) << 48);
@@ -224,10 +221,12 @@ template <int DEG>
 #endif
 __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
   __shared__ uint32_t s_h[4 * 256];
+  __shared__ uint32_t s_wc[8];
+  __shared__ unsigned long long s_base;
   for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) s_h[k] = 0;
   __syncthreads();
   const int64_t vn = in.n * fd.n_views;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x); b < vn;
        b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = b + threadIdx.x;
@@ -240,26 +239,44 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
 #else
     const int64_t s = t;
 #endif
-    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0u;
-    const unsigned valid = __ballot_sync(kFull, ok);
+    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0xffffffffu;
+    // the depth sort takes only the splats with tiles: (key, splat id)
+    // appended in any order (its ties are ordered by (fp64 depth, id)
+    // afterwards, depth_tie_fix_kernel), one global atomic per CTA iteration
+    const bool on = key != 0xffffffffu;
+    const unsigned bal = __ballot_sync(kFull, on);
+    if (lane == 0) s_wc[warp] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < 8; ++w) tot += s_wc[w];
+      s_base = tot ? atomicAdd(&out.hdr->n_onscreen, static_cast<unsigned long long>(tot)) : 0ull;
+    }
+    __syncthreads();
+    if (on) {
+      uint32_t pos = __popc(bal & lanemask_lt());
+      for (int w = 0; w < warp; ++w) pos += s_wc[w];
+      out.dkey[s_base + pos] = key;
+      out.dval[s_base + pos] = static_cast<uint32_t>(s);
+    }
 #if CGS_PROJECT_HIST_DIRECT
     // low three bytes of a depth key are spread over the digits: one shared
     // atomic per lane is cheaper than eight ballots; the top byte (sign and
     // high exponent bits) takes few values, so it is warp-aggregated
 #pragma unroll
     for (int p = 0; p < 3; ++p)
-      if (ok) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
+      if (on) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
     {
       const unsigned d = key >> 24;
-      const unsigned peers = warp_peers8(d) & valid;
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[3 * 256 + d], __popc(peers));
+      const unsigned peers = warp_peers8(d) & bal;
+      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_h[3 * 256 + d], __popc(peers));
     }
 #else
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       const unsigned d = (key >> (8 * p)) & 255u;
-      const unsigned peers = warp_peers8(d) & valid;
-      if (ok && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
+      const unsigned peers = warp_peers8(d) & bal;
+      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
     }
 #endif
   }
@@ -269,27 +286,32 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
 }
 
 // ---------------------------------------------------------------------------
-// Exact order inside runs of equal 32-bit depth keys: a stable insertion sort
-// of the run by the fp64 depth bits (positive doubles order as integers), so
-// ties of the fp64 depth keep splat index order.  Runs are short (a handful
-// of splats even at 4M Gaussians).  Splats without tiles (key ~0) are last
-// and untouched.
+// Exact order inside runs of equal 32-bit depth keys: an insertion sort of
+// the run by (fp64 depth bits, splat id) -- positive doubles order as
+// integers, and within one view the splat id orders as the Gaussian index --
+// so the order is the reference's lexsort((idx, tz)) (render.py:203) whatever
+// order the keys were appended in.  Runs are short (a handful of splats even
+// at 4M Gaussians).
 __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __restrict__ key,
                                                             uint32_t* __restrict__ val,
                                                             const uint64_t* __restrict__ depth_key,
-                                                            int64_t vn) {
+                                                            const unsigned long long* __restrict__ n_dev) {
+  const int64_t vn = static_cast<int64_t>(*n_dev);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i + 1 < vn;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = key[i];
-    if (k == 0xffffffffu || key[i + 1] != k || (i > 0 && key[i - 1] == k)) continue;
+    if (key[i + 1] != k || (i > 0 && key[i - 1] == k)) continue;
     int64_t e = i + 1;
     while (e < vn && key[e] == k) ++e;
     for (int64_t a = i + 1; a < e; ++a) {
       const uint32_t va = val[a];
       const uint64_t ka = depth_key[va];
       int64_t b = a - 1;
-      while (b >= i && depth_key[val[b]] > ka) {
-        val[b + 1] = val[b];
+      while (b >= i) {
+        const uint32_t vb = val[b];
+        const uint64_t kb = depth_key[vb];
+        if (kb < ka || (kb == ka && vb < va)) break;
+        val[b + 1] = vb;
         --b;
       }
       val[b + 1] = va;
@@ -314,10 +336,8 @@ struct PairOffsets {
 
 // hist_top: the depth sort's histogram of the key's top byte; splats without
 // tiles carry key ~0, so their count is hist_top[255].
-__global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views,
-                                       const uint32_t* hist_top, int64_t vn) {
+__global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views) {
   const unsigned long long raw = hdr->scratch[0];
-  hdr->n_onscreen = static_cast<unsigned long long>(vn) - (hist_top ? hist_top[255] : 0u);
   hdr->n_pairs_raw = raw;
   const bool over = raw > static_cast<unsigned long long>(pair_cap);
   hdr->n_pairs = over ? 0ULL : raw;
@@ -622,8 +642,9 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
   uint32_t* perm = L.dval;
   if (vn > 0) {
     uint32_t* kres;
-    int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, nullptr, vn, vn, 32, L.dsort, &kres, &perm,
-                                         st, /*hist_ready=*/true);
+    // the projection appended the splats with tiles (count: hdr->n_onscreen)
+    int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, &L.hdr->n_onscreen, vn, vn, 32, L.dsort,
+                                         &kres, &perm, st, /*hist_ready=*/true);
     if (rc) return rc;
     if (perm != L.dval) {
       set_error("depth sort: unexpected result buffer");
@@ -631,14 +652,14 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     }
     CGS_PROFILED("depth_tie_fix_kernel", st,
                  depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(kres, perm,
-                                                                           L.depth_key, vn));
+                                                                           L.depth_key,
+                                                                           &L.hdr->n_onscreen));
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
   }
-  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.rank_of}, nullptr, vn, vn, L.scan,
-                       &L.hdr->scratch[0], st);
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.rank_of}, &L.hdr->n_onscreen, vn,
+                       vn, L.scan, &L.hdr->scratch[0], st);
   if (rc) return rc;
-  finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views,
-                                          vn > 0 ? L.dsort.hist + 3 * 256 : nullptr, vn);
+  finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
   CGS_CHECK_LAUNCH("finalize_counts_kernel");
   return CGS_OK;
 }
