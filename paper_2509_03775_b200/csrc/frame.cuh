@@ -52,8 +52,11 @@ struct FrameLayout {
   uint32_t* pvals;         // pair_cap splat ids
   SortWs<uint16_t> psort16;
   SortWs<uint32_t> psort32;
-  uint32_t* rank_of;       // V*N: depth rank of each splat with tiles
-  uint32_t* last_rank;     // total_tiles: 1 + depth rank of the tile's last processed splat (0: none)
+  // total_tiles: (fp64 depth bits, splat id) of the tile's last processed
+  // splat -- the depth order's key, so splat s is in the tile's processed
+  // prefix iff (depth_key[s], s) <= it; (0, 0): none processed
+  uint64_t* tile_last_dk;
+  uint32_t* tile_last_sid;
   uint32_t* long_list;     // V*N: splats with more than kLongSplat pairs (count: hdr->scratch[2])
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
@@ -139,12 +142,12 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
     L.psort32 = carve_sort<uint32_t>(c, pc);
   }
   L.pvals = c.take<uint32_t>(pc);
-  L.rank_of = c.take<uint32_t>(vn1);
   L.long_list = c.take<uint32_t>(vn1);
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
-  L.last_rank = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.tile_last_dk = c.take<uint64_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.tile_last_sid = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.tile_order = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.n_ckpt = fd.total_tiles + pc / kChunk + 2;
   L.ckpt = c.take<float4>(L.n_ckpt * 256);

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
                                                           int total_tiles,
                                                           uint32_t* __restrict__ order,
                                                           uint32_t* __restrict__ zero_a,
-                                                          uint32_t* __restrict__ zero_b) {
+                                                          uint64_t* __restrict__ zero_b) {
   __shared__ uint32_t cnt[256];
   const int tid = threadIdx.x;
   auto bucket = [&](int t) -> uint32_t {
@@ -93,7 +93,10 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
   __syncthreads();
   for (int t = tid; t < total_tiles; t += blockDim.x) order[atomicAdd(&cnt[bucket(t)], 1u)] = t;
   if (zero_a)  // the forward's per-tile maxima start from 0 (split tiles combine with atomicMax)
-    for (int t = tid; t < total_tiles; t += blockDim.x) zero_a[t] = zero_b[t] = 0u;
+    for (int t = tid; t < total_tiles; t += blockDim.x) {
+      zero_a[t] = 0u;
+      zero_b[t] = 0ull;
+    }
 }
 
 // Per-pixel forward state.  `last` doubles as the done flag (last index + 1
@@ -192,8 +195,9 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
     FrameHeader* __restrict__ hdr, float* __restrict__ image,
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
-    uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
-    uint32_t* __restrict__ last_rank, float4* __restrict__ ckpt,
+    uint32_t* __restrict__ tile_nproc, const uint64_t* __restrict__ depth_key,
+    uint64_t* __restrict__ tile_last_dk, uint32_t* __restrict__ tile_last_sid,
+    float4* __restrict__ ckpt,
     uint32_t* __restrict__ refine_tiles, uint32_t* __restrict__ refine_mask,
     unsigned long long* __restrict__ trace) {
   constexpr int B = kFwdBatch, NT = kFwdThreads;
@@ -363,9 +367,10 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     uint32_t np = 0;
 #pragma unroll
     for (int w = 0; w < kFwdWarps; ++w) np = max(np, s_max[w]);
-    const uint32_t lr = np ? rank_of[pair_vals[rg.x + np - 1]] + 1 : 0u;  // ranks grow along the list
+    const uint32_t ls = np ? pair_vals[rg.x + np - 1] : 0u;
     tile_nproc[tile] = np;
-    last_rank[tile] = lr;
+    tile_last_dk[tile] = np ? depth_key[ls] : 0ull;
+    tile_last_sid[tile] = ls;
     if (trace) {
       unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x);
       t[0] = t_start;
@@ -741,7 +746,7 @@ int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       cudaStream_t st) {
   tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nproc, fd.total_tiles, L.tile_order,
                                         nproc ? nullptr : L.tile_nproc,
-                                        nproc ? nullptr : L.last_rank);
+                                        nproc ? nullptr : L.tile_last_dk);
   CGS_CHECK_LAUNCH("tile_order_kernel");
   return CGS_OK;
 }
@@ -753,7 +758,7 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
   CGS_PROFILED("raster_fwd_kernel", st,
                raster_fwd_kernel<<<fd.total_tiles, kFwdThreads, 0, st>>>(
                    fd, L.tile_order, L.ranges, vals, L.recs, L.hdr, image, final_T, counts,
-                   L.px_last, L.tile_nproc, L.rank_of, L.last_rank, L.ckpt, L.refine_tiles,
+                   L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.ckpt, L.refine_tiles,
                    L.refine_mask, tile_trace_buffer()));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
   {

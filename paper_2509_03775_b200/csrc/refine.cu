@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
     const uint32_t* __restrict__ refine_mask, uint32_t* __restrict__ refine_off,
     RefinePx* __restrict__ refine_px, int64_t refine_px_cap, float* __restrict__ image,
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
-    uint32_t* __restrict__ tile_nproc, const uint32_t* __restrict__ rank_of,
-    uint32_t* __restrict__ last_rank, const float* __restrict__ dL,
+    uint32_t* __restrict__ tile_nproc, const uint64_t* __restrict__ depth_key,
+    uint64_t* __restrict__ tile_last_dk, uint32_t* __restrict__ tile_last_sid,
+    const float* __restrict__ dL,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect,
     float* __restrict__ partials, int64_t partial9_offset) {
   __shared__ uint2 s_ck[kRefChunk];  // compacted in-box records of the chunk: (chunk index, splat id)
@@ -382,10 +383,7 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
           final_T[pix] = static_cast<float>(c.T);
           counts[pix] = c.cnt;
           px_last[pix] = c.last | kRefinedBit;
-          if (c.last > 0) {
-            atomicMax(&tile_nproc[tile], c.last);
-            atomicMax(&last_rank[tile], rank_of[pair_vals[rg.x + c.last - 1]] + 1);
-          }
+          if (c.last > 0) atomicMax(&tile_nproc[tile], c.last);
           if (s_off != 0xffffffffu) {
             RefinePx r;
             r.C[0] = c.P[0];
@@ -398,6 +396,14 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
           }
         }
         __syncthreads();
+      }
+    }
+    if (!BWD && tid == 0) {  // the tile's last processed splat after the re-walk
+      const uint32_t np = atomicOr(&tile_nproc[tile], 0u);  // this CTA's atomicMax results
+      if (np > 0) {
+        const uint32_t ls = pair_vals[rg.x + np - 1];
+        tile_last_dk[tile] = depth_key[ls];
+        tile_last_sid[tile] = ls;
       }
     }
     __syncthreads();
@@ -427,7 +433,7 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                  (refine_kernel<true><<<grid, kThreads, 0, st>>>(
                      fd, L.ranges, vals, L.recs, logits, L.n, L.hdr, L.refine_tiles, L.refine_mask,
                      L.refine_off, L.refine_px, L.refine_px_cap, nullptr, nullptr, nullptr,
-                     L.px_last, L.tile_nproc, L.rank_of, L.last_rank, dL, L.pair_off, L.rect,
+                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, dL, L.pair_off, L.rect,
                      partials, p9)));
     CGS_CHECK_LAUNCH("refine_bwd_kernel");
   } else {
@@ -435,7 +441,7 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                  (refine_kernel<false><<<grid, kThreads, 0, st>>>(
                      fd, L.ranges, vals, L.recs, logits, L.n, L.hdr, L.refine_tiles, L.refine_mask,
                      L.refine_off, L.refine_px, L.refine_px_cap, image, final_T, counts,
-                     L.px_last, L.tile_nproc, L.rank_of, L.last_rank, nullptr, nullptr, nullptr,
+                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, nullptr, nullptr, nullptr,
                      nullptr, 0)));
     CGS_CHECK_LAUNCH("refine_fwd_kernel");
   }

@@ -242,8 +242,9 @@ struct PairWalk {
   const uint64_t* pair_off;
   const uint32_t* n_tiles;
   const uint64_t* rect;
-  const uint32_t* rank_of;
-  const uint32_t* last_rank;
+  const uint64_t* depth_key;
+  const uint64_t* tile_last_dk;
+  const uint32_t* tile_last_sid;
   const float* partials;  // by emission index: [pair_cap x 8 | pair_cap]
   int64_t p9;             // offset of value 8 (8 * pair_cap)
 };
@@ -266,13 +267,14 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
   const int span = tx1 - tx0 + 1;
   const int v = static_cast<int>(s / n);
   const int tb = fd.cam[v].tile_base, ntx = fd.cam[v].ntx;
-  const uint32_t r = w.rank_of[s];
+  const uint64_t dk = w.depth_key[s];
   const double mx = w.recs[s].mx, my = w.recs[s].my;
   bool any = false;
   for (uint32_t k = k0; k < cnt; k += kstep) {
     const int ty = ty0 + static_cast<int>(k) / span, tx = tx0 + static_cast<int>(k) % span;
     const int t = tb + ty * ntx + tx;
-    if (r < w.last_rank[t]) {  // inside the tile's processed prefix
+    const uint64_t tk = w.tile_last_dk[t];
+    if (dk < tk || (dk == tk && static_cast<uint32_t>(s) <= w.tile_last_sid[t])) {  // in the processed prefix
       any = true;
       const int64_t e = static_cast<int64_t>(o + k);
       const float4* p4 = reinterpret_cast<const float4*>(w.partials) + 2 * e;
@@ -702,7 +704,7 @@ int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayo
 int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                        BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st) {
   if (fd.total_tiles > 0 && L.vn > 0) {
-    PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.rank_of, L.last_rank, B.partials,
+    PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.depth_key, L.tile_last_dk, L.tile_last_sid, B.partials,
                 8 * (L.pair_cap > 0 ? L.pair_cap : 1)};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {

@@ -76,16 +76,35 @@ struct ProjOut {
   FrameHeader* hdr;
 };
 
+// A splat's per-Gaussian inputs.
+struct ProjPre {
+  float px, py, pz, logit;
+  int32_t sh, sr;
+};
+
+__device__ __forceinline__ ProjPre load_pre(const ProjIn& in, int64_t i) {
+  ProjPre p;
+  p.px = in.pos[3 * i + 0];
+  p.py = in.pos[3 * i + 1];
+  p.pz = in.pos[3 * i + 2];
+  p.logit = in.logit[i];
+  p.sh = in.g2sh[i];
+  p.sr = in.g2sr[i];
+  return p;
+}
+
 // One (view, Gaussian) splat; returns its 32-bit depth sort key (~0: no tiles).
+// Quotients by the same divisor (1/tz, 1/det, 1/|view|) multiply by one
+// reciprocal: within an ulp of the reference's divisions, far inside the
+// decision bands (raster_common.cuh), like the reference's own einsum order.
 template <int DEG>
 __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDesc& fd,
-                                                const ProjOut& out, int64_t s) {
+                                                const ProjOut& out, int64_t s, const ProjPre& pre) {
   constexpr int NB = (DEG + 1) * (DEG + 1);
   constexpr int D = 3 * NB;
   const int v = static_cast<int>(s / in.n);
-  const int64_t i = s - static_cast<int64_t>(v) * in.n;
   const CamDev& cam = fd.cam[v];
-  const double px = in.pos[3 * i + 0], py = in.pos[3 * i + 1], pz = in.pos[3 * i + 2];
+  const double px = pre.px, py = pre.py, pz = pre.pz;
   // camera coordinates t = R p + trans (camera.py:29-32)
   const double tx = cam.R[0] * px + cam.R[1] * py + cam.R[2] * pz + cam.t[0];
   const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
@@ -94,17 +113,20 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
     out.n_tiles[s] = 0;
     return 0xffffffffu;
   }
-  const double* cv = in.sr_cov + static_cast<int64_t>(in.g2sr[i]) * 8;
+  const double2* cv2 = reinterpret_cast<const double2*>(in.sr_cov + static_cast<int64_t>(pre.sr) * 8);
+  const double2 c01 = cv2[0], c23 = cv2[1], c45 = cv2[2], c67 = cv2[3];
+  const double cv[7] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x};
   if (cv[6] != 0.0) {  // zero quaternion: reference raises ValueError
     out.n_tiles[s] = 0;
     out.hdr->stats.zero_quaternion = 1;
     return 0xffffffffu;
   }
-  const double mx = cam.fx * tx / tz + cam.cx;
-  const double my = cam.fy * ty / tz + cam.cy;
+  const double rz = 1.0 / tz;
+  const double mx = cam.fx * tx * rz + cam.cx;
+  const double my = cam.fy * ty * rz + cam.cy;
   // J (render.py:160-164) and M = J R (render.py:165)
-  const double j00 = cam.fx / tz, j02 = -cam.fx * tx / (tz * tz);
-  const double j11 = cam.fy / tz, j12 = -cam.fy * ty / (tz * tz);
+  const double j00 = cam.fx * rz, j02 = -cam.fx * tx * (rz * rz);
+  const double j11 = cam.fy * rz, j12 = -cam.fy * ty * (rz * rz);
   double m0[3], m1[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -138,13 +160,13 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   const int ty0 = static_cast<int>(y0) / kTile, ty1 = static_cast<int>(y1) / kTile;
   // view direction and SH colour (render.py:187-198)
   double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
-  const double len = sqrt((ox * ox + oy * oy) + oz * oz);
-  ox /= len;
-  oy /= len;
-  oz /= len;
+  const double rlen = 1.0 / sqrt((ox * ox + oy * oy) + oz * oz);
+  ox *= rlen;
+  oy *= rlen;
+  oz *= rlen;
   double B[NB];
   sh_basis<DEG>(ox, oy, oz, B);
-  const float* row = in.sh_rows + static_cast<int64_t>(in.g2sh[i]) * D;
+  const float* row = in.sh_rows + static_cast<int64_t>(pre.sh) * D;
   double col[3] = {0.0, 0.0, 0.0};
   if constexpr (D % 4 == 0) {
     const float4* r4 = reinterpret_cast<const float4*>(row);
@@ -165,10 +187,11 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   SplatRec rec;
   rec.mx = mx;
   rec.my = my;
-  rec.ca = c / det;  // conic = adj(Sigma2) / det (render.py:176-181)
-  rec.cb = -b / det;
-  rec.cc = a / det;
-  const double opac = 1.0 / (1.0 + exp(-static_cast<double>(in.logit[i])));
+  const double idet = 1.0 / det;
+  rec.ca = c * idet;  // conic = adj(Sigma2) / det (render.py:176-181)
+  rec.cb = -b * idet;
+  rec.cc = a * idet;
+  const double opac = 1.0 / (1.0 + exp(-static_cast<double>(pre.logit)));
   rec.opac = static_cast<float>(opac);
   rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
   rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
@@ -216,10 +239,13 @@ template <int DEG>
 #ifndef CGS_PROJECT_HIST_DIRECT
 #define CGS_PROJECT_HIST_DIRECT 1
 #endif
-#ifndef CGS_PROJECT_VIEW_INNER
-#define CGS_PROJECT_VIEW_INNER 1
+// 4 CTAs per SM (64 registers, a few spilled): the projection is latency
+// bound on its gathers; occupancy beats the spills (config 3: 345 -> 277 us;
+// loading the next iteration's inputs ahead measured no better)
+#ifndef CGS_PROJECT_MINB
+#define CGS_PROJECT_MINB 4
 #endif
-__global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
+__global__ void __launch_bounds__(256, CGS_PROJECT_MINB) project_kernel(ProjIn in, FrameDesc fd, ProjOut out) {
   __shared__ uint32_t s_h[4 * 256];
   __shared__ uint32_t s_wc[8];
   __shared__ unsigned long long s_base;
@@ -227,19 +253,18 @@ __global__ void __launch_bounds__(256) project_kernel(ProjIn in, FrameDesc fd, P
   __syncthreads();
   const int64_t vn = in.n * fd.n_views;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x); b < vn;
-       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // consecutive threads take the views of one Gaussian: its gathers
+  // (position, logit, indices, SR / SH rows) coalesce across the views
+  const int nv = fd.n_views;
+  auto gauss_of = [nv](int64_t t) { return nv == 1 ? t : t / nv; };
+  int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x);
+  for (; b < vn; b += stride) {
     const int64_t t = b + threadIdx.x;
     const bool ok = t < vn;
-#if CGS_PROJECT_VIEW_INNER
-    // consecutive threads take the views of one Gaussian: its gathers
-    // (position, logit, indices, SR / SH rows) coalesce across the views
-    const int64_t gi = t / fd.n_views;
+    const int64_t gi = gauss_of(t);
     const int64_t s = (t - gi * fd.n_views) * in.n + gi;
-#else
-    const int64_t s = t;
-#endif
-    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s) : 0xffffffffu;
+    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s, load_pre(in, gi)) : 0xffffffffu;
     // the depth sort takes only the splats with tiles: (key, splat id)
     // appended in any order (its ties are ordered by (fp64 depth, id)
     // afterwards, depth_tie_fix_kernel), one global atomic per CTA iteration
@@ -324,13 +349,9 @@ struct PairOffsets {
   const uint32_t* perm;
   const uint32_t* n_tiles;
   uint64_t* off;
-  uint32_t* rank_of;
   __device__ uint64_t load(int64_t r) const { return n_tiles[perm[r]]; }
   __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
-    if (!v) return;
-    const uint32_t s = perm[r];
-    off[s] = ex;
-    rank_of[s] = static_cast<uint32_t>(r);
+    if (v) off[perm[r]] = ex;
   }
 };
 
@@ -656,7 +677,7 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
                                                                            &L.hdr->n_onscreen));
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
   }
-  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.rank_of}, &L.hdr->n_onscreen, vn,
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off}, &L.hdr->n_onscreen, vn,
                        vn, L.scan, &L.hdr->scratch[0], st);
   if (rc) return rc;
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);

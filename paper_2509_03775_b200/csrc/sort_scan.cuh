@@ -299,8 +299,16 @@ struct SortSmem {
   uint32_t vals[kSortTile];
 };
 
+#ifndef CGS_SORT_EARLY_SCATTER
+#define CGS_SORT_EARLY_SCATTER 1
+#endif
+#ifdef CGS_SORT_MINB
+#define CGS_SORT_BOUNDS __launch_bounds__(256, CGS_SORT_MINB)
+#else
+#define CGS_SORT_BOUNDS __launch_bounds__(256)
+#endif
 template <typename K>
-__global__ void __launch_bounds__(256) onesweep_kernel(
+__global__ void CGS_SORT_BOUNDS onesweep_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     const unsigned long long* n_dev, int64_t n_host, int shift, int digit_bits,
@@ -381,22 +389,33 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     for (int w = 0; w < warp; ++w) wpre += S.scan_tmp[w];
     gbase = wpre + inc - h;
   }
-  // decoupled lookback for digit d over previous partitions
+  // decoupled lookback for digit d over previous partitions: publish this
+  // partition's count first, reorder the tile in shared memory (local ranks
+  // only; frees the key / value / rank registers before the lookback window
+  // is loaded), then walk back
   const int64_t tail = base + kSortTile - n;
   const uint32_t agg = cnt - ((d == 255 && tail > 0) ? static_cast<uint32_t>(tail) : 0u);
   uint32_t excl = 0;
   uint32_t* st = status + part * 256 + d;
-  if (part == 0) {
-    st_volatile(st, kSortPre | agg);
-  } else {
-    st_volatile(st, kSortAgg | agg);
+  st_volatile(st, (part == 0 ? kSortPre : kSortAgg) | agg);
+#if CGS_SORT_EARLY_SCATTER
+  __syncthreads();  // dstart complete
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
+    const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
+    S.keys[pos] = key[j];
+    S.vals[pos] = val[j];
+  }
+#endif
+  if (part != 0) {
     // Windowed lookback: kLookback independent status loads per round trip,
     // consumed in order until an inclusive prefix is found (an unpublished
     // slot makes the next window start there).  All partitions start
     // together, so partition p typically walks back ~p slots before it meets
     // an inclusive prefix: the window width sets the number of L2 round trips.
 #ifndef CGS_SORT_LOOKBACK
-#define CGS_SORT_LOOKBACK 32
+#define CGS_SORT_LOOKBACK 16
 #endif
     constexpr int kLookback = CGS_SORT_LOOKBACK;
     int64_t p = part - 1;
@@ -423,6 +442,7 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
   S.goff[d] = static_cast<int32_t>(gbase + excl) - static_cast<int32_t>(S.dstart[d]);
   __syncthreads();
   SORT_TRACE(part, 3);
+#if !CGS_SORT_EARLY_SCATTER
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
@@ -431,6 +451,7 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     S.vals[pos] = val[j];
   }
   __syncthreads();
+#endif
   const int nvalid = static_cast<int>(n - base < kSortTile ? n - base : kSortTile);
   for (int i = tid; i < nvalid; i += 256) {
     const K k = S.keys[i];

@@ -4,7 +4,10 @@ One process per GPU.  The scene state (positions, logits, indices, both
 codebooks and the host refcount / lineage / free-list mirrors) is replicated;
 each rank renders its own shard of the step's views; the only exchange is one
 sum-allreduce of the flat gradient buffer ``[d_pos | d_logit | d_SH | d_SR]``
-(``GradientSet.flat``), over NCCL on NVLink/NVSwitch.  The gradients are
+(``GradientSet.flat``), over NCCL on NVLink/NVSwitch, issued in two parts
+(engine.Trainer._enqueue_backward): ``[d_pos | d_logit]`` on a side stream as
+soon as the per-Gaussian gradients are written, overlapping the codebook
+reduce kernels, then ``[d_SH | d_SR]``.  The gradients are
 pre-scaled by 1 / (views per rank * world) so the sum is the mean over all
 views of the step.  Every rank then applies the identical SGLD update (same
 device Philox seed and offset) and the identical MCMC decisions (same host

@@ -11,8 +11,9 @@ from a warm-up render (pairs per Gaussian x the current N x headroom, so they
 grow with densify); an overflowing frame makes the SGLD kernels skip the
 update (no state change), as non-finite gradients do, and both latch a sticky
 device flag that is checked when the caller reads results.  Across GPUs, views are
-sharded by rank and the flat gradient buffer is summed with one NCCL
-allreduce (``torch.distributed``); MCMC decisions use the same host
+sharded by rank and the flat gradient buffer is summed by NCCL allreduce
+(``torch.distributed``; the per-Gaussian part on a side stream overlapping the
+codebook reduce, the codebook part after it); MCMC decisions use the same host
 Generator seed on every rank, so replicas stay identical with no broadcast.
 """
 
@@ -54,6 +55,7 @@ class Trainer:
         self.mcmc_every = mcmc_every
         self.world = world
         self.allreduce = allreduce
+        self._ar_stream = None
         self.headroom = pair_headroom
         h, w = self.cams[0].height, self.cams[0].width
         if any((c.height, c.width) != (h, w) for c in self.cams):
@@ -154,9 +156,28 @@ class Trainer:
         self.loss_ws.run(fr.image, self.gts, self.config.lambda_ssim, self.dL, 1.0)
 
     def _enqueue_backward(self):
-        self.frame.backward(self.dL, scale=1.0 / self.total_views, grads=self.grads, ws=self.bws)
-        if self.allreduce is not None:
-            self.allreduce(self.grads.flat)
+        scale = 1.0 / self.total_views
+        if self.allreduce is None:
+            self.frame.backward(self.dL, scale=scale, grads=self.grads, ws=self.bws)
+            return
+        # two allreduces: [d_pos | d_logit] on a side stream as soon as the
+        # per-Gaussian gradients are written, overlapping the codebook
+        # reduce kernels; [d_SH | d_SR] after them.  Element-wise sums, so the
+        # result equals one allreduce of the flat buffer.
+        cur = torch.cuda.current_stream(self.dev)
+        if self._ar_stream is None:
+            self._ar_stream = torch.cuda.Stream(self.dev)
+        ar = self._ar_stream
+
+        def head(g):
+            ar.wait_stream(cur)
+            with torch.cuda.stream(ar):
+                self.allreduce(g.flat[: 4 * g.opacity_logits.numel()])
+
+        g = self.frame.backward(self.dL, scale=scale, grads=self.grads, ws=self.bws,
+                                after_gaussians=head)
+        self.allreduce(g.flat[4 * g.opacity_logits.numel():])
+        cur.wait_stream(ar)
 
     def _enqueue_sgld(self):
         # cgs_frame_stats_t.overflow (byte 40 of the frame workspace): an

@@ -191,8 +191,13 @@ class Frame:
 
     # -- backward -------------------------------------------------------------
     def backward(self, dL: torch.Tensor, scale: float = 1.0, grads: "GradientSet" = None,
-                 ws: torch.Tensor = None) -> "GradientSet":
-        """Gradients of sum_v <dL_v, image_v> (scaled) for every parameter group."""
+                 ws: torch.Tensor = None, after_gaussians=None) -> "GradientSet":
+        """Gradients of sum_v <dL_v, image_v> (scaled) for every parameter group.
+
+        ``after_gaussians``, when given, is called once the per-Gaussian
+        gradients (positions, logits) are enqueued and before the codebook
+        reduce (the staged ABI), so a caller can start reducing them across
+        ranks on another stream while the codebook kernels run."""
         st = self.state
         dev = self.device
         if grads is None:
@@ -203,6 +208,19 @@ class Frame:
         self.scene = scene_struct(st)
         sh_off, sh_mem = st.code_csr("sh")
         sr_off, sr_mem = st.code_csr("sr")
+        if after_gaussians is not None:
+            args = (ctypes.byref(self.scene), self.c_cams, len(self.cams), nat.ptr(self.ws),
+                    self.ws.numel(), self.pair_cap)
+            h = nat.stream_handle(dev)
+            nat.call("cgs_raster_bwd", *args, nat.ptr(self.final_T), nat.ptr(dL), nat.ptr(ws),
+                     ws.numel(), h)
+            nat.call("cgs_gaussian_reduce_pullback", *args, float(scale), nat.ptr(ws), ws.numel(),
+                     nat.ptr(grads.positions), nat.ptr(grads.opacity_logits), h)
+            after_gaussians(grads)
+            nat.call("cgs_codebook_reduce", *args, float(scale), nat.ptr(sh_off), nat.ptr(sh_mem),
+                     nat.ptr(sr_off), nat.ptr(sr_mem), nat.ptr(ws), ws.numel(),
+                     nat.ptr(grads.sh_rows), nat.ptr(grads.sr_rows), h)
+            return grads
         nat.call("cgs_render_backward", ctypes.byref(self.scene), self.c_cams, len(self.cams),
                  nat.ptr(self.ws), self.ws.numel(), self.pair_cap, nat.ptr(self.final_T),
                  nat.ptr(dL), float(scale), nat.ptr(sh_off), nat.ptr(sh_mem), nat.ptr(sr_off),
