@@ -24,6 +24,42 @@ static std::vector<cudaEvent_t> g_prof_pool;
 static unsigned long long* g_tile_trace = nullptr;
 
 unsigned long long* tile_trace_buffer() { return g_tile_trace; }
+
+static std::mutex g_side_mu[kMaxDevices];
+static cudaStream_t g_side[kMaxDevices] = {};
+static cudaEvent_t g_side_ev[kMaxDevices][2] = {};
+
+SideFork::SideFork(cudaStream_t st) : main(st) {
+  if ((rc = current_device(&dev)) != 0) return;
+  g_side_mu[dev].lock();
+  cudaError_t e = cudaSuccess;
+  if (!g_side[dev]) {
+    e = cudaStreamCreateWithFlags(&g_side[dev], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side_ev[dev][0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_side_ev[dev][1], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(g_side_ev[dev][0], st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g_side[dev], g_side_ev[dev][0], 0);
+  if (e != cudaSuccess) {
+    rc = cuda_status(e, "side stream fork");
+    return;
+  }
+  side = g_side[dev];
+}
+
+int SideFork::join() {
+  if (!side) return rc;
+  cudaError_t e = cudaEventRecord(g_side_ev[dev][1], side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(main, g_side_ev[dev][1], 0);
+  side = nullptr;
+  if (e != cudaSuccess) rc = cuda_status(e, "side stream join");
+  return rc;
+}
+
+SideFork::~SideFork() {
+  join();
+  if (dev >= 0) g_side_mu[dev].unlock();
+}
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int current_device(int* dev) {

@@ -86,6 +86,22 @@ int cuda_status(cudaError_t e, const char* where);
 constexpr int kMaxDevices = 64;
 int current_device(int* dev);
 
+// Fork-join onto a second stream of the current device, for independent
+// kernels of one stage (captured into a CUDA graph as parallel branches when
+// the caller's stream is capturing).  The fork records an event on `st` that
+// the side stream waits on; the join makes `st` wait for the side stream.
+// The SideFork object holds the device's fork lock from fork to join, so
+// concurrent host threads cannot interleave their event pairs.
+struct SideFork {
+  cudaStream_t side = nullptr;
+  int dev = -1;
+  int rc = 0;
+  cudaStream_t main = nullptr;
+  explicit SideFork(cudaStream_t st);
+  int join();
+  ~SideFork();
+};
+
 #define CGS_CUDA(call)                                      \
   do {                                                      \
     cudaError_t e_ = (call);                                \

@@ -701,8 +701,22 @@ int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayo
   return CGS_OK;
 }
 
+static int launch_gauss_write(const cgs_scene_t* sc, const FrameDesc& fd, BwdLayout& B,
+                              float scale, float* gpos, float* glogit, cudaStream_t st) {
+  if (sc->n > 0) {
+    CGS_PROFILED("gauss_write_kernel", st,
+                 gauss_write_kernel<<<grid_for(sc->n, 256, 8), 256, 0, st>>>(B, sc->n, fd.n_views,
+                                                                             scale, gpos, glogit));
+    CGS_CHECK_LAUNCH("gauss_write_kernel");
+  }
+  return CGS_OK;
+}
+
+// write_gauss = false leaves the per-Gaussian gradient write to the codebook
+// stage (frame_backward runs it there beside the codebook reduce).
 int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
-                       BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st) {
+                       BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st,
+                       bool write_gauss = true) {
   if (fd.total_tiles > 0 && L.vn > 0) {
     PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.depth_key, L.tile_last_dk, L.tile_last_sid, B.partials,
                 8 * (L.pair_cap > 0 ? L.pair_cap : 1)};
@@ -715,19 +729,16 @@ int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLa
     }
     CGS_CHECK_LAUNCH("splat_reduce_kernel");
   }
-  if (sc->n > 0) {
-    CGS_PROFILED("gauss_write_kernel", st,
-                 gauss_write_kernel<<<grid_for(sc->n, 256, 8), 256, 0, st>>>(B, sc->n, fd.n_views,
-                                                                             scale, gpos, glogit));
-    CGS_CHECK_LAUNCH("gauss_write_kernel");
-  }
-  return CGS_OK;
+  return write_gauss ? launch_gauss_write(sc, fd, B, scale, gpos, glogit, st) : CGS_OK;
 }
 
+// The SH and SR codebook reduces (and, from frame_backward, the per-Gaussian
+// gradient write) are independent: SR (after the gradient write) runs on a
+// side stream beside SH.
 int bwd_stage_codebook(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                        BwdLayout& B, float scale, float* gsh, float* gsr,
                        const int32_t* const csr_off_in[2], const int32_t* const csr_mem_in[2],
-                       cudaStream_t st) {
+                       cudaStream_t st, float* gpos = nullptr, float* glogit = nullptr) {
   const int32_t* off[2];
   const int32_t* mem[2];
   const int32_t* idx[2] = {sc->g2sh, sc->g2sr};
@@ -744,6 +755,18 @@ int bwd_stage_codebook(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLa
       mem[b] = B.csr_mem[b];
     }
   }
+  SideFork fork(st);
+  if (fork.rc) return fork.rc;
+  if (gpos) {
+    const int rc = launch_gauss_write(sc, fd, B, scale, gpos, glogit, fork.side);
+    if (rc) return rc;
+  }
+  if (sc->sr_capacity > 0) {
+    CGS_PROFILED("sr_code_reduce_kernel", fork.side,
+                 sr_code_reduce_kernel<<<grid_for(sc->sr_capacity * 32, 256, 16), 256, 0, fork.side>>>(
+                     off[1], mem[1], sc->sr_capacity, sc->n, fd.n_views, B, sc->sr_rows, scale, gsr));
+    CGS_CHECK_LAUNCH("sr_code_reduce_kernel");
+  }
   if (sc->sh_capacity > 0) {
     switch (sc->sh_degree) {
       case 0: launch_sh_reduce<0>(off[0], mem[0], sc->sh_capacity, sc->n, fd.n_views, B, scale, gsh, st); break;
@@ -753,12 +776,7 @@ int bwd_stage_codebook(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLa
     }
     CGS_CHECK_LAUNCH("sh_code_reduce_kernel");
   }
-  if (sc->sr_capacity > 0) {
-    CGS_PROFILED("sr_code_reduce_kernel", st,
-                 sr_code_reduce_kernel<<<grid_for(sc->sr_capacity * 32, 256, 16), 256, 0, st>>>(
-                     off[1], mem[1], sc->sr_capacity, sc->n, fd.n_views, B, sc->sr_rows, scale, gsr));
-    CGS_CHECK_LAUNCH("sr_code_reduce_kernel");
-  }
+  if (int rc = fork.join()) return rc;
   bwd_stats_kernel<<<1, 1, 0, st>>>(const_cast<FrameHeader*>(L.hdr), B.hdr);
   CGS_CHECK_LAUNCH("bwd_stats_kernel");
   return CGS_OK;
@@ -769,8 +787,9 @@ int frame_backward(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout
                    float* gsh, float* gsr, const int32_t* const csr_off_in[2],
                    const int32_t* const csr_mem_in[2], cudaStream_t st) {
   int rc = bwd_stage_raster(sc, fd, L, B, dL, final_T, st);
-  if (!rc) rc = bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st);
-  if (!rc) rc = bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off_in, csr_mem_in, st);
+  if (!rc) rc = bwd_stage_pullback(sc, fd, L, B, scale, gpos, glogit, st, false);
+  if (!rc) rc = bwd_stage_codebook(sc, fd, L, B, scale, gsh, gsr, csr_off_in, csr_mem_in, st, gpos,
+                                   glogit);
   return rc;
 }
 
