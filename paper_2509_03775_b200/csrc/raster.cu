@@ -189,7 +189,12 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
 constexpr int kFwdThreads = 256;  // one pixel per thread
 constexpr int kFwdBatch = 256;
 constexpr int kFwdWarps = kFwdThreads / 32;
+#ifndef CGS_FWD_FIRST
+#define CGS_FWD_FIRST 128
+#endif
+constexpr int kFwdFirst = CGS_FWD_FIRST;  // first batch
 static_assert(kChunk % kFwdBatch == 0, "checkpoints sit on batch boundaries");
+static_assert(kFwdFirst > 0 && kFwdFirst <= kFwdBatch && kFwdFirst % 32 == 0, "first batch");
 __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     FrameDesc fd, const uint32_t* __restrict__ order, const uint2* __restrict__ ranges,
     const uint32_t* __restrict__ pair_vals, const SplatRec* __restrict__ recs,
@@ -244,14 +249,16 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   __syncthreads();
   uint32_t phase = 0;
   bool pending = false;
+  // batch ends: kFwdFirst, then the multiples of B (a tile whose pixels all
+  // terminate early stages only the first few splats of its list)
+  auto batch_end = [&](int b) { return min(b == 0 ? kFwdFirst : (b / B + 1) * B, n); };
   if (n > 0) {
-    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, min(B, n), tid, NT);
+    issue_records(s_raw, &s_bar, pair_vals, recs, rg.x, batch_end(0), tid, NT);
     pending = true;
   }
-  for (int b0 = 0; b0 < n; b0 += B) {
-    const int nb = min(B, n - b0);
-    mbar_wait(&s_bar, phase);
-    phase ^= 1;
+  for (int b0 = 0, bend = batch_end(0); b0 < n; b0 = bend, bend = batch_end(bend)) {
+    const int nb = bend - b0;
+    records_wait(&s_bar, phase);
     pending = false;
     if (tid < nb) {
       const Staged sg = stage_splat(s_raw[tid], cx, cy);
@@ -270,9 +277,9 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       s_mask[tid] = static_cast<uint8_t>(m8);
     }
     __syncthreads();
-    if (b0 + B < n) {
+    if (bend < n) {
       fence_proxy_async_smem();
-      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 + B, min(B, n - b0 - B), tid, NT);
+      issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + bend, batch_end(bend) - bend, tid, NT);
       pending = true;
     }
     const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
@@ -321,15 +328,15 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
 #endif
     }
     if (__syncthreads_count(p.done()) == NT) break;
-    if (b0 + B < n && ((b0 + B) % kChunk) == 0) {  // chunk boundary for the backward
+    if (bend < n && (bend % kChunk) == 0) {  // chunk boundary for the backward
       // T after the chunk and the chunk's own colour sum; colour restarts at 0
-      ckpt[ckpt_slot(rg.x, tile, (b0 + B) / kChunk) * kTilePixels + ly * kTile + lx] =
+      ckpt[ckpt_slot(rg.x, tile, bend / kChunk) * kTilePixels + ly * kTile + lx] =
           make_float4(p.T, p.r, p.g, p.b);
       p.r = p.g = p.b = 0.0f;
       ++n_ckpt;
     }
   }
-  if (pending) mbar_wait(&s_bar, phase);
+  if (pending) records_wait(&s_bar, phase);
   // Chunk sums -> suffix at each boundary (sum of the later chunks, so it
   // carries rounding relative to itself, like a back-to-front running sum)
   // and the pixel colour = sum of all chunks.  Only this thread's own writes.
@@ -660,8 +667,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     int buf = 0, cnb = 0;
     for (; b0 >= k0; b0 -= B) {
       const int nb = min(B, k_end - b0);
-      mbar_wait(&s_bar, phase);
-      phase ^= 1;
+      records_wait(&s_bar, phase);
       if (tid < B) {
         const int k = tid;
         if (k < nb) {

@@ -240,15 +240,49 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Bulk-copy records [first, first + nb) of a tile list into s_raw (all threads
-// of the CTA call it; thread 0 posts the expected byte count).
+// Copy records [first, first + nb) of a tile list into s_raw (all threads of
+// the CTA call it).  Default: each thread copies its own records with four
+// 16-byte cp.async (no per-lane serialisation: a bulk copy per record is
+// issued one lane at a time through the uniform datapath) and waits for them
+// itself (records_wait) -- the callers stage record k on thread k.  With
+// CGS_REC_CPASYNC=0: one bulk copy per record, completion on the mbarrier
+// (thread 0 posts the expected byte count).
+#ifndef CGS_REC_CPASYNC
+#define CGS_REC_CPASYNC 1
+#endif
+static_assert(sizeof(SplatRec) == 64, "records move as four 16-byte pieces");
 __device__ __forceinline__ void issue_records(SplatRec* s_raw, uint64_t* bar,
                                               const uint32_t* __restrict__ pair_vals,
                                               const SplatRec* __restrict__ recs, uint32_t first,
                                               int nb, int tid, int nthreads) {
+#if CGS_REC_CPASYNC
+  (void)bar;
+  for (int k = tid; k < nb; k += nthreads) {
+    const char* src = reinterpret_cast<const char*>(&recs[pair_vals[first + k]]);
+    const uint32_t dst = smem_u32(&s_raw[k]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + 16 * q)
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+#else
   if (tid == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nb) * sizeof(SplatRec));
   for (int k = tid; k < nb; k += nthreads)
     bulk_g2s(&s_raw[k], &recs[pair_vals[first + k]], sizeof(SplatRec), bar);
+#endif
+}
+
+// Completion of the last issue_records (this thread's copies, or the batch on
+// the mbarrier); flips the phase.
+__device__ __forceinline__ void records_wait(uint64_t* bar, uint32_t& phase) {
+#if CGS_REC_CPASYNC
+  (void)bar;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+#else
+  mbar_wait(bar, phase);
+#endif
+  phase ^= 1;
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {

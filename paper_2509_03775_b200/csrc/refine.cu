@@ -47,6 +47,11 @@ constexpr int kWarps = kThreads / 32;
 #endif
 constexpr int kEpt = CGS_REF_EPT;           // records per thread per chunk
 constexpr int kRefChunk = kThreads * kEpt;  // 1024
+#ifndef CGS_REF_FIRST
+#define CGS_REF_FIRST 256
+#endif
+constexpr int kRefFirst = CGS_REF_FIRST;
+static_assert(kRefFirst > 0 && kRefFirst <= kRefChunk, "first chunk");
 
 struct Carry {  // one flagged pixel, between chunks
   double T, P[3], C[3];
@@ -147,8 +152,11 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
       // chunk's are loaded while the current one is walked
       uint32_t sid[kEpt], nsid[kEpt];
       uint2 box[kEpt], nbox[kEpt];
+      // the first chunk is kRefFirst records (a flagged pixel usually
+      // terminates early in the list), later ones kRefChunk
+      auto chunk_len = [&](int c0) { return min(c0 == 0 ? kRefFirst : kRefChunk, n_walk - c0); };
       auto load_chunk = [&](int c0, uint32_t (&si)[kEpt], uint2 (&bx)[kEpt]) {
-        const int nb = min(kRefChunk, n_walk - c0);
+        const int nb = chunk_len(c0);
 #pragma unroll
         for (int i = 0; i < kEpt; ++i) {
           const int e = kEpt * tid + i;
@@ -161,14 +169,14 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
         }
       };
       if (n_walk > 0) load_chunk(0, nsid, nbox);
-      for (int c0 = 0; c0 < n_walk && s_alive > 0; c0 += kRefChunk) {
-        const int nb = min(kRefChunk, n_walk - c0);
+      for (int c0 = 0; c0 < n_walk && s_alive > 0; c0 += chunk_len(c0)) {
+        const int nb = chunk_len(c0);
 #pragma unroll
         for (int i = 0; i < kEpt; ++i) {
           sid[i] = nsid[i];
           box[i] = nbox[i];
         }
-        if (c0 + kRefChunk < n_walk) load_chunk(c0 + kRefChunk, nsid, nbox);
+        if (c0 + nb < n_walk) load_chunk(c0 + nb, nsid, nbox);
         (void)nb;
         for (int q = 0; q < npx; ++q) {
           if (s_car[q].done) continue;  // block-uniform
