@@ -44,7 +44,7 @@ struct FrameLayout {
   uint64_t* depth_key;     // V*N (f64 bits of camera z)
   uint32_t* dkey;          // V*N 32-bit depth sort keys
   uint32_t* dval;          // V*N depth sort payload (splat ids); depth rank -> splat
-  SortWs<uint32_t> dsort;
+  SortWs<uint32_t> dsort;  // depth sort (result: depth_perm)
   uint32_t* n_tiles;       // V*N
   uint64_t* rect;          // V*N packed tile rect
   uint64_t* pair_off;      // V*N per splat: first emission index of its pairs
@@ -79,6 +79,15 @@ struct FrameLayout {
   int tile_key_bits;
   int pair_result_alt;     // 1 if the tile-sorted pairs live in the sort's alt buffers
 };
+
+// Depth sort keys (project_kernel): 24 bits, 3 onesweep passes (an odd pass
+// count leaves the sorted splat ids in the sort's alternate value buffer);
+// depth_tie_fix_kernel writes the final order back into dval.
+constexpr int kDepthPasses = 3;
+constexpr uint32_t kDepthKeyBase = 0x3C23D70Au;  // fp32 bits of kNear = 0.01 rounded toward zero
+constexpr int kDepthKeyShift = 4;
+constexpr uint32_t kDepthKeyMax = (1u << (8 * kDepthPasses)) - 1u;
+inline uint32_t* depth_perm(const FrameLayout& L) { return L.dval; }
 
 inline int bits_for(int64_t v) {
   int b = 1;

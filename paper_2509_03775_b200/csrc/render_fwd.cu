@@ -225,7 +225,12 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   }
   out.recs[s] = rec;
   out.depth_key[s] = static_cast<uint64_t>(__double_as_longlong(tz));
-  const uint32_t key = __float_as_uint(__double2float_rz(tz));  // tz > 0: monotone bits
+  // 24-bit depth key: the fp32 bits of tz rounded toward zero (monotone for
+  // tz > 0), offset from the near plane's and dropping kDepthKeyShift low
+  // bits (relative resolution 2^-19; deeper than ~4e7 clamps) -- 3 sort passes
+  // instead of 4; equal keys are ordered by (fp64 depth, id) afterwards
+  const uint32_t kb = __float_as_uint(__double2float_rz(tz)) - kDepthKeyBase;
+  const uint32_t key = min(kb >> kDepthKeyShift, kDepthKeyMax);
   out.n_tiles[s] = static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
   out.rect[s] = static_cast<uint64_t>(tx0) | (static_cast<uint64_t>(tx1) << 16) |
                 (static_cast<uint64_t>(ty0) << 32) | (static_cast<uint64_t>(ty1) << 48);
@@ -285,20 +290,21 @@ __global__ void __launch_bounds__(256, CGS_PROJECT_MINB) project_kernel(ProjIn i
       out.dval[s_base + pos] = static_cast<uint32_t>(s);
     }
 #if CGS_PROJECT_HIST_DIRECT
-    // low three bytes of a depth key are spread over the digits: one shared
-    // atomic per lane is cheaper than eight ballots; the top byte (sign and
-    // high exponent bits) takes few values, so it is warp-aggregated
+    // low two bytes of a depth key are spread over the digits: one shared
+    // atomic per lane is cheaper than eight ballots; the top byte (high
+    // exponent bits) takes few values, so it is warp-aggregated
 #pragma unroll
-    for (int p = 0; p < 3; ++p)
+    for (int p = 0; p < kDepthPasses - 1; ++p)
       if (on) atomicAdd(&s_h[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
     {
-      const unsigned d = key >> 24;
+      const unsigned d = (key >> (8 * (kDepthPasses - 1))) & 255u;
       const unsigned peers = warp_peers8(d) & bal;
-      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_h[3 * 256 + d], __popc(peers));
+      if (on && lane == __ffs(peers) - 1)
+        atomicAdd(&s_h[(kDepthPasses - 1) * 256 + d], __popc(peers));
     }
 #else
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < kDepthPasses; ++p) {
       const unsigned d = (key >> (8 * p)) & 255u;
       const unsigned peers = warp_peers8(d) & bal;
       if (on && lane == __ffs(peers) - 1) atomicAdd(&s_h[p * 256 + d], __popc(peers));
@@ -311,36 +317,40 @@ __global__ void __launch_bounds__(256, CGS_PROJECT_MINB) project_kernel(ProjIn i
 }
 
 // ---------------------------------------------------------------------------
-// Exact order inside runs of equal 32-bit depth keys: an insertion sort of
-// the run by (fp64 depth bits, splat id) -- positive doubles order as
-// integers, and within one view the splat id orders as the Gaussian index --
-// so the order is the reference's lexsort((idx, tz)) (render.py:203) whatever
-// order the keys were appended in.  Runs are short (a handful of splats even
-// at 4M Gaussians).
+// Exact order inside runs of equal depth keys, into a second buffer: each
+// element of a run is placed at the run start + its rank by (fp64 depth bits,
+// splat id) among the run -- positive doubles order as integers, and within
+// one view the splat id orders as the Gaussian index -- so the order is the
+// reference's lexsort((idx, tz)) (render.py:203) whatever order the keys were
+// appended in; every other element is copied.  Runs are short (a few splats:
+// the 24-bit key resolves depth to 2^-19 relative), and one thread per
+// element keeps a long run parallel.
 __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __restrict__ key,
-                                                            uint32_t* __restrict__ val,
+                                                            const uint32_t* __restrict__ val,
+                                                            uint32_t* __restrict__ out,
                                                             const uint64_t* __restrict__ depth_key,
                                                             const unsigned long long* __restrict__ n_dev) {
   const int64_t vn = static_cast<int64_t>(*n_dev);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i + 1 < vn;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < vn;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = key[i];
-    if (key[i + 1] != k || (i > 0 && key[i - 1] == k)) continue;
-    int64_t e = i + 1;
-    while (e < vn && key[e] == k) ++e;
-    for (int64_t a = i + 1; a < e; ++a) {
-      const uint32_t va = val[a];
-      const uint64_t ka = depth_key[va];
-      int64_t b = a - 1;
-      while (b >= i) {
-        const uint32_t vb = val[b];
-        const uint64_t kb = depth_key[vb];
-        if (kb < ka || (kb == ka && vb < va)) break;
-        val[b + 1] = vb;
-        --b;
-      }
-      val[b + 1] = va;
+    const uint32_t vi = val[i];
+    const bool left = i > 0 && key[i - 1] == k, right = i + 1 < vn && key[i + 1] == k;
+    if (!left && !right) {
+      out[i] = vi;
+      continue;
     }
+    int64_t s = i, e = i + 1;
+    while (s > 0 && key[s - 1] == k) --s;
+    while (e < vn && key[e] == k) ++e;
+    const uint64_t di = depth_key[vi];
+    int64_t r = 0;
+    for (int64_t j = s; j < e; ++j) {
+      const uint32_t vj = val[j];
+      const uint64_t dj = depth_key[vj];
+      r += (dj < di || (dj == di && vj < vi)) ? 1 : 0;
+    }
+    out[s + r] = vi;
   }
 }
 
@@ -657,25 +667,27 @@ int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout&
 
 // Depth order of every splat of the frame (all views; the tile sort
 // separates the views again), then per-splat pair offsets in that order.
-// 4 passes over the 32-bit keys: the permutation ends in L.dval.
+// 3 passes over the 24-bit keys: the permutation ends in the sort's
+// alternate value buffer (depth_perm).
 int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
   const int64_t vn = L.vn;
-  uint32_t* perm = L.dval;
+  uint32_t* perm = depth_perm(L);
   if (vn > 0) {
     uint32_t* kres;
     // the projection appended the splats with tiles (count: hdr->n_onscreen)
-    int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, &L.hdr->n_onscreen, vn, vn, 32, L.dsort,
-                                         &kres, &perm, st, /*hist_ready=*/true);
+    int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, &L.hdr->n_onscreen, vn, vn,
+                                         8 * kDepthPasses, L.dsort, &kres, &perm, st,
+                                         /*hist_ready=*/true);
     if (rc) return rc;
-    if (perm != L.dval) {
+    if (perm != L.dsort.vals_alt) {
       set_error("depth sort: unexpected result buffer");
       return CGS_EINTERNAL;
     }
     CGS_PROFILED("depth_tie_fix_kernel", st,
-                 depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(kres, perm,
-                                                                           L.depth_key,
-                                                                           &L.hdr->n_onscreen));
+                 depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(
+                     kres, perm, L.dval, L.depth_key, &L.hdr->n_onscreen));
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
+    perm = depth_perm(L);
   }
   int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off}, &L.hdr->n_onscreen, vn,
                        vn, L.scan, &L.hdr->scratch[0], st);
@@ -686,8 +698,8 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
 }
 
 int frame_stage_duplicate(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
-  return L.tile_key_bytes == 2 ? emit_pairs_stage<uint16_t>(L, fd, L.psort16, L.dval, st)
-                               : emit_pairs_stage<uint32_t>(L, fd, L.psort32, L.dval, st);
+  return L.tile_key_bytes == 2 ? emit_pairs_stage<uint16_t>(L, fd, L.psort16, depth_perm(L), st)
+                               : emit_pairs_stage<uint32_t>(L, fd, L.psort32, depth_perm(L), st);
 }
 
 int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
