@@ -111,11 +111,14 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   const double px = g.pos[3 * gi + 0], py = g.pos[3 * gi + 1], pz = g.pos[3 * gi + 2];
   // colour path first (render.py:415-429), so its registers are free before
   // the geometric chain.
+  // quotients by one divisor multiply by its reciprocal (ulp-level, as the
+  // projection)
   double ox = px - cam.center[0], oy = py - cam.center[1], oz = pz - cam.center[2];
   const double len = sqrt((ox * ox + oy * oy) + oz * oz);
-  ox /= len;
-  oy /= len;
-  oz /= len;
+  const double rlen = 1.0 / len;
+  ox *= rlen;
+  oy *= rlen;
+  oz *= rlen;
   const SplatRec& rec = g.recs[s];
   // colour gate raw > 0 (render.py:418-419): the projection stored
   // max(raw, 0) in fp32, which is > 0 exactly when raw > 0 (fp64 decision)
@@ -139,7 +142,7 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
     float dv[3];
     sh_basis_grad_dot<DEG, float>(fx, fy, fz, wb, dv);
     const float vd = fx * dv[0] + fy * dv[1] + fz * dv[2];
-    const float il = static_cast<float>(1.0 / len);
+    const float il = static_cast<float>(rlen);
     dpc[0] = (dv[0] - fx * vd) * il;
     dpc[1] = (dv[1] - fy * vd) * il;
     dpc[2] = (dv[2] - fz * vd) * il;
@@ -162,8 +165,9 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
   const double ty = cam.R[3] * px + cam.R[4] * py + cam.R[5] * pz + cam.t[1];
   const double tz = cam.R[6] * px + cam.R[7] * py + cam.R[8] * pz + cam.t[2];
   const double fx = cam.fx, fy = cam.fy;
-  const double j00 = fx / tz, j02 = -fx * tx / (tz * tz);
-  const double j11 = fy / tz, j12 = -fy * ty / (tz * tz);
+  const double rz = 1.0 / tz, rz2 = rz * rz, rz3 = rz2 * rz;
+  const double j00 = fx * rz, j02 = -fx * tx * rz2;
+  const double j11 = fy * rz, j12 = -fy * ty * rz2;
   double M[2][3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -211,13 +215,12 @@ __device__ void pull_back_splat(const double* acc, int64_t s, uint32_t gi, const
     for (int c = 0; c < 3; ++c)
       dJ[a][c] = dM[a][0] * cam.R[c * 3 + 0] + dM[a][1] * cam.R[c * 3 + 1] + dM[a][2] * cam.R[c * 3 + 2];
   // d_t (render.py:404-412) and d_pos = d_t R (render.py:413)
-  const double z2 = tz * tz, z3 = z2 * tz;
   const double dmx = acc[4], dmy = acc[5];
   double dt[3];
-  dt[0] = dmx * fx / tz + dJ[0][2] * (-fx / z2);
-  dt[1] = dmy * fy / tz + dJ[1][2] * (-fy / z2);
-  dt[2] = dmx * (-fx * tx / z2) + dmy * (-fy * ty / z2) + dJ[0][0] * (-fx / z2) +
-          dJ[1][1] * (-fy / z2) + dJ[0][2] * (2 * fx * tx / z3) + dJ[1][2] * (2 * fy * ty / z3);
+  dt[0] = dmx * fx * rz + dJ[0][2] * (-fx * rz2);
+  dt[1] = dmy * fy * rz + dJ[1][2] * (-fy * rz2);
+  dt[2] = dmx * (-fx * tx * rz2) + dmy * (-fy * ty * rz2) + dJ[0][0] * (-fx * rz2) +
+          dJ[1][1] * (-fy * rz2) + dJ[0][2] * (2 * fx * tx * rz3) + dJ[1][2] * (2 * fy * ty * rz3);
   double dp[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) dp[k] = dt[0] * cam.R[0 + k] + dt[1] * cam.R[3 + k] + dt[2] * cam.R[6 + k];
@@ -407,10 +410,16 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
 #if CGS_PULLBACK_VIEW_INNER
     // consecutive threads take the views of one Gaussian (its gathers coalesce)
-    const int64_t gi = t / fd.n_views;
-    const int64_t s = (t - gi * fd.n_views) * n + gi;
+    const int64_t gi = fd.n_views == 1 ? t
+                       : (vn < (int64_t{1} << 31) ? static_cast<int64_t>(static_cast<uint32_t>(t) /
+                                                                         static_cast<uint32_t>(fd.n_views))
+                                                  : t / fd.n_views);
+    const int v = static_cast<int>(t - gi * fd.n_views);
+    const int64_t s = static_cast<int64_t>(v) * n + gi;
 #else
     const int64_t s = t;
+    const int v = static_cast<int>(s / n);
+    const int64_t gi = s - static_cast<int64_t>(v) * n;
 #endif
     if (!B.touched[s]) continue;
     const float4 a0 = B.acc0[s];
@@ -422,8 +431,7 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
     const double acc[9] = {a0.x, a0.y, a0.z, a0.w,
                            rq.ca * am.x + rq.cb * am.y, rq.cb * am.x + rq.cc * am.y,
                            -0.5 * aq.x, -aq.y, -0.5 * ar};
-    const int v = static_cast<int>(s / n);
-    pull_back_splat<DEG>(acc, s, static_cast<uint32_t>(s - static_cast<int64_t>(v) * n), fd.cam[v], g, B);
+    pull_back_splat<DEG>(acc, s, static_cast<uint32_t>(gi), fd.cam[v], g, B);
   }
 }
 
