@@ -268,13 +268,19 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
   const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
   const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
   const int span = tx1 - tx0 + 1;
-  const int v = static_cast<int>(s / n);
+  // splat ids are 32-bit: 32-bit division for the view
+  const int v = fd.n_views == 1 ? 0 : static_cast<int>(static_cast<uint32_t>(s) / static_cast<uint32_t>(n));
   const int tb = fd.cam[v].tile_base, ntx = fd.cam[v].ntx;
   const uint64_t dk = w.depth_key[s];
   const double mx = w.recs[s].mx, my = w.recs[s].my;
   bool any = false;
+  // tile (tx, ty) of pair k: stepped incrementally for kstep = 1
+  int ty = ty0 + static_cast<int>(k0) / span, tx = tx0 + static_cast<int>(k0) % span;
   for (uint32_t k = k0; k < cnt; k += kstep) {
-    const int ty = ty0 + static_cast<int>(k) / span, tx = tx0 + static_cast<int>(k) % span;
+    if (kstep != 1) {
+      ty = ty0 + static_cast<int>(k) / span;
+      tx = tx0 + static_cast<int>(k) % span;
+    }
     const int t = tb + ty * ntx + tx;
     const uint64_t tk = w.tile_last_dk[t];
     if (dk < tk || (dk == tk && static_cast<uint32_t>(s) <= w.tile_last_sid[t])) {  // in the processed prefix
@@ -290,6 +296,10 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
       acc[6] += (ox * ox * m0 + 2.0 * ox * m1x) + static_cast<double>(y.z);
       acc[7] += (ox * oy * m0 + (ox * m1y + oy * m1x)) + static_cast<double>(y.w);
       acc[8] += (oy * oy * m0 + 2.0 * oy * m1y) + static_cast<double>(w.partials[w.p9 + e]);
+    }
+    if (kstep == 1 && ++tx > tx1) {
+      tx = tx0;
+      ++ty;
     }
   }
   return any;

@@ -99,10 +99,10 @@ __device__ __forceinline__ ProjPre load_pre(const ProjIn& in, int64_t i) {
 // decision bands (raster_common.cuh), like the reference's own einsum order.
 template <int DEG>
 __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDesc& fd,
-                                                const ProjOut& out, int64_t s, const ProjPre& pre) {
+                                                const ProjOut& out, int64_t s, int v,
+                                                const ProjPre& pre) {
   constexpr int NB = (DEG + 1) * (DEG + 1);
   constexpr int D = 3 * NB;
-  const int v = static_cast<int>(s / in.n);
   const CamDev& cam = fd.cam[v];
   const double px = pre.px, py = pre.py, pz = pre.pz;
   // camera coordinates t = R p + trans (camera.py:29-32)
@@ -262,14 +262,18 @@ __global__ void __launch_bounds__(256, CGS_PROJECT_MINB) project_kernel(ProjIn i
   // consecutive threads take the views of one Gaussian: its gathers
   // (position, logit, indices, SR / SH rows) coalesce across the views
   const int nv = fd.n_views;
-  auto gauss_of = [nv](int64_t t) { return nv == 1 ? t : t / nv; };
+  auto gauss_of = [nv, vn](int64_t t) -> int64_t {
+    if (nv == 1) return t;
+    return vn < (int64_t{1} << 32) ? static_cast<uint32_t>(t) / static_cast<uint32_t>(nv) : t / nv;
+  };
   int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x);
   for (; b < vn; b += stride) {
     const int64_t t = b + threadIdx.x;
     const bool ok = t < vn;
     const int64_t gi = gauss_of(t);
-    const int64_t s = (t - gi * fd.n_views) * in.n + gi;
-    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s, load_pre(in, gi)) : 0xffffffffu;
+    const int v = static_cast<int>(t - gi * fd.n_views);
+    const int64_t s = static_cast<int64_t>(v) * in.n + gi;
+    const uint32_t key = ok ? project_one<DEG>(in, fd, out, s, v, load_pre(in, gi)) : 0xffffffffu;
     // the depth sort takes only the splats with tiles: (key, splat id)
     // appended in any order (its ties are ordered by (fp64 depth, id)
     // afterwards, depth_tie_fix_kernel), one global atomic per CTA iteration
