@@ -57,6 +57,9 @@ struct FrameLayout {
   // prefix iff (depth_key[s], s) <= it; (0, 0): none processed
   uint64_t* tile_last_dk;
   uint32_t* tile_last_sid;
+  // n_views: the largest tile_last_dk of the view -- a splat deeper than it
+  // is in no tile's processed prefix (the pair walk skips it)
+  unsigned long long* view_last_dk;
   uint32_t* long_list;     // V*N: splats with more than kLongSplat pairs (count: hdr->scratch[2])
   uint2* ranges;           // total_tiles [start, end)
   uint32_t* px_last;       // total_pixels
@@ -157,6 +160,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.tile_nproc = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.tile_last_dk = c.take<uint64_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.tile_last_sid = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
+  L.view_last_dk = c.take<unsigned long long>(fd.n_views > 0 ? fd.n_views : 1);
   L.tile_order = c.take<uint32_t>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.n_ckpt = fd.total_tiles + pc / kChunk + 2;
   L.ckpt = c.take<float4>(L.n_ckpt * 256);

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
     uint32_t* __restrict__ tile_nproc, const uint64_t* __restrict__ depth_key,
     uint64_t* __restrict__ tile_last_dk, uint32_t* __restrict__ tile_last_sid,
-    float4* __restrict__ ckpt,
+    unsigned long long* __restrict__ view_last_dk, float4* __restrict__ ckpt,
     uint32_t* __restrict__ refine_tiles, uint32_t* __restrict__ refine_mask,
     unsigned long long* __restrict__ trace) {
   constexpr int B = kFwdBatch, NT = kFwdThreads;
@@ -376,8 +376,10 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
     for (int w = 0; w < kFwdWarps; ++w) np = max(np, s_max[w]);
     const uint32_t ls = np ? pair_vals[rg.x + np - 1] : 0u;
     tile_nproc[tile] = np;
-    tile_last_dk[tile] = np ? depth_key[ls] : 0ull;
+    const uint64_t ldk = np ? depth_key[ls] : 0ull;
+    tile_last_dk[tile] = ldk;
     tile_last_sid[tile] = ls;
+    if (np) atomicMax(&view_last_dk[v], static_cast<unsigned long long>(ldk));
     if (trace) {
       unsigned long long* t = trace + 4 * static_cast<int64_t>(blockIdx.x);
       t[0] = t_start;
@@ -761,10 +763,11 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       const float* logits, float* image, float* final_T, int32_t* counts,
                       cudaStream_t st) {
   // L.tile_order was computed from the list lengths before the depth sort
+  CGS_CUDA(cudaMemsetAsync(L.view_last_dk, 0, (fd.n_views > 0 ? fd.n_views : 1) * sizeof(uint64_t), st));
   CGS_PROFILED("raster_fwd_kernel", st,
                raster_fwd_kernel<<<fd.total_tiles, kFwdThreads, 0, st>>>(
                    fd, L.tile_order, L.ranges, vals, L.recs, L.hdr, image, final_T, counts,
-                   L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.ckpt, L.refine_tiles,
+                   L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.view_last_dk, L.ckpt, L.refine_tiles,
                    L.refine_mask, tile_trace_buffer()));
   CGS_CHECK_LAUNCH("raster_fwd_kernel");
   {

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
     float* __restrict__ final_T, int32_t* __restrict__ counts, uint32_t* __restrict__ px_last,
     uint32_t* __restrict__ tile_nproc, const uint64_t* __restrict__ depth_key,
     uint64_t* __restrict__ tile_last_dk, uint32_t* __restrict__ tile_last_sid,
-    const float* __restrict__ dL,
+    unsigned long long* __restrict__ view_last_dk, const float* __restrict__ dL,
     const uint64_t* __restrict__ pair_off, const uint64_t* __restrict__ rect,
     float* __restrict__ partials, int64_t partial9_offset) {
   __shared__ uint2 s_ck[kRefChunk];  // compacted in-box records of the chunk: (chunk index, splat id)
@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
         const uint32_t ls = pair_vals[rg.x + np - 1];
         tile_last_dk[tile] = depth_key[ls];
         tile_last_sid[tile] = ls;
+        atomicMax(&view_last_dk[v], static_cast<unsigned long long>(depth_key[ls]));
       }
     }
     __syncthreads();
@@ -441,7 +442,7 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                  (refine_kernel<true><<<grid, kThreads, 0, st>>>(
                      fd, L.ranges, vals, L.recs, logits, L.n, L.hdr, L.refine_tiles, L.refine_mask,
                      L.refine_off, L.refine_px, L.refine_px_cap, nullptr, nullptr, nullptr,
-                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, dL, L.pair_off, L.rect,
+                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.view_last_dk, dL, L.pair_off, L.rect,
                      partials, p9)));
     CGS_CHECK_LAUNCH("refine_bwd_kernel");
   } else {
@@ -449,7 +450,7 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                  (refine_kernel<false><<<grid, kThreads, 0, st>>>(
                      fd, L.ranges, vals, L.recs, logits, L.n, L.hdr, L.refine_tiles, L.refine_mask,
                      L.refine_off, L.refine_px, L.refine_px_cap, image, final_T, counts,
-                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, nullptr, nullptr, nullptr,
+                     L.px_last, L.tile_nproc, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.view_last_dk, nullptr, nullptr, nullptr,
                      nullptr, 0)));
     CGS_CHECK_LAUNCH("refine_fwd_kernel");
   }

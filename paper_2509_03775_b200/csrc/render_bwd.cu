@@ -248,6 +248,7 @@ struct PairWalk {
   const uint64_t* depth_key;
   const uint64_t* tile_last_dk;
   const uint32_t* tile_last_sid;
+  const unsigned long long* view_last_dk;
   const float* partials;  // by emission index: [pair_cap x 8 | pair_cap]
   int64_t p9;             // offset of value 8 (8 * pair_cap)
 };
@@ -272,6 +273,7 @@ __device__ __forceinline__ bool walk_pairs(const PairWalk& w, const FrameDesc& f
   const int v = fd.n_views == 1 ? 0 : static_cast<int>(static_cast<uint32_t>(s) / static_cast<uint32_t>(n));
   const int tb = fd.cam[v].tile_base, ntx = fd.cam[v].ntx;
   const uint64_t dk = w.depth_key[s];
+  if (dk > w.view_last_dk[v]) return false;  // behind every tile's processed prefix
   const double mx = w.recs[s].mx, my = w.recs[s].my;
   bool any = false;
   // tile (tx, ty) of pair k: stepped incrementally for kstep = 1
@@ -736,7 +738,7 @@ int bwd_stage_pullback(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLa
                        BwdLayout& B, float scale, float* gpos, float* glogit, cudaStream_t st,
                        bool write_gauss = true) {
   if (fd.total_tiles > 0 && L.vn > 0) {
-    PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.depth_key, L.tile_last_dk, L.tile_last_sid, B.partials,
+    PairWalk pw{L.recs, L.pair_off, L.n_tiles, L.rect, L.depth_key, L.tile_last_dk, L.tile_last_sid, L.view_last_dk, B.partials,
                 8 * (L.pair_cap > 0 ? L.pair_cap : 1)};
     GaussIn gi{L.recs, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, L.sr_cov};
     switch (sc->sh_degree) {
