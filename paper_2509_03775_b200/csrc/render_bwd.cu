@@ -44,6 +44,7 @@ struct BwdLayout {
   double2* accm;       // V*N: sum dp d (centre-frame first moments, f64)
   double2* accq;       // V*N: sum dp dx^2, sum dp dx dy (second moments, f64)
   double* accr;        // V*N: sum dp dy^2
+  uint8_t* code_hit[2];  // sh_cap, sr_cap: the row has a touched member (pull_back_kernel)
   int32_t* csr_off[2];  // internal code CSR (sh, sr) when the caller passes none
   int32_t* csr_mem[2];
   void* csr_ws;
@@ -53,6 +54,15 @@ struct BwdLayout {
 };
 
 size_t code_csr_ws_bytes(int64_t n, int64_t cap);
+
+// Few touched splats (under 1/8 of the frame's, e.g. config 3 where a hundred
+// near-plane splats end every pixel): the pull-back flags the codebook rows
+// with a touched member and the codebook reduces skip the other rows' member
+// lists.  Dense frames skip the flags (their scattered writes cost more than
+// they save).  n_touched is final once the splat reduce kernels ran.
+__device__ __forceinline__ bool code_sparse(const BwdLayout& B, int64_t vn) {
+  return B.hdr->n_touched * 8ull < static_cast<unsigned long long>(vn);
+}
 
 inline BwdLayout plan_bwd(void* base, size_t cap, int64_t n, int n_views, int total_tiles,
                           int64_t pair_cap, int64_t sh_cap, int64_t sr_cap) {
@@ -72,6 +82,8 @@ inline BwdLayout plan_bwd(void* base, size_t cap, int64_t n, int n_views, int to
   B.accm = c.take<double2>(vn);
   B.accq = c.take<double2>(vn);
   B.accr = c.take<double>(vn);
+  B.code_hit[0] = c.take<uint8_t>(sh_cap > 0 ? sh_cap : 1);
+  B.code_hit[1] = c.take<uint8_t>(sr_cap > 0 ? sr_cap : 1);
   const int64_t n1 = n > 0 ? n : 1;
   B.csr_off[0] = c.take<int32_t>(sh_cap + 1);
   B.csr_mem[0] = c.take<int32_t>(n1);
@@ -418,6 +430,7 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
                                                         FrameDesc fd, int64_t n, int64_t vn,
                                                         GaussIn g, BwdLayout B) {
   if (fh->stats.overflow) return;
+  const bool sparse = code_sparse(B, vn);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < vn;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
 #if CGS_PULLBACK_VIEW_INNER
@@ -434,6 +447,10 @@ __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const Frame
     const int64_t gi = s - static_cast<int64_t>(v) * n;
 #endif
     if (!B.touched[s]) continue;
+    if (sparse) {  // the codebook reduces skip rows without a touched member
+      B.code_hit[0][g.g2sh[gi]] = 1;
+      B.code_hit[1][g.g2sr[gi]] = 1;
+    }
     const float4 a0 = B.acc0[s];
     const double2 am = B.accm[s], aq = B.accq[s];
     const double ar = B.accr[s];
@@ -489,18 +506,26 @@ __global__ void __launch_bounds__(128) sh_code_reduce_kernel(
   __shared__ float s_part[4][32][D + 1];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool sparse = code_sparse(B, n * n_views);
   bool bad = false;
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < cap;
        r += warps) {
+    float* out = gsh + r * D;
+    if (sparse && !B.code_hit[0][r]) {  // no touched member: the row's gradient is zero
+      for (int c = lane; c < D; c += 32) out[c] = 0.0f;
+      continue;
+    }
     const int m0 = off[r], m1 = off[r + 1];
     const int items = (m1 - m0) * n_views;
     float acc[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) acc[c] = 0.0f;
+    bool any = false;
     for (int t = lane; t < items; t += 32) {
-      const int mi = t / n_views, v = t - mi * n_views;
+      const int mi = n_views == 1 ? t : t / n_views, v = t - mi * n_views;
       const int64_t sp = static_cast<int64_t>(v) * n + mem[m0 + mi];
       if (!B.touched[sp]) continue;
+      any = true;
       const float4 vd = B.s_view[sp];
       const float4 dr = B.s_draw[sp];
       float Bv[NB];
@@ -512,8 +537,7 @@ __global__ void __launch_bounds__(128) sh_code_reduce_kernel(
         acc[3 * b + 2] = fmaf(Bv[b], dr.z, acc[3 * b + 2]);
       }
     }
-    float* out = gsh + r * D;
-    if (items == 0) {  // no member: the row's gradient is zero
+    if (!__any_sync(kFull, any)) {  // no member contributed: the row's gradient is zero
       for (int c = lane; c < D; c += 32) out[c] = 0.0f;
       continue;
     }
@@ -540,9 +564,15 @@ __global__ void __launch_bounds__(256) sr_code_reduce_kernel(
     int n_views, BwdLayout B, const float* __restrict__ sr_rows, float scale,
     float* __restrict__ gsr) {
   const int lane = threadIdx.x & 31;
+  const bool sparse = code_sparse(B, n * n_views);
   const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < cap;
        r += warps) {
+    if (sparse && !B.code_hit[1][r]) {  // no touched member: the row's gradient is zero
+      if (lane == 0)
+        for (int k = 0; k < 7; ++k) gsr[r * 7 + k] = 0.0f;
+      continue;
+    }
     const int m0 = off[r], m1 = off[r + 1];
     double s[6] = {0, 0, 0, 0, 0, 0};
     bool any = false;
@@ -715,6 +745,8 @@ int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayo
                      BwdLayout& B, const float* dL, const float* final_T, cudaStream_t st) {
   CGS_CUDA(cudaMemsetAsync(B.hdr, 0, sizeof(BwdHeader), st));
   if (L.vn > 0) CGS_CUDA(cudaMemsetAsync(B.touched, 0, L.vn, st));
+  if (sc->sh_capacity > 0) CGS_CUDA(cudaMemsetAsync(B.code_hit[0], 0, sc->sh_capacity, st));
+  if (sc->sr_capacity > 0) CGS_CUDA(cudaMemsetAsync(B.code_hit[1], 0, sc->sr_capacity, st));
   if (fd.total_tiles > 0 && L.vn > 0)
     return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed,
                              sc->opacity_logits, st);
