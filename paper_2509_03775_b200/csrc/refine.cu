@@ -48,7 +48,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kEpt = CGS_REF_EPT;           // records per thread per chunk
 constexpr int kRefChunk = kThreads * kEpt;  // 1024
 #ifndef CGS_REF_FIRST
-#define CGS_REF_FIRST 256
+#define CGS_REF_FIRST 1024
 #endif
 constexpr int kRefFirst = CGS_REF_FIRST;
 static_assert(kRefFirst > 0 && kRefFirst <= kRefChunk, "first chunk");
