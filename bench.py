@@ -754,8 +754,11 @@ def main():
     if not args.no_e2e:
         # config 1: BASELINE.json's run definition -- 100 iterations, forced
         # split + merge every 25, densify when the transition count crosses
-        # 100 -- whatever --steps is; graph re-captures fall inside the window
-        n_e2e = max(args.steps, 100) if args.config == 1 else args.steps
+        # 100 -- whatever --steps is; graph re-captures fall inside the window.
+        # Other configs: at least one MCMC period, so the window holds the
+        # events in their natural proportion
+        n_e2e = (max(args.steps, 100) if args.config == 1
+                 else max(args.steps, min(max(args.mcmc_every, 1), 1000)))
         ev0, dn0, cp0 = tr.mcmc_events, len(tr.densify_ms), tr.captures
         host_gt = (gts * 255.0).round().to(torch.uint8).cpu().pin_memory()
         # double-buffered device targets: step k+1's upload runs on a copy

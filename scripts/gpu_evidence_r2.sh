@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-2 evidence refresh: GPU tests, smoke, bench lines (config 1 default
+# run with e2e / drop-in / CPU baseline, reference arm, config 3 with MCMC,
+# config 4), live per-kernel lists, config-1 launch list and the full ncu
+# capture of the raster kernels (each ncu command after the same command
+# exited 0 without ncu).  Outputs under gpurun_out/ev/.
+D=gpurun_out/ev; mkdir -p $D
+timeout 900 python -m pytest tests -m gpu -q -x > $D/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -1 $D/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py > $D/bench_config1.json 2> $D/bench_config1.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $D/reference_arm_config1.json 2> $D/reference_arm.err; echo "ref rc=$?"
+timeout 1200 python bench.py --config 3 --steps 200 --warmup 5 --mcmc-every 100 --no-cpu-baseline > $D/bench_config3_mcmc.json 2> $D/bench_config3.err; echo "c3 rc=$?"
+timeout 1200 python bench.py --config 4 --steps 20 --warmup 3 --no-cpu-baseline > $D/bench_config4.json 2> $D/bench_config4.err; echo "c4 rc=$?"
+bash scripts/live_all.sh > $D/live_kernels_config1.txt 2>&1
+BENCH_ARGS="--config 3" bash scripts/live_all.sh > $D/live_kernels_config3.txt 2>&1
+CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > $D/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 160 --csv \
+    --log-file $D/launches_config1.csv $CMD > $D/ncu_l.log 2>&1; echo "ncu launches rc=$?"
+$CMD > $D/plain2.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"raster_fwd_kernel|raster_bwd_kernel|refine_kernel" \
+    -s 12 -c 4 -o $D/full_raster $CMD > $D/ncu_f.log 2>&1; echo "ncu full rc=$?"
+ls -la $D
