@@ -56,6 +56,8 @@ class Trainer:
         self.world = world
         self.allreduce = allreduce
         self._ar_stream = None
+        from .sampler import warm_host_paths
+        warm_host_paths(state.device)
         self.headroom = pair_headroom
         h, w = self.cams[0].height, self.cams[0].width
         if any((c.height, c.width) != (h, w) for c in self.cams):

@@ -248,6 +248,25 @@ def accept_split(state: ModelState, proposal: SplitProposal, lam: float, config:
     return False
 
 
+_WARM = set()
+
+
+def warm_host_paths(device) -> None:
+    """Pay the one-time costs of the MCMC host path up front (once per device):
+    numpy's lazily imported submodule behind np.unique and the lazily loaded
+    CUDA module of the row gather, ~70 ms together on the first merge
+    otherwise."""
+    key = str(device)
+    if key in _WARM:
+        return
+    import numpy.ma  # noqa: F401  (np.unique imports it on first use)
+    np.unique(np.zeros(2, np.int64))
+    if torch.device(device).type == "cuda":
+        z = torch.zeros((2, 7), dtype=torch.float32, device=device)
+        z.index_select(0, torch.zeros((1,), dtype=torch.int64, device=device)).cpu()
+    _WARM.add(key)
+
+
 def _rows_host(book, rows: np.ndarray) -> np.ndarray:
     if len(rows) == 0:
         return np.zeros((0, book.dim), np.float32)
@@ -826,6 +845,7 @@ def train(state: ModelState, views: list, config: SamplerConfig, iters: int,
     from .metrics import psnr as psnr_fn
     if rng is None:
         rng = np.random.default_rng(config.seed)
+    warm_host_paths(state.device)
     records = []
     for _ in range(iters):
         rec = train_step(state, views, config, rng)
