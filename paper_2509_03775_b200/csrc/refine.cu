@@ -40,15 +40,23 @@ namespace cgs {
 
 namespace {
 
-constexpr int kThreads = 256;
+// 128 threads x 6 records (768-record chunks; 4 CTAs per SM): config 3
+// (short walks -- its pixels end after ~60 splats -- in ~1500 tiles) 149 ->
+// 115 us for both kernels, config 1 (walks of ~1000) unchanged; 256 x 4 and
+// 128 x 4 / 128 x 8 measured worse on one or the other
+#ifndef CGS_REF_THREADS
+#define CGS_REF_THREADS 128
+#endif
+constexpr int kThreads = CGS_REF_THREADS;
 constexpr int kWarps = kThreads / 32;
+static_assert(kThreads % 32 == 0 && 8 % kWarps == 0, "the forward's 8 warp masks split evenly");
 #ifndef CGS_REF_EPT
-#define CGS_REF_EPT 4
+#define CGS_REF_EPT 6
 #endif
 constexpr int kEpt = CGS_REF_EPT;           // records per thread per chunk
-constexpr int kRefChunk = kThreads * kEpt;  // 1024
+constexpr int kRefChunk = kThreads * kEpt;  // 768
 #ifndef CGS_REF_FIRST
-#define CGS_REF_FIRST 1024
+#define CGS_REF_FIRST (CGS_REF_THREADS * CGS_REF_EPT)
 #endif
 constexpr int kRefFirst = CGS_REF_FIRST;
 static_assert(kRefFirst > 0 && kRefFirst <= kRefChunk, "first chunk");
@@ -63,7 +71,12 @@ struct Carry {  // one flagged pixel, between chunks
 }  // namespace
 
 template <bool BWD>
-__global__ void __launch_bounds__(kThreads) refine_kernel(
+#ifdef CGS_REF_MINB
+#define CGS_REF_BOUNDS __launch_bounds__(kThreads, CGS_REF_MINB)
+#else
+#define CGS_REF_BOUNDS __launch_bounds__(kThreads)
+#endif
+__global__ void CGS_REF_BOUNDS refine_kernel(
     FrameDesc fd, const uint2* __restrict__ ranges, const uint32_t* __restrict__ pair_vals,
     const SplatRec* __restrict__ recs, const float* __restrict__ logits, int64_t n_gauss,
     FrameHeader* __restrict__ hdr, const uint32_t* __restrict__ refine_tiles,
@@ -98,20 +111,26 @@ __global__ void __launch_bounds__(kThreads) refine_kernel(
     const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
     const uint2 rg = ranges[tile];
     const int n = static_cast<int>(rg.y - rg.x);
-    {  // flagged pixels, in the forward's warp / lane order (8x4 blocks)
-      const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
-      const bool in = tx * kTile + lx < cam.width && ty * kTile + ly < cam.height;
-      const uint32_t wm = refine_mask[static_cast<int64_t>(tile) * 8 + warp];
-      const bool f = in && ((wm >> lane) & 1u);
-      const unsigned bal = __ballot_sync(kFull, f);
-      if (lane == 0) s_cnt[warp] = __popc(bal);
-      __syncthreads();
-      int base = 0, tot = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        if (w < warp) base += s_cnt[w];
-        tot += s_cnt[w];
+    {  // flagged pixels, in the forward's warp / lane order (8 warps of 8x4 blocks)
+      int tot = 0;
+      for (int fw0 = 0; fw0 < 8; fw0 += kWarps) {
+        const int fw = fw0 + warp;
+        const int lx = (fw & 1) * 8 + (lane & 7), ly = (fw >> 1) * 4 + (lane >> 3);
+        const bool in = tx * kTile + lx < cam.width && ty * kTile + ly < cam.height;
+        const uint32_t wm = refine_mask[static_cast<int64_t>(tile) * 8 + fw];
+        const bool f = in && ((wm >> lane) & 1u);
+        const unsigned bal = __ballot_sync(kFull, f);
+        if (lane == 0) s_cnt[warp] = __popc(bal);
+        __syncthreads();
+        int base = tot, t_r = 0;
+        for (int w = 0; w < kWarps; ++w) {
+          if (w < warp) base += s_cnt[w];
+          t_r += s_cnt[w];
+        }
+        if (f) s_pix[base + __popc(bal & lanemask_lt())] = static_cast<uint16_t>(ly * kTile + lx);
+        tot += t_r;
+        __syncthreads();
       }
-      if (f) s_pix[base + __popc(bal & lanemask_lt())] = static_cast<uint16_t>(ly * kTile + lx);
       if (tid == 0) {
         s_npx = tot;
         if (!BWD) {
