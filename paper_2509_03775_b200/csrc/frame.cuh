@@ -48,6 +48,7 @@ struct FrameLayout {
   uint32_t* n_tiles;       // V*N
   uint64_t* rect;          // V*N packed tile rect
   uint64_t* pair_off;      // V*N per splat: first emission index of its pairs
+  uint64_t* off_rank;      // the same by depth rank (N_s; the emission reads it coalesced)
   void* pkeys;             // pair_cap tile keys (u16 or u32)
   uint32_t* pvals;         // pair_cap splat ids
   SortWs<uint16_t> psort16;
@@ -146,6 +147,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.n_tiles = c.take<uint32_t>(vn1);
   L.rect = c.take<uint64_t>(vn1);
   L.pair_off = c.take<uint64_t>(vn1);
+  L.off_rank = c.take<uint64_t>(vn1);
   if (L.tile_key_bytes == 2) {
     L.pkeys = c.take<uint16_t>(pc);
     L.psort16 = carve_sort<uint16_t>(c, pc);

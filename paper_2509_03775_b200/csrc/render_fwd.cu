@@ -363,8 +363,10 @@ struct PairOffsets {
   const uint32_t* perm;
   const uint32_t* n_tiles;
   uint64_t* off;
+  uint64_t* off_rank;
   __device__ uint64_t load(int64_t r) const { return n_tiles[perm[r]]; }
   __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
+    off_rank[r] = ex;
     if (v) off[perm[r]] = ex;
   }
 };
@@ -453,8 +455,8 @@ __device__ __forceinline__ void hist_rect(uint32_t* s_h, int* d0, int* base0, in
 
 template <typename KT>
 __device__ __forceinline__ void emit_warps(
-    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
-    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
+    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off_rank,
+    const uint64_t* __restrict__ rect,
     FrameHeader* __restrict__ hdr, const FrameDesc& fd, int64_t n, uint32_t* __restrict__ long_list,
     KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* s_h, int* d0, int* base0,
     int key_bits) {
@@ -468,7 +470,14 @@ __device__ __forceinline__ void emit_warps(
     const int64_t r = w * 32 + lane;
     const bool ok = r < ns;
     const uint32_t s = ok ? perm[r] : 0u;
-    const uint32_t cnt = ok ? n_tiles[s] : 0u;
+    // offset and tile count from the rank-ordered offsets (coalesced): the
+    // count is the next rank's offset minus this one's, the last rank's runs
+    // to the pair total (hdr->scratch[0], the scan's total)
+    const uint64_t o_r = ok ? off_rank[r] : 0ull;
+    uint64_t o_nx = __shfl_down_sync(kFull, o_r, 1);
+    if (ok && (lane == 31 || r + 1 >= ns))
+      o_nx = r + 1 < ns ? off_rank[r + 1] : static_cast<uint64_t>(hdr->scratch[0]);
+    const uint32_t cnt = ok ? static_cast<uint32_t>(o_nx - o_r) : 0u;
     const bool lng = cnt > kLongSplat;
     if (lng) long_list[atomicAdd(&hdr->scratch[2], 1ULL)] = s;
     const uint32_t c = lng ? 0u : cnt;  // pairs this warp emits for lane's splat
@@ -476,7 +485,7 @@ __device__ __forceinline__ void emit_warps(
     const uint32_t loc = inc - c;        // warp-local offset of lane's pairs
     const uint32_t total = __shfl_sync(kFull, inc, 31);
     if (total == 0) continue;
-    const uint64_t o = c ? off[s] : 0ULL;
+    const uint64_t o = o_r;
     const uint64_t rc = c ? rect[s] : 0ULL;
     const int v = ok ? static_cast<int>(s / static_cast<uint32_t>(n)) : 0;
     const int ntx = fd.cam[v].ntx;
@@ -507,8 +516,8 @@ __device__ __forceinline__ void emit_warps(
 
 template <typename KT>
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
-    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off,
-    const uint32_t* __restrict__ n_tiles, const uint64_t* __restrict__ rect,
+    const uint32_t* __restrict__ perm, const uint64_t* __restrict__ off_rank,
+    const uint64_t* __restrict__ rect,
     FrameHeader* __restrict__ hdr, FrameDesc fd, int64_t n, uint32_t* __restrict__ long_list,
     KT* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ hist, int key_bits) {
   const int passes = (key_bits + 7) / 8;
@@ -519,8 +528,8 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
   for (int k = threadIdx.x; k < 257; k += blockDim.x) s_d0[k] = 0;
   if (threadIdx.x == 0) s_base0 = 0;
   __syncthreads();
-  emit_warps<KT>(perm, off, n_tiles, rect, hdr, fd, n, long_list, keys, vals, s_h, s_d0,
-                 &s_base0, key_bits);
+  emit_warps<KT>(perm, off_rank, rect, hdr, fd, n, long_list, keys, vals, s_h, s_d0, &s_base0,
+                 key_bits);
   __syncthreads();
   if (threadIdx.x < 32) {  // low digit: prefix sum of the difference array (8 per lane)
     const int lane = threadIdx.x;
@@ -611,7 +620,7 @@ static int emit_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
   const int passes = (L.tile_key_bits + 7) / 8;
   CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
   CGS_PROFILED("emit_pairs_kernel", st,
-               emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.pair_off, L.n_tiles, L.rect, L.hdr,
+               emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.off_rank, L.rect, L.hdr,
                                                           fd, L.n, L.long_list,
                                                           static_cast<KT*>(L.pkeys), L.pvals,
                                                           ws.hist, L.tile_key_bits));
@@ -693,7 +702,7 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
     perm = depth_perm(L);
   }
-  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off}, &L.hdr->n_onscreen, vn,
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.off_rank}, &L.hdr->n_onscreen, vn,
                        vn, L.scan, &L.hdr->scratch[0], st);
   if (rc) return rc;
   finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
