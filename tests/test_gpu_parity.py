@@ -462,6 +462,19 @@ def test_staged_abi_equals_fused(cg):
     g2 = staged.backward_staged(dL, scale=0.5)
     for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
         assert torch.equal(getattr(g1, k), getattr(g2, k)), k
+    # the split form the multi-GPU trainer uses (per-Gaussian gradients
+    # handed to a callback before the codebook reduce) gives the same bits,
+    # and the callback sees the per-Gaussian part already final
+    seen = {}
+
+    def after(g):
+        torch.cuda.current_stream().synchronize()
+        seen["pos"] = g.positions.clone()
+
+    g3 = fused.backward(dL, scale=0.5, after_gaussians=after)
+    for k in ("positions", "opacity_logits", "sh_rows", "sr_rows"):
+        assert torch.equal(getattr(g1, k), getattr(g3, k)), k
+    assert torch.equal(seen["pos"], g1.positions)
 
 
 def test_deep_stack_chunked_backward_matches_oracle(cg):
