@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "../paper_2509_03775_b200/csrc/sort_scan.cuh"
 
 namespace cgs {
@@ -16,6 +18,10 @@ int cuda_status(cudaError_t e, const char* w) {
   return 2;
 }
 void note_launch() {}
+int current_device(int* dev) {
+  cudaGetDevice(dev);
+  return 0;
+}
 ProfScope::ProfScope(const char*, cudaStream_t s) : on(false), st(s) {}
 ProfScope::~ProfScope() {}
 }  // namespace cgs
@@ -86,25 +92,72 @@ static void run(int64_t n, int bits, int reps) {
     cudaFree(tr);
   }
 #endif
+  // the same without the histogram kernel (the frame pipeline fuses the
+  // digit histograms into the projection / emission kernels)
+  float nohist = 1e9;
+  for (int r = 0; r < reps; ++r) {
+    cudaMemcpyAsync(dk, k0, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dv, v0, n * 4, cudaMemcpyDeviceToDevice, st);
+    cudaEventRecord(a, st);
+    launch_radix_sort<K>(dk, dv, nullptr, n, n, bits, w, &ko, &vo, st, /*hist_ready=*/true);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    if (r > 0 && ms < nohist) nohist = ms;
+  }
+  printf("  passes only (histogram precomputed, as in the pipeline): %.1f us\n", nohist * 1000);
+  cudaMemcpyAsync(dk, k0, n * sizeof(K), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(dv, v0, n * 4, cudaMemcpyDeviceToDevice, st);
+  launch_radix_sort<K>(dk, dv, nullptr, n, n, bits, w, &ko, &vo, st);
+  cudaStreamSynchronize(st);
   std::vector<K> rk(n); std::vector<uint32_t> rv(n);
   cudaMemcpy(rk.data(), ko, n * sizeof(K), cudaMemcpyDeviceToHost);
   cudaMemcpy(rv.data(), vo, n * 4, cudaMemcpyDeviceToHost);
   bool ok = true;
   for (int64_t i = 1; i < n; ++i)
     if (rk[i - 1] > rk[i] || (rk[i - 1] == rk[i] && rv[i - 1] > rv[i])) { ok = false; break; }
-  printf("n=%9lld key=%zuB bits=%2d passes=%d  %8.1f us  (%.1f us/pass) %s\n", (long long)n,
-         sizeof(K), bits, (bits + 7) / 8, best * 1000, best * 1000 / ((bits + 7) / 8),
-         ok ? "sorted+stable" : "WRONG");
+  // CUB (the CUDA toolkit's DeviceRadixSort::SortPairs, stable LSD onesweep)
+  // on the same keys / values and bit range, for comparison
+  float cub_best = 1e9;
+  {
+    K* ck; uint32_t* cv;
+    cudaMalloc(&ck, n * sizeof(K)); cudaMalloc(&cv, n * 4);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, ck, v0, cv, static_cast<int>(n), 0, bits, st);
+    void* tmp; cudaMalloc(&tmp, tb);
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(a, st);
+      cub::DeviceRadixSort::SortPairs(tmp, tb, k0, ck, v0, cv, static_cast<int>(n), 0, bits, st);
+      cudaEventRecord(b, st);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      if (r > 0 && ms < cub_best) cub_best = ms;
+    }
+    std::vector<K> ck_h(n);
+    cudaMemcpy(ck_h.data(), ck, n * sizeof(K), cudaMemcpyDeviceToHost);
+    for (int64_t i = 0; i < n; ++i)
+      if (ck_h[i] != rk[i]) { ok = false; break; }
+    cudaFree(ck); cudaFree(cv); cudaFree(tmp);
+  }
+  const double bytes = 2.0 * n * (sizeof(K) + 4) * ((bits + 7) / 8);  // read + write per pass
+  printf("n=%9lld key=%zuB bits=%2d passes=%d  ours %8.1f us (%.1f us/pass, %.2f TB/s)  "
+         "CUB %8.1f us (%.2f TB/s)  %s\n", (long long)n, sizeof(K), bits, (bits + 7) / 8,
+         best * 1000, best * 1000 / ((bits + 7) / 8), bytes / (best * 1e-3) / 1e12, cub_best * 1000,
+         2.0 * n * (sizeof(K) + 4) * ((bits + 7) / 8) / (cub_best * 1e-3) / 1e12,
+         ok ? "sorted+stable, same keys as CUB" : "WRONG");
   cudaFree(dk); cudaFree(dv); cudaFree(k0); cudaFree(v0); cudaFree(ws);
 }
 
 int main(int argc, char** argv) {
   const int only = argc > 1 ? atoi(argv[1]) : -1;
-  if (only < 0 || only == 0) run<uint32_t>(100000, 32, 20);
-  if (only < 0 || only == 1) run<uint32_t>(400000, 32, 20);
-  if (only < 0 || only == 2) run<uint32_t>(4000000, 32, 10);
-  if (only < 0 || only == 3) run<uint16_t>(1100000, 10, 20);
-  if (only < 0 || only == 4) run<uint16_t>(1600000, 16, 20);
-  if (only < 0 || only == 5) run<uint32_t>(12000000, 14, 10);
+  // the frame pipeline's sorts: depth keys (24 bits) of the on-screen splats
+  // and tile keys of the pairs, at configs 1 / 3 / 4
+  if (only < 0 || only == 0) run<uint32_t>(350000, 24, 20);     // config 1 depth
+  if (only < 0 || only == 1) run<uint16_t>(1070000, 10, 20);    // config 1 tiles
+  if (only < 0 || only == 2) run<uint32_t>(2950000, 24, 10);    // config 3 depth
+  if (only < 0 || only == 3) run<uint16_t>(12200000, 14, 10);   // config 3 tiles
+  if (only < 0 || only == 4) run<uint32_t>(4400000, 24, 10);    // config 4 depth
+  if (only < 0 || only == 5) run<uint16_t>(18500000, 13, 10);   // config 4 tiles
+  if (only < 0 || only == 6) run<uint32_t>(16000000, 32, 10);   // large, full 32-bit keys
   return 0;
 }
