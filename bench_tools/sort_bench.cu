@@ -62,7 +62,7 @@ static void run(int64_t n, int bits, int reps) {
   }
 #ifdef CGS_SORT_TRACE
   {
-    const int64_t parts = ceil_div(n, kSortTile);
+    const int64_t parts = ceil_div(n, sort_tile_for(n));
     unsigned long long* tr;
     cudaMalloc(&tr, parts * 5 * sizeof(unsigned long long));
     cudaMemset(tr, 0, parts * 5 * sizeof(unsigned long long));

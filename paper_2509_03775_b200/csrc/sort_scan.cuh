@@ -203,12 +203,38 @@ int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t 
 // per-digit decoupled lookback across partitions, smem reorder, coalesced
 // scatter.  Status words: 30-bit count, flag in bits 30..31.
 // ===========================================================================
-constexpr int kSortWarps = 8;
+// Two partition shapes, chosen from the sort's capacity: 8 warps x 16 keys
+// (4096 per partition) for small sorts, 16 warps x 12 keys (6144) for large
+// ones (capacity above 4 M) -- twice the resident warps per SM and fewer partitions on the
+// decoupled lookback (bench_tools/sort_bench.cu: a 12.2 M-pair tile sort
+// 342 -> 311 us, 18.5 M 478 -> 444 us; the small config-1 sorts keep 8 x 16).
+#ifndef CGS_SORT_WARPS
+#define CGS_SORT_WARPS 8
+#endif
+#ifndef CGS_SORT_LARGE_WARPS
+#define CGS_SORT_LARGE_WARPS 16
+#endif
+#ifndef CGS_SORT_LARGE_ITEMS
+#define CGS_SORT_LARGE_ITEMS 12
+#endif
+#ifndef CGS_SORT_BACKOFF
+#define CGS_SORT_BACKOFF 0  // ns; 0: spin
+#endif
+#ifndef CGS_SORT_LARGE_N
+#define CGS_SORT_LARGE_N (4 << 20)
+#endif
+constexpr int kSortWarps = CGS_SORT_WARPS;  // >= 8: the first 8 warps own the 256 digits
+constexpr int kSortThreads = kSortWarps * 32;
 #ifndef CGS_SORT_ITEMS
 #define CGS_SORT_ITEMS 16
 #endif
 constexpr int kSortItems = CGS_SORT_ITEMS;
 constexpr int kSortTile = kSortWarps * 32 * kSortItems;  // 4096
+constexpr int kSortLargeWarps = CGS_SORT_LARGE_WARPS, kSortLargeItems = CGS_SORT_LARGE_ITEMS;
+inline bool sort_large(int64_t n_cap) { return n_cap > CGS_SORT_LARGE_N; }
+inline int64_t sort_tile_for(int64_t n_cap) {
+  return sort_large(n_cap) ? kSortLargeWarps * 32 * kSortLargeItems : kSortTile;
+}
 constexpr unsigned kSortAgg = 1u << 30;
 constexpr unsigned kSortPre = 2u << 30;
 constexpr unsigned kSortVal = (1u << 30) - 1;
@@ -226,7 +252,7 @@ struct SortWs {
 
 template <typename K>
 inline size_t sort_ws_bytes(int64_t n_cap) {
-  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kSortTile);
+  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, sort_tile_for(n_cap));
   const int passes = static_cast<int>(sizeof(K));
   return align_up(n_cap * sizeof(K)) + align_up(n_cap * sizeof(uint32_t)) +
          align_up(passes * 256 * 4) + align_up(passes * parts * 256 * 4) + 256 + 4 * 256;
@@ -235,7 +261,7 @@ inline size_t sort_ws_bytes(int64_t n_cap) {
 template <typename K>
 inline SortWs<K> carve_sort(Carver& c, int64_t n_cap) {
   SortWs<K> w;
-  w.max_parts = ceil_div(n_cap > 0 ? n_cap : 1, kSortTile);
+  w.max_parts = ceil_div(n_cap > 0 ? n_cap : 1, sort_tile_for(n_cap));
   w.passes_cap = static_cast<int>(sizeof(K));
   w.keys_alt = c.take<K>(n_cap > 0 ? n_cap : 1);
   w.vals_alt = c.take<uint32_t>(n_cap > 0 ? n_cap : 1);
@@ -288,51 +314,48 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SORT_TRACE(part, i)
 #endif
 
-template <typename K>
+template <typename K, int WARPS, int ITEMS>
 struct SortSmem {
-  uint32_t wcnt[kSortWarps * 256];
+  uint32_t wcnt[WARPS * 256];
   uint32_t dstart[256];
   int32_t goff[256];
-  uint32_t scan_tmp[kSortWarps];
+  uint32_t scan_tmp[WARPS];
   unsigned part;
-  K keys[kSortTile];
-  uint32_t vals[kSortTile];
+  K keys[WARPS * 32 * ITEMS];
+  uint32_t vals[WARPS * 32 * ITEMS];
 };
 
 #ifndef CGS_SORT_EARLY_SCATTER
 #define CGS_SORT_EARLY_SCATTER 1
 #endif
-#ifdef CGS_SORT_MINB
-#define CGS_SORT_BOUNDS __launch_bounds__(256, CGS_SORT_MINB)
-#else
-#define CGS_SORT_BOUNDS __launch_bounds__(256)
-#endif
-template <typename K>
-__global__ void CGS_SORT_BOUNDS onesweep_kernel(
+template <typename K, int WARPS, int ITEMS>
+__global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
     const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
     const unsigned long long* n_dev, int64_t n_host, int shift, int digit_bits,
     const uint32_t* __restrict__ hist, uint32_t* status, unsigned* counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem<K>& S = *reinterpret_cast<SortSmem<K>*>(smem_raw);
+  static_assert(WARPS >= 8 && WARPS % 8 == 0, "digit phase: 256 digit-owning threads");
+  constexpr int kThreads = WARPS * 32, kTile = kThreads * ITEMS;
+  SortSmem<K, WARPS, ITEMS>& S = *reinterpret_cast<SortSmem<K, WARPS, ITEMS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned dmask = (1u << digit_bits) - 1u;  // only the low key_bits are sorted on
   if (tid == 0) S.part = atomicAdd(counter, 1u);
-  for (int i = tid; i < kSortWarps * 256; i += 256) S.wcnt[i] = 0;
+  for (int i = tid; i < WARPS * 256; i += kThreads) S.wcnt[i] = 0;
   __syncthreads();
   const int64_t part = S.part;
   const int64_t n = dev_count(n_dev, n_host);
-  const int64_t nparts = ceil_div(n, kSortTile);
+  const int64_t nparts = ceil_div(n, kTile);
   if (part >= nparts) return;
-  const int64_t base = part * kSortTile;
-  const int64_t wbase = base + static_cast<int64_t>(warp) * 32 * kSortItems;
+  const int64_t base = part * kTile;
+  const int64_t wbase = base + static_cast<int64_t>(warp) * 32 * ITEMS;
   SORT_TRACE(part, 0);
 
-  K key[kSortItems];
-  uint32_t val[kSortItems];
-  uint32_t rank[kSortItems];
+  K key[ITEMS];
+  uint32_t val[ITEMS];
+  uint32_t rank[ITEMS];
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const int64_t i = wbase + j * 32 + lane;
     const bool ok = i < n;
     key[j] = ok ? keys_in[i] : static_cast<K>(~static_cast<K>(0));
@@ -342,14 +365,14 @@ __global__ void CGS_SORT_BOUNDS onesweep_kernel(
   {
     uint32_t sink = 0;
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) sink += static_cast<uint32_t>(key[j]) + val[j];
+    for (int j = 0; j < ITEMS; ++j) sink += static_cast<uint32_t>(key[j]) + val[j];
     if (sink == 0x12345678u) g_sort_trace[0] = 0;
     SORT_TRACE(part, 1);
   }
 #endif
   uint32_t* wc = S.wcnt + warp * 256;
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
     const unsigned peers = warp_peers_bits(d, digit_bits);
     const unsigned before = wc[d];
@@ -360,55 +383,59 @@ __global__ void CGS_SORT_BOUNDS onesweep_kernel(
   }
   __syncthreads();
   SORT_TRACE(part, 2);
-  // thread tid owns digit d = tid: exclusive over warps, then over digits
-  const int d = tid;
+  // thread tid < 256 owns digit d = tid: exclusive over warps, then over
+  // digits (whole warps 0-7; the others only pass the barriers)
+  const bool owner = tid < 256;
+  const int d = owner ? tid : 255;
   uint32_t cnt = 0;
+  if (owner) {
 #pragma unroll
-  for (int w = 0; w < kSortWarps; ++w) {
-    const uint32_t c = S.wcnt[w * 256 + d];
-    S.wcnt[w * 256 + d] = cnt;
-    cnt += c;
+    for (int w = 0; w < WARPS; ++w) {
+      const uint32_t c = S.wcnt[w * 256 + d];
+      S.wcnt[w * 256 + d] = cnt;
+      cnt += c;
+    }
   }
   {
-    const uint32_t inc = warp_incl_scan(cnt);
-    if (lane == 31) S.scan_tmp[warp] = inc;
+    const uint32_t inc = owner ? warp_incl_scan(cnt) : 0u;
+    if (owner && lane == 31) S.scan_tmp[warp] = inc;
     __syncthreads();
     uint32_t wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += S.scan_tmp[w];
-    S.dstart[d] = wpre + inc - cnt;
+    for (int w = 0; w < warp && w < 8; ++w) wpre += S.scan_tmp[w];
+    if (owner) S.dstart[d] = wpre + inc - cnt;
   }
   // global digit base = exclusive scan of the pass histogram
-  const uint32_t h = hist[d];
+  const uint32_t h = owner ? hist[d] : 0u;
   uint32_t gbase;
   {
     __syncthreads();
-    const uint32_t inc = warp_incl_scan(h);
-    if (lane == 31) S.scan_tmp[warp] = inc;
+    const uint32_t inc = owner ? warp_incl_scan(h) : 0u;
+    if (owner && lane == 31) S.scan_tmp[warp] = inc;
     __syncthreads();
     uint32_t wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += S.scan_tmp[w];
+    for (int w = 0; w < warp && w < 8; ++w) wpre += S.scan_tmp[w];
     gbase = wpre + inc - h;
   }
   // decoupled lookback for digit d over previous partitions: publish this
   // partition's count first, reorder the tile in shared memory (local ranks
   // only; frees the key / value / rank registers before the lookback window
   // is loaded), then walk back
-  const int64_t tail = base + kSortTile - n;
+  const int64_t tail = base + kTile - n;
   const uint32_t agg = cnt - ((d == 255 && tail > 0) ? static_cast<uint32_t>(tail) : 0u);
   uint32_t excl = 0;
   uint32_t* st = status + part * 256 + d;
-  st_volatile(st, (part == 0 ? kSortPre : kSortAgg) | agg);
+  if (owner) st_volatile(st, (part == 0 ? kSortPre : kSortAgg) | agg);
 #if CGS_SORT_EARLY_SCATTER
   __syncthreads();  // dstart complete
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
     const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
     S.keys[pos] = key[j];
     S.vals[pos] = val[j];
   }
 #endif
-  if (part != 0) {
+  if (owner && part != 0) {
     // Windowed lookback: kLookback independent status loads per round trip,
     // consumed in order until an inclusive prefix is found (an unpublished
     // slot makes the next window start there).  All partitions start
@@ -436,15 +463,21 @@ __global__ void CGS_SORT_BOUNDS onesweep_kernel(
         }
       }
       p -= k;
+#if CGS_SORT_BACKOFF
+      // no progress (the next slot is unpublished): back off before
+      // re-polling, so spinning partitions do not steal issue slots and L2
+      // bandwidth from the ones they wait for
+      if (!done && k == 0) __nanosleep(CGS_SORT_BACKOFF);
+#endif
     }
     st_volatile(st, kSortPre | (excl + agg));
   }
-  S.goff[d] = static_cast<int32_t>(gbase + excl) - static_cast<int32_t>(S.dstart[d]);
+  if (owner) S.goff[d] = static_cast<int32_t>(gbase + excl) - static_cast<int32_t>(S.dstart[d]);
   __syncthreads();
   SORT_TRACE(part, 3);
 #if !CGS_SORT_EARLY_SCATTER
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < ITEMS; ++j) {
     const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
     const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
     S.keys[pos] = key[j];
@@ -452,8 +485,8 @@ __global__ void CGS_SORT_BOUNDS onesweep_kernel(
   }
   __syncthreads();
 #endif
-  const int nvalid = static_cast<int>(n - base < kSortTile ? n - base : kSortTile);
-  for (int i = tid; i < nvalid; i += 256) {
+  const int nvalid = static_cast<int>(n - base < kTile ? n - base : kTile);
+  for (int i = tid; i < nvalid; i += kThreads) {
     const K k = S.keys[i];
     const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & dmask);
     const int64_t o = static_cast<int64_t>(S.goff[dd]) + i;
@@ -483,22 +516,32 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
     CGS_CHECK_LAUNCH("sort_hist_kernel");
   }
   static bool attr_set[kMaxDevices] = {};  // per device ordinal
-  const size_t smem = sizeof(SortSmem<K>);
+  using SmallSmem = SortSmem<K, kSortWarps, kSortItems>;
+  using LargeSmem = SortSmem<K, kSortLargeWarps, kSortLargeItems>;
+  const bool large = sort_large(n_cap);
+  const size_t smem = large ? sizeof(LargeSmem) : sizeof(SmallSmem);
   int dev = 0;
   if (int rc = current_device(&dev)) return rc;
   if (!attr_set[dev]) {
-    CGS_CUDA(cudaFuncSetAttribute(onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    CGS_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, kSortWarps, kSortItems>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(SmallSmem))));
+    CGS_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, kSortLargeWarps, kSortLargeItems>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(LargeSmem))));
     attr_set[dev] = true;
   }
   K* kin = keys;
   uint32_t* vin = vals;
   K* kout = ws.keys_alt;
   uint32_t* vout = ws.vals_alt;
-  const unsigned grid = static_cast<unsigned>(ceil_div(n_cap > 0 ? n_cap : 1, kSortTile));
+  const unsigned grid = static_cast<unsigned>(ceil_div(n_cap > 0 ? n_cap : 1, sort_tile_for(n_cap)));
+  auto kern = large ? onesweep_kernel<K, kSortLargeWarps, kSortLargeItems>
+                    : onesweep_kernel<K, kSortWarps, kSortItems>;
+  const int threads = large ? kSortLargeWarps * 32 : kSortThreads;
   for (int p = 0; p < passes; ++p) {
     const int dbits = key_bits - 8 * p < 8 ? key_bits - 8 * p : 8;
-    CGS_PROFILED("onesweep_kernel", st, onesweep_kernel<K><<<grid, 256, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p, dbits,
+    CGS_PROFILED("onesweep_kernel", st, kern<<<grid, threads, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, 8 * p, dbits,
                                                 ws.hist + p * 256,
                                                 ws.status + static_cast<size_t>(p) * ws.max_parts * 256,
                                                 ws.counter + p));
