@@ -340,6 +340,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
   SortSmem<K, WARPS, ITEMS>& S = *reinterpret_cast<SortSmem<K, WARPS, ITEMS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned dmask = (1u << digit_bits) - 1u;  // only the low key_bits are sorted on
+  auto digit_of = [&](K k) -> unsigned {
+    if constexpr (sizeof(K) <= 4) return (static_cast<uint32_t>(k) >> shift) & dmask;
+    else return static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & dmask);
+  };
   if (tid == 0) S.part = atomicAdd(counter, 1u);
   for (int i = tid; i < WARPS * 256; i += kThreads) S.wcnt[i] = 0;
   __syncthreads();
@@ -371,16 +375,25 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
   }
 #endif
   uint32_t* wc = S.wcnt + warp * 256;
+  // ranking within the warp, in item order; the full-byte case (every pass
+  // but a narrow last one) has its 8 ballots unrolled without the per-bit
+  // width test
+  auto rank_all = [&](auto peers_of) {
 #pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const unsigned d = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
-    const unsigned peers = warp_peers_bits(d, digit_bits);
-    const unsigned before = wc[d];
-    rank[j] = before + __popc(peers & lanemask_lt());
-    __syncwarp();
-    if (lane == __ffs(peers) - 1) wc[d] = before + __popc(peers);
-    __syncwarp();
-  }
+    for (int j = 0; j < ITEMS; ++j) {
+      const unsigned d = digit_of(key[j]);
+      const unsigned peers = peers_of(d);
+      const unsigned before = wc[d];
+      rank[j] = before + __popc(peers & lanemask_lt());
+      __syncwarp();
+      if (lane == __ffs(peers) - 1) wc[d] = before + __popc(peers);
+      __syncwarp();
+    }
+  };
+  if (digit_bits == 8)
+    rank_all([](unsigned d) { return warp_peers8(d); });
+  else
+    rank_all([&](unsigned d) { return warp_peers_bits(d, digit_bits); });
   __syncthreads();
   SORT_TRACE(part, 2);
   // thread tid < 256 owns digit d = tid: exclusive over warps, then over
@@ -429,7 +442,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
   __syncthreads();  // dstart complete
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
-    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
+    const unsigned dd = digit_of(key[j]);
     const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
     S.keys[pos] = key[j];
     S.vals[pos] = val[j];
@@ -478,7 +491,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
 #if !CGS_SORT_EARLY_SCATTER
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
-    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(key[j]) >> shift) & dmask);
+    const unsigned dd = digit_of(key[j]);
     const uint32_t pos = S.dstart[dd] + wc[dd] + rank[j];
     S.keys[pos] = key[j];
     S.vals[pos] = val[j];
@@ -488,7 +501,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
   const int nvalid = static_cast<int>(n - base < kTile ? n - base : kTile);
   for (int i = tid; i < nvalid; i += kThreads) {
     const K k = S.keys[i];
-    const unsigned dd = static_cast<unsigned>((static_cast<uint64_t>(k) >> shift) & dmask);
+    const unsigned dd = digit_of(k);
     const int64_t o = static_cast<int64_t>(S.goff[dd]) + i;
     keys_out[o] = k;
     vals_out[o] = S.vals[i];
