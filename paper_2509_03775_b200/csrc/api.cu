@@ -641,6 +641,7 @@ struct CopyScanOp {
   uint32_t* out;
   __device__ uint64_t load(int64_t i) const { return in[i]; }
   __device__ void store(int64_t i, uint64_t ex, uint64_t) const { out[i] = static_cast<uint32_t>(ex); }
+  __device__ void finish(uint64_t) const {}
 };
 
 template <typename K>

@@ -376,16 +376,24 @@ int recon_loss(const float* img, const float* gt, int nv, int H, int W, double l
   CGS_CHECK_LAUNCH("ssim_stats_kernel");
   const double inv_size = 1.0 / (3.0 * H * W);
   const double inv_count = has_ssim ? 1.0 / (3.0 * (H - 10.0) * (W - 10.0)) : 0.0;
-  if (dL) {
-    CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, sizeof(GradSmem), st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
-                                           (has_ssim && lam != 0.0) ? 1 : 0, L, dL, win));
-    CGS_CHECK_LAUNCH("ssim_grad_kernel");
-  }
   const int64_t nb = static_cast<int64_t>(blocks_x(W)) * blocks_y(H) * 3;
-  loss_final_kernel<<<nv, 256, 0, st>>>(L, nb, lam, inv_size, inv_count, has_ssim ? 1 : 0,
-                                        losses);
+  if (!dL) {
+    loss_final_kernel<<<nv, 256, 0, st>>>(L, nb, lam, inv_size, inv_count, has_ssim ? 1 : 0,
+                                          losses);
+    CGS_CHECK_LAUNCH("loss_final_kernel");
+    return CGS_OK;
+  }
+  // the loss values (reporting only) beside the image gradient, on a side
+  // stream: both read only ssim_stats' output
+  SideFork fork(st);
+  if (fork.rc) return fork.rc;
+  loss_final_kernel<<<nv, 256, 0, fork.side>>>(L, nb, lam, inv_size, inv_count, has_ssim ? 1 : 0,
+                                               losses);
   CGS_CHECK_LAUNCH("loss_final_kernel");
-  return CGS_OK;
+  CGS_PROFILED("ssim_grad_kernel", st, ssim_grad_kernel<<<grid, 256, sizeof(GradSmem), st>>>(img, gt, H, W, lam, inv_size, inv_count, gscale,
+                                         (has_ssim && lam != 0.0) ? 1 : 0, L, dL, win));
+  CGS_CHECK_LAUNCH("ssim_grad_kernel");
+  return fork.join();
 }
 
 }  // namespace cgs

@@ -693,6 +693,7 @@ struct CsrOffsets {
   int32_t* off;
   __device__ uint64_t load(int64_t r) const { return counts[r]; }
   __device__ void store(int64_t r, uint64_t ex, uint64_t) const { off[r] = static_cast<int32_t>(ex); }
+  __device__ void finish(uint64_t) const {}
 };
 
 int build_code_csr(const int32_t* idx, int64_t n, int64_t cap, int32_t* off, int32_t* mem,

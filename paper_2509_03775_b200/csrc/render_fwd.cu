@@ -364,26 +364,28 @@ struct PairOffsets {
   const uint32_t* n_tiles;
   uint64_t* off;
   uint64_t* off_rank;
+  FrameHeader* hdr;
+  int64_t pair_cap;
+  int n_views;
   __device__ uint64_t load(int64_t r) const { return n_tiles[perm[r]]; }
   __device__ void store(int64_t r, uint64_t ex, uint64_t v) const {
     off_rank[r] = ex;
     if (v) off[perm[r]] = ex;
   }
+  // pair total -> frame counts and the overflow flag (the rest of the
+  // frame reads these)
+  __device__ void finish(uint64_t raw) const {
+    const bool over = raw > static_cast<unsigned long long>(pair_cap);
+    hdr->n_pairs_raw = raw;
+    hdr->n_pairs = over ? 0ULL : raw;
+    hdr->stats.n_onscreen = static_cast<int64_t>(hdr->n_onscreen);
+    hdr->stats.n_pairs = static_cast<int64_t>(raw);
+    hdr->stats.overflow = over ? 1 : 0;
+    hdr->stats.pair_capacity = pair_cap;
+    hdr->stats.n_views = n_views;
+  }
 };
 
-// hist_top: the depth sort's histogram of the key's top byte; splats without
-// tiles carry key ~0, so their count is hist_top[255].
-__global__ void finalize_counts_kernel(FrameHeader* hdr, int64_t pair_cap, int n_views) {
-  const unsigned long long raw = hdr->scratch[0];
-  hdr->n_pairs_raw = raw;
-  const bool over = raw > static_cast<unsigned long long>(pair_cap);
-  hdr->n_pairs = over ? 0ULL : raw;
-  hdr->stats.n_onscreen = static_cast<int64_t>(hdr->n_onscreen);
-  hdr->stats.n_pairs = static_cast<int64_t>(raw);
-  hdr->stats.overflow = over ? 1 : 0;
-  hdr->stats.pair_capacity = pair_cap;
-  hdr->stats.n_views = n_views;
-}
 
 // Warp-cooperative pair emission in depth order: a warp takes 32
 // consecutive depth ranks and writes the pairs of those with at most
@@ -702,11 +704,9 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
     perm = depth_perm(L);
   }
-  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.off_rank}, &L.hdr->n_onscreen, vn,
+  int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.off_rank, L.hdr, L.pair_cap, fd.n_views}, &L.hdr->n_onscreen, vn,
                        vn, L.scan, &L.hdr->scratch[0], st);
   if (rc) return rc;
-  finalize_counts_kernel<<<1, 1, 0, st>>>(L.hdr, L.pair_cap, fd.n_views);
-  CGS_CHECK_LAUNCH("finalize_counts_kernel");
   return CGS_OK;
 }
 

@@ -84,6 +84,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Exclusive scan.  Op provides:
 //   __device__ uint64_t load(int64_t i) const;
 //   __device__ void store(int64_t i, uint64_t exclusive, uint64_t value) const;
+//   __device__ void finish(uint64_t total) const;  (called once, with the total)
 // Partitions of 8 warps x 8 rounds x 32 lanes; within a warp every round is
 // 32 consecutive elements (coalesced), so the running sum follows index
 // order.  Status words: value in bits 0..61, flag in 62..63.
@@ -174,7 +175,10 @@ __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long lo
     }
     if (lane == 0) {
       s_prefix = excl;
-      if (part == nparts - 1 && total) *total = excl + agg;
+      if (part == nparts - 1) {
+        if (total) *total = excl + agg;
+        op.finish(excl + agg);  // the scan's total, once (the last partition)
+      }
     }
   }
   __syncthreads();

@@ -266,6 +266,7 @@ struct EligibleOp {
   __device__ void store(int64_t i, uint64_t ex, uint64_t v) const {
     if (v) out[ex] = static_cast<int32_t>(i);
   }
+  __device__ void finish(uint64_t) const {}
 };
 
 __global__ void copy_count_kernel(const unsigned long long* src, int64_t* dst) {
@@ -367,6 +368,7 @@ struct OpacScan {
     return static_cast<uint64_t>(o * kOpacFix);
   }
   __device__ void store(int64_t i, uint64_t ex, uint64_t v) const { incl[i] = ex + v; }
+  __device__ void finish(uint64_t) const {}
 };
 
 __global__ void densify_select_kernel(const uint64_t* __restrict__ incl, int64_t n,
