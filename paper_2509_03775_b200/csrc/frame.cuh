@@ -49,6 +49,7 @@ struct FrameLayout {
   uint64_t* rect;          // V*N packed tile rect
   uint64_t* pair_off;      // V*N per splat: first emission index of its pairs
   uint64_t* off_rank;      // the same by depth rank (N_s; the emission reads it coalesced)
+  uint32_t* tie_runs;      // starts of equal-depth-key runs longer than 256 (count: hdr->scratch[1])
   void* pkeys;             // pair_cap tile keys (u16 or u32)
   uint32_t* pvals;         // pair_cap splat ids
   SortWs<uint16_t> psort16;
@@ -148,6 +149,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.rect = c.take<uint64_t>(vn1);
   L.pair_off = c.take<uint64_t>(vn1);
   L.off_rank = c.take<uint64_t>(vn1);
+  L.tie_runs = c.take<uint32_t>(vn1 / 256 + 16);
   if (L.tile_key_bytes == 2) {
     L.pkeys = c.take<uint16_t>(pc);
     L.psort16 = carve_sort<uint16_t>(c, pc);

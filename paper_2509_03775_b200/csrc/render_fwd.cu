@@ -14,6 +14,7 @@
 //                   sort by tile id: the per-tile append order of _bin_tiles
 //                   (render.py:240-254)
 //   raster_fwd      raster.cu
+#include <atomic>
 #include <cmath>
 
 #include "frame.cuh"
@@ -328,12 +329,19 @@ __global__ void __launch_bounds__(256, CGS_PROJECT_MINB) project_kernel(ProjIn i
 // reference's lexsort((idx, tz)) (render.py:203) whatever order the keys were
 // appended in; every other element is copied.  Runs are short (a few splats:
 // the 24-bit key resolves depth to 2^-19 relative), and one thread per
-// element keeps a long run parallel.
+// element keeps a run parallel.  An element never scans further than
+// kTieDirect either way: a longer run (many splats at one depth, e.g. a
+// fronto-parallel plane) is listed by its first element and sorted by
+// depth_tie_long_kernel instead.
+constexpr int kTieDirect = 256;
+constexpr int kTieSmem = 8192;  // longest run sorted in shared memory (bitonic)
 __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __restrict__ key,
                                                             const uint32_t* __restrict__ val,
                                                             uint32_t* __restrict__ out,
                                                             const uint64_t* __restrict__ depth_key,
-                                                            const unsigned long long* __restrict__ n_dev) {
+                                                            const unsigned long long* __restrict__ n_dev,
+                                                            uint32_t* __restrict__ long_runs,
+                                                            unsigned long long* __restrict__ n_long) {
   const int64_t vn = static_cast<int64_t>(*n_dev);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < vn;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -345,8 +353,12 @@ __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __re
       continue;
     }
     int64_t s = i, e = i + 1;
-    while (s > 0 && key[s - 1] == k) --s;
-    while (e < vn && key[e] == k) ++e;
+    while (s > 0 && key[s - 1] == k && i - s <= kTieDirect) --s;
+    while (e < vn && key[e] == k && e - i <= kTieDirect) ++e;
+    if (e - s > kTieDirect) {  // a long run: its first element lists it
+      if (!left) long_runs[atomicAdd(n_long, 1ull)] = static_cast<uint32_t>(i);
+      continue;
+    }
     const uint64_t di = depth_key[vi];
     int64_t r = 0;
     for (int64_t j = s; j < e; ++j) {
@@ -355,6 +367,98 @@ __global__ void __launch_bounds__(256) depth_tie_fix_kernel(const uint32_t* __re
       r += (dj < di || (dj == di && vj < vi)) ? 1 : 0;
     }
     out[s + r] = vi;
+  }
+}
+
+// One CTA per long run (depth_tie_fix_kernel's list): (fp64 depth bits, id)
+// pairs bitonic-sorted in shared memory for runs up to kTieSmem; a longer run
+// falls back to the per-element rank (quadratic in its length, but correct).
+__global__ void __launch_bounds__(1024) depth_tie_long_kernel(const uint32_t* __restrict__ key,
+                                                              const uint32_t* __restrict__ val,
+                                                              uint32_t* __restrict__ out,
+                                                              const uint64_t* __restrict__ depth_key,
+                                                              const unsigned long long* __restrict__ n_dev,
+                                                              const uint32_t* __restrict__ long_runs,
+                                                              const unsigned long long* __restrict__ n_long) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kTieSmem);
+  __shared__ int s_more;
+  const int64_t vn = static_cast<int64_t>(*n_dev);
+  const int64_t nl = static_cast<int64_t>(*n_long);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t q = blockIdx.x; q < nl; q += gridDim.x) {
+    const int64_t s = long_runs[q];
+    const uint32_t k = key[s];
+    // run end: advance a CTA-wide window until an element differs
+    int64_t e = s;
+    for (;;) {
+      const int64_t j = e + tid;
+      const bool same = j < vn && key[j] == k;
+      const int all = __syncthreads_and(same);
+      if (all) {
+        e += nt;
+        continue;
+      }
+      // first differing position in this window
+      if (tid == 0) s_more = nt;
+      __syncthreads();
+      if (!same) atomicMin(&s_more, tid);
+      __syncthreads();
+      e += s_more;
+      __syncthreads();
+      break;
+    }
+    const int64_t L = e - s;
+    if (L <= kTieSmem) {
+      int P = 1;
+      while (P < L) P <<= 1;
+      for (int t = tid; t < P; t += nt) {
+        if (t < L) {
+          const uint32_t v = val[s + t];
+          sv[t] = v;
+          sk[t] = depth_key[v];
+        } else {
+          sv[t] = 0xffffffffu;
+          sk[t] = ~0ull;
+        }
+      }
+      __syncthreads();
+      for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int t = tid; t < P; t += nt) {
+            const int o = t ^ stride;
+            if (o > t) {
+              const bool up = (t & size) == 0;
+              const bool gt = sk[t] > sk[o] || (sk[t] == sk[o] && sv[t] > sv[o]);
+              if (gt == up) {
+                const uint64_t tk = sk[t];
+                sk[t] = sk[o];
+                sk[o] = tk;
+                const uint32_t tv = sv[t];
+                sv[t] = sv[o];
+                sv[o] = tv;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int t = tid; t < L; t += nt) out[s + t] = sv[t];
+      __syncthreads();
+    } else {
+      for (int64_t i = s + tid; i < e; i += nt) {
+        const uint32_t vi = val[i];
+        const uint64_t di = depth_key[vi];
+        int64_t r = 0;
+        for (int64_t j = s; j < e; ++j) {
+          const uint32_t vj = val[j];
+          const uint64_t dj = depth_key[vj];
+          r += (dj < di || (dj == di && vj < vi)) ? 1 : 0;
+        }
+        out[s + r] = vi;
+      }
+    }
   }
 }
 
@@ -700,8 +804,24 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     }
     CGS_PROFILED("depth_tie_fix_kernel", st,
                  depth_tie_fix_kernel<<<grid_for(vn, 256, 8), 256, 0, st>>>(
-                     kres, perm, L.dval, L.depth_key, &L.hdr->n_onscreen));
+                     kres, perm, L.dval, L.depth_key, &L.hdr->n_onscreen, L.tie_runs,
+                     &L.hdr->scratch[1]));
     CGS_CHECK_LAUNCH("depth_tie_fix_kernel");
+    {  // long runs (none in a typical frame: the kernel returns at once)
+      constexpr size_t smem = kTieSmem * (sizeof(uint64_t) + sizeof(uint32_t));
+      static std::atomic<bool> attr[kMaxDevices] = {};
+      int dev = 0;
+      if (int e = current_device(&dev)) return e;
+      if (!attr[dev].load()) {
+        CGS_CUDA(cudaFuncSetAttribute(depth_tie_long_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr[dev].store(true);
+      }
+      depth_tie_long_kernel<<<148, 1024, smem, st>>>(kres, perm, L.dval, L.depth_key,
+                                                     &L.hdr->n_onscreen, L.tie_runs,
+                                                     &L.hdr->scratch[1]);
+      CGS_CHECK_LAUNCH("depth_tie_long_kernel");
+    }
     perm = depth_perm(L);
   }
   int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.off_rank, L.hdr, L.pair_cap, fd.n_views}, &L.hdr->n_onscreen, vn,

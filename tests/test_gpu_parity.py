@@ -360,6 +360,51 @@ def _config1_view0():
     return (a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows, a.cameras[0])
 
 
+def _plane_scene(n, seed=5):
+    """n splats on the plane z = 0 seen by an axis-aligned camera: every splat
+    has exactly the same fp64 depth, so the depth order inside each tile is
+    the Gaussian index alone -- one run of n equal depth keys (the long-run
+    path of the depth tie fix: shared-memory bitonic sort up to 8192, the
+    per-element rank beyond)."""
+    from paper_2509_03775_b200 import camera, scenes
+    a = scenes.config0(seed)
+    rng = np.random.default_rng(seed)
+    side = 96
+    cam = camera.Camera(rotation=np.eye(3), translation=np.array([0.0, 0.0, 4.0]), fx=96.0,
+                        fy=96.0, cx=side / 2, cy=side / 2, width=side, height=side)
+    pos = np.zeros((n, 3), np.float32)
+    pos[:, :2] = rng.uniform(-1.6, 1.6, size=(n, 2))
+    perm = rng.permutation(n)  # index order unrelated to position
+    pos = pos[perm]
+    idx = rng.integers(0, a.sr_rows.shape[0], n).astype(np.int32)
+    logit = rng.normal(-2.0, 0.5, n).astype(np.float32)
+    return pos, logit, idx, idx, a.sh_rows, a.sr_rows, cam
+
+
+@pytest.mark.parametrize("n", [2000, 12000])
+def test_equal_depth_plane_order_bit_exact(cg, n):
+    """A run of n splats at one exact depth (longer than the per-element tie
+    fix handles): tile lists and per-tile order equal the oracle's (index
+    order), and the image matches."""
+    from oracle import cgs_oracle as O
+    pos, logit, g2sh, g2sr, sh, sr, cam = _plane_scene(n)
+    st = cg.ModelState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    fr = cg.render_frame(st, [cam])
+    offs, ids = fr.tile_lists()
+    ost = O.OState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    ocam = O.cam_from_any(cam)
+    proj = O.project(ost, ocam)
+    assert len(np.unique(proj["t"][:, 2])) == 1  # one exact depth
+    roffs, members = O.bin_tiles(proj, ocam)
+    rids = proj["idx"][proj["order"][members]]
+    assert np.array_equal(offs, roffs)
+    assert np.array_equal(ids, rids)
+    ref = O.raster_forward(ost, ocam)
+    img = fr.image.view(cam.height, cam.width, 3).cpu().numpy()
+    assert np.allclose(img, ref["image"], rtol=RTOL, atol=ATOL)
+    assert np.array_equal(fr.counts.view(cam.height, cam.width).cpu().numpy(), ref["counts"])
+
+
 @pytest.mark.parametrize("make", [_crowded_scene, _config1_view0], ids=["crowded", "config1"])
 def test_full_size_tile_lists_bit_exact(cg, make):
     """Tile lists (binning + per-tile fp64 depth order) at full size vs the oracle's
