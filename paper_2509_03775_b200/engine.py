@@ -130,8 +130,11 @@ class Trainer:
             if self._pairs_per_gaussian is None:
                 probe = Frame(st, self.cams).run_checked()
                 self._pairs_per_gaussian = probe.stats().n_pairs / max(st.num_gaussians, 1)
-            # pairs grow with N (densify): rescale, never shrink
-            cap = int(self._pairs_per_gaussian * st.num_gaussians * self.headroom) + 4096
+            # pairs grow with N (densify): sized for the Gaussian capacity, so
+            # densify inside it keeps every buffer (a GB-scale reallocation
+            # costs tens of milliseconds); never shrinks
+            ncap = max(st.gaussians.capacity, st.num_gaussians)
+            cap = int(self._pairs_per_gaussian * ncap * self.headroom) + 4096
             self.pair_cap = max(self.pair_cap or 0, cap)
             self._capacity_buffers()
             self.frame = Frame(st, self.cams, pair_capacity=self.pair_cap, ws=self._frame_ws)
