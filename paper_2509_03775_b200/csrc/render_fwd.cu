@@ -3,13 +3,14 @@
 //   sr_precompute   Sigma3 per SR codebook row (render.py:85-91, 168-169)
 //   project         per (view, Gaussian): fp64 EWA projection, codebook gather,
 //                   SH colour, pixel/tile rect, depth keys (render.py:145-203,110-115)
-//   depth order     all splats of the frame, one stable LSD onesweep on the
-//                   fp32-rounded-toward-zero depth (monotone in the fp64 depth),
-//                   input in splat index order; runs of equal 32-bit keys are
-//                   re-sorted by the exact fp64 depth (stable insertion sort).
+//   depth order     the splats with tiles (compacted by the projection), one
+//                   3-pass LSD onesweep on a 24-bit key (fp32 depth bits above
+//                   the near plane, monotone in the fp64 depth); runs of equal
+//                   keys are re-ordered by (fp64 depth, splat id)
 //                   = np.lexsort((idx, tz)) (render.py:203), per view
 //   pair offsets    one decoupled-lookback scan over the splats' tile counts in
-//                   depth order
+//                   depth order (per splat and per depth rank; the last
+//                   partition writes the frame counts)
 //   emit + sort     (tile, splat) pairs in depth order, stable onesweep radix
 //                   sort by tile id: the per-tile append order of _bin_tiles
 //                   (render.py:240-254)
