@@ -55,10 +55,21 @@ constexpr int kLT = 32;            // outputs per CTA side
 constexpr int kLH = kLT + 10;      // halo side (42)
 constexpr int kLP = kLH + 1;       // padded smem row (floats)
 
+// The five windowed moments are filtered in fp32 on values shifted by 0.5:
+// x' = x - 0.5 keeps |x'| <= ~0.5, so the variance m2 - m0^2 and covariance
+// m4 - m0 m1 carry an absolute fp32 error of ~1e-8, far below C2 = 9e-4 that
+// every SSIM denominator adds (the SSIM value moves by ~1e-9 relative; the
+// per-window SSIM and its seeds are then formed in fp64).  The seeds are the
+// derivatives with respect to the shifted moments (m0, m2, m4): the adjoint
+// sum  F(d0) + 2 x' F(d2) + y' F(d4)  then has less cancellation than the
+// unshifted form.  Max elementwise deviation of the SSIM image gradient from
+// the float64 reference on the golden cases: 3.8e-5 relative (3.1e-5 with
+// fp64 moments and fp32 unshifted seeds).
+constexpr float kSsimShift = 0.5f;
 struct StatsSmem {
   float sa[kLH][kLP];
   float sb[kLH][kLP];
-  double hm[5][kLH][kLT];
+  float hm[5][kLH][kLT + 1];
   double red_s[8], red_l[8];
 };
 
@@ -69,7 +80,7 @@ struct GradSmem {
 
 // grid: (ceil(W/32), ceil(H/32), view*3 + channel); block 256.
 #ifndef CGS_SSIM_MINB
-#define CGS_SSIM_MINB 3
+#define CGS_SSIM_MINB 4
 #endif
 __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const float* __restrict__ img,
                                                          const float* __restrict__ gt, int H, int W,
@@ -107,8 +118,8 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
       la[q] = lb[q] = 0.0f;
       if (e < kLH * kLH && gx < W && gy < H) {
         const int64_t o = (static_cast<int64_t>(gy) * W + gx) * 3 + ch;
-        la[q] = __ldg(A + o);
-        lb[q] = __ldg(Bm + o);
+        la[q] = __ldg(A + o) - kSsimShift;
+        lb[q] = __ldg(Bm + o) - kSsimShift;
       }
     }
 #pragma unroll
@@ -124,7 +135,7 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
     // horizontal: 42 rows x 8 segments of 4 outputs
     for (int it = tid; it < kLH * 8; it += 256) {
       const int row = it >> 3, c0 = (it & 7) * 4;
-      double av[14], bv[14];
+      float av[14], bv[14];
 #pragma unroll
       for (int i = 0; i < 14; ++i) {
         av[i] = S.sa[row][c0 + i];
@@ -132,11 +143,12 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
       }
 #pragma unroll
       for (int o = 0; o < 4; ++o) {
-        double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+        float m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
 #pragma unroll
         for (int j = 0; j < 11; ++j) {
-          const double a = av[o + j], b = bv[o + j], k = win.k[j];
-          m0 += k * a; m1 += k * b; m2 += k * a * a; m3 += k * b * b; m4 += k * a * b;
+          const float a = av[o + j], b = bv[o + j], k = static_cast<float>(win.k[j]);
+          const float ka = k * a, kb = k * b;
+          m0 += ka; m1 += kb; m2 = fmaf(ka, a, m2); m3 = fmaf(kb, b, m3); m4 = fmaf(ka, b, m4);
         }
         S.hm[0][row][c0 + o] = m0; S.hm[1][row][c0 + o] = m1; S.hm[2][row][c0 + o] = m2;
         S.hm[3][row][c0 + o] = m3; S.hm[4][row][c0 + o] = m4;
@@ -145,17 +157,17 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
     __syncthreads();
     // vertical: 32 columns x 8 segments of 4 outputs (one item per thread)
     const int col = tid & 31, r0 = (tid >> 5) * 4;
-    double m[5][4];
+    float m[5][4];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
-      double hv[14];
+      float hv[14];
 #pragma unroll
       for (int i = 0; i < 14; ++i) hv[i] = S.hm[q][r0 + i][col];
 #pragma unroll
       for (int o = 0; o < 4; ++o) {
-        double acc = 0.0;
+        float acc = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 11; ++j) acc += win.k[j] * hv[o + j];
+        for (int j = 0; j < 11; ++j) acc = fmaf(static_cast<float>(win.k[j]), hv[o + j], acc);
         m[q][o] = acc;
       }
     }
@@ -166,17 +178,23 @@ __global__ void __launch_bounds__(256, CGS_SSIM_MINB) ssim_stats_kernel(const fl
     for (int o = 0; o < 4; ++o) {
       const int uy = y0 + r0 + o;
       if (ux >= Wv || uy >= Hv) continue;
-      const double mx = m[0][o], my = m[1][o];
-      const double vx = m[2][o] - mx * mx, vy = m[3][o] - my * my, cxy = m[4][o] - mx * my;
+      // shifted moments m0..m4 -> means, (co)variances (shift-invariant)
+      const double m0 = m[0][o], m1 = m[1][o];
+      const double vx = m[2][o] - m0 * m0, vy = m[3][o] - m1 * m1, cxy = m[4][o] - m0 * m1;
+      const double mx = m0 + kSsimShift, my = m1 + kSsimShift;
       const double C1 = 1e-4, C2 = 9e-4;
       const double A1 = 2 * mx * my + C1, A2 = 2 * cxy + C2;
       const double B1 = mx * mx + my * my + C1, B2 = vx + vy + C2;
       const double F = 1.0 / (B1 * B2);
       const double sv = A1 * A2 * F;
       s_acc += sv;
-      const double d_mx = 2 * my * F * (A2 - A1) - 2 * mx * sv * (1.0 / B1 - 1.0 / B2);
-      const double d_ex2 = -sv / B2;
-      const double d_exy = 2 * A1 * F;
+      // seeds: dS/dm0, dS/dm2, dS/dm4 (metrics.py:96-109 in the shifted
+      // variables: dS/dmu_x - 2 m0 dS/dvar_x - m1 dS/dcov, dS/dvar_x, dS/dcov)
+      const double d_var = -sv / B2;
+      const double d_cov = 2 * A1 * F;
+      const double d_mx = sv * (2 * my / A1 - 2 * mx / B1) - 2 * m0 * d_var - m1 * d_cov;
+      const double d_ex2 = d_var;
+      const double d_exy = d_cov;
       const int64_t pos = static_cast<int64_t>(uy) * Wv + ux;
       sd[pos] = static_cast<float>(d_mx);
       sd[vn + pos] = static_cast<float>(d_ex2);
@@ -293,7 +311,8 @@ __global__ void __launch_bounds__(256, CGS_SSIMG_MINB) ssim_grad_kernel(const fl
     const int64_t off = (static_cast<int64_t>(py) * W + px) * 3 + ch;
     const double a = A[off], b = Bm[off];
     double gs = 0.0;
-    if (ssim_on) gs = (r[0][o] + 2.0 * a * r[1][o] + b * r[2][o]) * inv_count;
+    if (ssim_on)  // adjoint in the shifted variables (the stats kernel's seeds)
+      gs = (r[0][o] + 2.0 * (a - kSsimShift) * r[1][o] + (b - kSsimShift) * r[2][o]) * inv_count;
     const double sgn = a > b ? 1.0 : (a < b ? -1.0 : 0.0);
     double g = (1.0 - lam) * sgn * inv_size;
     if (lam != 0.0) g -= lam * gs;
