@@ -331,6 +331,18 @@ CGS_API int cgs_split_eligible(const int32_t* idx, int64_t n, const int32_t* ref
                        int32_t* eligible, int64_t* count, void* workspace,
                        size_t workspace_bytes, cgs_stream_t stream);
 
+/* Split proposals on the device (throughput trainer, device-noise mode; the
+ * reference-parity path draws on the host, cgs_host_split_decide): for each
+ * candidate c, u[c] = eps_split * N(0, I_dim) and a uniform from Philox
+ * (seed, counter, c); prob[c] = exp(min(0, -lam - log q)), log q =
+ * -0.5 |u|^2 c_q [+ corr] (sampler.py:138-164); accept[c] = uniform <
+ * prob[c].  Refcount skips (sampler.py:350-351) are the caller's.  u: (n_cand,
+ * dim) f64, prob f64, accept i8, all device. */
+CGS_API int cgs_split_propose(int64_t n_cand, int32_t dim, double eps_split, double c_q,
+                              int32_t use_corr, double corr, double lam, uint64_t seed,
+                              uint64_t counter, double* u, double* prob, int8_t* accept,
+                              cgs_stream_t stream);
+
 /* Accepted splits in proposal order (sampler.py:202-209): for each j,
  * rows[new_row[j]] = f32(f64(rows[old_row[j]]) + u[j]) and idx[gauss[j]] =
  * new_row[j].  u: (k, dim) f64. */

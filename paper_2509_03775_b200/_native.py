@@ -79,6 +79,7 @@ I64 = ctypes.c_int64
 SZ = ctypes.c_size_t
 F32 = ctypes.c_float
 F64 = ctypes.c_double
+U64 = ctypes.c_uint64
 CAMP = ctypes.POINTER(CCamera)
 SCNP = ctypes.POINTER(CScene)
 
@@ -120,6 +121,7 @@ SIGNATURES = {
     "cgs_host_split_decide": (I32, [P, P, I64, P, P, I64, I32, F64, F64, F64, I32, F64, P, P, P, P,
                                     P]),
     "cgs_apply_splits": (I32, [P, I32, P, P, P, P, P, I64, P]),
+    "cgs_split_propose": (I32, [I64, I32, F64, F64, I32, F64, F64, U64, U64, P, P, P, P]),
     "cgs_apply_remap": (I32, [P, I64, P, I64, P]),
     "cgs_densify_append": (I32, [P, P, P, P, I64, P, P, I64, P]),
     "cgs_densify_select_workspace_bytes": (SZ, [I64]),

@@ -149,6 +149,9 @@ int split_eligible(const int32_t* idx, int64_t n, const int32_t* rc, int32_t* ou
                    void* ws, size_t ws_bytes, cudaStream_t st);
 int apply_splits(float* rows, int dim, int32_t* idx, const int64_t* gauss, const int32_t* old_row,
                  const int32_t* new_row, const double* u, int64_t k, cudaStream_t st);
+int split_propose(int64_t n_cand, int dim, double es, double c_q, int use_corr, double corr,
+                  double lam, uint64_t seed, uint64_t ctr, double* u, double* prob, int8_t* accept,
+                  cudaStream_t st);
 int apply_remap(int32_t* idx, int64_t n, const int32_t* remap, int64_t len, cudaStream_t st);
 int densify_append(float* pos, float* logit, int32_t* g2sh, int32_t* g2sr, int64_t n,
                    const int64_t* src, const double* jit, int64_t k, cudaStream_t st);
@@ -596,6 +599,17 @@ int cgs_split_eligible(const int32_t* idx, int64_t n, const int32_t* refcount, i
                        cgs_stream_t stream) {
   return split_eligible(idx, n, refcount, eligible, count, workspace, workspace_bytes,
                         static_cast<cudaStream_t>(stream));
+}
+
+int cgs_split_propose(int64_t n_cand, int32_t dim, double eps_split, double c_q, int32_t use_corr,
+                      double corr, double lam, uint64_t seed, uint64_t counter, double* u,
+                      double* prob, int8_t* accept, cgs_stream_t stream) {
+  if (n_cand < 0 || dim < 1 || (n_cand > 0 && (!u || !prob || !accept))) {
+    set_error("split_propose: invalid arguments");
+    return CGS_EINVAL;
+  }
+  return split_propose(n_cand, dim, eps_split, c_q, use_corr, corr, lam, seed, counter, u, prob,
+                       accept, static_cast<cudaStream_t>(stream));
 }
 
 int cgs_apply_splits(float* rows, int32_t dim, int32_t* idx, const int64_t* gauss,

@@ -302,6 +302,52 @@ __global__ void apply_splits_kernel(float* rows, int dim, int32_t* idx, const in
   }
 }
 
+// Split proposals drawn on the device (the throughput trainer's device-noise
+// mode; the reference-parity path keeps numpy's stream on the host,
+// mcmc_host.cu): per candidate c, u = eps_split * N(0, I_dim) and a uniform
+// from counter-based Philox (seed, ctr, c), log A = -lam - log q with log q =
+// -0.5 |u|^2 c_q [+ corr] (sampler.py:138-164), accept = uniform < exp(min(0,
+// log A)).  The refcount-dependent skips are settled on the host afterwards
+// (they do not change the draws here: each candidate has its own counters).
+__global__ void __launch_bounds__(256) split_propose_kernel(int64_t n_cand, int dim, double es,
+                                                            double c_q, int use_corr, double corr,
+                                                            double lam, uint64_t seed,
+                                                            uint64_t ctr, double* __restrict__ u,
+                                                            double* __restrict__ prob,
+                                                            int8_t* __restrict__ accept) {
+  for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < n_cand;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double u2 = 0.0;
+    for (int j = 0; j < dim; ++j) {
+      const double z = __dmul_rn(es, philox_normal(seed, ctr, 4, static_cast<uint64_t>(c) * dim + j));
+      u[c * dim + j] = z;
+      u2 = __fma_rn(z, z, u2);
+    }
+    double log_q = -0.5 * u2 * c_q;
+    if (use_corr) log_q += corr;
+    const double log_a = -lam - log_q;
+    const double p = exp(fmin(0.0, log_a));
+    const uint4 r = philox(make_uint4(static_cast<unsigned>(c), static_cast<unsigned>(c >> 32), 5u,
+                                      static_cast<unsigned>(ctr)),
+                           make_uint2(static_cast<unsigned>(seed), static_cast<unsigned>(seed >> 32)));
+    const double coin =
+        static_cast<double>(((static_cast<uint64_t>(r.x) << 21) ^ r.y) & ((1ULL << 53) - 1)) * 0x1.0p-53;
+    prob[c] = p;
+    accept[c] = coin < p ? 1 : 0;
+  }
+}
+
+int split_propose(int64_t n_cand, int dim, double es, double c_q, int use_corr, double corr,
+                  double lam, uint64_t seed, uint64_t ctr, double* u, double* prob, int8_t* accept,
+                  cudaStream_t st) {
+  if (n_cand <= 0) return CGS_OK;
+  split_propose_kernel<<<grid_for(n_cand, 256, 4), 256, 0, st>>>(n_cand, dim, es, c_q, use_corr,
+                                                                 corr, lam, seed, ctr, u, prob,
+                                                                 accept);
+  CGS_CHECK_LAUNCH("split_propose_kernel");
+  return CGS_OK;
+}
+
 int apply_splits(float* rows, int dim, int32_t* idx, const int64_t* gauss, const int32_t* old_row,
                  const int32_t* new_row, const double* u, int64_t k, cudaStream_t st) {
   if (k <= 0) return CGS_OK;

@@ -556,6 +556,9 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
     lam = config.lambda_for(which)
     es, em = config.eps_for(which)
     if not config.exact_ratio:
+        if config.device_noise and book.device.type == "cuda":
+            _split_device(state, which, book, cand, rows, config, rec, lam, es, em)
+            return
         moves = _split_loop_native(book, cand, rows, config, rng, rec, lam, es, em)
         if moves is not None:
             _apply_split_batch(state, which, moves)
@@ -593,6 +596,80 @@ def split_step(state: ModelState, views, config: SamplerConfig, rng, rec: Transi
             moves.append((i, row, new_row, u))
             rec.accepts += 1
     _apply_split_batch(state, which, moves)
+
+
+def settle_split(rows: np.ndarray, accept: np.ndarray, refcount: np.ndarray):
+    """The reference loop's refcount skips (sampler.py:349-364) for candidates
+    whose accept coins are already drawn: candidate c is tried iff its row's
+    refcount, lowered by the accepts of the earlier candidates of that row, is
+    still >= 2; it is executed iff tried and accepted.  Vectorised: counting
+    the raw accept flags of earlier same-row candidates is exact, since once a
+    row reaches refcount 1 all its later candidates are skipped anyway.
+    Returns (tried, executed) boolean arrays in candidate order."""
+    rows = np.asarray(rows, dtype=np.int64)
+    acc = np.asarray(accept, dtype=bool)
+    n = len(rows)
+    if n == 0:
+        return np.zeros(0, bool), np.zeros(0, bool)
+    order = np.argsort(rows, kind="stable")
+    r_sorted, a_sorted = rows[order], acc[order].astype(np.int64)
+    cum = np.cumsum(a_sorted) - a_sorted
+    starts = np.flatnonzero(np.r_[True, r_sorted[1:] != r_sorted[:-1]])
+    before = cum - np.repeat(cum[starts], np.diff(np.r_[starts, n]))
+    tried = np.empty(n, dtype=bool)
+    tried[order] = before < np.asarray(refcount)[r_sorted] - 1
+    return tried, tried & acc
+
+
+def _split_device(state: ModelState, which: str, book, cand, rows, config: SamplerConfig,
+                  rec: TransitionRecord, lam: float, es: float, em: float) -> None:
+    """Throughput (device-noise) mode: the split proposals and coins of all
+    candidates drawn on the device at once (cgs_split_propose, Philox keyed by
+    (seed, iteration, candidate)) instead of one numpy draw after another;
+    the refcount skips of the reference loop (sampler.py:350-351) are then
+    settled on the host in candidate order: a row's candidates are tried while
+    its refcount is >= 2, and each accepted one lowers it.  Same proposal
+    distribution and acceptance rule as the reference; a different random
+    stream (like the device SGLD noise)."""
+    n_cand, dim = len(cand), book.dim
+    dev = book.device
+    u = torch.empty((n_cand, dim), dtype=torch.float64, device=dev)
+    prob = torch.empty((n_cand,), dtype=torch.float64, device=dev)
+    acc = torch.empty((n_cand,), dtype=torch.int8, device=dev)
+    c_q = 1.0 / es ** 2 - 1.0 / em ** 2
+    use_corr = 1 if config.normalization_correction else 0
+    corr = dim * math.log(em / es) if use_corr else 0.0
+    ctr = (int(state.iteration) << 1) | (0 if which == "sh" else 1)
+    nat.call("cgs_split_propose", n_cand, dim, float(es), float(c_q), use_corr, float(corr),
+             float(lam), int(config.seed) & 0xFFFFFFFFFFFFFFFF, ctr, nat.ptr(u), nat.ptr(prob),
+             nat.ptr(acc), nat.stream_handle(dev))
+    acc_h = acc.cpu().numpy().astype(bool)
+    prob_h = prob.cpu().numpy()
+    rows64 = np.ascontiguousarray(rows, dtype=np.int64)
+    tried, dec = settle_split(rows64, acc_h, book.refcount)
+    rec.accept_probs.extend(prob_h[tried].tolist())
+    rec.attempts += int(tried.sum())
+    take = np.flatnonzero(dec)
+    if len(take) == 0:
+        return
+    new_rows = np.empty(len(take), dtype=np.int32)
+    for j, c in enumerate(take.tolist()):
+        row = int(rows64[c])
+        rc = book.refcount
+        rc[row] -= 1  # decref of the old row (it stays >= 1)
+        new_rows[j] = book.alloc_index(parent=row)  # lowest free row
+        book.mutations += 1
+        rec.accepts += 1
+    _, idx = _book_of(state, which)
+    g = nat.upload(np.asarray(cand, np.int64)[take], dev)
+    o = nat.upload(rows64[take].astype(np.int32), dev)
+    nw = nat.upload(new_rows, dev)
+    ut = u.index_select(0, nat.upload(take.astype(np.int64), dev)).contiguous()
+    nat.call("cgs_apply_splits", nat.ptr(book.rows), book.dim, nat.ptr(idx), nat.ptr(g), nat.ptr(o),
+             nat.ptr(nw), nat.ptr(ut), len(take), nat.stream_handle(dev))
+    book.mutations += 1
+    state.touch(assignments=True)
+    state.prefetch_host_index(which)
 
 
 def _eligible(hidx: np.ndarray, refcount: np.ndarray) -> np.ndarray:

@@ -77,3 +77,24 @@ def test_host_eligible_matches_numpy():
     idx = rng.integers(0, k, size=1_000_003).astype(np.int32)
     assert np.array_equal(S._eligible(idx, rc), np.flatnonzero(rc[idx] >= 2))
     assert len(S._eligible(idx[:0], rc)) == 0
+
+
+def test_settle_split_matches_sequential_loop():
+    """sampler.settle_split (the device-proposal split's host bookkeeping)
+    equals the reference loop's sequential refcount skips (sampler.py:349-364)."""
+    from paper_2509_03775_b200.sampler import settle_split
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        k = int(rng.integers(1, 40))
+        rc0 = rng.integers(0, 6, size=k).astype(np.int64)
+        n = int(rng.integers(0, 300))
+        rows = rng.integers(0, k, size=n).astype(np.int64)
+        acc = rng.random(n) < rng.uniform(0.1, 0.9)
+        tried, dec = settle_split(rows, acc, rc0)
+        rc = rc0.copy()
+        for c in range(n):
+            exp_tried = rc[rows[c]] >= 2
+            assert tried[c] == exp_tried, (trial, c)
+            assert dec[c] == (exp_tried and acc[c])
+            if exp_tried and acc[c]:
+                rc[rows[c]] -= 1
