@@ -38,6 +38,11 @@ __host__ __device__ __forceinline__ int64_t ckpt_slot(uint32_t start, int tile, 
   return static_cast<int64_t>(start / kChunk) + tile + (j - 1);
 }
 
+#ifndef CGS_ONESWEEP_TILE_SORT  // 1: always the two-pass onesweep tile sort (comparisons)
+#define CGS_ONESWEEP_TILE_SORT 0
+#endif
+constexpr bool kForceOnesweepTileSort = CGS_ONESWEEP_TILE_SORT != 0;
+
 struct FrameLayout {
   FrameHeader* hdr;
   SplatRec* recs;          // V*N
@@ -83,7 +88,30 @@ struct FrameLayout {
   int tile_key_bytes;      // 2 or 4
   int tile_key_bits;
   int pair_result_alt;     // 1 if the tile-sorted pairs live in the sort's alt buffers
+  // One-pass counting tile sort (tile_count / matrix scan / tile_scatter,
+  // render_fwd.cu) for frames of at most kCountMaxTiles tiles: chunk c of
+  // 2^count_log2 pairs, tile t -> tcount[t * C + c], C = live chunks.
+  int count_sort;
+  int count_log2;
+  int64_t count_chunks_cap;
+  uint32_t* tcount;            // total_tiles x count_chunks_cap
+  uint32_t* toff;              // count_chunks_cap x total_tiles (scan result, chunk-major)
+  unsigned long long* tcount_n;  // total_tiles x live chunks (the matrix scan's length)
+  ScanWs tscan;
 };
+
+// Counting tile sort limits: the scatter keeps a u16 counter per (warp,
+// tile) plus a u32 offset per tile in shared memory (20 B per tile, and 2 KB
+// of duplicate-test tags per warp), and its
+// chunk prefix over 8 warps must fit u16 (chunks <= 32768 pairs).
+constexpr int kCountWarps = 8;
+constexpr int kCountMaxTiles = 10496;  // (20 B per tile + 16 KB) <= 227 KB
+constexpr int kCountMaxLog2 = 15;
+inline int count_chunk_log2(int tiles) {  // >= 4 pairs per tile and chunk, 4096 .. 32768
+  int l = 12;
+  while (l < kCountMaxLog2 && (1LL << l) < 4LL * tiles) ++l;
+  return l;
+}
 
 // Depth sort keys (project_kernel): 24 bits, 3 onesweep passes (an odd pass
 // count leaves the sorted splat ids in the sort's alternate value buffer);
@@ -158,6 +186,16 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
     L.psort32 = carve_sort<uint32_t>(c, pc);
   }
   L.pvals = c.take<uint32_t>(pc);
+  L.count_sort = (L.tile_key_bytes == 2 && fd.total_tiles > 0 && fd.total_tiles <= kCountMaxTiles &&
+                  !kForceOnesweepTileSort) ? 1 : 0;
+  if (L.count_sort) {
+    L.count_log2 = count_chunk_log2(fd.total_tiles);
+    L.count_chunks_cap = (pc + (1LL << L.count_log2) - 1) >> L.count_log2;
+    L.tcount = c.take<uint32_t>(static_cast<size_t>(fd.total_tiles) * L.count_chunks_cap);
+    L.toff = c.take<uint32_t>(static_cast<size_t>(fd.total_tiles) * L.count_chunks_cap);
+    L.tcount_n = c.take<unsigned long long>(1);
+    L.tscan = carve_scan(c, static_cast<int64_t>(fd.total_tiles) * L.count_chunks_cap);
+  }
   L.long_list = c.take<uint32_t>(vn1);
   L.ranges = c.take<uint2>(fd.total_tiles > 0 ? fd.total_tiles : 1);
   L.px_last = c.take<uint32_t>(fd.total_pixels > 0 ? fd.total_pixels : 1);
@@ -179,7 +217,7 @@ inline FrameLayout plan_frame(void* base, size_t cap_bytes, int64_t n, const Fra
   L.sr_cov = c.take<double>((sr_cap > 0 ? sr_cap : 1) * 8);
   L.bytes = c.off + 256;
   const int ppasses = (L.tile_key_bits + 7) / 8;
-  L.pair_result_alt = (ppasses % 2) == 1;
+  L.pair_result_alt = L.count_sort ? 1 : (ppasses % 2) == 1;  // the scatter writes vals_alt
   return L;
 }
 

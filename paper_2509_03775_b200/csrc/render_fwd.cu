@@ -11,9 +11,11 @@
 //   pair offsets    one decoupled-lookback scan over the splats' tile counts in
 //                   depth order (per splat and per depth rank; the last
 //                   partition writes the frame counts)
-//   emit + sort     (tile, splat) pairs in depth order, stable onesweep radix
-//                   sort by tile id: the per-tile append order of _bin_tiles
-//                   (render.py:240-254)
+//   emit + sort     (tile, splat) pairs in depth order, stable sort by tile
+//                   id: the per-tile append order of _bin_tiles
+//                   (render.py:240-254) -- a one-pass counting sort (count
+//                   per chunk, matrix scan, ranked scatter) for frames of at
+//                   most kCountMaxTiles tiles, else a 2-pass onesweep
 //   raster_fwd      raster.cu
 #include <atomic>
 #include <cmath>
@@ -597,7 +599,7 @@ __device__ __forceinline__ void emit_warps(
     const int v = ok ? static_cast<int>(s / static_cast<uint32_t>(n)) : 0;
     const int ntx = fd.cam[v].ntx;
     const int tbase = fd.cam[v].tile_base;
-    if (c) hist_rect(s_h, d0, base0, passes, rc, ntx, tbase);
+    if (c && passes) hist_rect(s_h, d0, base0, passes, rc, ntx, tbase);
     for (uint32_t q0 = 0; q0 < total; q0 += 32) {
       const uint32_t q = q0 + lane;
       const uint32_t end = loc + c;
@@ -712,6 +714,273 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const KT* __restrict__
 }
 
 // ---------------------------------------------------------------------------
+// One-pass counting tile sort (frames of <= kCountMaxTiles tiles).  The
+// emission order is (depth rank, tile row-major in the splat's rect) and a
+// splat meets each tile once, so a stable sort by tile only has to keep the
+// emission order among the pairs of one tile (render.py:240-254).  Pairs are
+// cut into chunks of 2^count_log2 consecutive emission indices:
+//   tile_count   per chunk, the count of each tile -> tcount[t * C + c]
+//   scan_kernel  exclusive scan of the flattened tile-major matrix: entry
+//                (t, c) becomes the first output position of chunk c's pairs
+//                of tile t (all chunks of earlier tiles come first)
+//   tile_scatter per chunk, 8 warps over 8 consecutive slices: each warp
+//                counts its slice per tile (u16 counters in shared memory),
+//                an exclusive sum over the warps places the slices, then each
+//                warp walks its slice in order, 32 pairs at a time ranked by
+//                match.any peers, and writes each splat id at its position.
+// One read of the keys to count, one read of keys + ids and one write of the
+// ids to scatter, against 2 onesweep passes (keys and ids read and written
+// twice, plus the per-digit lookback) -- and the tile ranges come out of the
+// scan (no tile_ranges pass).
+// Loads are batched ahead of their use (the counting is shared-memory
+// atomics and ordered shared updates, so without it every iteration waits a
+// full memory latency).
+constexpr int kCountLoadBatch = 8;
+
+__global__ void __launch_bounds__(256) tile_count_kernel(const uint16_t* __restrict__ keys,
+                                                         const FrameHeader* __restrict__ hdr,
+                                                         int tiles, int log2cp,
+                                                         uint32_t* __restrict__ tcount,
+                                                         unsigned long long* __restrict__ scan_n) {
+  extern __shared__ uint32_t s_cnt[];  // tiles
+  const int64_t np = static_cast<int64_t>(hdr->n_pairs);  // 0 on overflow
+  const int64_t C = (np + (1LL << log2cp) - 1) >> log2cp;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *scan_n = static_cast<unsigned long long>(tiles) * C;
+  const int64_t c = blockIdx.x;
+  if (c >= C) return;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) s_cnt[t] = 0u;
+  __syncthreads();
+  const int64_t b = c << log2cp;
+  const int64_t e = min(b + static_cast<int64_t>(1LL << log2cp), np);
+  // chunk starts are 8 KB aligned: 16-byte loads of 8 keys, kCountLoadBatch
+  // of them in flight per thread
+  constexpr int64_t kStep = 8 * 256;
+  for (int64_t i0 = b + 8 * threadIdx.x; i0 < e; i0 += kCountLoadBatch * kStep) {
+    uint4 q[kCountLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const int64_t i = i0 + u * kStep;
+      q[u] = i + 8 <= e ? *reinterpret_cast<const uint4*>(keys + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const int64_t i = i0 + u * kStep;
+      if (i + 8 <= e) {
+        const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          atomicAdd(&s_cnt[w[k] & 0xffffu], 1u);
+          atomicAdd(&s_cnt[w[k] >> 16], 1u);
+        }
+      } else {
+        for (int64_t j = i; j < e; ++j) atomicAdd(&s_cnt[keys[j]], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) tcount[t * C + c] = s_cnt[t];
+}
+
+// In-place exclusive scan of the tile-major count matrix, each result also
+// written to the chunk-major matrix the scatter reads one row of (the
+// scattered transposing stores are fire-and-forget here; as loads in the
+// scatter they would stall it).
+struct TileCountScan {
+  uint32_t* m;           // tiles x C, tile-major
+  uint32_t* mt;          // C x tiles, chunk-major
+  const unsigned long long* n;  // tiles * C
+  uint32_t tiles;
+  __device__ uint64_t load(int64_t i) const { return m[i]; }
+  __device__ void store(int64_t i, uint64_t ex, uint64_t) const {
+    const uint32_t C = static_cast<uint32_t>(*n / tiles);
+    const uint32_t t = static_cast<uint32_t>(i) / C, c = static_cast<uint32_t>(i) - t * C;
+    mt[static_cast<int64_t>(c) * tiles + t] = static_cast<uint32_t>(ex);
+  }
+  __device__ void finish(uint64_t) const {}
+};
+
+// Timing experiments only (wrong results): 1 no stores, 2 no ranking pass,
+// 3 prologue only, 4 no duplicate test, 5 also no counter atomics, 6 also no
+// stores.  Config 3 (12.2 M pairs): 184 / 144 / 35 / 12 / 137 / 124 / 66 us
+// -- the scattered id stores (~58 us) and the phase-c loads (~31 us) at 8
+// warps per SM (the per-warp counter rows) are the floor of this design.
+#ifndef CGS_SCATTER_DIAG
+#define CGS_SCATTER_DIAG 0
+#endif
+constexpr int kCountKeyLoads = 16;
+constexpr int kTagSlots = 2048;  // per-warp duplicate test slots (u8 lane ids)  // phase a: a 4096-key slice in one round of loads
+
+__global__ void __launch_bounds__(kCountWarps * 32) tile_scatter_kernel(
+    const uint16_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+    const FrameHeader* __restrict__ hdr, int tiles, int log2cp, int key_bits,
+    const uint32_t* __restrict__ toff, uint32_t* __restrict__ out, uint2* __restrict__ ranges) {
+  extern __shared__ uint32_t s_dyn[];
+  const int tpad = (tiles + 1) & ~1;  // u16 rows of whole words
+  uint32_t* s_off = s_dyn;                                          // tiles
+  uint16_t* s_pre = reinterpret_cast<uint16_t*>(s_dyn + tpad);      // kCountWarps x tpad
+  const int64_t np = static_cast<int64_t>(hdr->n_pairs);
+  const int64_t C = (np + (1LL << log2cp) - 1) >> log2cp;
+  const int64_t c = blockIdx.x;
+  if (c >= C) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = kCountWarps * 32;
+  const uint32_t* row = toff + c * tiles;  // this chunk's first position per tile
+  for (int t = tid; t < tiles; t += NT) s_off[t] = row[t];
+  uint32_t* s_pre32 = reinterpret_cast<uint32_t*>(s_pre);
+  for (int k = tid; k < kCountWarps * tpad / 2; k += NT) s_pre32[k] = 0u;
+  __syncthreads();
+  if (c == 0)  // chunk 0's entries are the tile starts
+    for (int t = tid; t < tiles; t += NT)
+      ranges[t] = make_uint2(s_off[t], t + 1 < tiles ? s_off[t + 1] : static_cast<uint32_t>(np));
+  const int64_t b = c << log2cp;
+  const int64_t e = min(b + static_cast<int64_t>(1LL << log2cp), np);
+  const int64_t slice = (1LL << log2cp) / kCountWarps;  // 512 .. 4096, a multiple of 256
+  const int64_t wb = min(b + warp * slice, e), we = min(wb + slice, e);
+  uint16_t* my = s_pre + warp * tpad;
+  uint32_t* my32 = reinterpret_cast<uint32_t*>(my);
+  uint8_t* tag = reinterpret_cast<uint8_t*>(s_pre + kCountWarps * tpad) + warp * kTagSlots;
+  if (CGS_SCATTER_DIAG == 3) return;
+  {  // the warp's slice per tile: 16-byte loads of 8 keys (slices are 1 KB aligned), all at once
+    uint4 q[kCountKeyLoads];
+#pragma unroll
+    for (int u = 0; u < kCountKeyLoads; ++u) {
+      const int64_t i = wb + 8 * lane + u * 256;
+      q[u] = i + 8 <= we ? *reinterpret_cast<const uint4*>(keys + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kCountKeyLoads; ++u) {
+      const int64_t i = wb + 8 * lane + u * 256;
+      if (i + 8 <= we) {
+        const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          atomicAdd(&my32[(w[k] & 0xffffu) >> 1], 1u << ((w[k] & 1u) << 4));
+          atomicAdd(&my32[w[k] >> 17], 1u << (((w[k] >> 16) & 1u) << 4));
+        }
+      } else {
+        for (int64_t j = i; j < we && j < i + 8; ++j) {
+          const uint32_t t = keys[j];
+          atomicAdd(&my32[t >> 1], 1u << ((t & 1u) << 4));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < tiles; t += NT) {  // slices placed in warp order
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kCountWarps; ++w) {
+      const uint32_t x = s_pre[w * tpad + t];
+      s_pre[w * tpad + t] = static_cast<uint16_t>(run);
+      run += x;
+    }
+  }
+  __syncthreads();
+  // In order, 32 pairs at a time; the next kCountLoadBatch groups load while
+  // this batch is ranked.  Per group the leader of each peer set (ballots
+  // over the key bits) takes its range with one shared atomic that returns
+  // the counter; a warp's atomics on one word execute in program order, so
+  // the ranges follow the emission order.
+  if (CGS_SCATTER_DIAG == 2) return;
+  uint32_t tk[kCountLoadBatch], sv[kCountLoadBatch];
+  auto load_batch = [&](int64_t g0, uint32_t (&k)[kCountLoadBatch], uint32_t (&v)[kCountLoadBatch]) {
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const int64_t i = g0 + u * 32 + lane;
+      k[u] = i < we ? static_cast<uint32_t>(keys[i]) : 0xffffffffu;
+      v[u] = i < we ? vals[i] : 0u;
+    }
+  };
+  load_batch(wb, tk, sv);
+  for (int64_t g0 = wb; g0 < we; g0 += kCountLoadBatch * 32) {
+    uint32_t nk[kCountLoadBatch], nv[kCountLoadBatch];
+    load_batch(g0 + kCountLoadBatch * 32, nk, nv);
+    // Peers (lanes with the same tile): most groups have none.  Each lane
+    // writes its id into a per-warp tag slot of its tile (t mod kTagSlots)
+    // and reads it back; if no lane lost its slot the 32 tiles are distinct.
+    // Otherwise one ballot per key bit.
+    unsigned peers[kCountLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const uint32_t t = tk[u];
+      const bool ok = t != 0xffffffffu;
+      bool lost = false;
+      if (CGS_SCATTER_DIAG < 4) {
+        if (ok) tag[t & (kTagSlots - 1)] = static_cast<uint8_t>(lane);
+        __syncwarp();
+        lost = ok && tag[t & (kTagSlots - 1)] != lane;
+        __syncwarp();
+      }
+      peers[u] = 1u << lane;
+      if (CGS_SCATTER_DIAG < 4 && __any_sync(kFull, lost)) {
+        unsigned pm = kFull;
+        for (int bit = 0; bit < key_bits; ++bit) {
+          const bool on = (t >> bit) & 1u;
+          const unsigned bal = __ballot_sync(kFull, on);
+          pm &= on ? bal : ~bal;
+        }
+        if (ok) peers[u] = pm;
+      }
+    }
+    uint32_t old[kCountLoadBatch];
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const uint32_t t = tk[u];
+      old[u] = 0u;
+      if (CGS_SCATTER_DIAG < 5 && t != 0xffffffffu && (peers[u] & lanemask_lt()) == 0u)
+        old[u] = atomicAdd(&my32[t >> 1], static_cast<uint32_t>(__popc(peers[u])) << ((t & 1u) << 4)) >>
+                 ((t & 1u) << 4);
+    }
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      const uint32_t t = tk[u];
+      const uint32_t base = __shfl_sync(kFull, old[u], __ffs(peers[u]) - 1) & 0xffffu;
+      if (t != 0xffffffffu && ((CGS_SCATTER_DIAG != 1 && CGS_SCATTER_DIAG < 6) || sv[u] == 0xfffffffu))
+        out[s_off[t] + base + __popc(peers[u] & lanemask_lt())] = sv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kCountLoadBatch; ++u) {
+      tk[u] = nk[u];
+      sv[u] = nv[u];
+    }
+  }
+}
+
+static int count_sort_pairs(FrameLayout& L, const FrameDesc& fd, cudaStream_t st) {
+  const int T = fd.total_tiles;
+  const size_t smem_count = static_cast<size_t>(T) * sizeof(uint32_t);
+  const int tpad = (T + 1) & ~1;
+  const size_t smem_scatter = static_cast<size_t>(tpad) * 4 + static_cast<size_t>(kCountWarps) * tpad * 2 +
+                              static_cast<size_t>(kCountWarps) * kTagSlots;
+  static std::atomic<bool> attr[kMaxDevices] = {};
+  int dev = 0;
+  if (int e = current_device(&dev)) return e;
+  if (!attr[dev].load()) {
+    constexpr int kMaxCount = kCountMaxTiles * 4;
+    constexpr int kMaxScatter = (kCountMaxTiles + 1) * 4 + kCountWarps * (kCountMaxTiles + 1) * 2 +
+                                kCountWarps * kTagSlots;
+    CGS_CUDA(cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxCount));
+    CGS_CUDA(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxScatter));
+    attr[dev].store(true);
+  }
+  const unsigned grid = static_cast<unsigned>(L.count_chunks_cap > 0 ? L.count_chunks_cap : 1);
+  const uint16_t* keys = static_cast<const uint16_t*>(L.pkeys);
+  CGS_PROFILED("tile_count_kernel", st,
+               tile_count_kernel<<<grid, 256, smem_count, st>>>(keys, L.hdr, T, L.count_log2,
+                                                                L.tcount, L.tcount_n));
+  CGS_CHECK_LAUNCH("tile_count_kernel");
+  CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * T, st));
+  int rc = launch_scan<TileCountScan, 24>(TileCountScan{L.tcount, L.toff, L.tcount_n, static_cast<uint32_t>(T)}, L.tcount_n, 0,
+                       static_cast<int64_t>(T) * L.count_chunks_cap, L.tscan, nullptr, st);
+  if (rc) return rc;
+  CGS_PROFILED("tile_scatter_kernel", st,
+               tile_scatter_kernel<<<grid, kCountWarps * 32, smem_scatter, st>>>(
+                   keys, L.pvals, L.hdr, T, L.count_log2, bits_for(T), L.toff, sorted_pair_vals(L), L.ranges));
+  CGS_CHECK_LAUNCH("tile_scatter_kernel");
+  return CGS_OK;
+}
+
+// ---------------------------------------------------------------------------
 template <int DEG>
 static void launch_project(const ProjIn& in, const FrameDesc& fd, const ProjOut& out,
                            int64_t vn, cudaStream_t st) {
@@ -723,18 +992,20 @@ template <typename KT>
 static int emit_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
                             const uint32_t* perm, cudaStream_t st) {
   const int eg = grid_for(L.vn, 256, 16);
-  // the emission kernels also build the tile sort's digit histogram
-  const int passes = (L.tile_key_bits + 7) / 8;
-  CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
+  // the emission kernels also build the onesweep tile sort's digit histogram
+  // (key_bits 0: none, the counting tile sort counts for itself)
+  const int key_bits = L.count_sort ? 0 : L.tile_key_bits;
+  const int passes = (key_bits + 7) / 8;
+  if (passes) CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
   CGS_PROFILED("emit_pairs_kernel", st,
                emit_pairs_kernel<KT><<<eg, 256, 0, st>>>(perm, L.off_rank, L.rect, L.hdr,
                                                           fd, L.n, L.long_list,
                                                           static_cast<KT*>(L.pkeys), L.pvals,
-                                                          ws.hist, L.tile_key_bits));
+                                                          ws.hist, key_bits));
   CGS_CHECK_LAUNCH("emit_pairs_kernel");
   emit_long_pairs_kernel<KT><<<148 * 4, 256, 0, st>>>(L.long_list, L.pair_off, L.n_tiles, L.rect,
                                                        L.hdr, fd, L.n, static_cast<KT*>(L.pkeys),
-                                                       L.pvals, ws.hist, L.tile_key_bits);
+                                                       L.pvals, ws.hist, key_bits);
   CGS_CHECK_LAUNCH("emit_long_pairs_kernel");
   return CGS_OK;
 }
@@ -837,6 +1108,7 @@ int frame_stage_duplicate(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) 
 }
 
 int frame_stage_sort_pairs(const FrameDesc& fd, FrameLayout& L, cudaStream_t st) {
+  if (L.count_sort) return count_sort_pairs(L, fd, st);
   return L.tile_key_bytes == 2 ? sort_pairs_stage<uint16_t>(L, fd, L.psort16, st)
                                : sort_pairs_stage<uint32_t>(L, fd, L.psort32, st);
 }

@@ -118,10 +118,12 @@ inline ScanWs carve_scan(Carver& c, int64_t n_cap) {
   return w;
 }
 
-template <class Op>
+template <class Op, int ROUNDS = kScanRounds>
 __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long long* n_dev,
                                                    int64_t n_host, ScanWs ws,
                                                    unsigned long long* total) {
+  constexpr int kScanRounds = ROUNDS;  // elements per lane (the partition is 256 x ROUNDS)
+  constexpr int kScanTile = kScanWarps * kScanRounds * 32;
   __shared__ unsigned s_part;
   __shared__ unsigned long long s_warp[kScanWarps];
   __shared__ unsigned long long s_prefix;
@@ -190,13 +192,17 @@ __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long lo
   }
 }
 
-template <class Op>
+template <class Op, int ROUNDS = kScanRounds>
 int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t n_cap,
                 const ScanWs& ws, unsigned long long* total, cudaStream_t st) {
-  CGS_CUDA(cudaMemsetAsync(ws.status, 0, ws.max_parts * sizeof(unsigned long long), st));
+  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanWarps * ROUNDS * 32);
+  if (parts > ws.max_parts) {
+    set_error("scan: workspace too small");
+    return CGS_EINTERNAL;
+  }
+  CGS_CUDA(cudaMemsetAsync(ws.status, 0, parts * sizeof(unsigned long long), st));
   CGS_CUDA(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st));
-  const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanTile);
-  CGS_PROFILED("scan_kernel", st, scan_kernel<Op><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total));
+  CGS_PROFILED("scan_kernel", st, scan_kernel<Op, ROUNDS><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total));
   CGS_CHECK_LAUNCH("scan_kernel");
   return CGS_OK;
 }

@@ -2,7 +2,7 @@
 # Live per-kernel launch durations of one bench configuration (graphs off,
 # CUDA events on the launch stream, one kernel profiled per run).
 # usage: BENCH_ARGS="--config 3" bash scripts/live_all.sh
-KS="project_kernel onesweep_kernel depth_tie_fix_kernel scan_kernel emit_pairs_kernel raster_fwd_kernel
+KS="project_kernel onesweep_kernel depth_tie_fix_kernel scan_kernel emit_pairs_kernel tile_count_kernel tile_scatter_kernel raster_fwd_kernel
 refine_fwd_kernel ssim_stats_kernel ssim_grad_kernel raster_bwd_kernel refine_bwd_kernel splat_reduce_kernel
 pull_back_kernel gauss_write_kernel sh_code_reduce_kernel sr_code_reduce_kernel sr_precompute_kernel sgld_kernel"
 for k in $KS; do

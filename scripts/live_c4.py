@@ -14,7 +14,8 @@ a = scenes.config4(0)
 st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows)
 lib = nat.library()
 KERNELS = ["project_kernel", "onesweep_kernel", "scan_kernel", "depth_tie_fix_kernel",
-           "emit_pairs_kernel", "raster_fwd_kernel", "refine_fwd_kernel"]
+           "emit_pairs_kernel", "tile_count_kernel", "tile_scatter_kernel", "raster_fwd_kernel",
+           "refine_fwd_kernel"]
 for B in [int(x) for x in (sys.argv[1:] or ["1", "16"])]:
     frames = [cg.Frame(st, a.cameras[i:i + B]).run_checked() for i in range(0, 16, B)]
     for f in frames:
