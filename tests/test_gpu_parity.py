@@ -426,6 +426,33 @@ def test_full_size_tile_lists_bit_exact(cg, make):
         assert lens.max() > 4096 and np.any((lens > 2048) & (lens <= 4096)) and np.any(lens <= 2048)
 
 
+def _wide_scene(w, h):
+    """Config-0 Gaussians seen by one large view: 7500 tiles (counting tile
+    sort, 32768-pair chunks) or 12288 tiles (above kCountMaxTiles: the
+    two-pass onesweep tile sort)."""
+    from paper_2509_03775_b200 import camera, scenes
+    a = scenes.config0(11)
+    cam = camera.ring_cameras(1, (0.0, 0.0, 0.0), 3.0, 0.0, float(w) / 2, w, h)[0]
+    return a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows, a.sr_rows, cam
+
+
+@pytest.mark.parametrize("wh", [(1600, 1200), (2048, 1536)], ids=["counting", "onesweep"])
+def test_large_view_tile_lists_bit_exact(cg, wh):
+    """Both tile-sort paths (render_fwd.cu) give _bin_tiles' lists (render.py:240-254)."""
+    from oracle import cgs_oracle as O
+    pos, logit, g2sh, g2sr, sh, sr, cam = _wide_scene(*wh)
+    st = cg.ModelState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    fr = cg.render_frame(st, [cam])
+    offs, ids = fr.tile_lists()
+    ost = O.OState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    ocam = O.cam_from_any(cam)
+    proj = O.project(ost, ocam)
+    roffs, members = O.bin_tiles(proj, ocam)
+    assert np.array_equal(offs, roffs)
+    assert np.array_equal(ids, proj["idx"][proj["order"][members]])
+    assert roffs[-1] > 40000  # several chunks
+
+
 def _giant_scene(seed=5, n=240, giants=6, size=320):
     """A few near-plane Gaussians covering every one of 400 tiles (> kLongSplat
     pairs: CTA-per-splat emission and reduction) among ordinary ones."""
