@@ -518,17 +518,22 @@ def run_render(args, world, rank, local):
         tot = float(t.item())
     px_job = sum(c.width * c.height for c in a.cameras)
     value = args.steps * px_job / (tot / 1000.0) / 1e6
-    # e2e: the same renders plus the D2H copy of every image into pinned memory
-    hosts = [torch.empty(f.image.shape, dtype=torch.float32).pin_memory() for f in frames]
+    # e2e: the same renders as the reference's `contrags render` delivers them
+    # (cli.py:209-220: 8-bit RGB, save_png's bytes): each frame quantized on the
+    # device (cgs_quantize8) and its bytes copied into pinned host memory
+    u8s = [torch.empty(f.image.shape, dtype=torch.uint8, device=dev) for f in frames]
+    hosts = [torch.empty(f.image.shape, dtype=torch.uint8).pin_memory() for f in frames]
     e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(args.steps)]
+    sh = nat.stream_handle(dev)
     torch.cuda.synchronize()
     for k in range(args.steps):
         flush.zero_()
         e_ev[k][0].record()
-        for f, h in zip(frames, hosts):
+        for f, u, h in zip(frames, u8s, hosts):
             f.run()
-            h.copy_(f.image, non_blocking=True)
+            nat.call("cgs_quantize8", nat.ptr(f.image), f.image.numel(), nat.ptr(u), sh)
+            h.copy_(u, non_blocking=True)
         e_ev[k][1].record()
     torch.cuda.synchronize()
     e_tot = sum(s.elapsed_time(e) for s, e in e_ev)
@@ -555,7 +560,9 @@ def run_render(args, world, rank, local):
                "gpu_launches": launches, "clocks": clk,
                "e2e": {"value": args.steps * px_job / (e_tot / 1000.0) / 1e6, "unit": "Mpix/s",
                        "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": int(sum(h.numel() * 4 for h in hosts)) * world},
+                       "d2h_bytes_per_step": int(sum(h.numel() for h in hosts)) * world,
+                       "note": "8-bit RGB images as cmd_render writes them (device quantize8, "
+                               "then D2H of the bytes)"},
                "cpu_baseline": cpu,
                "frame": {"pairs": int(sum(x.n_pairs for x in stats)),
                          "onscreen": int(sum(x.n_onscreen for x in stats))}}

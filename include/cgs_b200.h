@@ -279,6 +279,13 @@ CGS_API int cgs_recon_loss(const float* image, const float* gt, int32_t n_views,
                    float* dL_dimage, double* losses, void* workspace, size_t workspace_bytes,
                    cgs_stream_t stream);
 
+/* 8-bit image output: out[i] = clip(rint(values[i] * 255), 0, 255) with the
+ * product and rounding in float64 (round half to even) -- the bytes the
+ * reference's save_png writes for a rendered image and the grid of its
+ * quantize8 (modelio.py:137-153; cli.py:209-237 cmd_render / cmd_eval).
+ * values, out: device, n entries (an HxWx3 image: n = 3 H W). */
+CGS_API int cgs_quantize8(const float* values, int64_t n, uint8_t* out, cgs_stream_t stream);
+
 /* Device address of the backward workspace's non-finite flag: nonzero when
  * any gradient entry cgs_render_backward (or the staged backward) wrote was
  * non-finite.  Pure address arithmetic on the workspace pointer. */

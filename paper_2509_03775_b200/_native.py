@@ -116,6 +116,7 @@ SIGNATURES = {
     "cgs_sgld_update": (I32, [P, P, I64, P, I32, P, I64, P, P, I64, I64, I64, P, P, P, P,
                               ctypes.POINTER(CSgldParams), P, P, P, P, P, P]),
     "cgs_split_eligible": (I32, [P, I64, P, P, P, P, SZ, P]),
+    "cgs_quantize8": (I32, [P, I64, P, P]),
     "cgs_host_split_eligible": (I32, [P, I64, P, I64, P, P, I32]),
     "cgs_backward_nonfinite_flag": (P, [P]),
     "cgs_host_split_decide": (I32, [P, P, I64, P, P, I64, I32, F64, F64, F64, I32, F64, P, P, P, P,

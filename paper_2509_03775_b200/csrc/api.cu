@@ -145,6 +145,7 @@ int sgld_update(float* pos, float* logit, int64_t n, float* sh, int D, const int
                 int64_t sr_cap, const cgs_sgld_params_t* hp, const double* npos,
                 const double* nlog, const double* nsh, const double* nsr, int32_t* flags,
                 cudaStream_t st);
+int quantize8(const float* x, int64_t n, uint8_t* out, cudaStream_t st);
 int split_eligible(const int32_t* idx, int64_t n, const int32_t* rc, int32_t* out, int64_t* count,
                    void* ws, size_t ws_bytes, cudaStream_t st);
 int apply_splits(float* rows, int dim, int32_t* idx, const int64_t* gauss, const int32_t* old_row,
@@ -592,6 +593,14 @@ int cgs_sgld_update(float* positions, float* opacity_logits, int64_t n, float* s
                      sr_live, n_sr_live, grad_positions, grad_logits, grad_sh_rows, grad_sr_rows,
                      sh_capacity, sr_capacity, params_host, noise_pos, noise_logit, noise_sh,
                      noise_sr, flags, static_cast<cudaStream_t>(stream));
+}
+
+int cgs_quantize8(const float* values, int64_t n, uint8_t* out, cgs_stream_t stream) {
+  if (n < 0 || (n > 0 && (!values || !out))) {
+    set_error("quantize8: invalid arguments");
+    return CGS_EINVAL;
+  }
+  return quantize8(values, n, out, static_cast<cudaStream_t>(stream));
 }
 
 int cgs_split_eligible(const int32_t* idx, int64_t n, const int32_t* refcount, int32_t* eligible,

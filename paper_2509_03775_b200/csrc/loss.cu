@@ -415,4 +415,41 @@ int recon_loss(const float* img, const float* gt, int nv, int H, int W, double l
   return fork.join();
 }
 
+
+// 8-bit image output (reference modelio.py:137-153: save_png's bytes and
+// quantize8's grid): clip(rint(x * 255), 0, 255) evaluated in float64 on the
+// fp32 values, as numpy does on the image (rint: round half to even).  Four
+// values per thread, 16-byte loads when the buffer allows.
+__global__ void __launch_bounds__(256) quantize8_kernel(const float* __restrict__ x, int64_t n,
+                                                        uint8_t* __restrict__ out) {
+  auto q = [](float v) -> uint32_t {
+    double r = rint(static_cast<double>(v) * 255.0);
+    r = r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);  // NaN -> 0 like numpy's clip + cast
+    return r == r ? static_cast<uint32_t>(r) : 0u;
+  };
+  const int64_t n4 = n / 4;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (reinterpret_cast<uintptr_t>(out) & 3u) == 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (vec) {
+      const float4 v = reinterpret_cast<const float4*>(x)[i];
+      reinterpret_cast<uint32_t*>(out)[i] = q(v.x) | (q(v.y) << 8) | (q(v.z) << 16) | (q(v.w) << 24);
+    } else {
+      for (int k = 0; k < 4; ++k) out[4 * i + k] = static_cast<uint8_t>(q(x[4 * i + k]));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const int64_t j = 4 * n4 + threadIdx.x;
+    out[j] = static_cast<uint8_t>(q(x[j]));
+  }
+}
+
+int quantize8(const float* x, int64_t n, uint8_t* out, cudaStream_t st) {
+  if (n <= 0) return CGS_OK;
+  const int64_t n4 = (n + 3) / 4;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n4 + 255) / 256, 148 * 8));
+  CGS_PROFILED("quantize8_kernel", st, quantize8_kernel<<<grid, 256, 0, st>>>(x, n, out));
+  CGS_CHECK_LAUNCH("quantize8_kernel");
+  return CGS_OK;
+}
 }  // namespace cgs

@@ -124,3 +124,21 @@ def psnr(rendered, ground_truth, cap: float = PSNR_CAP_DB) -> float:
     if mse == 0.0:
         return cap
     return -10.0 * math.log10(mse)
+
+
+def evaluate(state, views) -> dict:
+    """``contrags eval`` (cli.py:223-237) on the device: for each (camera,
+    ground truth) view, PSNR and SSIM of the 8-bit-quantized render
+    (quantize8) against the ground truth; returns the per-view lists and their
+    means."""
+    from .modelio import quantize8
+    from .render import Frame
+    psnrs, ssims = [], []
+    for cam, gt in views:
+        fr = Frame(state, [cam]).run_checked()
+        rendered = quantize8(fr.view_image(0))
+        psnrs.append(psnr(rendered, gt))
+        ssims.append(ssim(rendered, gt))
+    return {"psnr": psnrs, "ssim": ssims, "mean_psnr": float(np.mean(psnrs)),
+            "mean_ssim": float(np.mean(ssims))}
+

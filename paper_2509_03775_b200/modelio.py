@@ -129,3 +129,41 @@ def write_metrics_csv(records, path) -> None:
                 str(r.live_sh), str(r.live_sr),
                 _csv_float(r.recon), _csv_float(r.total), _csv_float(r.psnr),
             ]) + "\n")
+
+
+# ---------------------------------------------------------------------------
+# 8-bit images (reference modelio.py:137-153)
+
+def image_to_u8(image: torch.Tensor) -> torch.Tensor:
+    """Device HxWx3 (or flat) float image -> uint8 on the same device: the
+    bytes the reference's save_png writes, clip(rint(x * 255), 0, 255) in
+    float64 (the cgs_quantize8 kernel)."""
+    from . import _native as nat
+    if not (isinstance(image, torch.Tensor) and image.is_cuda):
+        raise TypeError("image_to_u8 takes a CUDA tensor (numpy images: quantize8)")
+    x = image.detach().to(torch.float32).contiguous()
+    out = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    nat.call("cgs_quantize8", nat.ptr(x), x.numel(), nat.ptr(out), nat.stream_handle(x.device))
+    return out
+
+
+_GRID8 = {}
+
+
+def _grid8(device) -> torch.Tensor:
+    """k / 255 for k = 0..255 as numpy divides (a scalar division on the device
+    may multiply by the reciprocal instead)."""
+    g = _GRID8.get(device)
+    if g is None:
+        g = _GRID8[device] = torch.as_tensor(np.arange(256, dtype=np.float64) / 255.0).to(device)
+    return g
+
+
+def quantize8(image):
+    """Round a float image onto the 8-bit grid (modelio.py:151-153).  A CUDA
+    tensor is quantized on the device (float64 result on the device); an array
+    is rounded on the host exactly as the reference does."""
+    if isinstance(image, torch.Tensor) and image.is_cuda:
+        return _grid8(image.device)[image_to_u8(image).long()]
+    return np.clip(np.rint(np.asarray(image, dtype=np.float64) * 255.0), 0, 255) / 255.0
+

@@ -336,6 +336,23 @@ def render_frame(state: ModelState, cams) -> Frame:
     return Frame(state, cams).run_checked()
 
 
+def render_u8(state: ModelState, cams) -> list:
+    """The rendered views as 8-bit HxWx3 host arrays -- the PNG bytes the
+    reference's ``contrags render`` writes per view (cli.py:209-220:
+    rasterize_forward + save_png).  Views go through batched frames of up to
+    16; each frame's images are quantized on the device (cgs_quantize8) and
+    copied to the host as bytes."""
+    from .modelio import image_to_u8
+    cams = list(cams)
+    out = []
+    for i in range(0, len(cams), nat.MAX_VIEWS):
+        fr = Frame(state, cams[i:i + nat.MAX_VIEWS]).run_checked()
+        u8 = image_to_u8(fr.image).cpu().numpy()
+        for b, h, w in fr._pix_slices():
+            out.append(u8[3 * b: 3 * (b + h * w)].reshape(h, w, 3))
+    return out
+
+
 def rasterize_forward(state: ModelState, cam: Camera) -> RenderArtifacts:
     """Front-to-back compositing over 16x16 tiles, black background (render.py:287-315)."""
     fr = render_frame(state, [cam])
