@@ -399,7 +399,8 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
 // d_conic 3) are summed over the tile's pixels in fixed order: per warp a
 // 12-shuffle transposed reduction, then the 4 warps in shared memory.
 struct PixBwd {
-  float T, gr, gg, gb, sr, sg, sb;
+  float T, gr, gg, gb;
+  float sdot;  // suffix colour . dL/dC: only this dot product enters dL/dalpha
   uint32_t last;
 };
 
@@ -437,14 +438,12 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float t, float 
   o[0] = fmaf(w, p.gr, o[0]);  // d colour += weight * dL (render.py:351-352)
   o[1] = fmaf(w, p.gg, o[1]);
   o[2] = fmaf(w, p.gb, o[2]);
-  // dC/dalpha = c T_before - suffix / (1 - alpha) (render.py:357-359)
-  const float dCr = fmaf(cr, Tb, -p.sr * iom);
-  const float dCg = fmaf(cg, Tb, -p.sg * iom);
-  const float dCb = fmaf(cb, Tb, -p.sb * iom);
-  const float da = dCr * p.gr + dCg * p.gg + dCb * p.gb;
-  p.sr = fmaf(w, cr, p.sr);
-  p.sg = fmaf(w, cg, p.sg);
-  p.sb = fmaf(w, cb, p.sb);
+  // dC/dalpha = c T_before - suffix / (1 - alpha) (render.py:357-359); dotted
+  // with dL/dC: T_before (c . g) - (suffix . g) / (1 - alpha), the suffix kept
+  // as its running dot product with g (suffix += w c  =>  sdot += w (c . g))
+  const float cdot = fmaf(cr, p.gr, fmaf(cg, p.gg, cb * p.gb));
+  const float da = fmaf(Tb, cdot, -p.sdot * iom);
+  p.sdot = fmaf(w, cdot, p.sdot);
   p.T = Tb;
   if (flow) {
     const float dp = da * al;
@@ -468,6 +467,10 @@ __device__ __forceinline__ bool bwd_pixel(PixBwd& p, uint32_t k, float t, float 
 #define CGS_BWD_BATCH 64
 #endif
 constexpr int kBwdBatch = CGS_BWD_BATCH;
+#ifndef CGS_BWD_PAIR_REDUCE
+#define CGS_BWD_PAIR_REDUCE 1
+#endif
+constexpr bool kBwdPairReduce = CGS_BWD_PAIR_REDUCE != 0;
 static_assert(kBwdBatch % 32 == 0 && kChunk % kBwdBatch == 0 && kBwdBatch <= 256,
               "batch: whole ballots, whole batches per chunk, u8 hit-list entries");
 
@@ -583,6 +586,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   // tile-centred pixel coordinates (stage_splat); also the moments' coordinates
   const float flx = static_cast<float>(lx) - kTileHalf, fly = static_cast<float>(ly) - kTileHalf;
   const int slot = reduce9_slot(lane);
+  const int slot18 = reduce_slot(18, lane);
   uint8_t* my_list = s_list[warp];
   const uint32_t n_units = unit_ctl[0];
   // splat jj of buffer cb: sum the present warps in fixed order and store
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     const float4* ck = last_chunk ? nullptr
                                   : ckpt + ckpt_slot(rg.x, tile, k_end / kChunk) * kTilePixels;
 
-    PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
+    PixBwd q0{1.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0u};
     PixBwd q1 = q0;
     auto load_px = [&](PixBwd& q, int py, int lyy) {
       if (px < cam.width && py < cam.height) {
@@ -647,9 +651,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         } else {
           const float4 c = ck[lyy * kTile + lx];
           q.T = c.x;
-          q.sr = c.y;
-          q.sg = c.z;
-          q.sb = c.w;
+          q.sdot = fmaf(c.y, q.gr, fmaf(c.z, q.gg, c.w * q.gb));
         }
       }
     };
@@ -703,19 +705,39 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
         issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
       }
       const int hits = warp_hit_list<B>(s_mask[buf], nb, warp, lane, my_list);
-      for (int i = hits - 1; i >= 0; --i) {
-        const int j = my_list[i];
+      // Hits in reverse order; two at a time (CGS_BWD_PAIR_REDUCE) the 18
+      // values of both splats go through one transposed warp reduction (20
+      // shuffles instead of 24).  The pixel updates stay sequential.
+      auto hit_values = [&](int j, float* o) -> bool {
         const uint32_t k = static_cast<uint32_t>(b0 + j);
-        float o[9];
-#pragma unroll
-        for (int u = 0; u < 9; ++u) o[u] = 0.0f;
         const float4 a = s_a[buf][j];
         const float4 b = s_b[buf][j];
         const float2 nc = s_n[buf][j];
         const float t0 = staged_t(a, b, flx, fly);
         const float t1 = staged_t(a, b, flx, fly + 4.0f);
-        bool any = bwd_pixel(q0, k, t0, b.w, nc.x, nc.y, flx, fly, o);
-        any = bwd_pixel(q1, k, t1, b.w, nc.x, nc.y, flx, fly + 4.0f, o) || any;
+        const bool any = bwd_pixel(q0, k, t0, b.w, nc.x, nc.y, flx, fly, o);
+        return bwd_pixel(q1, k, t1, b.w, nc.x, nc.y, flx, fly + 4.0f, o) || any;
+      };
+      int i = hits - 1;
+      if (kBwdPairReduce && !TRACE) {
+        for (; i >= 1; i -= 2) {
+          const int ja = my_list[i], jb = my_list[i - 1];
+          float o[18];
+#pragma unroll
+          for (int u = 0; u < 18; ++u) o[u] = 0.0f;
+          bool any = hit_values(ja, o);
+          any = hit_values(jb, o + 9) || any;
+          float red = 0.0f;
+          if (__any_sync(kFull, any)) red = warp_reduce_t<18>(o);
+          if (slot18 >= 0) s_red[buf][warp][slot18 < 9 ? ja : jb][slot18 < 9 ? slot18 : slot18 - 9] = red;
+        }
+      }
+      for (; i >= 0; --i) {
+        const int j = my_list[i];
+        float o[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) o[u] = 0.0f;
+        const bool any = hit_values(j, o);
         if (TRACE && lane == 0)  // diagnostics: lanes with a contribution per warp hit
           atomicAdd(trace + 8 * static_cast<int64_t>(fd.total_tiles) + __popc(__ballot_sync(kFull, any)), 1ull);
         else if (TRACE) __ballot_sync(kFull, any);

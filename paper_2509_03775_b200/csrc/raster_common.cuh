@@ -192,6 +192,54 @@ __device__ __forceinline__ float warp_reduce9(const float (&o)[9]) {
   return v1 + __shfl_xor_sync(full, v1, 1);
 }
 
+// The same transposed reduction for N values (N <= 32): at each butterfly
+// level (16, 8, 4, 2, 1) a lane keeps the lower or upper half of its list
+// (padded with a zero when odd) and adds its partner's copy of it; 20
+// shuffles for N = 18 (two splats' 9 values) against 2 x 12.
+template <int N, int H>
+__device__ __forceinline__ void reduce_level(const float* in, float* out, int lane) {
+  constexpr int LO = (N + 1) / 2;
+  const bool up = lane & H;
+#pragma unroll
+  for (int j = 0; j < LO; ++j) {
+    const float lo = in[j], hi = j + LO < N ? in[j + LO] : 0.0f;
+    out[j] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, H);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ float warp_reduce_t(const float (&o)[N]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int N1 = (N + 1) / 2, N2 = (N1 + 1) / 2, N3 = (N2 + 1) / 2, N4 = (N3 + 1) / 2;
+  float a[N1], b[N2], c[N3], d[N4], e[1];
+  reduce_level<N, 16>(o, a, lane);
+  reduce_level<N1, 8>(a, b, lane);
+  reduce_level<N2, 4>(b, c, lane);
+  reduce_level<N3, 2>(c, d, lane);
+  reduce_level<N4, 1>(d, e, lane);
+  return e[0];
+}
+
+// Value index held by `lane` after warp_reduce_t<N>, or -1 (a padding zero).
+__host__ __device__ constexpr int reduce_slot(int n, int lane) {
+  // the lane's list: len entries (padded), the first `real` of them original
+  // indices base, base + 1, ...
+  int base = 0, len = n, real = n;
+  for (int h = 16; h >= 1; h >>= 1) {
+    const int lo = (len + 1) / 2;
+    if (lane & h) {
+      base += lo;
+      real = real > lo ? real - lo : 0;
+    } else {
+      real = real < lo ? real : lo;
+    }
+    len = lo;
+  }
+  return real == 1 ? base : -1;
+}
+static_assert(reduce_slot(9, 10) == 4 && reduce_slot(9, 24) == 8 && reduce_slot(9, 1) == -1,
+              "warp_reduce_t<9> holds warp_reduce9's values on its even lanes");
+
 // Value index held by `lane` after warp_reduce9, or -1.
 __device__ __forceinline__ int reduce9_slot(int lane) {
   constexpr unsigned kMask = (1u << 0) | (1u << 2) | (1u << 4) | (1u << 8) | (1u << 10) |
