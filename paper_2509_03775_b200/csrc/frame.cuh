@@ -246,6 +246,15 @@ int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* fi
 
 // Emission index of pair (splat s, tile t): pairs of a splat are emitted in
 // row-major order over its tile rect starting at pair_off[s].
+__device__ __forceinline__ uint64_t emission_index_of(uint64_t po, uint64_t rc, const FrameDesc& fd,
+                                                      int64_t n, uint32_t s, int tile) {
+  const int tx0 = static_cast<int>(rc & 0xffff), tx1 = static_cast<int>((rc >> 16) & 0xffff);
+  const int ty0 = static_cast<int>((rc >> 32) & 0xffff);
+  const int v = static_cast<int>(s / static_cast<uint32_t>(n));
+  const int lt = tile - fd.cam[v].tile_base;
+  const int ty = lt / fd.cam[v].ntx, tx = lt - ty * fd.cam[v].ntx;
+  return po + static_cast<uint64_t>((ty - ty0) * (tx1 - tx0 + 1) + (tx - tx0));
+}
 __device__ __forceinline__ uint64_t emission_index(const uint64_t* pair_off, const uint64_t* rect,
                                                    const FrameDesc& fd, int64_t n, uint32_t s,
                                                    int tile) {

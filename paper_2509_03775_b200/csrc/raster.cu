@@ -665,6 +665,18 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
     int b0 = k0 + ((k_end - 1 - k0) / B) * B;
     fence_proxy_async_smem();  // s_raw was read by the previous unit's staging
     issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0, min(B, k_end - b0), tid, 128);
+    // the staging thread of record k also needs the splat's rect and first
+    // pair index (its emission index): loaded one batch ahead, with the records
+    uint32_t pre_s = 0;
+    uint64_t pre_rc = 0, pre_po = 0;
+    auto prefetch_eidx = [&](int first, int cnt) {
+      if (tid < cnt) {
+        pre_s = pair_vals[rg.x + first + tid];
+        pre_rc = rect[pre_s];
+        pre_po = pair_off[pre_s];
+      }
+    };
+    prefetch_eidx(b0, min(B, k_end - b0));
     // Two-buffer pipeline: threads [0, B) stage batch i while threads
     // [B, 2B) combine batch i-1 (its staged values and warp sums live in the
     // other buffer), so a batch costs two barriers instead of three.
@@ -680,8 +692,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
           s_a[buf][k] = sg.a;
           s_b[buf][k] = sg.b;
           s_n[buf][k] = sg.c;
-          s_eidx[buf][k] = static_cast<uint32_t>(
-              emission_index(pair_off, rect, fd, n, pair_vals[rg.x + b0 + k], tile));
+          s_eidx[buf][k] = static_cast<uint32_t>(emission_index_of(pre_po, pre_rc, fd, n, pre_s, tile));
           uint32_t m = quad_mask(local_rect(r, tx * kTile, ty * kTile));
 #if CGS_BWD_EIGEN_CULL
 #pragma unroll
@@ -703,6 +714,7 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
       if (b0 > k0) {
         fence_proxy_async_smem();
         issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + b0 - B, B, tid, 128);
+        prefetch_eidx(b0 - B, B);
       }
       const int hits = warp_hit_list<B>(s_mask[buf], nb, warp, lane, my_list);
       // Hits in reverse order; two at a time (CGS_BWD_PAIR_REDUCE) the 18
