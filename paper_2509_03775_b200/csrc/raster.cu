@@ -175,6 +175,43 @@ __device__ __forceinline__ uint32_t block8x4_mask(uint32_t rc) {
   return m;
 }
 
+// CGS_FWD_HALF: 16-bit mask of the 4x4 blocks a contribution box meets, bit
+// 4 qy + qx for the block (4 qx, 4 qy) -- the half (lane >> 4) of warp w is
+// bit 2 w + (lane >> 4) (fwd_px_x / fwd_px_y).
+__device__ __forceinline__ uint32_t block4x4_mask(uint32_t rc) {
+  const int x0 = static_cast<int8_t>(rc & 0xff), x1 = static_cast<int8_t>((rc >> 8) & 0xff);
+  const int y0 = static_cast<int8_t>((rc >> 16) & 0xff), y1 = static_cast<int8_t>(rc >> 24);
+  uint32_t cm = 0, m = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (x1 >= 4 * q && x0 <= 4 * q + 3) cm |= 1u << q;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (y1 >= 4 * q && y0 <= 4 * q + 3) m |= cm << (4 * q);
+  return m;
+}
+
+// Two ordered hit lists per warp, one per half-warp (bits 2 warp and
+// 2 warp + 1 of the 16-bit masks); returns this lane's half's count.
+template <int NB>
+__device__ __forceinline__ int warp_hit_lists2(const uint16_t* s_mask, int nb, int warp, int lane,
+                                               uint8_t* list0, uint8_t* list1) {
+  int c0 = 0, c1 = 0;
+  const unsigned lt = lanemask_lt();
+#pragma unroll
+  for (int c = 0; c < NB / 32; ++c) {
+    const int j = c * 32 + lane;
+    const uint32_t m = j < nb ? (s_mask[j] >> (2 * warp)) & 3u : 0u;
+    const unsigned b0 = __ballot_sync(kFull, m & 1u), b1 = __ballot_sync(kFull, m & 2u);
+    if (m & 1u) list0[c0 + __popc(b0 & lt)] = static_cast<uint8_t>(j);
+    if (m & 2u) list1[c1 + __popc(b1 & lt)] = static_cast<uint8_t>(j);
+    c0 += __popc(b0);
+    c1 += __popc(b1);
+  }
+  __syncwarp();
+  return (lane >> 4) ? c1 : c0;
+}
+
 #ifndef CGS_FWD_PAIRS
 #define CGS_FWD_PAIRS 1
 #endif
@@ -210,8 +247,13 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   __shared__ __align__(128) SplatRec s_raw[B];
   // staged splats, one 48-byte entry each (a, b, colour): one address per hit
   __shared__ float4 s_st[B][3];
+#if CGS_FWD_HALF
+  __shared__ uint16_t s_mask[B];
+  __shared__ uint8_t s_list[kFwdWarps][2][B];
+#else
   __shared__ uint8_t s_mask[B];
   __shared__ uint8_t s_list[kFwdWarps][B];
+#endif
   __shared__ uint32_t s_max[kFwdWarps];
   __shared__ __align__(8) uint64_t s_bar;
   if (hdr->stats.overflow) return;
@@ -222,14 +264,18 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
   const int lt = tile - cam.tile_base;
   const int ty = lt / cam.ntx, tx = lt - ty * cam.ntx;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lx = (warp & 1) * 8 + (lane & 7), ly = (warp >> 1) * 4 + (lane >> 3);
+  const int lx = fwd_px_x(warp, lane), ly = fwd_px_y(warp, lane);
   const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool in = px < cam.width && py < cam.height;
   const uint2 rg = ranges[tile];
   const int n = static_cast<int>(rg.y - rg.x);
   const double cx = tile_centre(tx), cy = tile_centre(ty);
   const float flx = static_cast<float>(lx) - kTileHalf, fly = static_cast<float>(ly) - kTileHalf;
+#if CGS_FWD_HALF
+  uint8_t* my_list = s_list[warp][lane >> 4];
+#else
   uint8_t* my_list = s_list[warp];
+#endif
   PixState p{1.0f, 0.0f, 0.0f, 0.0f, 0, in ? 0u : 1u, CGS_REFINE_ALL != 0};
   int n_ckpt = 0;
   // fp32 alpha to blend (render.py:274-279); the caller keeps it when it is
@@ -265,6 +311,18 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       s_st[tid][0] = sg.a;
       s_st[tid][1] = sg.b;
       s_st[tid][2] = make_float4(sg.c.x, sg.c.y, 0.0f, 0.0f);
+#if CGS_FWD_HALF
+      uint32_t m8 = block4x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile));
+#if CGS_FWD_EIGEN_CULL
+#pragma unroll
+      for (int w = 0; w < 16; ++w) {  // 4x4 blocks the ellipse cannot reach
+        const float x0 = (w & 3) * 4 - kTileHalf, y0 = (w >> 2) * 4 - kTileHalf;
+        if ((m8 >> w) & 1u)
+          if (!staged_may_hit(sg.a, sg.b, x0, x0 + 3.0f, y0, y0 + 3.0f)) m8 &= ~(1u << w);
+      }
+#endif
+      s_mask[tid] = static_cast<uint16_t>(m8);
+#else
       uint32_t m8 = block8x4_mask(local_rect(s_raw[tid], tx * kTile, ty * kTile));
 #if CGS_FWD_EIGEN_CULL
 #pragma unroll
@@ -275,6 +333,7 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       }
 #endif
       s_mask[tid] = static_cast<uint8_t>(m8);
+#endif
     }
     __syncthreads();
     if (bend < n) {
@@ -282,7 +341,11 @@ __global__ void __launch_bounds__(kFwdThreads, CGS_FWD_MINB) raster_fwd_kernel(
       issue_records(s_raw, &s_bar, pair_vals, recs, rg.x + bend, batch_end(bend) - bend, tid, NT);
       pending = true;
     }
+#if CGS_FWD_HALF
+    const int hits = warp_hit_lists2<B>(s_mask, nb, warp, lane, s_list[warp][0], s_list[warp][1]);
+#else
     const int hits = warp_hit_list<B>(s_mask, nb, warp, lane, my_list);
+#endif
     if (!p.done()) {
 #if CGS_FWD_PAIRS
       // two hits per iteration: both alphas are independent of the blend

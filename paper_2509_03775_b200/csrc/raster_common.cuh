@@ -392,6 +392,21 @@ __device__ __forceinline__ Staged stage_splat(const SplatRec& r, double cx, doub
   return st;
 }
 
+// Pixel of lane `lane` of forward warp `w` (tile-local; raster_fwd_kernel and
+// the order refine.cu reads its flag masks in).  Warp w owns the 8x4 block
+// ((w & 1) * 8, (w >> 1) * 4).  With CGS_FWD_HALF each half-warp h = lane >> 4
+// owns the 4x4 half (4 h, 0) of it and walks its own hit list; otherwise the
+// lanes cover the block row by row.
+#ifndef CGS_FWD_HALF
+#define CGS_FWD_HALF 1
+#endif
+__host__ __device__ constexpr int fwd_px_x(int w, int lane) {
+  return CGS_FWD_HALF ? (w & 1) * 8 + (lane >> 4) * 4 + (lane & 3) : (w & 1) * 8 + (lane & 7);
+}
+__host__ __device__ constexpr int fwd_px_y(int w, int lane) {
+  return CGS_FWD_HALF ? (w >> 1) * 4 + ((lane >> 2) & 3) : (w >> 1) * 4 + (lane >> 3);
+}
+
 // Centre of tile column / row t in pixel coordinates (stage_splat's origin);
 // pixel x of the tile sits at centre + (x - 7.5).
 __device__ __forceinline__ double tile_centre(int t) { return static_cast<double>(t * kTile + kTile / 2); }

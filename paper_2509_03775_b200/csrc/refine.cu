@@ -115,7 +115,7 @@ __global__ void CGS_REF_BOUNDS refine_kernel(
       int tot = 0;
       for (int fw0 = 0; fw0 < 8; fw0 += kWarps) {
         const int fw = fw0 + warp;
-        const int lx = (fw & 1) * 8 + (lane & 7), ly = (fw >> 1) * 4 + (lane >> 3);
+        const int lx = fwd_px_x(fw, lane), ly = fwd_px_y(fw, lane);
         const bool in = tx * kTile + lx < cam.width && ty * kTile + ly < cam.height;
         const uint32_t wm = refine_mask[static_cast<int64_t>(tile) * 8 + fw];
         const bool f = in && ((wm >> lane) & 1u);

@@ -97,6 +97,26 @@ __device__ __forceinline__ ProjPre load_pre(const ProjIn& in, int64_t i) {
   return p;
 }
 
+#ifndef CGS_PROJECT_SH32
+#define CGS_PROJECT_SH32 1
+#endif
+constexpr float kShGateRel = 4e-6f;  // >= 4x the fp32 colour error bound per sum|c|
+
+// Float64 colour max(raw + 0.5, 0) of one SH row at unit direction (x, y, z)
+// in the reference's order (render.py:187-198), rounded to fp32.
+template <int DEG>
+__device__ __noinline__ void sh_colour64(const float* __restrict__ row, double x, double y,
+                                         double z, float* rgb) {
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  double B[NB];
+  sh_basis<DEG>(x, y, z, B);
+  double col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < 3 * NB; ++e) col[e % 3] += B[e / 3] * static_cast<double>(__ldg(row + e));
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) rgb[ch] = static_cast<float>(fmax(col[ch] + 0.5, 0.0));
+}
+
 // One (view, Gaussian) splat; returns its 32-bit depth sort key (~0: no tiles).
 // Quotients by the same divisor (1/tz, 1/det, 1/|view|) multiply by one
 // reciprocal: within an ulp of the reference's divisions, far inside the
@@ -168,26 +188,52 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   ox *= rlen;
   oy *= rlen;
   oz *= rlen;
-  double B[NB];
-  sh_basis<DEG>(ox, oy, oz, B);
   const float* row = in.sh_rows + static_cast<int64_t>(pre.sh) * D;
-  double col[3] = {0.0, 0.0, 0.0};
-  if constexpr (D % 4 == 0) {
-    const float4* r4 = reinterpret_cast<const float4*>(row);
+  float rgb[3];
+#if CGS_PROJECT_SH32
+  {
+    // fp32 basis and sum (no float->double conversions: 3(d+1)^2 of them per
+    // splat ran at the conversion pipe's quarter rate).  The only discrete
+    // decision on the colour is the gate raw > 0 of max(raw + 0.5, 0)
+    // (render.py:198, 418-419); the fp32 raw is within 9e-7 sum|c| of the
+    // float64 one (basis error <= 1.8e-7 absolute with |B| <= 0.75, 16-term
+    // FMA chain), so a raw within kShGateRel sum|c| of the gate is
+    // recomputed in float64 (sh_colour64, out of line: rare).  Elsewhere the
+    // value differs from the float64 one by that bound (far inside the image
+    // tolerance).
+    float Bf[NB];
+    sh_basis_f<DEG>(static_cast<float>(ox), static_cast<float>(oy), static_cast<float>(oz), Bf);
+    float c3[3] = {0.0f, 0.0f, 0.0f}, a3[3] = {0.0f, 0.0f, 0.0f};
+    auto acc = [&](int e, float v) {
+      c3[e % 3] = fmaf(Bf[e / 3], v, c3[e % 3]);
+      a3[e % 3] += fabsf(v);
+    };
+    if constexpr (D % 4 == 0) {
+      const float4* r4 = reinterpret_cast<const float4*>(row);
 #pragma unroll
-    for (int q = 0; q < D / 4; ++q) {
-      const float4 f = __ldg(r4 + q);
-      const float fv[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int e = 4 * q + u;
-        col[e % 3] += B[e / 3] * static_cast<double>(fv[u]);
+      for (int q = 0; q < D / 4; ++q) {
+        const float4 v = __ldg(r4 + q);
+        acc(4 * q + 0, v.x);
+        acc(4 * q + 1, v.y);
+        acc(4 * q + 2, v.z);
+        acc(4 * q + 3, v.w);
       }
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int e = 0; e < D; ++e) col[e % 3] += B[e / 3] * static_cast<double>(__ldg(row + e));
+      for (int e = 0; e < D; ++e) acc(e, __ldg(row + e));
+    }
+    bool near = false;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float raw = c3[ch] + 0.5f;
+      near |= fabsf(raw) <= fmaf(kShGateRel, a3[ch], 1e-7f);
+      rgb[ch] = fmaxf(raw, 0.0f);
+    }
+    if (near) sh_colour64<DEG>(row, ox, oy, oz, rgb);
   }
+#else
+  sh_colour64<DEG>(row, ox, oy, oz, rgb);
+#endif
   SplatRec rec;
   rec.mx = mx;
   rec.my = my;
@@ -197,9 +243,9 @@ __device__ __forceinline__ uint32_t project_one(const ProjIn& in, const FrameDes
   rec.cc = a * idet;
   const double opac = 1.0 / (1.0 + exp(-static_cast<double>(pre.logit)));
   rec.opac = static_cast<float>(opac);
-  rec.r = static_cast<float>(fmax(col[0] + 0.5, 0.0));
-  rec.g = static_cast<float>(fmax(col[1] + 0.5, 0.0));
-  rec.b = static_cast<float>(fmax(col[2] + 0.5, 0.0));
+  rec.r = rgb[0];
+  rec.g = rgb[1];
+  rec.b = rgb[2];
   // Contribution box for the raster's warp-level skip: pixels whose centre
   // lies outside the bounding box of {d : o exp(-d^T conic d / 2) >= 1/255}
   // have alpha < 1/255 in the reference's float64 arithmetic (render.py:
