@@ -426,6 +426,48 @@ def test_full_size_tile_lists_bit_exact(cg, make):
         assert lens.max() > 4096 and np.any((lens > 2048) & (lens <= 4096)) and np.any(lens <= 2048)
 
 
+def _multi_plane_scene(seed=9, planes=48):
+    """Splats on 48 planes z = const seen by an axis-aligned camera: each
+    plane is one run of equal depth keys, 1-300 splats long, so the sorted
+    keys hold runs inside one tie-fix window, across window edges and longer
+    than the window's halo or the per-element limit."""
+    from paper_2509_03775_b200 import camera, scenes
+    a = scenes.config0(seed)
+    rng = np.random.default_rng(seed)
+    side = 96
+    cam = camera.Camera(rotation=np.eye(3), translation=np.array([0.0, 0.0, 4.0]), fx=96.0,
+                        fy=96.0, cx=side / 2, cy=side / 2, width=side, height=side)
+    lens = rng.integers(1, 300, planes)
+    z = np.repeat(np.linspace(-1.0, 1.4, planes), lens).astype(np.float32)
+    n = len(z)
+    pos = np.zeros((n, 3), np.float32)
+    pos[:, :2] = rng.uniform(-1.3, 1.3, size=(n, 2))
+    pos[:, 2] = z
+    pos = pos[rng.permutation(n)]
+    idx = rng.integers(0, a.sr_rows.shape[0], n).astype(np.int32)
+    logit = rng.normal(-2.0, 0.5, n).astype(np.float32)
+    return pos, logit, idx, idx, a.sh_rows, a.sr_rows, cam
+
+
+def test_equal_depth_runs_order_bit_exact(cg):
+    """Many runs of equal depth keys of lengths 1-300 (depth tie fix: window
+    ranks, window-crossing and long runs): tile lists equal the oracle's."""
+    from oracle import cgs_oracle as O
+    pos, logit, g2sh, g2sr, sh, sr, cam = _multi_plane_scene()
+    st = cg.ModelState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    fr = cg.render_frame(st, [cam])
+    offs, ids = fr.tile_lists()
+    ost = O.OState.from_arrays(pos, logit, g2sh, g2sr, sh, sr)
+    ocam = O.cam_from_any(cam)
+    proj = O.project(ost, ocam)
+    roffs, members = O.bin_tiles(proj, ocam)
+    rids = proj["idx"][proj["order"][members]]
+    assert np.array_equal(offs, roffs)
+    assert np.array_equal(ids, rids)
+    ref = O.raster_forward(ost, ocam)
+    assert np.array_equal(fr.counts.view(cam.height, cam.width).cpu().numpy(), ref["counts"])
+
+
 def _wide_scene(w, h):
     """Config-0 Gaussians seen by one large view: 7500 tiles (counting tile
     sort, 32768-pair chunks) or 12288 tiles (above kCountMaxTiles: the
@@ -817,3 +859,48 @@ def test_config4_batched_strips_match_oracle(cg):
         assert np.array_equal(fr.view_counts(v).cpu().numpy(), fw["counts"]), v
         assert np.allclose(fr.view_image(v).cpu().numpy(), fw["image"], rtol=RTOL, atol=ATOL), v
         assert np.allclose(fr.view_T(v).cpu().numpy(), fw["final_T"], rtol=RTOL, atol=ATOL), v
+
+
+def test_colour_gate_knife_edge_matches_oracle(cg):
+    """SH rows whose float64 colour max(raw + 0.5, 0) sits within a few fp32
+    ulps of the gate raw = 0 (render.py:198, 418-419): the projection's fp32
+    colour path must hand them to its float64 recompute, so every gate and the
+    gated SH gradients equal the oracle's."""
+    from gpu_helpers import group_rel
+    from oracle import cgs_oracle as O
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config0(11)
+    sh = a.sh_rows.copy()
+    c0 = np.float32(-0.5 / O.sh_basis(np.array([[0.0, 0.0, 1.0]]), 0)[0, 0])
+    for r in range(96):  # rows 0..95: DC terms k ulps from the gate, no view dependence
+        for ch in range(3):
+            k = (r + 7 * ch) % 41 - 20
+            v = c0
+            for _ in range(abs(k)):
+                v = np.nextafter(v, np.float32(np.inf) if k > 0 else np.float32(-np.inf))
+            sh[r, ch] = v
+        sh[r, 3:] = 0.0
+    g2sh = (np.arange(a.positions.shape[0]) % 128).astype(np.int32)  # most splats on knife-edge rows
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, g2sh, a.g2sr, sh, a.sr_rows)
+    cam = a.cameras[0]
+    art = cg.rasterize_forward(st, cam)
+    ost = O.OState.from_arrays(a.positions, a.opacity_logits, g2sh, a.g2sr, sh, a.sr_rows)
+    ocam = O.cam_from_any(cam)
+    proj = O.project(ost, ocam)
+    sp = art.frame.splats(0)
+    idx = proj["idx"]
+    on = sp["n_tiles"][idx] > 0
+    knife = np.isin(g2sh[idx], np.arange(96)) & on
+    assert knife.sum() > 500
+    raw = proj["color_raw"]
+    assert ((np.abs(raw[knife]) < 1e-6).sum()) > 500  # really on the edge
+    assert np.array_equal(sp["colors"][idx][on] > 0, raw[on] > 0)
+    img = art.image.cpu().numpy()
+    fw = O.raster_forward(ost, ocam)
+    assert np.allclose(img, fw["image"], rtol=RTOL, atol=ATOL)
+    dL = np.random.default_rng(2).normal(0, 1e-3, img.shape)
+    g = cg.rasterize_backward(st, cam, art, dL).numpy()
+    og = O.raster_backward(ost, ocam, dL)
+    for k in ("sh_rows", "positions"):
+        assert group_rel(g[k], og[k]) <= 1e-4, (k, group_rel(g[k], og[k]))
+        assert np.allclose(g[k], og[k], rtol=RTOL, atol=ATOL), (k, np.abs(g[k] - og[k]).max())
