@@ -1,7 +1,8 @@
 // Tile rasterizer kernels, forward and backward (reference render.py:265-377).
 //
 // Forward: one CTA per 16x16 tile, 256 threads, one pixel each, warp w on
-// the 8x4 block ((w & 1) * 8, (w >> 1) * 4).  Backward: persistent CTAs of
+// the 8x4 block ((w & 1) * 8, (w >> 1) * 4), each half-warp on one 4x4 half
+// of it with its own hit list (fwd_px_x / fwd_px_y).  Backward: persistent CTAs of
 // 128 threads over (tile, 256-splat chunk) work units; warp w on the 8x8
 // quadrant ((w & 1) * 8, (w >> 1) * 8), each lane on pixels (x, y) and
 // (x, y + 4) (two pixels per lane amortise its per-splat warp reduction); a
