@@ -838,7 +838,9 @@ struct TileCountScan {
   uint32_t tiles;
   __device__ uint64_t load(int64_t i) const { return m[i]; }
   __device__ void store(int64_t i, uint64_t ex, uint64_t) const {
-    const uint32_t C = static_cast<uint32_t>(*n / tiles);
+    // tiles x C < 2^32 (kCountMaxTiles x the chunk count); __ldg lets the
+    // compiler load the count once per thread, not once per element
+    const uint32_t C = static_cast<uint32_t>(__ldg(n)) / tiles;
     const uint32_t t = static_cast<uint32_t>(i) / C, c = static_cast<uint32_t>(i) - t * C;
     mt[static_cast<int64_t>(c) * tiles + t] = static_cast<uint32_t>(ex);
   }

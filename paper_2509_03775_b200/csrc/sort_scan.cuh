@@ -85,9 +85,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 //   __device__ uint64_t load(int64_t i) const;
 //   __device__ void store(int64_t i, uint64_t exclusive, uint64_t value) const;
 //   __device__ void finish(uint64_t total) const;  (called once, with the total)
-// Partitions of 8 warps x 8 rounds x 32 lanes; within a warp every round is
-// 32 consecutive elements (coalesced), so the running sum follows index
-// order.  Status words: value in bits 0..61, flag in 62..63.
+// Partitions of 8 warps x 32 lanes x ROUNDS consecutive elements per lane
+// (lane-major inside a warp, so the running sum follows index order).  Status words: value in bits 0..61, flag in 62..63.
 // ===========================================================================
 constexpr int kScanWarps = 8;
 #ifndef CGS_SCAN_ROUNDS
@@ -134,18 +133,30 @@ __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long lo
   const int64_t n = dev_count(n_dev, n_host);
   const int64_t nparts = n > 0 ? ceil_div(n, kScanTile) : 1;
   if (part >= nparts) return;
+  // lane l of a warp owns the ROUNDS consecutive elements wbase + l ROUNDS
+  // + j, so its loads are independent of each other and issue together
+  // (a round-per-32-elements layout had ptxas sink them into the shuffle
+  // rounds: ~2 loads in flight), its running sum is local and one warp scan
+  // of the lane totals places it
   const int64_t wbase = part * kScanTile + static_cast<int64_t>(warp) * kScanRounds * 32;
+  const int64_t lbase = wbase + static_cast<int64_t>(lane) * kScanRounds;
 
   unsigned long long v[kScanRounds], ex[kScanRounds];
-  unsigned long long run = 0;
 #pragma unroll
   for (int j = 0; j < kScanRounds; ++j) {
-    const int64_t i = wbase + j * 32 + lane;
+    const int64_t i = lbase + j;
     v[j] = (i < n) ? op.load(i) : 0ULL;
-    unsigned long long inc = warp_incl_scan(v[j]);
-    ex[j] = run + inc - v[j];
-    run += __shfl_sync(kFull, inc, 31);
   }
+  unsigned long long lrun = 0;
+#pragma unroll
+  for (int j = 0; j < kScanRounds; ++j) {
+    ex[j] = lrun;
+    lrun += v[j];
+  }
+  const unsigned long long linc = warp_incl_scan(lrun);
+  const unsigned long long run = __shfl_sync(kFull, linc, 31);
+#pragma unroll
+  for (int j = 0; j < kScanRounds; ++j) ex[j] += linc - lrun;
   if (lane == 0) s_warp[warp] = run;
   __syncthreads();
   if (warp == 0) {
@@ -187,7 +198,7 @@ __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long lo
   const unsigned long long base = s_prefix + s_warp[warp];
 #pragma unroll
   for (int j = 0; j < kScanRounds; ++j) {
-    const int64_t i = wbase + j * 32 + lane;
+    const int64_t i = lbase + j;
     if (i < n) op.store(i, base + ex[j], v[j]);
   }
 }
