@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--codenn-rows", type=int, default=65536)
     ap.add_argument("--views-per-frame", type=int, default=1,
                     help="config 4: poses rendered per batched frame")
+    ap.add_argument("--render-streams", type=int, default=2,
+                    help="config 4: CUDA streams the frames are rendered on (frames are "
+                         "independent: one frame's latency-bound sort / scan phases overlap "
+                         "another's raster)")
     return ap.parse_args()
 
 
@@ -484,10 +488,28 @@ def run_render(args, world, rank, local):
     frames = [cg.Frame(st, g).run_checked() for g in groups]  # sizes the pair buffers
     flush = torch.empty((64 * 1024 * 1024,), dtype=torch.float32, device=dev)
     lib = nat.library()
+    # frames (own workspaces) round-robin over S streams, forked from and
+    # joined back into the current stream, so the events around a step on the
+    # current stream time all of it
+    S = max(1, args.render_streams)
+    main_s = torch.cuda.current_stream(dev)
+    streams = [main_s] + [torch.cuda.Stream(device=dev) for _ in range(S - 1)]
+
+    def fan(work):
+        fork = torch.cuda.Event()
+        fork.record(main_s)
+        for s in streams[1:]:
+            s.wait_event(fork)
+        for i, f in enumerate(frames):
+            with torch.cuda.stream(streams[i % S]):
+                work(i, f)
+        for s in streams[1:]:
+            e = torch.cuda.Event()
+            e.record(s)
+            main_s.wait_event(e)
 
     def step():
-        for f in frames:
-            f.run()
+        fan(lambda i, f: f.run())
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -525,15 +547,17 @@ def run_render(args, world, rank, local):
     hosts = [torch.empty(f.image.shape, dtype=torch.uint8).pin_memory() for f in frames]
     e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(args.steps)]
-    sh = nat.stream_handle(dev)
+    def deliver(i, f):
+        f.run()
+        nat.call("cgs_quantize8", nat.ptr(f.image), f.image.numel(), nat.ptr(u8s[i]),
+                 nat.stream_handle(dev))
+        hosts[i].copy_(u8s[i], non_blocking=True)
+
     torch.cuda.synchronize()
     for k in range(args.steps):
         flush.zero_()
         e_ev[k][0].record()
-        for f, u, h in zip(frames, u8s, hosts):
-            f.run()
-            nat.call("cgs_quantize8", nat.ptr(f.image), f.image.numel(), nat.ptr(u), sh)
-            h.copy_(u, non_blocking=True)
+        fan(deliver)
         e_ev[k][1].record()
     torch.cuda.synchronize()
     e_tot = sum(s.elapsed_time(e) for s, e in e_ev)
@@ -554,6 +578,7 @@ def run_render(args, world, rank, local):
                "vs_baseline": None, "dtype": "f32 (fp64 projection geometry)",
                "data": "synthetic (seeded scene, SURVEY.md §8(d)); random-init codebooks",
                "config": {"workload": workload_name(4), "views_per_frame": B,
+                          "streams": S,
                           "poses_per_gpu": len(mine), "gaussians": a.n,
                           "l2": "flushed (256 MB write) between timed iterations",
                           "parallelism": f"dp{world} (poses sharded, no collective)"},

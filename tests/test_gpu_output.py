@@ -92,3 +92,32 @@ def test_evaluate_matches_oracle(cg):
     assert np.isclose(r["ssim"][0], O.ssim(q, gt), rtol=1e-4, atol=1e-5)
     assert np.isclose(r["mean_psnr"], np.mean(r["psnr"]))
     assert r["psnr"][1] > 40.0  # quantization noise only
+
+
+def test_frames_on_concurrent_streams_equal_serial(cg):
+    """Frames (own workspaces) rendered concurrently on several streams, as
+    the config-4 batch path does, give the serial renders bit for bit."""
+    from paper_2509_03775_b200 import scenes
+    a = scenes.config1(3, n=20000, views=6, size=96)
+    st = cg.ModelState.from_arrays(a.positions, a.opacity_logits, a.g2sh, a.g2sr, a.sh_rows,
+                                   a.sr_rows)
+    frames = [cg.Frame(st, [c]).run_checked() for c in a.cameras]
+    ref = [f.image.clone() for f in frames]
+    for f in frames:
+        f.image.zero_()
+    main = torch.cuda.current_stream()
+    streams = [main, torch.cuda.Stream(), torch.cuda.Stream()]
+    fork = torch.cuda.Event()
+    fork.record(main)
+    for s in streams[1:]:
+        s.wait_event(fork)
+    for i, f in enumerate(frames):
+        with torch.cuda.stream(streams[i % 3]):
+            f.run()
+    for s in streams[1:]:
+        e = torch.cuda.Event()
+        e.record(s)
+        main.wait_event(e)
+    torch.cuda.synchronize()
+    for f, r in zip(frames, ref):
+        assert torch.equal(f.image, r)
