@@ -356,8 +356,19 @@ int cgs_frame_stats(const void* workspace, cgs_frame_stats_t* out, cgs_stream_t 
   }
   const FrameHeader* h = static_cast<const FrameHeader*>(workspace);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  CGS_CUDA(cudaMemcpyAsync(out, &h->stats, sizeof(cgs_frame_stats_t), cudaMemcpyDeviceToHost, st));
+  FrameHeader hh;
+  CGS_CUDA(cudaMemcpyAsync(&hh, h, sizeof(FrameHeader), cudaMemcpyDeviceToHost, st));
   CGS_CUDA(cudaStreamSynchronize(st));
+  *out = hh.stats;
+  // the float64 re-walk's counters, kept where the refine kernels count them
+  // (no publishing kernel in the step)
+  out->n_refined_tiles = static_cast<int64_t>(hh.scratch[3]);
+  out->n_refined_pixels = static_cast<int64_t>(hh.scratch[4]);
+  out->diag_last_mismatch = static_cast<int64_t>(hh.scratch[5]);
+  out->diag_count_mismatch = static_cast<int64_t>(hh.scratch[6]);
+  const uint32_t te = static_cast<uint32_t>(hh.scratch[7]), ae = static_cast<uint32_t>(hh.scratch[7] >> 32);
+  std::memcpy(&out->diag_max_T_err, &te, sizeof(float));
+  std::memcpy(&out->diag_max_alpha_err, &ae, sizeof(float));
   return CGS_OK;
 }
 

@@ -837,15 +837,6 @@ __global__ void __launch_bounds__(128) raster_bwd_kernel(
   }
 }
 
-// Publish the exactness counters in the frame stats (cgs_frame_stats).
-__global__ void refine_stats_kernel(FrameHeader* hdr) {
-  hdr->stats.n_refined_tiles = static_cast<int64_t>(hdr->scratch[3]);
-  hdr->stats.n_refined_pixels = static_cast<int64_t>(hdr->scratch[4]);
-  hdr->stats.diag_last_mismatch = static_cast<int64_t>(hdr->scratch[5]);
-  hdr->stats.diag_count_mismatch = static_cast<int64_t>(hdr->scratch[6]);
-  hdr->stats.diag_max_T_err = __uint_as_float(static_cast<unsigned int>(hdr->scratch[7]));
-  hdr->stats.diag_max_alpha_err = __uint_as_float(static_cast<unsigned int>(hdr->scratch[7] >> 32));
-}
 
 // ---------------------------------------------------------------------------
 int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t* nproc,
@@ -873,8 +864,6 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                                  nullptr, st);
     if (rc) return rc;
   }
-  refine_stats_kernel<<<1, 1, 0, st>>>(L.hdr);
-  CGS_CHECK_LAUNCH("refine_stats_kernel");
   return CGS_OK;
 }
 

@@ -429,6 +429,11 @@ template <int DEG>
 __global__ void __launch_bounds__(128, CGS_PB_MINB) pull_back_kernel(const FrameHeader* __restrict__ fh,
                                                         FrameDesc fd, int64_t n, int64_t vn,
                                                         GaussIn g, BwdLayout B) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the backward's counters are final here (cgs_frame_stats)
+    FrameHeader* h = const_cast<FrameHeader*>(fh);
+    h->stats.n_processed = static_cast<int64_t>(B.hdr->n_processed);
+    h->stats.n_touched = static_cast<int64_t>(B.hdr->n_touched);
+  }
   if (fh->stats.overflow) return;
   const bool sparse = code_sparse(B, vn);
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < vn;
@@ -644,11 +649,6 @@ __global__ void __launch_bounds__(256) sr_code_reduce_kernel(
   }
 }
 
-// Publish the backward's counters in the frame header (cgs_frame_stats).
-__global__ void bwd_stats_kernel(FrameHeader* fh, const BwdHeader* bh) {
-  fh->stats.n_processed = static_cast<int64_t>(bh->n_processed);
-  fh->stats.n_touched = static_cast<int64_t>(bh->n_touched);
-}
 
 // ---------------------------------------------------------------------------
 // code -> members CSR: stable onesweep of (code, gaussian) pairs + offsets.
@@ -830,8 +830,6 @@ int bwd_stage_codebook(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLa
     CGS_CHECK_LAUNCH("sh_code_reduce_kernel");
   }
   if (int rc = fork.join()) return rc;
-  bwd_stats_kernel<<<1, 1, 0, st>>>(const_cast<FrameHeader*>(L.hdr), B.hdr);
-  CGS_CHECK_LAUNCH("bwd_stats_kernel");
   return CGS_OK;
 }
 

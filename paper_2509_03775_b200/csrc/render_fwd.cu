@@ -536,6 +536,8 @@ struct PairOffsets {
     hdr->stats.overflow = over ? 1 : 0;
     hdr->stats.pair_capacity = pair_cap;
     hdr->stats.n_views = n_views;
+    hdr->stats.n_processed = 0;  // the backward's counters (pull_back_kernel publishes them)
+    hdr->stats.n_touched = 0;
   }
 };
 
