@@ -242,7 +242,8 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
                   const float* dL, float* partials, cudaStream_t st);
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
-                      const float* logits, cudaStream_t st);
+                      const float* logits, cudaStream_t st, void* zero_first = nullptr,
+                      size_t zero_bytes = 0);
 
 // Emission index of pair (splat s, tile t): pairs of a splat are emitted in
 // row-major order over its tile rect starting at pair_off[s].

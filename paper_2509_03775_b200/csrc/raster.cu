@@ -60,7 +60,9 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
                                                           int total_tiles,
                                                           uint32_t* __restrict__ order,
                                                           uint32_t* __restrict__ zero_a,
-                                                          uint64_t* __restrict__ zero_b) {
+                                                          uint64_t* __restrict__ zero_b,
+                                                          unsigned long long* __restrict__ zero_v,
+                                                          int n_views) {
   __shared__ uint32_t cnt[256];
   const int tid = threadIdx.x;
   auto bucket = [&](int t) -> uint32_t {
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restric
       zero_a[t] = 0u;
       zero_b[t] = 0ull;
     }
+  if (zero_v)  // and its per-view maxima of the last processed depth keys
+    for (int v = tid; v < n_views; v += blockDim.x) zero_v[v] = 0ull;
 }
 
 // Per-pixel forward state.  `last` doubles as the done flag (last index + 1
@@ -544,7 +548,9 @@ static_assert(kBwdBatch % 32 == 0 && kChunk % kBwdBatch == 0 && kBwdBatch <= 256
 __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __restrict__ nproc,
                                                           int total_tiles,
                                                           uint2* __restrict__ units,
-                                                          uint32_t* __restrict__ ctl) {
+                                                          uint32_t* __restrict__ ctl,
+                                                          uint32_t* __restrict__ zero,
+                                                          int n_zero) {
   // Full chunks (length kChunk, the longest) first, in tile order, placed by
   // a block scan of per-tile counts (no shared-atomic contention on one
   // bucket); then the partial last chunks by length, longest first, through
@@ -558,6 +564,7 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
   };
   if (tid < 256) cnt[tid] = 0;
   if (tid == 0) s_full = 0;
+  for (int k = tid; k < n_zero; k += blockDim.x) zero[k] = 0u;  // the caller's header (no memset node)
   __syncthreads();
   uint32_t full = 0;
   for (int t = tid; t < total_tiles; t += blockDim.x) {
@@ -843,7 +850,9 @@ int launch_tile_order(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       cudaStream_t st) {
   tile_order_kernel<<<1, 1024, 0, st>>>(L.ranges, nproc, fd.total_tiles, L.tile_order,
                                         nproc ? nullptr : L.tile_nproc,
-                                        nproc ? nullptr : L.tile_last_dk);
+                                        nproc ? nullptr : L.tile_last_dk,
+                                        nproc ? nullptr : L.view_last_dk,
+                                        fd.n_views > 0 ? fd.n_views : 1);
   CGS_CHECK_LAUNCH("tile_order_kernel");
   return CGS_OK;
 }
@@ -852,7 +861,7 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
                       const float* logits, float* image, float* final_T, int32_t* counts,
                       cudaStream_t st) {
   // L.tile_order was computed from the list lengths before the depth sort
-  CGS_CUDA(cudaMemsetAsync(L.view_last_dk, 0, (fd.n_views > 0 ? fd.n_views : 1) * sizeof(uint64_t), st));
+  // (tile_order_kernel also zeroed the per-tile and per-view maxima)
   CGS_PROFILED("raster_fwd_kernel", st,
                raster_fwd_kernel<<<fd.total_tiles, kFwdThreads, 0, st>>>(
                    fd, L.tile_order, L.ranges, vals, L.recs, L.hdr, image, final_T, counts,
@@ -869,8 +878,10 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
-                      const float* logits, cudaStream_t st) {
-  unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl);
+                      const float* logits, cudaStream_t st, void* zero_first, size_t zero_bytes) {
+  unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl,
+                                        static_cast<uint32_t*>(zero_first),
+                                        static_cast<int>(zero_bytes / sizeof(uint32_t)));
   CGS_CHECK_LAUNCH("unit_order_kernel");
   // persistent grid: every resident CTA slot (per device ordinal)
   static std::atomic<int> resident_dev[kMaxDevices] = {};

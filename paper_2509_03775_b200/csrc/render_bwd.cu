@@ -338,9 +338,13 @@ template <int DEG>
 __global__ void __launch_bounds__(256, CGS_SR_MINB) splat_reduce_kernel(PairWalk pw, const FrameHeader* __restrict__ fh,
                                                            FrameDesc fd, int64_t n, int64_t vn,
                                                            GaussIn g, BwdLayout B) {
-  if (fh->stats.overflow) return;
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (fh->stats.overflow) {  // touched is written here for every splat (no memset before)
+    for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < vn; s += stride)
+      B.touched[s] = 0;
+    return;
+  }
   for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x); base < vn; base += stride) {
     const int64_t s = base + threadIdx.x;
     const bool ok = s < vn;
@@ -372,8 +376,9 @@ __global__ void __launch_bounds__(256, CGS_SR_MINB) splat_reduce_kernel(PairWalk
     }
     const unsigned tm = __ballot_sync(kFull, ok && touched);
     if (lane == 0 && tm) atomicAdd(&B.hdr->n_touched, static_cast<unsigned long long>(__popc(tm)));
-    if (!ok || huge) continue;
-    B.touched[s] = touched ? 1 : 0;
+    if (!ok) continue;
+    B.touched[s] = touched ? 1 : 0;  // huge: 0 here, splat_reduce_long_kernel (next) sets 1
+    if (huge) continue;
     if (!touched) continue;
     store_splat_acc(B, s, acc);
   }
@@ -744,13 +749,15 @@ static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap
 // earlier stages left in the backward workspace).
 int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                      BwdLayout& B, const float* dL, const float* final_T, cudaStream_t st) {
+  // both codebooks' row flags, carved back to back: one memset node
+  CGS_CUDA(cudaMemsetAsync(B.code_hit[0], 0,
+                           (B.code_hit[1] + (sc->sr_capacity > 0 ? sc->sr_capacity : 1)) - B.code_hit[0],
+                           st));
+  if (fd.total_tiles > 0 && L.vn > 0)  // unit_order_kernel zeroes B.hdr, splat_reduce writes every touched flag
+    return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed,
+                             sc->opacity_logits, st, B.hdr, sizeof(BwdHeader));
   CGS_CUDA(cudaMemsetAsync(B.hdr, 0, sizeof(BwdHeader), st));
   if (L.vn > 0) CGS_CUDA(cudaMemsetAsync(B.touched, 0, L.vn, st));
-  if (sc->sh_capacity > 0) CGS_CUDA(cudaMemsetAsync(B.code_hit[0], 0, sc->sh_capacity, st));
-  if (sc->sr_capacity > 0) CGS_CUDA(cudaMemsetAsync(B.code_hit[1], 0, sc->sr_capacity, st));
-  if (fd.total_tiles > 0 && L.vn > 0)
-    return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed,
-                             sc->opacity_logits, st);
   return CGS_OK;
 }
 

@@ -28,7 +28,13 @@ namespace cgs {
 // ---------------------------------------------------------------------------
 // Sigma3 = R(q/|q|) diag(exp(2 ls)) R^T per SR row; slot 6 flags |q| == 0.
 __global__ void __launch_bounds__(256) sr_precompute_kernel(const float* __restrict__ rows,
-                                                            int64_t cap, double* __restrict__ out) {
+                                                            int64_t cap, double* __restrict__ out,
+                                                            uint32_t* __restrict__ zero_a, int na,
+                                                            uint32_t* __restrict__ zero_b, int nb) {
+  if (blockIdx.x == 0) {  // the frame header and the depth-sort histogram (no memset nodes)
+    for (int k = threadIdx.x; k < na; k += blockDim.x) zero_a[k] = 0u;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) zero_b[k] = 0u;
+  }
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < cap;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float* row = rows + r * 7;
@@ -789,11 +795,14 @@ __global__ void __launch_bounds__(256) tile_count_kernel(const uint16_t* __restr
                                                          const FrameHeader* __restrict__ hdr,
                                                          int tiles, int log2cp,
                                                          uint32_t* __restrict__ tcount,
-                                                         unsigned long long* __restrict__ scan_n) {
+                                                         unsigned long long* __restrict__ scan_n,
+                                                         uint2* __restrict__ ranges) {
   extern __shared__ uint32_t s_cnt[];  // tiles
   const int64_t np = static_cast<int64_t>(hdr->n_pairs);  // 0 on overflow
   const int64_t C = (np + (1LL << log2cp) - 1) >> log2cp;
   if (blockIdx.x == 0 && threadIdx.x == 0) *scan_n = static_cast<unsigned long long>(tiles) * C;
+  if (C == 0 && blockIdx.x == 0)  // no pairs: empty ranges (else tile_scatter's chunk 0 writes them)
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) ranges[t] = make_uint2(0u, 0u);
   const int64_t c = blockIdx.x;
   if (c >= C) return;
   for (int t = threadIdx.x; t < tiles; t += blockDim.x) s_cnt[t] = 0u;
@@ -1017,9 +1026,8 @@ static int count_sort_pairs(FrameLayout& L, const FrameDesc& fd, cudaStream_t st
   const uint16_t* keys = static_cast<const uint16_t*>(L.pkeys);
   CGS_PROFILED("tile_count_kernel", st,
                tile_count_kernel<<<grid, 256, smem_count, st>>>(keys, L.hdr, T, L.count_log2,
-                                                                L.tcount, L.tcount_n));
+                                                                L.tcount, L.tcount_n, L.ranges));
   CGS_CHECK_LAUNCH("tile_count_kernel");
-  CGS_CUDA(cudaMemsetAsync(L.ranges, 0, sizeof(uint2) * T, st));
   int rc = launch_scan<TileCountScan, 24>(TileCountScan{L.tcount, L.toff, L.tcount_n, static_cast<uint32_t>(T)}, L.tcount_n, 0,
                        static_cast<int64_t>(T) * L.count_chunks_cap, L.tscan, nullptr, st);
   if (rc) return rc;
@@ -1084,16 +1092,20 @@ static int sort_pairs_stage(FrameLayout& L, const FrameDesc& fd, SortWs<KT>& ws,
 int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout& L,
                         double* sr_cov, cudaStream_t st) {
   const int64_t vn = L.vn;
-  CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
-  if (sc->sr_capacity > 0) {
+  static_assert(sizeof(FrameHeader) % sizeof(uint32_t) == 0, "header zeroed as words");
+  if (sc->sr_capacity > 0) {  // it also zeroes the frame header and the depth-sort histogram
     CGS_PROFILED("sr_precompute_kernel", st,
                  sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(
-                     sc->sr_rows, sc->sr_capacity, sr_cov));
+                     sc->sr_rows, sc->sr_capacity, sr_cov, reinterpret_cast<uint32_t*>(L.hdr),
+                     static_cast<int>(sizeof(FrameHeader) / sizeof(uint32_t)), L.dsort.hist,
+                     4 * 256));
     CGS_CHECK_LAUNCH("sr_precompute_kernel");
+  } else {
+    CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
+    CGS_CUDA(cudaMemsetAsync(L.dsort.hist, 0, 4 * 256 * sizeof(uint32_t), st));
   }
   if (vn > 0) {
     ProjIn in{sc->n, sc->positions, sc->opacity_logits, sc->g2sh, sc->g2sr, sc->sh_rows, sr_cov};
-    CGS_CUDA(cudaMemsetAsync(L.dsort.hist, 0, 4 * 256 * sizeof(uint32_t), st));
     ProjOut out{L.recs, L.depth_key, L.dkey, L.dval, L.dsort.hist, L.n_tiles, L.rect, L.hdr};
     switch (sc->sh_degree) {
       case 0: launch_project<0>(in, fd, out, vn, st); break;

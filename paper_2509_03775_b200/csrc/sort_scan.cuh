@@ -211,8 +211,11 @@ int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t 
     set_error("scan: workspace too small");
     return CGS_EINTERNAL;
   }
-  CGS_CUDA(cudaMemsetAsync(ws.status, 0, parts * sizeof(unsigned long long), st));
-  CGS_CUDA(cudaMemsetAsync(ws.counter, 0, sizeof(unsigned), st));
+  // status words and counter are carved back to back: one memset node
+  CGS_CUDA(cudaMemsetAsync(ws.status, 0,
+                           reinterpret_cast<const char*>(ws.counter + 1) -
+                               reinterpret_cast<const char*>(ws.status),
+                           st));
   CGS_PROFILED("scan_kernel", st, scan_kernel<Op, ROUNDS><<<static_cast<unsigned>(parts), 256, 0, st>>>(op, n_dev, n_host, ws, total));
   CGS_CHECK_LAUNCH("scan_kernel");
   return CGS_OK;
@@ -542,9 +545,12 @@ int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, 
   if (passes < 1) passes = 1;
   if (passes > ws.passes_cap) return CGS_EINVAL;
   if (!hist_ready) CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
+  // status words and the partition counters are carved back to back: one
+  // memset node for both (a graph's memset nodes cost ~2-3 us each)
   CGS_CUDA(cudaMemsetAsync(ws.status, 0,
-                           static_cast<size_t>(passes) * ws.max_parts * 256 * sizeof(uint32_t), st));
-  CGS_CUDA(cudaMemsetAsync(ws.counter, 0, 64 * sizeof(unsigned), st));
+                           reinterpret_cast<const char*>(ws.counter + 64) -
+                               reinterpret_cast<const char*>(ws.status),
+                           st));
   if (!hist_ready) {  // else the producer of the keys already filled ws.hist
     CGS_PROFILED("sort_hist_kernel", st, sort_hist_kernel<K><<<grid_for(n_cap, 256, 4), 256, 0, st>>>(keys, n_dev, n_host, key_bits, ws.hist));
     CGS_CHECK_LAUNCH("sort_hist_kernel");
