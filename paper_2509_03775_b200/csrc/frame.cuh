@@ -98,6 +98,9 @@ struct FrameLayout {
   uint32_t* toff;              // count_chunks_cap x total_tiles (scan result, chunk-major)
   unsigned long long* tcount_n;  // total_tiles x live chunks (the matrix scan's length)
   ScanWs tscan;
+  // set by frame_stage_project when sr_precompute zeroed the depth sort's and
+  // the scans' states (host-side flag: the stages run in order on one stream)
+  bool states_zeroed = false;
 };
 
 // Counting tile sort limits: the scatter keeps a u16 counter per (warp,
@@ -243,7 +246,8 @@ int launch_refine(bool bwd, const FrameDesc& fd, const FrameLayout& L, const uin
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
                       const float* logits, cudaStream_t st, void* zero_first = nullptr,
-                      size_t zero_bytes = 0);
+                      size_t zero_bytes = 0, void* zero_second = nullptr,
+                      size_t zero_bytes2 = 0);
 
 // Emission index of pair (splat s, tile t): pairs of a splat are emitted in
 // row-major order over its tile rect starting at pair_off[s].

@@ -550,7 +550,9 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
                                                           uint2* __restrict__ units,
                                                           uint32_t* __restrict__ ctl,
                                                           uint32_t* __restrict__ zero,
-                                                          int n_zero) {
+                                                          int n_zero,
+                                                          uint32_t* __restrict__ zero2,
+                                                          int n_zero2) {
   // Full chunks (length kChunk, the longest) first, in tile order, placed by
   // a block scan of per-tile counts (no shared-atomic contention on one
   // bucket); then the partial last chunks by length, longest first, through
@@ -564,7 +566,8 @@ __global__ void __launch_bounds__(1024) unit_order_kernel(const uint32_t* __rest
   };
   if (tid < 256) cnt[tid] = 0;
   if (tid == 0) s_full = 0;
-  for (int k = tid; k < n_zero; k += blockDim.x) zero[k] = 0u;  // the caller's header (no memset node)
+  for (int k = tid; k < n_zero; k += blockDim.x) zero[k] = 0u;  // the caller's spans (no memset nodes)
+  for (int k = tid; k < n_zero2; k += blockDim.x) zero2[k] = 0u;
   __syncthreads();
   uint32_t full = 0;
   for (int t = tid; t < total_tiles; t += blockDim.x) {
@@ -878,10 +881,13 @@ int launch_raster_fwd(const FrameDesc& fd, const FrameLayout& L, const uint32_t*
 
 int launch_raster_bwd(const FrameDesc& fd, const FrameLayout& L, const float* final_T,
                       const float* dL, float* partials, unsigned long long* n_processed,
-                      const float* logits, cudaStream_t st, void* zero_first, size_t zero_bytes) {
+                      const float* logits, cudaStream_t st, void* zero_first, size_t zero_bytes,
+                      void* zero_second, size_t zero_bytes2) {
   unit_order_kernel<<<1, 1024, 0, st>>>(L.tile_nproc, fd.total_tiles, L.units, L.unit_ctl,
                                         static_cast<uint32_t*>(zero_first),
-                                        static_cast<int>(zero_bytes / sizeof(uint32_t)));
+                                        static_cast<int>(zero_bytes / sizeof(uint32_t)),
+                                        static_cast<uint32_t*>(zero_second),
+                                        static_cast<int>(zero_bytes2 / sizeof(uint32_t)));
   CGS_CHECK_LAUNCH("unit_order_kernel");
   // persistent grid: every resident CTA slot (per device ordinal)
   static std::atomic<int> resident_dev[kMaxDevices] = {};

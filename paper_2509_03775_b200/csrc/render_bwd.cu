@@ -749,13 +749,14 @@ static void launch_sh_reduce(const int32_t* off, const int32_t* mem, int64_t cap
 // earlier stages left in the backward workspace).
 int bwd_stage_raster(const cgs_scene_t* sc, const FrameDesc& fd, const FrameLayout& L,
                      BwdLayout& B, const float* dL, const float* final_T, cudaStream_t st) {
-  // both codebooks' row flags, carved back to back: one memset node
-  CGS_CUDA(cudaMemsetAsync(B.code_hit[0], 0,
-                           (B.code_hit[1] + (sc->sr_capacity > 0 ? sc->sr_capacity : 1)) - B.code_hit[0],
-                           st));
-  if (fd.total_tiles > 0 && L.vn > 0)  // unit_order_kernel zeroes B.hdr, splat_reduce writes every touched flag
+  // both codebooks' row flags, carved back to back (whole words: the
+  // carver aligns every region)
+  const size_t hit_bytes =
+      align_up(static_cast<size_t>((B.code_hit[1] + (sc->sr_capacity > 0 ? sc->sr_capacity : 1)) - B.code_hit[0]), 4);
+  if (fd.total_tiles > 0 && L.vn > 0)  // unit_order_kernel zeroes B.hdr and the row flags, splat_reduce writes every touched flag
     return launch_raster_bwd(fd, L, final_T, dL, B.partials, &B.hdr->n_processed,
-                             sc->opacity_logits, st, B.hdr, sizeof(BwdHeader));
+                             sc->opacity_logits, st, B.hdr, sizeof(BwdHeader), B.code_hit[0], hit_bytes);
+  CGS_CUDA(cudaMemsetAsync(B.code_hit[0], 0, hit_bytes, st));
   CGS_CUDA(cudaMemsetAsync(B.hdr, 0, sizeof(BwdHeader), st));
   if (L.vn > 0) CGS_CUDA(cudaMemsetAsync(B.touched, 0, L.vn, st));
   return CGS_OK;

@@ -27,13 +27,19 @@ namespace cgs {
 
 // ---------------------------------------------------------------------------
 // Sigma3 = R(q/|q|) diag(exp(2 ls)) R^T per SR row; slot 6 flags |q| == 0.
+struct ZeroSpans {  // word ranges sr_precompute zeroes for the rest of the frame
+  uint32_t* p[5];
+  int64_t n[5];
+};
 __global__ void __launch_bounds__(256) sr_precompute_kernel(const float* __restrict__ rows,
                                                             int64_t cap, double* __restrict__ out,
-                                                            uint32_t* __restrict__ zero_a, int na,
-                                                            uint32_t* __restrict__ zero_b, int nb) {
-  if (blockIdx.x == 0) {  // the frame header and the depth-sort histogram (no memset nodes)
-    for (int k = threadIdx.x; k < na; k += blockDim.x) zero_a[k] = 0u;
-    for (int k = threadIdx.x; k < nb; k += blockDim.x) zero_b[k] = 0u;
+                                                            ZeroSpans z) {
+  {  // the frame header, depth-sort histogram and the sort / scan states (no memset nodes)
+    const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+      for (int64_t k = t0; k < z.n[q]; k += nt) z.p[q][k] = 0u;
   }
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < cap;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1029,7 +1035,8 @@ static int count_sort_pairs(FrameLayout& L, const FrameDesc& fd, cudaStream_t st
                                                                 L.tcount, L.tcount_n, L.ranges));
   CGS_CHECK_LAUNCH("tile_count_kernel");
   int rc = launch_scan<TileCountScan, 24>(TileCountScan{L.tcount, L.toff, L.tcount_n, static_cast<uint32_t>(T)}, L.tcount_n, 0,
-                       static_cast<int64_t>(T) * L.count_chunks_cap, L.tscan, nullptr, st);
+                       static_cast<int64_t>(T) * L.count_chunks_cap, L.tscan, nullptr, st,
+                       /*state_ready=*/L.states_zeroed);
   if (rc) return rc;
   CGS_PROFILED("tile_scatter_kernel", st,
                tile_scatter_kernel<<<grid, kCountWarps * 32, smem_scatter, st>>>(
@@ -1093,13 +1100,29 @@ int frame_stage_project(const cgs_scene_t* sc, const FrameDesc& fd, FrameLayout&
                         double* sr_cov, cudaStream_t st) {
   const int64_t vn = L.vn;
   static_assert(sizeof(FrameHeader) % sizeof(uint32_t) == 0, "header zeroed as words");
-  if (sc->sr_capacity > 0) {  // it also zeroes the frame header and the depth-sort histogram
+  L.states_zeroed = false;
+  if (sc->sr_capacity > 0) {
+    // it also zeroes the frame header, the depth-sort histogram and the
+    // depth sort's / the two scans' states (the later launches skip their memsets)
+    ZeroSpans z{};
+    auto put = [&](int q, void* p, size_t bytes) {
+      z.p[q] = static_cast<uint32_t*>(p);
+      z.n[q] = static_cast<int64_t>(bytes / sizeof(uint32_t));
+    };
+    put(0, L.hdr, sizeof(FrameHeader));
+    put(1, L.dsort.hist, 4 * 256 * sizeof(uint32_t));
+    const ZeroSpan a = sort_state_span(L.dsort), b = scan_state_span(L.scan);
+    put(2, a.p, a.bytes);
+    put(3, b.p, b.bytes);
+    if (L.count_sort) {
+      const ZeroSpan c = scan_state_span(L.tscan);
+      put(4, c.p, c.bytes);
+    }
     CGS_PROFILED("sr_precompute_kernel", st,
                  sr_precompute_kernel<<<grid_for(sc->sr_capacity, 256, 4), 256, 0, st>>>(
-                     sc->sr_rows, sc->sr_capacity, sr_cov, reinterpret_cast<uint32_t*>(L.hdr),
-                     static_cast<int>(sizeof(FrameHeader) / sizeof(uint32_t)), L.dsort.hist,
-                     4 * 256));
+                     sc->sr_rows, sc->sr_capacity, sr_cov, z));
     CGS_CHECK_LAUNCH("sr_precompute_kernel");
+    L.states_zeroed = true;
   } else {
     CGS_CUDA(cudaMemsetAsync(L.hdr, 0, sizeof(FrameHeader), st));
     CGS_CUDA(cudaMemsetAsync(L.dsort.hist, 0, 4 * 256 * sizeof(uint32_t), st));
@@ -1130,7 +1153,7 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     // the projection appended the splats with tiles (count: hdr->n_onscreen)
     int rc = launch_radix_sort<uint32_t>(L.dkey, L.dval, &L.hdr->n_onscreen, vn, vn,
                                          8 * kDepthPasses, L.dsort, &kres, &perm, st,
-                                         /*hist_ready=*/true);
+                                         /*hist_ready=*/true, /*state_ready=*/L.states_zeroed);
     if (rc) return rc;
     if (perm != L.dsort.vals_alt) {
       set_error("depth sort: unexpected result buffer");
@@ -1159,7 +1182,7 @@ int frame_stage_sort_depth(const FrameDesc& fd, FrameLayout& L, cudaStream_t st)
     perm = depth_perm(L);
   }
   int rc = launch_scan(PairOffsets{perm, L.n_tiles, L.pair_off, L.off_rank, L.hdr, L.pair_cap, fd.n_views}, &L.hdr->n_onscreen, vn,
-                       vn, L.scan, &L.hdr->scratch[0], st);
+                       vn, L.scan, &L.hdr->scratch[0], st, /*state_ready=*/L.states_zeroed);
   if (rc) return rc;
   return CGS_OK;
 }

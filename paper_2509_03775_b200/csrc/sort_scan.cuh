@@ -203,15 +203,28 @@ __global__ void __launch_bounds__(256) scan_kernel(Op op, const unsigned long lo
   }
 }
 
+// The byte range a scan's launch zeroes (status words + counter).
+struct ZeroSpan {
+  void* p;
+  size_t bytes;
+};
+inline ZeroSpan scan_state_span(const ScanWs& ws) {
+  return {ws.status, static_cast<size_t>(reinterpret_cast<const char*>(ws.counter + 1) -
+                                         reinterpret_cast<const char*>(ws.status))};
+}
+
 template <class Op, int ROUNDS = kScanRounds>
 int launch_scan(Op op, const unsigned long long* n_dev, int64_t n_host, int64_t n_cap,
-                const ScanWs& ws, unsigned long long* total, cudaStream_t st) {
+                const ScanWs& ws, unsigned long long* total, cudaStream_t st,
+                bool state_ready = false) {
   const int64_t parts = ceil_div(n_cap > 0 ? n_cap : 1, kScanWarps * ROUNDS * 32);
   if (parts > ws.max_parts) {
     set_error("scan: workspace too small");
     return CGS_EINTERNAL;
   }
-  // status words and counter are carved back to back: one memset node
+  // status words and counter are carved back to back: one memset node, none
+  // when an earlier kernel zeroed them (state_ready: scan_state_span)
+  if (!state_ready)
   CGS_CUDA(cudaMemsetAsync(ws.status, 0,
                            reinterpret_cast<const char*>(ws.counter + 1) -
                                reinterpret_cast<const char*>(ws.status),
@@ -537,16 +550,26 @@ __global__ void __launch_bounds__(WARPS * 32, 2) onesweep_kernel(
 // n_host; n_cap bounds it) on the low key_bits.  Returns, through
 // out_keys/out_vals, the buffers holding the result (the inputs or the
 // workspace alternates, depending on the pass count).
+// The byte range a sort's launch zeroes (status words + counters).
+template <typename K>
+inline ZeroSpan sort_state_span(const SortWs<K>& ws) {
+  return {ws.status, static_cast<size_t>(reinterpret_cast<const char*>(ws.counter + 64) -
+                                         reinterpret_cast<const char*>(ws.status))};
+}
+
 template <typename K>
 int launch_radix_sort(K* keys, uint32_t* vals, const unsigned long long* n_dev, int64_t n_host,
                       int64_t n_cap, int key_bits, const SortWs<K>& ws, K** out_keys,
-                      uint32_t** out_vals, cudaStream_t st, bool hist_ready = false) {
+                      uint32_t** out_vals, cudaStream_t st, bool hist_ready = false,
+                      bool state_ready = false) {
   int passes = (key_bits + 7) / 8;
   if (passes < 1) passes = 1;
   if (passes > ws.passes_cap) return CGS_EINVAL;
   if (!hist_ready) CGS_CUDA(cudaMemsetAsync(ws.hist, 0, passes * 256 * sizeof(uint32_t), st));
   // status words and the partition counters are carved back to back: one
-  // memset node for both (a graph's memset nodes cost ~2-3 us each)
+  // memset node for both (a graph's memset nodes cost ~2-3 us each), none
+  // when an earlier kernel zeroed them (state_ready: sort_state_span)
+  if (!state_ready)
   CGS_CUDA(cudaMemsetAsync(ws.status, 0,
                            reinterpret_cast<const char*>(ws.counter + 64) -
                                reinterpret_cast<const char*>(ws.status),
