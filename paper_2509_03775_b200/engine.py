@@ -26,7 +26,7 @@ import torch
 
 from . import _native as nat
 from .metrics import LossWorkspace
-from .model import ModelState, densify
+from .model import ModelState, densify, densify_prepare
 from .render import Frame, GradientSet, backward_workspace_bytes
 from .sampler import (SamplerConfig, SamplerError, TransitionRecord, merge_step, sgld_update,
                       split_step)
@@ -101,6 +101,9 @@ class Trainer:
         self._cap_stream = None
         self.captures = 0
         state.prefetch_host_index()  # the MCMC loop reads the assignments from the host
+        if config.densify_every > 0 and config.device_noise:  # its buffers outside any timed window
+            ncap = max(state.gaussians.capacity, state.num_gaussians)
+            densify_prepare(state, ncap, int(config.densify_growth * ncap) + 1)
 
     # -- buffers ---------------------------------------------------------------
     def _capacity_buffers(self):
